@@ -1,0 +1,182 @@
+/*
+ * glsgpu.h -- the C-ABI drop-in boundary of the B200-native GLS-PCG (PCG-Aug, SUR) solver.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types in the signatures).  Every entry point
+ * replaces one piece of the reference's C++ hot path (citations are /root/reference paths):
+ *
+ *   glsgpu_sur_create / _create_device   make_sur + sur_preconditioner (per-block Householder QR)
+ *                                        proj/include/gls/structured.hpp:63,105-108;
+ *                                        proj/src/structured.cpp:97-105,416-453,479-486
+ *   glsgpu_apply_pi / _xstar_t / _xstar  IndefinitePreconditioner::apply_pi/apply_xstar_t/apply_xstar
+ *                                        proj/include/gls/preconditioner.hpp:36-38;
+ *                                        proj/src/preconditioner.cpp:9-28, structured.cpp:307-340
+ *   glsgpu_sigma_apply                   SymmetricOperator::apply, Kronecker branch
+ *                                        proj/include/gls/operators.hpp:18,22; proj/src/operators.cpp:42-50
+ *   glsgpu_operator_norm_probe           operator_norm_probe  proj/include/gls/pcg.hpp:132; pcg.cpp:233-244
+ *   glsgpu_sur_solve                     pcg_aug(embed_sur(sur), *sur_preconditioner(sur), w1, z1, cfg,
+ *                                        true_beta)  proj/include/gls/pcg.hpp:80-83; proj/src/pcg.cpp:36-229,346-350
+ *   glsgpu_counters / _reset_counters    IndefinitePreconditioner::counters / reset_apply_counters
+ *                                        proj/include/gls/preconditioner.hpp:40-41; preconditioner.cpp:30-35
+ *
+ * Errors: every call returns a status code; the codes map 1:1 onto the reference's gls::Error
+ * subclasses (proj/include/gls/errors.hpp:10-88) and glsgpu_last_error_message() holds the text.
+ * There is no CPU fallback: without a CUDA device, creation fails with GLSGPU_ERR_NO_DEVICE.
+ *
+ * Layouts (as the reference, proj/include/gls/dense_matrix.hpp:13-15): column-major.  X is the
+ * concatenation [X_0 | ... | X_{G-1}] as one M x n matrix (n = sum n_i); Y is M x G; Omega is G x G;
+ * every m-vector (m = G*M) is stacked equation-major, i.e. equation b owns [b*M, (b+1)*M).
+ */
+#ifndef GLSGPU_H
+#define GLSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (gls::Error subclasses, proj/include/gls/errors.hpp). */
+enum {
+  GLSGPU_OK = 0,
+  GLSGPU_ERR_DIMENSION_MISMATCH = 1,  /* gls::DimensionMismatch */
+  GLSGPU_ERR_RANK_DEFICIENT = 2,      /* gls::RankDeficient ("block i is rank deficient") */
+  GLSGPU_ERR_SINGULAR_D = 3,          /* gls::SingularD (non-positive block scale) */
+  GLSGPU_ERR_SINGULAR_TRIANGULAR = 4, /* gls::SingularTriangular */
+  GLSGPU_ERR_CUDA = 10,               /* CUDA runtime failure */
+  GLSGPU_ERR_NO_DEVICE = 11,          /* no CUDA device: there is no CPU fallback */
+  GLSGPU_ERR_OUT_OF_MEMORY = 12,
+  GLSGPU_ERR_UNSUPPORTED = 13,        /* shape outside this build's kernels (e.g. n_i > 512, G > 512) */
+  GLSGPU_ERR_INVALID = 14,            /* null handle / bad argument */
+  GLSGPU_ERR_NCCL = 15
+};
+
+/* gls::Termination (proj/include/gls/glm.hpp:26), same order. */
+enum { GLSGPU_CONVERGED = 0, GLSGPU_BREAKDOWN = 1, GLSGPU_STAGNATION = 2, GLSGPU_MAXITER = 3, GLSGPU_DIRECT = 4 };
+
+/* How X*v enters the residual update r -= lambda (Sigma u + X v)  (proj/src/pcg.cpp:154-155). */
+enum {
+  GLSGPU_XV_X = 0,  /* reference-faithful: the original X times v (bitwise the reference's row sums) */
+  GLSGPU_XV_QR = 1  /* Q (R v) with R v kept by the recurrence s = Q'r + mu s: X is not streamed */
+};
+
+/* gls::PcgConfig (proj/include/gls/pcg.hpp:12-30) plus device-execution knobs. */
+typedef struct {
+  double tol_rel;            /* stop when c_{i+1} <= tol_rel^2 c_1 */
+  int64_t max_iter;          /* 0 -> m - n + 1 */
+  double breakdown_tol;      /* 1e-14 */
+  int64_t stagnation_window; /* 5 */
+  double growth_tol;         /* 1e4 */
+  int64_t growth_window;     /* 10 */
+  int64_t record_z_every;    /* 1 */
+  /* --- device knobs (not in the reference) --- */
+  int32_t diag_every;        /* trace diagnostics (aug_residual_norm, dual_feas_norm, rmse) every k rows;
+                                1 = every row as the reference; 0 = row 0 and the terminating row only */
+  int32_t xv_mode;           /* GLSGPU_XV_X or GLSGPU_XV_QR */
+  int32_t graph_chunk;       /* PCG iterations per CUDA-graph launch (0 = auto) */
+  int32_t kernel_timing;     /* 1 = record CUDA events around every streaming pass (glsgpu_kernel_stats) */
+} glsgpu_pcg_config;
+
+/* gls::PcgTraceRow (proj/include/gls/pcg.hpp:32-39).  Diagnostics not computed are NaN. */
+typedef struct {
+  int64_t iter;
+  double c;
+  double aug_residual_norm;
+  double dual_feas_norm;
+  double rmse;
+  int64_t elapsed_ns;
+} glsgpu_trace_row;
+
+/* GlsSolution / PcgTrace scalars (proj/include/gls/glm.hpp:30-37, pcg.hpp:41-51). */
+typedef struct {
+  int64_t iterations;
+  int32_t termination;
+  int32_t w1_projected;
+  int64_t breakdown_iteration; /* -1 when absent */
+  double residual_seminorm;
+  int64_t n_rows;              /* trace rows (iterations + 1) */
+  double sigma_scale;          /* operator_norm_probe(Sigma) used by the breakdown test */
+  double solve_ms;             /* device time of the solve (CUDA events on the solver stream) */
+} glsgpu_result;
+
+/* gls::CostCounters (proj/include/gls/preconditioner.hpp:15-22). */
+typedef struct {
+  uint64_t factorizations;
+  uint64_t factor_multiplies;
+  uint64_t pi_applies;
+  uint64_t xstar_t_applies;
+  uint64_t xstar_applies;
+  uint64_t apply_multiplies;
+} glsgpu_counters_t;
+
+/* Per streaming pass timing (kernel_timing = 1). */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double total_ms;
+  double bytes_per_launch;     /* algorithmic bytes of one launch */
+} glsgpu_kernel_stat;
+
+typedef struct glsgpu_sur glsgpu_sur; /* opaque: one SUR operator resident on one device */
+
+int glsgpu_device_count(int* count);
+const char* glsgpu_last_error_message(void);
+const char* glsgpu_version(void);
+
+/* make_sur + sur_preconditioner from HOST buffers (copied to the device; the QR runs there).
+ * block_scale may be NULL (D = I).  On RankDeficient / SingularD, *bad_block gets the block. */
+int glsgpu_sur_create(int G, int64_t M, const int64_t* n_i, const double* X, const double* Y,
+                      const double* omega, const double* block_scale, int device, glsgpu_sur** out,
+                      int* bad_block);
+
+/* Same from DEVICE-resident X (ld >= M, column-major) and Y (ld >= M): no host copy of the big
+ * inputs.  The caller keeps X_dev / Y_dev alive for the handle's lifetime. */
+int glsgpu_sur_create_device(int G, int64_t M, const int64_t* n_i, const double* X_dev, int64_t ldx,
+                             const double* Y_dev, int64_t ldy, const double* omega, const double* block_scale,
+                             int device, glsgpu_sur** out, int* bad_block);
+
+/* Re-run the setup QR from the resident X (the per-solve setup cost; bench steps time it). */
+int glsgpu_sur_refactor(glsgpu_sur* h, int* bad_block);
+
+int glsgpu_sur_destroy(glsgpu_sur* h);
+int glsgpu_sur_dims(const glsgpu_sur* h, int* G, int64_t* M, int64_t* n);
+/* The solver's CUDA stream (cudaStream_t as void*), for callers that time on it. */
+void* glsgpu_sur_stream(const glsgpu_sur* h);
+
+/* Probe-level operator applies on HOST vectors (sizes m -> m, m -> n, n -> m). */
+int glsgpu_apply_pi(glsgpu_sur* h, const double* xi, double* out);
+int glsgpu_apply_xstar_t(glsgpu_sur* h, const double* xi, double* out);
+int glsgpu_apply_xstar(glsgpu_sur* h, const double* v, double* out);
+int glsgpu_sigma_apply(glsgpu_sur* h, const double* x, double* out);
+int glsgpu_operator_norm_probe(glsgpu_sur* h, int64_t iters, double* norm);
+
+int glsgpu_counters(const glsgpu_sur* h, glsgpu_counters_t* out);
+int glsgpu_reset_apply_counters(glsgpu_sur* h);
+
+/* pcg_aug on the SUR model.  w1 (m), z1 (n), beta_true (n) may be NULL (zeros / no rmse).
+ * b_out (n) required; w_out (m) and rows (rows_cap) optional. */
+int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg, const double* w1, const double* z1,
+                     const double* beta_true, double* b_out, double* w_out, glsgpu_trace_row* rows,
+                     int64_t rows_cap, glsgpu_result* res);
+
+void glsgpu_default_config(glsgpu_pcg_config* cfg);
+
+/* Kernel statistics of the last solve with kernel_timing = 1; returns the number written. */
+int glsgpu_kernel_stats(const glsgpu_sur* h, glsgpu_kernel_stat* out, int cap);
+
+/* Test / bench helpers (not part of the reference surface) ---------------------------------- */
+/* Copy Q (M x n, ld M) and the concatenated R blocks to host. */
+int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R);
+/* Fill count doubles of device memory with N(0,1) draws of the counter-based stream (seed, stream). */
+int glsgpu_synth_normal(double* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t stream,
+                        int device);
+/* Device-side y_b = X_b beta_b + (Z Omega_half)_b for synthetic inputs (Z drawn from stream 3). */
+int glsgpu_synth_response(int G, int64_t M, const int64_t* n_i, const double* X_dev, int64_t ldx,
+                          const double* beta, const double* omega_half, uint64_t seed, double* Y_dev,
+                          int64_t ldy, int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GLSGPU_H */

@@ -1,0 +1,613 @@
+/*
+ * oracle/gls_oracle.c -- TEST INFRASTRUCTURE ONLY (the parity checker, never the product).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load this library.  The product path (paper_2510_14471_b200, libglsgpu.so) never links
+ * or calls it and fails loudly when its CUDA extension is missing.
+ *
+ * What it is: a plain-C restatement of the reference's PCG-Aug solver (Algorithm 3, the
+ * "Recovery" variant) for SUR models with the per-block QR preconditioner and the Kronecker
+ * covariance Sigma = Omega (x) I_M.  It follows the reference line by line; the only change is
+ * that the dense block-diagonal X the reference materialises in embed_sur
+ * (/root/reference/proj/src/structured.cpp:107-119) is never formed: every X apply /
+ * X-transpose apply / Frobenius norm visits the blocks in the same column and row order, which
+ * is bitwise identical because the off-block entries contribute exact +-0.
+ *
+ * Compile WITHOUT fused multiply-add contraction (-ffp-contract=off, no -march) so the
+ * arithmetic matches the reference's default x86-64 SSE2 code generation.
+ *
+ * Parity pin: tests/test_oracle_vs_reference.py checks this restatement bitwise against the
+ * reference itself, compiled from /root/reference by oracle/Makefile into oracle/_ref/.
+ *
+ * Layout (same as the reference): all matrices column-major.  X and Q are the concatenation of
+ * the blocks [X_0 | X_1 | ... ] as one M x n matrix (block b owns columns [p0_b, p0_b + n_b));
+ * R is the concatenation of the n_b x n_b blocks; Y and every m-vector are M x G column-major
+ * (equation b owns rows [b*M, (b+1)*M) of the stacked vector).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <float.h>
+#include <time.h>
+
+#define ORC_OK 0
+#define ORC_DIMENSION_MISMATCH 1
+#define ORC_RANK_DEFICIENT 2
+#define ORC_SINGULAR_D 3
+#define ORC_SINGULAR_TRIANGULAR 4
+#define ORC_NO_MEMORY 12
+
+/* Termination, same order as gls::Termination (proj/include/gls/glm.hpp:26). */
+enum { T_CONVERGED = 0, T_BREAKDOWN = 1, T_STAGNATION = 2, T_MAXITER = 3, T_DIRECT = 4 };
+
+/* Mirrors gls::PcgConfig (proj/include/gls/pcg.hpp:12-30). */
+typedef struct {
+  double tol_rel;
+  int64_t max_iter;
+  double breakdown_tol;
+  int64_t stagnation_window;
+  double growth_tol;
+  int64_t growth_window;
+  int64_t record_z_every;
+} orc_config;
+
+/* Mirrors gls::PcgTraceRow (proj/include/gls/pcg.hpp:32-39). */
+typedef struct {
+  int64_t iter;
+  double c;
+  double aug_residual_norm;
+  double dual_feas_norm;
+  double rmse;
+  int64_t elapsed_ns;
+} orc_trace_row;
+
+/* Result: GlsSolution + PcgTrace scalars (proj/include/gls/glm.hpp:30-37, pcg.hpp:41-51). */
+typedef struct {
+  int64_t iterations;
+  int32_t termination;
+  int32_t w1_projected;
+  int64_t breakdown_iteration; /* -1 when absent */
+  double residual_seminorm;
+  int64_t n_rows;              /* trace rows written (iterations + 1) */
+  double sigma_scale;          /* operator_norm_probe result */
+} orc_result;
+
+/* ------------------------------------------------------------------ dense helpers
+ * proj/src/dense_matrix.cpp:69-91,165-202 */
+
+static double vdot(int64_t n, const double* a, const double* b) {
+  double acc = 0.0;
+  for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
+  return acc;
+}
+static double vnorm2(int64_t n, const double* a) { return sqrt(vdot(n, a, a)); }
+
+/* y = A x (column-major rows x cols, leading dim ld), skipping x_j == 0 (dense_matrix.cpp:69-79) */
+static void gemv(int64_t rows, int64_t cols, const double* a, int64_t ld, const double* x, double* y) {
+  for (int64_t i = 0; i < rows; ++i) y[i] = 0.0;
+  for (int64_t j = 0; j < cols; ++j) {
+    const double xj = x[j];
+    if (xj == 0.0) continue;
+    const double* cj = a + j * ld;
+    for (int64_t i = 0; i < rows; ++i) y[i] += cj[i] * xj;
+  }
+}
+/* y = A' x, sequential dot per column (dense_matrix.cpp:81-91) */
+static void gemv_t(int64_t rows, int64_t cols, const double* a, int64_t ld, const double* x, double* y) {
+  for (int64_t j = 0; j < cols; ++j) {
+    const double* cj = a + j * ld;
+    double acc = 0.0;
+    for (int64_t i = 0; i < rows; ++i) acc += cj[i] * x[i];
+    y[j] = acc;
+  }
+}
+
+/* ------------------------------------------------------------------ linalg
+ * Householder QR: proj/src/linalg.cpp:24-117.  a is m x n (ld = m), overwritten with the packed
+ * reflectors (unit-head convention, packed(k,k) = v0); beta[k] = 2/v'v; rdiag[k] = alpha. */
+static void householder_factor(int64_t m, int64_t n, double* w, double* beta, double* rdiag) {
+  for (int64_t k = 0; k < n; ++k) {
+    double norm_x = 0.0;
+    for (int64_t i = k; i < m; ++i) norm_x = hypot(norm_x, w[i + k * m]);
+    if (norm_x == 0.0) {
+      beta[k] = 0.0;
+      rdiag[k] = 0.0;
+      continue;
+    }
+    const double wkk = w[k + k * m];
+    const double alpha = wkk >= 0.0 ? -norm_x : norm_x;
+    const double v0 = wkk - alpha;
+    beta[k] = -1.0 / (alpha * v0);
+    w[k + k * m] = v0;
+    for (int64_t i = k + 1; i < m; ++i) w[i + k * m] /= v0;
+    const double beta_hat = beta[k] * v0 * v0;
+    for (int64_t j = k + 1; j < n; ++j) {
+      double s = w[k + j * m];
+      for (int64_t i = k + 1; i < m; ++i) s += w[i + k * m] * w[i + j * m];
+      s *= beta_hat;
+      w[k + j * m] -= s;
+      for (int64_t i = k + 1; i < m; ++i) w[i + j * m] -= s * w[i + k * m];
+    }
+    rdiag[k] = alpha;
+  }
+}
+
+/* check_rank: proj/src/linalg.cpp:55-63 (kDefaultRankTol = 1e-10, linalg.hpp:10) */
+static int check_rank(int64_t n, const double* rdiag, double rank_tol) {
+  double max_d = 0.0, min_d = INFINITY;
+  for (int64_t k = 0; k < n; ++k) {
+    const double d = fabs(rdiag[k]);
+    if (d > max_d) max_d = d;
+    if (d < min_d) min_d = d;
+  }
+  if (max_d == 0.0 || min_d <= rank_tol * max_d) return ORC_RANK_DEFICIENT;
+  return ORC_OK;
+}
+
+/* form_q_columns(f, 0, n): proj/src/linalg.cpp:77-95; q is m x n (ld = ldq) */
+static void form_q(int64_t m, int64_t n, const double* packed, const double* beta, double* q, int64_t ldq) {
+  for (int64_t j = 0; j < n; ++j) {
+    for (int64_t i = 0; i < m; ++i) q[i + j * ldq] = 0.0;
+    q[j + j * ldq] = 1.0;
+  }
+  for (int64_t k = n; k-- > 0;) {
+    if (beta[k] == 0.0) continue;
+    const double v0 = packed[k + k * m];
+    const double beta_hat = beta[k] * v0 * v0;
+    for (int64_t j = 0; j < n; ++j) {
+      double* qj = q + j * ldq;
+      double s = qj[k];
+      for (int64_t i = k + 1; i < m; ++i) s += packed[i + k * m] * qj[i];
+      s *= beta_hat;
+      qj[k] -= s;
+      for (int64_t i = k + 1; i < m; ++i) qj[i] -= s * packed[i + k * m];
+    }
+  }
+}
+
+/* qr_thin: proj/src/linalg.cpp:110-117.  a: m x n (ld = lda), q: m x n (ld = ldq), r: n x n. */
+int orc_qr_thin(int64_t m, int64_t n, const double* a, int64_t lda, double scale, double* q, int64_t ldq,
+                double* r) {
+  if (m < n || n == 0) return ORC_DIMENSION_MISMATCH;
+  double* w = (double*)malloc(sizeof(double) * (size_t)(m * n));
+  double* beta = (double*)malloc(sizeof(double) * (size_t)n);
+  double* rdiag = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!w || !beta || !rdiag) { free(w); free(beta); free(rdiag); return ORC_NO_MEMORY; }
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < m; ++i) w[i + j * m] = a[i + j * lda] * scale; /* DenseMatrix *= w */
+  householder_factor(m, n, w, beta, rdiag);
+  int st = check_rank(n, rdiag, 1e-10);
+  if (st == ORC_OK) {
+    form_q(m, n, w, beta, q, ldq);
+    /* extract_r: proj/src/linalg.cpp:65-73 */
+    for (int64_t j = 0; j < n; ++j) {
+      for (int64_t i = 0; i < n; ++i) r[i + j * n] = 0.0;
+      for (int64_t i = 0; i < j; ++i) r[i + j * n] = w[i + j * m];
+      r[j + j * n] = rdiag[j];
+    }
+  }
+  free(w); free(beta); free(rdiag);
+  return st;
+}
+
+/* tri_solve(R, b) with R upper triangular: proj/src/linalg.cpp:119-145 (Left side). */
+static int tri_solve(int64_t n, const double* r, double* x, int transpose) {
+  for (int64_t i = 0; i < n; ++i)
+    if (r[i + i * n] == 0.0) return ORC_SINGULAR_TRIANGULAR;
+  if (!transpose) {
+    for (int64_t i = n; i-- > 0;) {
+      double s = x[i];
+      for (int64_t j = i + 1; j < n; ++j) s -= r[i + j * n] * x[j];
+      x[i] = s / r[i + i * n];
+    }
+  } else {
+    for (int64_t i = 0; i < n; ++i) {
+      double s = x[i];
+      for (int64_t j = 0; j < i; ++j) s -= r[j + i * n] * x[j];
+      x[i] = s / r[i + i * n];
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ the SUR operator
+ * SurPreconditioner / BlockQrPreconditioner: proj/src/structured.cpp:282-363,416-453. */
+typedef struct {
+  int G;
+  int64_t M;
+  int64_t n; /* total params */
+  const int64_t* nb;
+  int64_t* p0;  /* first parameter index per block */
+  int64_t* r0;  /* offset of R_b in the concatenated R */
+  double* Q;    /* M x n */
+  double* R;    /* concatenated */
+  double* wts;  /* 1/sqrt(block_scale) */
+  double* local;
+  double* tvec;
+} orc_sur;
+
+static void orc_sur_free(orc_sur* s) {
+  if (!s) return;
+  free(s->p0); free(s->r0); free(s->Q); free(s->R); free(s->wts); free(s->local); free(s->tvec);
+  free(s);
+}
+
+static int64_t total_params(int G, const int64_t* nb) {
+  int64_t n = 0;
+  for (int b = 0; b < G; ++b) n += nb[b];
+  return n;
+}
+
+/* Build the operator: per block, qr_thin of w * X_b (structured.cpp:427-450). bad_block gets the
+ * failing block index for RankDeficient / SingularD. */
+static int orc_sur_build(int G, int64_t M, const int64_t* nb, const double* X, const double* scale,
+                         orc_sur** out, int* bad_block) {
+  *out = NULL;
+  if (G < 1) return ORC_DIMENSION_MISMATCH;
+  orc_sur* s = (orc_sur*)calloc(1, sizeof(orc_sur));
+  if (!s) return ORC_NO_MEMORY;
+  s->G = G; s->M = M; s->nb = nb; s->n = total_params(G, nb);
+  int64_t rtot = 0, nmax = 0;
+  for (int b = 0; b < G; ++b) { rtot += nb[b] * nb[b]; if (nb[b] > nmax) nmax = nb[b]; }
+  s->p0 = (int64_t*)malloc(sizeof(int64_t) * G);
+  s->r0 = (int64_t*)malloc(sizeof(int64_t) * G);
+  s->Q = (double*)malloc(sizeof(double) * (size_t)(M * s->n));
+  s->R = (double*)malloc(sizeof(double) * (size_t)(rtot > 0 ? rtot : 1));
+  s->wts = (double*)malloc(sizeof(double) * G);
+  s->local = (double*)malloc(sizeof(double) * (size_t)M);
+  s->tvec = (double*)malloc(sizeof(double) * (size_t)(nmax > 0 ? nmax : 1));
+  if (!s->p0 || !s->r0 || !s->Q || !s->R || !s->wts || !s->local || !s->tvec) { orc_sur_free(s); return ORC_NO_MEMORY; }
+  int64_t p = 0, r = 0;
+  for (int b = 0; b < G; ++b) {
+    if (scale && scale[b] <= 0.0) { if (bad_block) *bad_block = b; orc_sur_free(s); return ORC_SINGULAR_D; }
+    const double w = scale ? 1.0 / sqrt(scale[b]) : 1.0 / sqrt(1.0);
+    s->wts[b] = w;
+    s->p0[b] = p; s->r0[b] = r;
+    int st = orc_qr_thin(M, nb[b], X + p * M, M, w, s->Q + p * M, M, s->R + r);
+    if (st != ORC_OK) { if (bad_block) *bad_block = b; orc_sur_free(s); return st; }
+    p += nb[b]; r += nb[b] * nb[b];
+  }
+  *out = s;
+  return ORC_OK;
+}
+
+/* pi_impl: proj/src/structured.cpp:307-317 */
+static void sur_pi(const orc_sur* s, const double* xi, double* out) {
+  const int64_t M = s->M;
+  for (int b = 0; b < s->G; ++b) {
+    const double w = s->wts[b];
+    const int64_t nbb = s->nb[b];
+    const double* Qb = s->Q + s->p0[b] * M;
+    double* local = s->local;
+    for (int64_t i = 0; i < M; ++i) local[i] = xi[b * M + i] * w;             /* gather */
+    gemv_t(M, nbb, Qb, M, local, s->tvec);                                      /* Q' local */
+    for (int64_t i = 0; i < M; ++i) out[b * M + i] = 0.0;
+    /* proj = Q t, then local -= proj: do it in the reference's order (apply then subtract) */
+    double* proj = out + b * M; /* reuse output slot as proj scratch */
+    gemv(M, nbb, Qb, M, s->tvec, proj);
+    for (int64_t i = 0; i < M; ++i) local[i] -= proj[i];
+    for (int64_t i = 0; i < M; ++i) out[b * M + i] = local[i] * w;              /* scatter */
+  }
+}
+
+/* xstar_t_impl: proj/src/structured.cpp:319-328 */
+static int sur_xstar_t(const orc_sur* s, const double* xi, double* out) {
+  const int64_t M = s->M;
+  for (int b = 0; b < s->G; ++b) {
+    const double w = s->wts[b];
+    const int64_t nbb = s->nb[b];
+    double* local = s->local;
+    for (int64_t i = 0; i < M; ++i) local[i] = xi[b * M + i] * w;
+    gemv_t(M, nbb, s->Q + s->p0[b] * M, M, local, out + s->p0[b]);
+    int st = tri_solve(nbb, s->R + s->r0[b], out + s->p0[b], 0);
+    if (st) return st;
+  }
+  return ORC_OK;
+}
+
+/* xstar_impl: proj/src/structured.cpp:330-340 */
+static int sur_xstar(const orc_sur* s, const double* v, double* out) {
+  const int64_t M = s->M;
+  for (int b = 0; b < s->G; ++b) {
+    const double w = s->wts[b];
+    const int64_t nbb = s->nb[b];
+    double* vi = s->tvec;
+    memcpy(vi, v + s->p0[b], sizeof(double) * (size_t)nbb);
+    int st = tri_solve(nbb, s->R + s->r0[b], vi, 1);
+    if (st) return st;
+    gemv(M, nbb, s->Q + s->p0[b] * M, M, vi, s->local);
+    for (int64_t i = 0; i < M; ++i) out[b * M + i] = s->local[i] * w;
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ structured X applies
+ * The reference applies the dense embed_sur X (structured.cpp:107-119) with
+ * DenseMatrix::apply / apply_transpose (dense_matrix.cpp:69-91).  Per block, same order. */
+static void x_apply(int G, int64_t M, const int64_t* nb, const double* X, const double* v, double* y) {
+  int64_t p = 0;
+  for (int b = 0; b < G; ++b) {
+    gemv(M, nb[b], X + p * M, M, v + p, y + b * M);
+    p += nb[b];
+  }
+}
+static void x_apply_t(int G, int64_t M, const int64_t* nb, const double* X, const double* w, double* out) {
+  int64_t p = 0;
+  for (int b = 0; b < G; ++b) {
+    gemv_t(M, nb[b], X + p * M, M, w + b * M, out + p);
+    p += nb[b];
+  }
+}
+static double x_frobenius(int G, int64_t M, const int64_t* nb, const double* X) {
+  /* DenseMatrix::frobenius_norm (dense_matrix.cpp:93-97): storage order, off-block zeros add +0 */
+  const int64_t n = total_params(G, nb);
+  double acc = 0.0;
+  for (int64_t k = 0; k < M * n; ++k) acc += X[k] * X[k];
+  (void)G;
+  return sqrt(acc);
+}
+
+/* ------------------------------------------------------------------ Kronecker Sigma apply
+ * SymmetricOperator::apply Kron branch (proj/src/operators.cpp:45-50): vec(reshape(x,M,G) * core)
+ * with operator* (dense_matrix.cpp:125-139): j -> p -> i, skipping core(p,j) == 0. */
+void orc_kron_apply(int G, int64_t M, const double* omega, const double* x, double* out) {
+  for (int64_t k = 0; k < M * G; ++k) out[k] = 0.0;
+  for (int j = 0; j < G; ++j) {
+    double* cj = out + (int64_t)j * M;
+    for (int p = 0; p < G; ++p) {
+      const double bpj = omega[p + (int64_t)j * G];
+      if (bpj == 0.0) continue;
+      const double* ap = x + (int64_t)p * M;
+      for (int64_t i = 0; i < M; ++i) cj[i] += ap[i] * bpj;
+    }
+  }
+}
+
+/* operator_norm_probe: proj/src/pcg.cpp:233-244 */
+double orc_norm_probe(int G, int64_t M, const double* omega, int64_t iters) {
+  const int64_t m = M * G;
+  double* v = (double*)malloc(sizeof(double) * (size_t)m);
+  double* t = (double*)malloc(sizeof(double) * (size_t)m);
+  for (int64_t i = 0; i < m; ++i) v[i] = 1.0 / sqrt((double)m);
+  double nrm = 0.0;
+  for (int64_t it = 0; it < iters; ++it) {
+    orc_kron_apply(G, M, omega, v, t);
+    memcpy(v, t, sizeof(double) * (size_t)m);
+    nrm = vnorm2(m, v);
+    if (nrm == 0.0) { free(v); free(t); return 0.0; }
+    for (int64_t i = 0; i < m; ++i) v[i] /= nrm;
+  }
+  free(v); free(t);
+  return nrm;
+}
+
+/* ------------------------------------------------------------------ exported operator probes */
+int orc_sur_setup(int G, int64_t M, const int64_t* nb, const double* X, const double* scale, double* Q_out,
+                  double* R_out, int* bad_block) {
+  orc_sur* s = NULL;
+  int st = orc_sur_build(G, M, nb, X, scale, &s, bad_block);
+  if (st) return st;
+  memcpy(Q_out, s->Q, sizeof(double) * (size_t)(M * s->n));
+  int64_t rtot = 0;
+  for (int b = 0; b < G; ++b) rtot += nb[b] * nb[b];
+  memcpy(R_out, s->R, sizeof(double) * (size_t)rtot);
+  orc_sur_free(s);
+  return ORC_OK;
+}
+
+/* kind: 0 = apply_pi (m -> m), 1 = apply_xstar_t (m -> n), 2 = apply_xstar (n -> m) */
+int orc_sur_apply(int G, int64_t M, const int64_t* nb, const double* X, const double* scale, int kind,
+                  const double* in, double* out) {
+  orc_sur* s = NULL;
+  int bad = -1;
+  int st = orc_sur_build(G, M, nb, X, scale, &s, &bad);
+  if (st) return st;
+  if (kind == 0) sur_pi(s, in, out);
+  else if (kind == 1) st = sur_xstar_t(s, in, out);
+  else st = sur_xstar(s, in, out);
+  orc_sur_free(s);
+  return st;
+}
+
+static int64_t now_ns(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+}
+
+/* ------------------------------------------------------------------ run_aug, Recovery variant
+ * proj/src/pcg.cpp:36-229 (entered through pcg_aug, pcg.cpp:346-350), with
+ * glm = embed_sur(sur) and precond = sur_preconditioner(sur[, block_scale]).
+ *
+ * w1 / z1 may be NULL (zeros); beta_true may be NULL (rmse = NaN).  rows may be NULL (trace not
+ * returned); otherwise it must hold max_iter + 1 rows.  b_out: n, w_out: m (may be NULL). */
+int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y, const double* omega,
+                    const double* scale, const double* w1, const double* z1, const orc_config* cfg,
+                    const double* beta_true, double* b_out, double* w_out, orc_trace_row* rows,
+                    int64_t rows_cap, orc_result* res, int* bad_block) {
+  const int64_t m = M * G;
+  orc_sur* s = NULL;
+  int st = orc_sur_build(G, M, nb, X, scale, &s, bad_block);
+  if (st) return st;
+  const int64_t n = s->n;
+  if (m < n) { orc_sur_free(s); return ORC_DIMENSION_MISMATCH; } /* make_glm: m > n (glm.cpp:10-16) */
+
+  const int64_t max_iter = cfg->max_iter ? cfg->max_iter : (m - n + 1); /* pcg.cpp:34,46-47 */
+  const int64_t stride = cfg->record_z_every ? cfg->record_z_every : 1;
+  const double sigma_scale = orc_norm_probe(G, M, omega, 12);
+  const int64_t start = now_ns();
+
+  size_t mb = sizeof(double) * (size_t)m, nbytes = sizeof(double) * (size_t)(n > 0 ? n : 1);
+  double *w = malloc(mb), *sw = malloc(mb), *r = malloc(mb), *pr = malloc(mb), *u = malloc(mb), *su = malloc(mb),
+         *xv = malloc(mb), *tmp = malloc(mb), *w_best = malloc(mb), *sw_best = malloc(mb);
+  double *z = malloc(nbytes), *v = malloc(nbytes), *xtw = malloc(nbytes), *est = malloc(nbytes),
+         *xr = malloc(nbytes);
+  if (!w || !sw || !r || !pr || !u || !su || !xv || !tmp || !w_best || !sw_best || !z || !v || !xtw || !est || !xr) {
+    st = ORC_NO_MEMORY;
+    goto done;
+  }
+  int64_t nrows = 0;
+  res->w1_projected = 0;
+  res->breakdown_iteration = -1;
+  res->sigma_scale = sigma_scale;
+
+  /* Enforce X'w1 = 0 (pcg.cpp:55-66) */
+  if (w1) memcpy(w, w1, mb); else memset(w, 0, mb);
+  {
+    x_apply_t(G, M, nb, X, w, xtw);
+    const double feas = vnorm2(n, xtw);
+    const double sc = x_frobenius(G, M, nb, X) * vnorm2(m, w);
+    if (feas > 1e-14 * sc && feas > 0.0) {
+      st = sur_xstar(s, xtw, tmp);
+      if (st) goto done;
+      for (int64_t i = 0; i < m; ++i) w[i] -= tmp[i];
+      res->w1_projected = 1;
+    }
+  }
+  if (z1) memcpy(z, z1, nbytes); else memset(z, 0, nbytes);
+  orc_kron_apply(G, M, omega, w, sw);                                   /* sw = Sigma w */
+  x_apply(G, M, nb, X, z, xv);
+  for (int64_t i = 0; i < m; ++i) r[i] = (sw[i] + xv[i]) - Y[i];         /* sub(add(sw, Xz), y) */
+  sur_pi(s, r, pr);
+  double c = vdot(m, r, pr);
+  if (c < 0.0) c = 0.0;                                                  /* max(dot, 0) */
+  const double c1 = c;
+  const double threshold = cfg->tol_rel * cfg->tol_rel * c1;
+
+  /* c_floor (pcg.cpp:79-86) */
+  const double kEpsC = DBL_EPSILON;
+  double pi_gain = 0.0;
+#define C_FLOOR(rn2, prn)                                                          \
+  ((rn2) > 0.0 ? (pi_gain = fmax(pi_gain, (prn) / sqrt(rn2))) : 0.0,               \
+   16.0 * kEpsC * fmax(pi_gain, 1e-3) * (rn2))
+  (void)C_FLOOR(vdot(m, r, r), vnorm2(m, pr));
+
+  memcpy(u, pr, mb);
+  st = sur_xstar_t(s, r, v);
+  if (st) goto done;
+
+  /* recover(sw) = X*'(y - sw) and push_row (pcg.cpp:96-116) */
+#define RECOVER(swsel, outv)                                           \
+  do {                                                                 \
+    for (int64_t i_ = 0; i_ < m; ++i_) tmp[i_] = Y[i_] - (swsel)[i_];  \
+    st = sur_xstar_t(s, tmp, (outv));                                  \
+    if (st) goto done;                                                 \
+  } while (0)
+#define PUSH_ROW(iter_, cval_, sampled_)                                                       \
+  do {                                                                                         \
+    if (rows && nrows < rows_cap) {                                                            \
+      orc_trace_row* row_ = &rows[nrows];                                                      \
+      row_->iter = (iter_);                                                                    \
+      row_->c = (cval_);                                                                       \
+      x_apply(G, M, nb, X, est, tmp);                                                          \
+      for (int64_t i_ = 0; i_ < m; ++i_) tmp[i_] = Y[i_] - (sw[i_] + tmp[i_]);                 \
+      row_->aug_residual_norm = vnorm2(m, tmp);                                                \
+      x_apply_t(G, M, nb, X, w, xtw);                                                          \
+      row_->dual_feas_norm = vnorm2(n, xtw);                                                   \
+      if ((sampled_) && beta_true) {                                                           \
+        double acc_ = 0.0;                                                                     \
+        for (int64_t k_ = 0; k_ < n; ++k_) { const double d_ = est[k_] - beta_true[k_]; acc_ += d_ * d_; } \
+        row_->rmse = sqrt(acc_ / (double)n);                                                   \
+      } else {                                                                                 \
+        row_->rmse = NAN;                                                                      \
+      }                                                                                        \
+      row_->elapsed_ns = now_ns() - start;                                                     \
+    }                                                                                          \
+    ++nrows;                                                                                   \
+  } while (0)
+
+  RECOVER(sw, est);
+  PUSH_ROW(0, c, 1);
+
+  memcpy(w_best, w, mb);
+  memcpy(sw_best, sw, mb);
+  double c_best = c;
+  int64_t best_iter = 0, stagnant = 0, done_it = 0;
+  int term = T_MAXITER;
+
+  if (c1 == 0.0) {
+    term = T_CONVERGED;
+  } else {
+    for (int64_t i = 1; i <= max_iter; ++i) {
+      orc_kron_apply(G, M, omega, u, su);                               /* su = Sigma u */
+      const double d = vdot(m, u, su);
+      if (fabs(d) <= cfg->breakdown_tol * vdot(m, u, u) * sigma_scale) {
+        term = T_BREAKDOWN;
+        res->breakdown_iteration = i;
+        break;
+      }
+      const double lambda = c / d;
+      for (int64_t k = 0; k < m; ++k) w[k] += -lambda * u[k];          /* axpy(-lambda, u, w) */
+      for (int64_t k = 0; k < m; ++k) sw[k] += -lambda * su[k];        /* axpy(-lambda, su, sw) */
+      x_apply(G, M, nb, X, v, xv);
+      for (int64_t k = 0; k < m; ++k) r[k] -= lambda * (su[k] + xv[k]);
+      sur_pi(s, r, pr);
+      double c_next = vdot(m, r, pr);
+      done_it = i;
+
+      const int sampled = (i % stride == 0) || c_next <= threshold || i == max_iter;
+      RECOVER(sw, est);
+      PUSH_ROW(i, c_next, sampled);
+
+      const double floor_c = C_FLOOR(vdot(m, r, r), vnorm2(m, pr));
+      const int exhausted = fabs(c_next) <= floor_c / 64.0 || (fabs(c_next) <= floor_c && c_next <= 1e-6 * c);
+      if (c_next < 0.0 && fabs(c_next) > floor_c) {
+        term = T_BREAKDOWN;
+        res->breakdown_iteration = i;
+        break;
+      }
+      if (c_next < 0.0) c_next = 0.0;
+      if (c_next < c_best) {
+        c_best = c_next;
+        memcpy(w_best, w, mb);
+        memcpy(sw_best, sw, mb);
+        best_iter = i;
+      }
+      if (c_next <= threshold || exhausted) {
+        term = T_CONVERGED;
+        break;
+      }
+      if (fabs(c_next - c) <= 1e-15 * c) {
+        if (++stagnant >= cfg->stagnation_window) {
+          term = T_STAGNATION;
+          break;
+        }
+      } else {
+        stagnant = 0;
+      }
+      if (c_next > cfg->growth_tol * c_best && i - best_iter >= cfg->growth_window) {
+        term = T_BREAKDOWN;
+        res->breakdown_iteration = i;
+        break;
+      }
+      const double mu = c_next / c;
+      c = c_next;
+      st = sur_xstar_t(s, r, xr);
+      if (st) goto done;
+      for (int64_t k = 0; k < n; ++k) v[k] = xr[k] + mu * v[k];
+      for (int64_t k = 0; k < m; ++k) u[k] = pr[k] + mu * u[k];
+    }
+  }
+
+  {
+    const int keep_last = term == T_CONVERGED;
+    const double* w_sel = keep_last ? w : w_best;
+    const double* sw_sel = keep_last ? sw : sw_best;
+    if (w_out) memcpy(w_out, w_sel, mb);
+    RECOVER(sw_sel, b_out);
+    res->iterations = done_it;
+    res->termination = term;
+    res->residual_seminorm = keep_last ? c : c_best;
+    res->n_rows = nrows;
+  }
+#undef C_FLOOR
+#undef RECOVER
+#undef PUSH_ROW
+
+done:
+  free(w); free(sw); free(r); free(pr); free(u); free(su); free(xv); free(tmp); free(w_best); free(sw_best);
+  free(z); free(v); free(xtw); free(est); free(xr);
+  orc_sur_free(s);
+  return st;
+}

@@ -1,0 +1,192 @@
+// oracle/ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A C-ABI shim over the UNMODIFIED reference library (gls_core), compiled from the sources under
+// /root/reference/proj by oracle/Makefile into oracle/_ref/libglsref.so.  It runs the reference's
+// own literal hot-path call
+//     pcg_aug(embed_sur(sur), *sur_preconditioner(sur[, scale]), w1, z1, cfg)
+// (proj/src/pcg.cpp:346-350, proj/src/structured.cpp:107-119,479-486) on flat arrays, so the
+// oracle restatement (gls_oracle.c) and the GPU path can be pinned against the reference itself.
+// Nothing here is reference source: it only calls the reference's public API.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "gls/errors.hpp"
+#include "gls/pcg.hpp"
+#include "gls/structured.hpp"
+
+namespace {
+
+struct Config {
+  double tol_rel;
+  int64_t max_iter;
+  double breakdown_tol;
+  int64_t stagnation_window;
+  double growth_tol;
+  int64_t growth_window;
+  int64_t record_z_every;
+};
+
+struct TraceRow {
+  int64_t iter;
+  double c;
+  double aug_residual_norm;
+  double dual_feas_norm;
+  double rmse;
+  int64_t elapsed_ns;
+};
+
+struct Result {
+  int64_t iterations;
+  int32_t termination;
+  int32_t w1_projected;
+  int64_t breakdown_iteration;
+  double residual_seminorm;
+  int64_t n_rows;
+  double sigma_scale;
+};
+
+int code_of(const gls::Error& e) {
+  if (dynamic_cast<const gls::DimensionMismatch*>(&e)) return 1;
+  if (dynamic_cast<const gls::RankDeficient*>(&e)) return 2;
+  if (dynamic_cast<const gls::SingularD*>(&e)) return 3;
+  if (dynamic_cast<const gls::SingularTriangular*>(&e)) return 4;
+  return 99;
+}
+
+gls::SurModel build_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y,
+                        const double* omega) {
+  std::vector<gls::DenseMatrix> blocks;
+  int64_t p = 0;
+  for (int b = 0; b < G; ++b) {
+    gls::DenseMatrix blk(M, nb[b]);
+    std::memcpy(blk.data(), X + p * M, sizeof(double) * M * nb[b]);
+    blocks.push_back(std::move(blk));
+    p += nb[b];
+  }
+  gls::DenseMatrix y(M, G);
+  if (Y) std::memcpy(y.data(), Y, sizeof(double) * M * G);
+  gls::DenseMatrix s0(G, G);
+  if (omega) std::memcpy(s0.data(), omega, sizeof(double) * G * G);
+  return gls::make_sur(std::move(blocks), std::move(y), std::move(s0));
+}
+
+thread_local char g_msg[512];
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_msg; }
+
+int ref_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y,
+                    const double* omega, const double* scale, const double* w1, const double* z1,
+                    const Config* cfg, const double* beta_true, double* b_out, double* w_out,
+                    TraceRow* rows, int64_t rows_cap, Result* res) {
+  try {
+    gls::SurModel sur = build_sur(G, M, nb, X, Y, omega);
+    gls::Glm glm = gls::embed_sur(sur);
+    std::unique_ptr<gls::IndefinitePreconditioner> op =
+        scale ? gls::sur_preconditioner(sur, gls::Vector(scale, scale + G))
+              : gls::sur_preconditioner(sur);
+    const std::size_t m = glm.x.rows(), n = glm.x.cols();
+    gls::Vector w(m, 0.0), z(n, 0.0);
+    if (w1) w.assign(w1, w1 + m);
+    if (z1) z.assign(z1, z1 + n);
+    gls::PcgConfig pc;
+    pc.tol_rel = cfg->tol_rel;
+    pc.max_iter = static_cast<std::size_t>(cfg->max_iter);
+    pc.breakdown_tol = cfg->breakdown_tol;
+    pc.stagnation_window = static_cast<std::size_t>(cfg->stagnation_window);
+    pc.growth_tol = cfg->growth_tol;
+    pc.growth_window = static_cast<std::size_t>(cfg->growth_window);
+    pc.record_z_every = static_cast<std::size_t>(cfg->record_z_every);
+    gls::Vector beta;
+    if (beta_true) beta.assign(beta_true, beta_true + n);
+    gls::AugSolveResult out = gls::pcg_aug(glm, *op, w, z, pc, beta_true ? &beta : nullptr);
+    std::memcpy(b_out, out.solution.b.data(), sizeof(double) * n);
+    if (w_out) std::memcpy(w_out, out.solution.w.data(), sizeof(double) * m);
+    res->iterations = static_cast<int64_t>(out.solution.iterations);
+    res->termination = static_cast<int32_t>(out.solution.termination);
+    res->w1_projected = out.trace.w1_projected ? 1 : 0;
+    res->breakdown_iteration =
+        out.trace.breakdown_iteration ? static_cast<int64_t>(*out.trace.breakdown_iteration) : -1;
+    res->residual_seminorm = out.solution.residual_seminorm;
+    res->n_rows = static_cast<int64_t>(out.trace.rows.size());
+    res->sigma_scale = gls::operator_norm_probe(glm.sigma);
+    if (rows) {
+      const int64_t k = std::min<int64_t>(rows_cap, res->n_rows);
+      for (int64_t i = 0; i < k; ++i) {
+        const auto& r = out.trace.rows[i];
+        rows[i] = TraceRow{static_cast<int64_t>(r.iter), r.c, r.aug_residual_norm, r.dual_feas_norm,
+                           r.rmse, r.elapsed_ns};
+      }
+    }
+    return 0;
+  } catch (const gls::Error& e) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", e.what());
+    return code_of(e);
+  } catch (const std::exception& e) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", e.what());
+    return 98;
+  }
+}
+
+// kind: 0 = apply_pi, 1 = apply_xstar_t, 2 = apply_xstar  (proj/src/preconditioner.cpp:9-28)
+int ref_sur_apply(int G, int64_t M, const int64_t* nb, const double* X, const double* scale, int kind,
+                  const double* in, double* out) {
+  try {
+    gls::SurModel sur = build_sur(G, M, nb, X, nullptr, nullptr);
+    auto op = scale ? gls::sur_preconditioner(sur, gls::Vector(scale, scale + G))
+                    : gls::sur_preconditioner(sur);
+    gls::Vector res;
+    if (kind == 0) res = op->apply_pi(gls::Vector(in, in + op->rows()));
+    else if (kind == 1) res = op->apply_xstar_t(gls::Vector(in, in + op->rows()));
+    else res = op->apply_xstar(gls::Vector(in, in + op->params()));
+    std::memcpy(out, res.data(), sizeof(double) * res.size());
+    return 0;
+  } catch (const gls::Error& e) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", e.what());
+    return code_of(e);
+  }
+}
+
+// Kronecker apply through SymmetricOperator::kronecker_identity (proj/src/operators.cpp:20-26,45-50)
+int ref_kron_apply(int G, int64_t M, const double* omega, const double* x, double* out) {
+  try {
+    gls::DenseMatrix core(G, G);
+    std::memcpy(core.data(), omega, sizeof(double) * G * G);
+    auto op = gls::SymmetricOperator::kronecker_identity(core, M);
+    gls::Vector r = op.apply(gls::Vector(x, x + M * G));
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const gls::Error& e) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", e.what());
+    return code_of(e);
+  }
+}
+
+double ref_norm_probe(int G, int64_t M, const double* omega) {
+  gls::DenseMatrix core(G, G);
+  std::memcpy(core.data(), omega, sizeof(double) * G * G);
+  return gls::operator_norm_probe(gls::SymmetricOperator::kronecker_identity(core, M));
+}
+
+// Thin QR (proj/src/linalg.cpp:110-117) with the SUR scaling w = 1/sqrt(scale).
+int ref_qr_thin(int64_t m, int64_t n, const double* a, double* q, double* r) {
+  try {
+    gls::DenseMatrix am(m, n);
+    std::memcpy(am.data(), a, sizeof(double) * m * n);
+    gls::QrThin qr = gls::qr_thin(am);
+    std::memcpy(q, qr.q.data(), sizeof(double) * m * n);
+    std::memcpy(r, qr.r.data(), sizeof(double) * n * n);
+    return 0;
+  } catch (const gls::Error& e) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", e.what());
+    return code_of(e);
+  }
+}
+
+}  // extern "C"

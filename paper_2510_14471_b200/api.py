@@ -1,0 +1,382 @@
+"""Python mirror of the reference's SUR solver API, backed by the B200 library through its C-ABI.
+
+Names, argument meaning and error behaviour follow the reference (/root/reference/proj/include/gls):
+
+  make_sur(blocks, y, sigma0) -> SurModel                     structured.hpp:53-63, structured.cpp:97-105
+  sur_preconditioner(sur[, block_scale]) -> preconditioner    structured.hpp:105-108, structured.cpp:416-486
+      .rows() .params() .apply_pi .apply_xstar_t .apply_xstar .counters() .reset_apply_counters()
+                                                              preconditioner.hpp:30-53, preconditioner.cpp:9-47
+  cost_counters(op) -> CostReport                             preconditioner.hpp:56-64, preconditioner.cpp:37-47
+  pcg_aug(sur, op, w1, z1, config, true_beta) -> AugSolveResult    pcg.hpp:80-83 (Glm = embed_sur(sur))
+  operator_norm_probe(op_or_sur, iters=12)                    pcg.hpp:132
+  PcgConfig / PcgTraceRow / PcgTrace / GlsSolution / Termination   pcg.hpp:12-51, glm.hpp:26-37
+  GlsError and subclasses                                     errors.hpp:10-88
+
+The difference from the reference is the one the SURVEY calls the dense-embedding wall: the reference
+takes `Glm glm = embed_sur(sur)` (a dense (G M) x n X); here the solver takes the SurModel itself and
+never forms it (SURVEY.md s7 "hard parts").
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+_P = C.POINTER(C.c_double)
+_PI64 = C.POINTER(C.c_int64)
+
+
+# ------------------------------------------------------------------------------------------ errors
+class GlsError(RuntimeError):
+    """gls::Error (errors.hpp:10-14)."""
+
+
+class DimensionMismatch(GlsError):
+    pass
+
+
+class RankDeficient(GlsError):
+    pass
+
+
+class SingularD(GlsError):
+    pass
+
+
+class SingularTriangular(GlsError):
+    pass
+
+
+class DeviceError(GlsError):
+    """CUDA failure / no device / unsupported shape (not in the reference: the device side)."""
+
+
+_ERRORS = {1: DimensionMismatch, 2: RankDeficient, 3: SingularD, 4: SingularTriangular}
+
+
+def _check(code: int, lib=None):
+    if code == 0:
+        return
+    lib = lib or L.load()
+    msg = lib.glsgpu_last_error_message().decode()
+    raise _ERRORS.get(code, DeviceError)(f"[{code}] {msg}")
+
+
+def _dp(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_P)
+
+
+# ------------------------------------------------------------------------------------------ types
+class Termination(enum.IntEnum):
+    """gls::Termination (glm.hpp:26)."""
+    Converged = 0
+    Breakdown = 1
+    Stagnation = 2
+    MaxIter = 3
+    Direct = 4
+
+
+@dataclasses.dataclass
+class PcgConfig:
+    """gls::PcgConfig (pcg.hpp:12-30) plus the device knobs of glsgpu_pcg_config."""
+    tol_rel: float = 1e-10
+    max_iter: int = 0
+    breakdown_tol: float = 1e-14
+    stagnation_window: int = 5
+    growth_tol: float = 1e4
+    growth_window: int = 10
+    record_z_every: int = 1
+    diag_every: int = 1        # trace diagnostics every k rows (1 = as the reference; 0 = row 0 + final; -1 = none)
+    xv_mode: str = "x"         # "x": X v with the original X (reference); "qr": Q (R v) by recurrence
+    graph_chunk: int = 0
+    kernel_timing: bool = False
+
+    def to_c(self) -> L.PcgConfigC:
+        return L.PcgConfigC(self.tol_rel, self.max_iter, self.breakdown_tol, self.stagnation_window, self.growth_tol,
+                            self.growth_window, self.record_z_every, self.diag_every,
+                            1 if self.xv_mode == "qr" else 0, self.graph_chunk, 1 if self.kernel_timing else 0)
+
+
+TRACE_DTYPE = np.dtype([("iter", np.int64), ("c", np.float64), ("aug_residual_norm", np.float64),
+                        ("dual_feas_norm", np.float64), ("rmse", np.float64), ("elapsed_ns", np.int64)])
+
+
+@dataclasses.dataclass
+class PcgTrace:
+    rows: np.ndarray                      # TRACE_DTYPE records, len == iterations + 1
+    termination: Termination
+    breakdown_iteration: Optional[int]
+    w1_projected: bool
+
+
+@dataclasses.dataclass
+class GlsSolution:
+    b: np.ndarray
+    w: Optional[np.ndarray]
+    iterations: int
+    termination: Termination
+    residual_seminorm: float
+
+
+@dataclasses.dataclass
+class AugSolveResult:
+    solution: GlsSolution
+    trace: PcgTrace
+    sigma_scale: float = float("nan")
+    solve_ms: float = float("nan")
+
+
+@dataclasses.dataclass
+class CostCounters:
+    factorizations: int
+    factor_multiplies: int
+    pi_applies: int
+    xstar_t_applies: int
+    xstar_applies: int
+    apply_multiplies: int
+
+
+@dataclasses.dataclass
+class CostReport:
+    factorizations: int
+    factor_multiplies: int
+    total_applies: int
+    apply_multiplies: int
+    multiplies_per_apply: float
+
+
+@dataclasses.dataclass
+class SurModel:
+    """gls::SurModel (structured.hpp:53-61): X_i blocks (M x n_i), Y (M x G), sigma0 (G x G).
+
+    Stored as the concatenation X = [X_0 | ... | X_{G-1}] (M x n, column-major) plus widths.
+    """
+    X: np.ndarray
+    nb: np.ndarray
+    y: np.ndarray
+    sigma0: np.ndarray
+
+    def obs(self) -> int:
+        return int(self.y.shape[0])
+
+    def equations(self) -> int:
+        return int(len(self.nb))
+
+    def total_params(self) -> int:
+        return int(self.nb.sum())
+
+
+def make_sur(blocks: Sequence[np.ndarray], y: np.ndarray, sigma0: np.ndarray) -> SurModel:
+    """make_sur (structured.cpp:97-105): same checks, same messages."""
+    if len(blocks) == 0:
+        raise DimensionMismatch("make_sur: need at least one block")
+    y = np.asfortranarray(y, dtype=np.float64)
+    if y.ndim != 2 or y.shape[1] != len(blocks):
+        raise DimensionMismatch("make_sur: Y/blocks mismatch")
+    for b in blocks:
+        if b.shape[0] != y.shape[0]:
+            raise DimensionMismatch("make_sur: block row mismatch")
+    sigma0 = np.asfortranarray(sigma0, dtype=np.float64)
+    if sigma0.shape != (len(blocks), len(blocks)):
+        raise DimensionMismatch("make_sur: Sigma0 must be G x G")
+    nb = np.array([b.shape[1] for b in blocks], dtype=np.int64)
+    X = np.asfortranarray(np.concatenate([np.asarray(b, dtype=np.float64) for b in blocks], axis=1)) \
+        if int(nb.sum()) > 0 else np.zeros((y.shape[0], 0), order="F")
+    return SurModel(X=X, nb=nb, y=y, sigma0=sigma0)
+
+
+def sur_from_problem(prob) -> SurModel:
+    """SurModel of a synth.SurProblem (already concatenated)."""
+    return SurModel(X=np.asfortranarray(prob.X), nb=np.asarray(prob.nb, dtype=np.int64),
+                    y=np.asfortranarray(prob.Y), sigma0=np.asfortranarray(prob.omega))
+
+
+# ------------------------------------------------------------------------------------------ operator
+class GpuSurPreconditioner:
+    """The SUR indefinite preconditioner (SurPreconditioner, structured.cpp:416-453) resident on a B200.
+
+    Construction runs the per-block Householder QR on the device (TSQR tree per block).
+    """
+
+    def __init__(self, sur: SurModel, block_scale: Optional[np.ndarray] = None, device: int = 0):
+        self._lib = L.load()
+        self.sur = sur
+        self._h = C.c_void_p()
+        nb = np.ascontiguousarray(sur.nb, dtype=np.int64)
+        self._nb = nb
+        bad = C.c_int(-1)
+        scale = None if block_scale is None else np.ascontiguousarray(block_scale, dtype=np.float64)
+        if scale is not None and scale.shape != (len(nb),):
+            raise DimensionMismatch("sur_preconditioner: need one scale per block")
+        X = np.asfortranarray(sur.X, dtype=np.float64)
+        Y = np.asfortranarray(sur.y, dtype=np.float64)
+        om = np.asfortranarray(sur.sigma0, dtype=np.float64)
+        code = self._lib.glsgpu_sur_create(len(nb), sur.obs(), nb.ctypes.data_as(_PI64), _dp(X), _dp(Y), _dp(om),
+                                           _dp(scale), device, C.byref(self._h), C.byref(bad))
+        self.bad_block = bad.value
+        _check(code, self._lib)
+        self.m = sur.obs() * len(nb)
+        self.n = int(nb.sum())
+
+    @classmethod
+    def from_device(cls, G: int, M: int, nb, X_ptr: int, ldx: int, Y_ptr: int, ldy: int, omega: np.ndarray,
+                    block_scale=None, device: int = 0) -> "GpuSurPreconditioner":
+        """Operator over device-resident X / Y (bench path: no host copy of the big inputs)."""
+        self = cls.__new__(cls)
+        self._lib = L.load()
+        self.sur = None
+        self._h = C.c_void_p()
+        self._nb = np.ascontiguousarray(nb, dtype=np.int64)
+        bad = C.c_int(-1)
+        om = np.asfortranarray(omega, dtype=np.float64)
+        scale = None if block_scale is None else np.ascontiguousarray(block_scale, dtype=np.float64)
+        code = self._lib.glsgpu_sur_create_device(G, M, self._nb.ctypes.data_as(_PI64), C.c_void_p(X_ptr), ldx,
+                                                  C.c_void_p(Y_ptr), ldy, _dp(om), _dp(scale), device,
+                                                  C.byref(self._h), C.byref(bad))
+        self.bad_block = bad.value
+        _check(code, self._lib)
+        self.m = M * G
+        self.n = int(self._nb.sum())
+        return self
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.glsgpu_sur_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stream_ptr(self) -> int:
+        return int(self._lib.glsgpu_sur_stream(self._h) or 0)
+
+    def rows(self) -> int:
+        return self.m
+
+    def params(self) -> int:
+        return self.n
+
+    def _apply(self, fn, vec, nin, nout):
+        v = np.ascontiguousarray(vec, dtype=np.float64).reshape(-1)
+        if v.size != nin:
+            name = {"glsgpu_apply_pi": "apply_pi", "glsgpu_apply_xstar_t": "apply_xstar_t",
+                    "glsgpu_apply_xstar": "apply_xstar"}.get(fn, fn)
+            raise DimensionMismatch(f"{name}: size mismatch")
+        out = np.empty(nout)
+        _check(getattr(self._lib, fn)(self._h, _dp(v), _dp(out)), self._lib)
+        return out
+
+    def apply_pi(self, xi):
+        return self._apply("glsgpu_apply_pi", xi, self.m, self.m)
+
+    def apply_xstar_t(self, xi):
+        return self._apply("glsgpu_apply_xstar_t", xi, self.m, self.n)
+
+    def apply_xstar(self, v):
+        return self._apply("glsgpu_apply_xstar", v, self.n, self.m)
+
+    def sigma_apply(self, x):
+        return self._apply("glsgpu_sigma_apply", x, self.m, self.m)
+
+    def counters(self) -> CostCounters:
+        c = L.CountersC()
+        _check(self._lib.glsgpu_counters(self._h, C.byref(c)), self._lib)
+        return CostCounters(c.factorizations, c.factor_multiplies, c.pi_applies, c.xstar_t_applies, c.xstar_applies,
+                            c.apply_multiplies)
+
+    def reset_apply_counters(self):
+        _check(self._lib.glsgpu_reset_apply_counters(self._h), self._lib)
+
+    def factors(self):
+        Q = np.zeros((self.m // len(self._nb), self.n), order="F")
+        R = np.zeros(int((self._nb * self._nb).sum()))
+        _check(self._lib.glsgpu_get_factors(self._h, _dp(Q), _dp(R)), self._lib)
+        return Q, R
+
+    def refactor(self):
+        bad = C.c_int(-1)
+        _check(self._lib.glsgpu_sur_refactor(self._h, C.byref(bad)), self._lib)
+
+    def kernel_stats(self) -> List[dict]:
+        arr = (L.KernelStatC * 16)()
+        k = self._lib.glsgpu_kernel_stats(self._h, arr, 16)
+        return [dict(name=arr[i].name.decode(), launches=int(arr[i].launches), total_ms=float(arr[i].total_ms),
+                     bytes_per_launch=float(arr[i].bytes_per_launch)) for i in range(k)]
+
+
+def sur_preconditioner(sur: SurModel, block_scale: Optional[np.ndarray] = None, device: int = 0) -> GpuSurPreconditioner:
+    """sur_preconditioner (structured.cpp:479-486)."""
+    return GpuSurPreconditioner(sur, block_scale, device)
+
+
+def cost_counters(op: GpuSurPreconditioner) -> CostReport:
+    """cost_counters (preconditioner.cpp:37-47)."""
+    c = op.counters()
+    total = c.pi_applies + c.xstar_t_applies + c.xstar_applies
+    return CostReport(c.factorizations, c.factor_multiplies, total, c.apply_multiplies,
+                      (c.apply_multiplies / total) if total else 0.0)
+
+
+def operator_norm_probe(op: GpuSurPreconditioner, iters: int = 12) -> float:
+    out = C.c_double()
+    _check(op._lib.glsgpu_operator_norm_probe(op.handle, iters, C.byref(out)), op._lib)
+    return out.value
+
+
+def pcg_aug(sur_or_op, precond: Optional[GpuSurPreconditioner] = None, w1=None, z1=None,
+            config: Optional[PcgConfig] = None, true_beta=None, want_w: bool = True,
+            want_trace: bool = True) -> AugSolveResult:
+    """pcg_aug (pcg.cpp:346-350 -> run_aug, Recovery variant) on the SUR model, on the device.
+
+    `sur_or_op` is the SurModel (the reference passes embed_sur(sur)); `precond` its
+    sur_preconditioner (built here when None).
+    """
+    op = precond if precond is not None else (sur_or_op if isinstance(sur_or_op, GpuSurPreconditioner)
+                                              else sur_preconditioner(sur_or_op))
+    cfg = config or PcgConfig()
+    m, n = op.m, op.n
+    if w1 is not None and np.asarray(w1).size != m or z1 is not None and np.asarray(z1).size != n:
+        raise DimensionMismatch("pcg_aug: bad initial iterate size")
+    w1a = None if w1 is None else np.ascontiguousarray(w1, dtype=np.float64)
+    z1a = None if z1 is None else np.ascontiguousarray(z1, dtype=np.float64)
+    bt = None if true_beta is None else np.ascontiguousarray(true_beta, dtype=np.float64)
+    max_iter = cfg.max_iter if cfg.max_iter else m - n + 1
+    cap = (max_iter + 1) if want_trace else 0
+    rows = (L.TraceRowC * max(cap, 1))()
+    b = np.empty(n)
+    w = np.empty(m) if want_w else None
+    res = L.ResultC()
+    cc = cfg.to_c()
+    code = op._lib.glsgpu_sur_solve(op.handle, C.byref(cc), _dp(w1a), _dp(z1a), _dp(bt), _dp(b), _dp(w),
+                                    rows if want_trace else None, cap, C.byref(res))
+    _check(code, op._lib)
+    k = min(res.n_rows, cap)
+    tr = np.frombuffer(rows, dtype=TRACE_DTYPE, count=k).copy() if want_trace else np.zeros(0, TRACE_DTYPE)
+    term = Termination(res.termination)
+    sol = GlsSolution(b=b, w=w, iterations=int(res.iterations), termination=term,
+                      residual_seminorm=float(res.residual_seminorm))
+    trace = PcgTrace(rows=tr, termination=term,
+                     breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
+                     w1_projected=bool(res.w1_projected))
+    return AugSolveResult(solution=sol, trace=trace, sigma_scale=float(res.sigma_scale), solve_ms=float(res.solve_ms))
+
+
+def device_count() -> int:
+    lib = L.load()
+    n = C.c_int(0)
+    lib.glsgpu_device_count(C.byref(n))
+    return n.value

@@ -1,0 +1,1249 @@
+// glsgpu.cu -- host runtime + C-ABI of the B200-native SUR PCG-Aug solver (include/glsgpu.h).
+//
+// One glsgpu_sur handle = one SUR operator resident on one device: X, Q (the per-block thin QR
+// factors, TSQR-built on the device), R, Y, Omega and the solver state.  The PCG-Aug iteration
+// (proj/src/pcg.cpp:134-211) runs entirely on the device: three streaming passes per iteration
+// (A: u update + Kronecker Sigma u + d; B: w/sw/r updates + Q'r; C: Pi r + c) with the scalar
+// control in single-CTA kernels between them, captured into CUDA graphs of `graph_chunk`
+// iterations; the host only checks the device's `active` flag between graph launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/glsgpu.h"
+#include "kernels.cuh"
+
+using namespace glsgpu;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+struct GErr {
+  int code;
+  std::string msg;
+  int block;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg, int block = -1) { throw GErr{code, msg, block}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) fail(GLSGPU_ERR_OUT_OF_MEMORY, std::string(what) + ": out of device memory");
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+    fail(GLSGPU_ERR_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+  fail(GLSGPU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+#define CKL(name) cuda_check(cudaGetLastError(), name)
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+template <typename T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+constexpr int64_t QR_SMEM_BYTES = 200 * 1024;
+
+struct Timer {
+  cudaEvent_t a{}, b{};
+};
+
+}  // namespace
+
+struct glsgpu_sur {
+  int dev = 0;
+  cudaStream_t s = nullptr;
+  int G = 0;
+  int64_t M = 0, ldm = 0, n = 0, CH = 0;
+  int nch = 0, nmax = 0;
+  std::vector<int> nb;
+  std::vector<int64_t> p0, r0;
+  std::vector<double> wts;
+  int* d_nb = nullptr;
+  int64_t *d_p0 = nullptr, *d_r0 = nullptr;
+  double* d_wts = nullptr;
+  const double* X = nullptr;
+  int64_t ldx = 0;
+  double* X_own = nullptr;
+  const double* Y = nullptr;
+  int64_t ldy = 0;
+  double* Y_own = nullptr;
+  double *Q = nullptr, *R = nullptr, *omegaT = nullptr;
+  std::vector<double> omega_h;
+  // TSQR plan
+  struct Level {
+    int64_t first, count;  // item range
+    int smem_bytes;
+    int64_t max_rows;
+    bool any_global;
+  };
+  std::vector<Level> qr_levels;
+  QrItem* d_items = nullptr;
+  double* qr_store = nullptr;
+  double* qr_tau = nullptr;
+  double* qr_scratch = nullptr;
+  int64_t qr_slot = 0;
+  int* d_rank_flags = nullptr;
+  // width classes for the column passes
+  int* d_blk_narrow = nullptr;
+  int* d_blk_wide = nullptr;
+  int n_narrow = 0, n_wide = 0;
+  // solver buffers
+  bool solver_ready = false;
+  double *wb[3] = {nullptr, nullptr, nullptr}, *swb[3] = {nullptr, nullptr, nullptr};
+  double *r = nullptr, *u = nullptr, *su = nullptr, *pr = nullptr;
+  double *t = nullptr, *vs = nullptr, *est = nullptr, *t2 = nullptr, *xtw = nullptr, *zvec = nullptr,
+         *beta_d = nullptr;
+  double *tpart = nullptr, *rpart = nullptr, *partA = nullptr, *partC = nullptr, *scal = nullptr;
+  int* d_stop = nullptr;
+  SolveState* st = nullptr;
+  SolveState* st_host = nullptr;  // pinned
+  TraceRowD* rows_d = nullptr;
+  int64_t rows_cap_d = 0;
+  double frob_x = -1.0;
+  glsgpu_counters_t counters{};
+  uint64_t pi_cost = 0, xstar_t_cost = 0, xstar_cost = 0;
+  std::vector<glsgpu_kernel_stat> kstats;
+  // graphs
+  cudaGraphExec_t graph = nullptr;
+  int graph_chunk = 0, graph_xmode = -1, graph_diag = -2, graph_timing = -1;
+  std::vector<cudaEvent_t> tev;  // timing events captured into the graph
+};
+
+namespace {
+
+Geo geo_of(const glsgpu_sur* h) {
+  Geo g;
+  g.G = h->G;
+  g.nch = h->nch;
+  g.M = h->M;
+  g.ldm = h->ldm;
+  g.n = h->n;
+  g.CH = h->CH;
+  g.nb = h->d_nb;
+  g.p0 = h->d_p0;
+  g.r0 = h->d_r0;
+  g.wts = h->d_wts;
+  return g;
+}
+
+int kron_cpl(int G) {
+  if (G <= 32) return 1;
+  if (G <= 64) return 2;
+  if (G <= 128) return 4;
+  if (G <= 256) return 8;
+  return 16;
+}
+
+// out = (Omega (x) I) x with the CTA partials; in_mode per k_kron.
+void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const double* div, double* u_io, double* out,
+                 double* partials, int in_mode, const SolveState* st, int* grid_out) {
+  const int cpl = kron_cpl(h->G);
+  const int rw = cpl >= 16 ? 2 : 4;
+  const int tr = 8 * rw;
+  const int64_t ntiles = h->ldm / tr;
+  const int grid = (int)std::min<int64_t>(ntiles, GRID_CAP);
+  const size_t smem = (size_t)h->G * tr * sizeof(double);
+  if (grid_out) *grid_out = grid;
+#define KRON_CASE(C, RW)                                                                                       \
+  k_kron<C, RW><<<grid, NT, smem, h->s>>>(h->G, h->ldm, ntiles, h->omegaT, src, prv, div, u_io, out, partials, \
+                                          in_mode, st)
+  switch (cpl) {
+    case 1: KRON_CASE(1, 4); break;
+    case 2: KRON_CASE(2, 4); break;
+    case 4: KRON_CASE(4, 4); break;
+    case 8: KRON_CASE(8, 4); break;
+    default: KRON_CASE(16, 2); break;
+  }
+#undef KRON_CASE
+  CKL("k_kron");
+}
+
+int kron_grid(const glsgpu_sur* h) {
+  const int cpl = kron_cpl(h->G);
+  const int tr = 8 * (cpl >= 16 ? 2 : 4);
+  return (int)std::min<int64_t>(h->ldm / tr, GRID_CAP);
+}
+
+int rowpass_grid(const glsgpu_sur* h) { return (int)std::min<int64_t>((int64_t)h->G * h->nch, GRID_CAP); }
+
+// gate: 0 none, 1 st->active, 2 st->diag_now
+template <int MODE>
+void launch_colpass(glsgpu_sur* h, ColArgs a, const SolveState* st) {
+  Geo g = geo_of(h);
+  if (h->n_narrow) {
+    a.blocks = h->d_blk_narrow;
+    k_colpass<MODE, true><<<h->n_narrow * h->nch, NT, 0, h->s>>>(g, a, st);
+    CKL("k_colpass fused");
+  }
+  if (h->n_wide) {
+    a.blocks = h->d_blk_wide;
+    k_colpass<MODE, false><<<h->n_wide * h->nch, NT, (size_t)h->CH * sizeof(double), h->s>>>(g, a, st);
+    CKL("k_colpass panels");
+  }
+}
+
+void launch_reduce_t(glsgpu_sur* h, double* out, const SolveState* st, int gate) {
+  const int per = NT / 32;
+  const int64_t grid = (h->n + per - 1) / per;
+  k_reduce_t<<<(unsigned)grid, NT, 0, h->s>>>(h->tpart, h->n, h->nch, out, st, gate);
+  CKL("k_reduce_t");
+}
+
+ColArgs base_args(glsgpu_sur* h) {
+  ColArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.A = h->Q;
+  a.lda = h->ldm;
+  a.X = h->X;
+  a.ldx = h->ldx;
+  a.u = h->u;
+  a.su = h->su;
+  for (int i = 0; i < 3; ++i) {
+    a.wb[i] = h->wb[i];
+    a.swb[i] = h->swb[i];
+  }
+  a.r = h->r;
+  a.y = h->Y;
+  a.ldy = h->ldy;
+  a.tpart = h->tpart;
+  a.rpart = h->rpart;
+  a.avalid = h->ldm;
+  a.gate = 0;
+  return a;
+}
+
+// ------------------------------------------------------------------------------------------ setup
+void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const double* block_scale) {
+  h->G = G;
+  h->M = M;
+  h->ldm = round_up(M, 32);
+  h->nb.resize(G);
+  h->p0.resize(G);
+  h->r0.resize(G);
+  h->wts.resize(G);
+  int64_t p = 0, r = 0;
+  int nmax = 0;
+  for (int b = 0; b < G; ++b) {
+    h->nb[b] = (int)n_i[b];
+    h->p0[b] = p;
+    h->r0[b] = r;
+    p += n_i[b];
+    r += n_i[b] * n_i[b];
+    nmax = std::max<int>(nmax, (int)n_i[b]);
+    // w = 1/sqrt(scale) (structured.cpp:430)
+    h->wts[b] = 1.0 / std::sqrt(block_scale ? block_scale[b] : 1.0);
+  }
+  h->n = p;
+  h->nmax = nmax;
+  // row chunk of the column passes: 256-row multiples, at most ~64 chunks per block
+  h->CH = std::min<int64_t>(16384, std::max<int64_t>(256, round_up((h->ldm + 63) / 64, 256)));
+  h->nch = (int)((h->ldm + h->CH - 1) / h->CH);
+  h->d_nb = dalloc<int>(G);
+  h->d_p0 = dalloc<int64_t>(G);
+  h->d_r0 = dalloc<int64_t>(G);
+  h->d_wts = dalloc<double>(G);
+  CK(cudaMemcpy(h->d_nb, h->nb.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_p0, h->p0.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_r0, h->r0.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_wts, h->wts.data(), sizeof(double) * G, cudaMemcpyHostToDevice));
+  std::vector<int> narrow, wide;
+  for (int b = 0; b < G; ++b) (h->nb[b] <= 32 ? narrow : wide).push_back(b);
+  h->n_narrow = (int)narrow.size();
+  h->n_wide = (int)wide.size();
+  h->d_blk_narrow = dalloc<int>(narrow.size());
+  h->d_blk_wide = dalloc<int>(wide.size());
+  if (!narrow.empty())
+    CK(cudaMemcpy(h->d_blk_narrow, narrow.data(), sizeof(int) * narrow.size(), cudaMemcpyHostToDevice));
+  if (!wide.empty()) CK(cudaMemcpy(h->d_blk_wide, wide.data(), sizeof(int) * wide.size(), cudaMemcpyHostToDevice));
+  // pass cost model of finalize() (structured.cpp:296-305)
+  h->pi_cost = h->xstar_t_cost = h->xstar_cost = 0;
+  for (int b = 0; b < G; ++b) {
+    const uint64_t rr = (uint64_t)M, nn = (uint64_t)h->nb[b];
+    h->pi_cost += 2 * rr * nn + 2 * rr;
+    h->xstar_t_cost += rr * nn + nn * (nn + 1) / 2 + rr;
+    h->xstar_cost += rr * nn + nn * (nn + 1) / 2 + rr;
+  }
+  h->counters = glsgpu_counters_t{};
+  h->counters.factorizations = (uint64_t)G;
+}
+
+int64_t qr_leaf_rows(int n) {
+  // panel rows per chunk: the panel (rows x n doubles) in <= 200 KB of shared memory when possible,
+  // at least 2n rows, at most 1024 (the register column of k_qr_formq).
+  int64_t L = (QR_SMEM_BYTES / 8) / n;
+  L = std::min<int64_t>(L, 1024);
+  L = L / 32 * 32;
+  if (L < 2 * n) L = std::min<int64_t>(1024, round_up(2 * n, 32));
+  return L;
+}
+
+void build_qr_plan(glsgpu_sur* h) {
+  struct BT {
+    int64_t L;
+    std::vector<int64_t> rows, nchs, tau_off, store_off;
+  };
+  std::vector<BT> trees(h->G);
+  int64_t store_total = 0, tau_total = 0;
+  int depth_max = 0;
+  for (int b = 0; b < h->G; ++b) {
+    BT& t = trees[b];
+    const int n = h->nb[b];
+    t.L = qr_leaf_rows(n);
+    int64_t rows = h->ldm;
+    for (int lvl = 0;; ++lvl) {
+      const int64_t nchk = std::max<int64_t>(1, (rows + t.L - 1) / t.L);
+      t.rows.push_back(rows);
+      t.nchs.push_back(nchk);
+      t.tau_off.push_back(tau_total);
+      tau_total += nchk * n;
+      if (lvl == 0) t.store_off.push_back(-1);
+      else {
+        t.store_off.push_back(store_total);
+        store_total += rows * n;
+      }
+      if (nchk == 1) break;
+      rows = nchk * n;
+    }
+    depth_max = std::max<int>(depth_max, (int)t.rows.size() - 1);
+  }
+  h->qr_store = dalloc<double>(store_total);
+  h->qr_tau = dalloc<double>(tau_total);
+  std::vector<QrItem> items;
+  h->qr_levels.clear();
+  int64_t slot = 0;
+  bool any_global = false;
+  for (int lvl = 0; lvl <= depth_max; ++lvl) {
+    glsgpu_sur::Level L{(int64_t)items.size(), 0, 0, 0, false};
+    for (int b = 0; b < h->G; ++b) {
+      const BT& t = trees[b];
+      if ((int)t.rows.size() <= lvl) continue;
+      const int n = h->nb[b];
+      const int64_t rows = t.rows[lvl], nchk = t.nchs[lvl];
+      const bool top = (lvl == (int)t.rows.size() - 1);
+      double* store_l = lvl == 0 ? nullptr : h->qr_store + t.store_off[lvl];
+      double* store_next = top ? nullptr : h->qr_store + t.store_off[lvl + 1];
+      const int64_t rows_next = top ? 0 : t.rows[lvl + 1];
+      for (int64_t c = 0; c < nchk; ++c) {
+        QrItem it;
+        std::memset(&it, 0, sizeof(it));
+        it.r0 = c * rows / nchk;
+        it.rows = (c + 1) * rows / nchk - it.r0;
+        it.n = n;
+        if (lvl == 0) {
+          it.src = h->X + h->p0[b] * h->ldx;
+          it.lds = h->ldx;
+          it.valid = h->M;
+          it.scale = h->wts[b];
+          it.refl = h->Q + h->p0[b] * h->ldm;
+          it.ldr = h->ldm;
+        } else {
+          it.src = store_l;
+          it.lds = rows;
+          it.valid = rows;
+          it.scale = 1.0;
+          it.refl = store_l;
+          it.ldr = rows;
+        }
+        it.tau = h->qr_tau + t.tau_off[lvl] + c * n;
+        if (top) {
+          it.rout = h->R + h->r0[b];
+          it.ldo = n;
+          it.qpar = nullptr;
+          it.ldp = 0;
+        } else {
+          it.rout = store_next + c * n;
+          it.ldo = rows_next;
+          it.qpar = store_next + c * n;
+          it.ldp = rows_next;
+        }
+        const int64_t bytes = it.rows * n * (int64_t)sizeof(double);
+        it.smem = bytes <= QR_SMEM_BYTES ? 1 : 0;
+        if (it.smem) L.smem_bytes = std::max<int>(L.smem_bytes, (int)bytes);
+        else {
+          L.any_global = true;
+          any_global = true;
+          slot = std::max<int64_t>(slot, it.rows * n);
+        }
+        L.max_rows = std::max<int64_t>(L.max_rows, it.rows);
+        items.push_back(it);
+      }
+    }
+    L.count = (int64_t)items.size() - L.first;
+    h->qr_levels.push_back(L);
+  }
+  h->d_items = dalloc<QrItem>(items.size());
+  CK(cudaMemcpy(h->d_items, items.data(), sizeof(QrItem) * items.size(), cudaMemcpyHostToDevice));
+  h->qr_slot = slot;
+  if (any_global) h->qr_scratch = dalloc<double>((size_t)slot * 2 * 148);
+  h->d_rank_flags = dalloc<int>(h->G);
+}
+
+void run_qr(glsgpu_sur* h) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
+    CK(cudaFuncSetAttribute(k_qr_formq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
+    CK(cudaFuncSetAttribute(k_qr_formq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
+    CK(cudaFuncSetAttribute(k_qr_formq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
+    attr_done = true;
+  }
+  // zero Q (its padding rows stay zero) -- the level-0 reflectors overwrite the rest
+  CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)(h->ldm * h->n), h->s));
+  const int nl = (int)h->qr_levels.size();
+  for (int l = 0; l < nl; ++l) {
+    const auto& L = h->qr_levels[l];
+    const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
+    k_qr_factor<<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch, h->qr_slot);
+    CKL("k_qr_factor");
+  }
+  for (int l = nl - 1; l >= 0; --l) {
+    const auto& L = h->qr_levels[l];
+    const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
+    if (L.max_rows <= 256)
+      k_qr_formq<8><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch, h->qr_slot);
+    else if (L.max_rows <= 512)
+      k_qr_formq<16><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch,
+                                                           h->qr_slot);
+    else
+      k_qr_formq<32><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch,
+                                                           h->qr_slot);
+    CKL("k_qr_formq");
+  }
+  Geo g = geo_of(h);
+  k_rank_check<<<(h->G + 127) / 128, 128, 0, h->s>>>(g, h->R, h->d_rank_flags);
+  CKL("k_rank_check");
+  std::vector<int> flags(h->G);
+  CK(cudaMemcpyAsync(flags.data(), h->d_rank_flags, sizeof(int) * h->G, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  for (int b = 0; b < h->G; ++b)
+    if (flags[b]) fail(GLSGPU_ERR_RANK_DEFICIENT, "sur_preconditioner: block " + std::to_string(b) + " is rank deficient", b);
+}
+
+void validate(int G, int64_t M, const int64_t* n_i, const double* block_scale, const double* omega) {
+  if (G < 1) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_sur: need at least one block");
+  if (!n_i || !omega) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create: null argument");
+  if (M < 1) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_sur: block row mismatch");
+  if (G > 512) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: G > 512 equations is outside this build's Kronecker kernel");
+  for (int b = 0; b < G; ++b) {
+    if (block_scale && !(block_scale[b] > 0.0))
+      fail(GLSGPU_ERR_SINGULAR_D, "sur_preconditioner: scales must be positive", b);
+    if (n_i[b] < 1 || M < n_i[b]) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "qr: need rows >= cols >= 1", b);
+    if (n_i[b] > 512) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: block width > 512 is outside this build's kernels", b);
+  }
+  int64_t n = 0;
+  for (int b = 0; b < G; ++b) n += n_i[b];
+  if (M * G <= n) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_glm: need m > n >= 1");
+}
+
+void upload_omega(glsgpu_sur* h, const double* omega) {
+  const int G = h->G;
+  h->omega_h.assign(omega, omega + (size_t)G * G);
+  std::vector<double> ot((size_t)G * G);
+  for (int p = 0; p < G; ++p)
+    for (int c = 0; c < G; ++c) ot[(size_t)p * G + c] = omega[p + (size_t)c * G];  // row p of Omega
+  h->omegaT = dalloc<double>((size_t)G * G);
+  CK(cudaMemcpy(h->omegaT, ot.data(), sizeof(double) * G * G, cudaMemcpyHostToDevice));
+}
+
+void alloc_common(glsgpu_sur* h) {
+  h->Q = dalloc<double>((size_t)(h->ldm * h->n));
+  int64_t rtot = 0;
+  for (int b = 0; b < h->G; ++b) rtot += (int64_t)h->nb[b] * h->nb[b];
+  h->R = dalloc<double>((size_t)rtot);
+  build_qr_plan(h);
+}
+
+void destroy_impl(glsgpu_sur* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->s) cudaStreamSynchronize(h->s);
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (auto e : h->tev) cudaEventDestroy(e);
+  void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
+                  h->qr_store, h->qr_tau, h->qr_scratch, h->d_rank_flags, h->d_blk_narrow, h->d_blk_wide,
+                  h->wb[0], h->wb[1], h->wb[2], h->swb[0], h->swb[1], h->swb[2], h->r, h->u, h->su, h->pr, h->t,
+                  h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,
+                  h->scal, h->d_stop, h->st, h->rows_d};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->st_host) cudaFreeHost(h->st_host);
+  if (h->s) cudaStreamDestroy(h->s);
+  delete h;
+}
+
+glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* omega, const double* block_scale,
+                          int device) {
+  validate(G, M, n_i, block_scale, omega);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    fail(GLSGPU_ERR_NO_DEVICE, "glsgpu: no CUDA device available (there is no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev) fail(GLSGPU_ERR_INVALID, "glsgpu: bad device ordinal");
+  CK(cudaSetDevice(device));
+  glsgpu_sur* h = new glsgpu_sur();
+  h->dev = device;
+  try {
+    CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    build_geometry(h, G, M, n_i, block_scale);
+    upload_omega(h, omega);
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  return h;
+}
+
+void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
+  if (!h->solver_ready) {
+    const size_t mv = (size_t)(h->ldm * h->G);
+    for (int i = 0; i < 3; ++i) {
+      h->wb[i] = dalloc<double>(mv);
+      h->swb[i] = dalloc<double>(mv);
+    }
+    h->r = dalloc<double>(mv);
+    h->u = dalloc<double>(mv);
+    h->su = dalloc<double>(mv);
+    h->pr = dalloc<double>(mv);
+    h->t = dalloc<double>(h->n);
+    h->vs = dalloc<double>(h->n);
+    h->est = dalloc<double>(h->n);
+    h->t2 = dalloc<double>(h->n);
+    h->xtw = dalloc<double>(h->n);
+    h->zvec = dalloc<double>(h->n);
+    h->beta_d = dalloc<double>(h->n);
+    h->tpart = dalloc<double>((size_t)h->n * h->nch);
+    h->rpart = dalloc<double>((size_t)h->G * h->nch);
+    h->partA = dalloc<double>(GRID_CAP * 3);
+    h->partC = dalloc<double>(GRID_CAP * 3);
+    h->scal = dalloc<double>(64);
+    h->d_stop = dalloc<int>(1);
+    h->st = dalloc<SolveState>(1);
+    CK(cudaMallocHost(&h->st_host, sizeof(SolveState)));
+    for (int i = 0; i < 3; ++i) {
+      CK(cudaMemsetAsync(h->wb[i], 0, mv * sizeof(double), h->s));
+      CK(cudaMemsetAsync(h->swb[i], 0, mv * sizeof(double), h->s));
+    }
+    CK(cudaMemsetAsync(h->r, 0, mv * sizeof(double), h->s));
+    CK(cudaMemsetAsync(h->u, 0, mv * sizeof(double), h->s));
+    CK(cudaMemsetAsync(h->su, 0, mv * sizeof(double), h->s));
+    CK(cudaMemsetAsync(h->pr, 0, mv * sizeof(double), h->s));
+    h->solver_ready = true;
+    // kron kernels: >48 KB dynamic shared memory at large G
+    CK(cudaFuncSetAttribute(k_kron<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 8));
+    CK(cudaFuncSetAttribute(k_kron<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16 * 8));
+    CK(cudaFuncSetAttribute(k_colpass<MODE_B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(h->CH * 8)));
+    CK(cudaFuncSetAttribute(k_colpass<MODE_QT_R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(h->CH * 8)));
+    CK(cudaFuncSetAttribute(k_colpass<MODE_QT_D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(h->CH * 8)));
+    CK(cudaFuncSetAttribute(k_colpass<MODE_QT_V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(h->CH * 8)));
+    CK(cudaFuncSetAttribute(k_colpass<MODE_DIAG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(h->CH * 8)));
+  }
+  if (rows_cap > h->rows_cap_d) {
+    if (h->rows_d) CK(cudaFree(h->rows_d));
+    h->rows_d = dalloc<TraceRowD>((size_t)rows_cap);
+    h->rows_cap_d = rows_cap;
+  }
+}
+
+// m-vector host (ld M per equation) <-> device (ld ldm)
+void h2d_mvec(glsgpu_sur* h, double* dst, const double* src) {
+  CK(cudaMemcpy2DAsync(dst, h->ldm * sizeof(double), src, h->M * sizeof(double), h->M * sizeof(double), h->G,
+                       cudaMemcpyHostToDevice, h->s));
+}
+void d2h_mvec(glsgpu_sur* h, double* dst, const double* src) {
+  CK(cudaMemcpy2DAsync(dst, h->M * sizeof(double), src, h->ldm * sizeof(double), h->M * sizeof(double), h->G,
+                       cudaMemcpyDeviceToHost, h->s));
+}
+
+// t_out = (Q' (w_b x))_b partials reduced: a Q'-apply of an m-vector already on the device.
+void qt_apply(glsgpu_sur* h, int mode, const double* vin, double* out, const SolveState* st, int sel_best) {
+  ColArgs a = base_args(h);
+  a.vin = vin;
+  a.sel_best = sel_best;
+  if (mode == MODE_QT_R) launch_colpass<MODE_QT_R>(h, a, nullptr);
+  else if (mode == MODE_QT_D) launch_colpass<MODE_QT_D>(h, a, st);
+  else launch_colpass<MODE_QT_V>(h, a, nullptr);
+  launch_reduce_t(h, out, nullptr, 0);
+}
+
+double norm_probe(glsgpu_sur* h, int64_t iters) {
+  // operator_norm_probe (pcg.cpp:233-244): v = 1/sqrt(m); repeat: v = Sigma v; nrm = |v|; v /= nrm.
+  ensure_solver(h, 1);
+  const int64_t m = h->M * h->G;
+  const double v0 = 1.0 / std::sqrt(static_cast<double>(m));
+  // v0 in u (rows < M of each column), zero padding
+  CK(cudaMemsetAsync(h->u, 0, sizeof(double) * h->ldm * h->G, h->s));
+  std::vector<double> ones((size_t)h->M, v0);
+  for (int b = 0; b < h->G; ++b)
+    CK(cudaMemcpyAsync(h->u + (int64_t)b * h->ldm, ones.data(), sizeof(double) * h->M, cudaMemcpyHostToDevice, h->s));
+  CK(cudaMemsetAsync(h->d_stop, 0, sizeof(int), h->s));
+  CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->s));
+  double* a = h->u;
+  double* b = h->su;
+  int grid = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    launch_kron(h, a, nullptr, h->scal, nullptr, b, h->partA, it == 0 ? 0 : 1, nullptr, &grid);
+    k_probe_step<<<1, NT, 0, h->s>>>(h->partA, grid, h->scal, h->d_stop);
+    CKL("k_probe_step");
+    std::swap(a, b);
+  }
+  double nrm = 0.0;
+  CK(cudaMemcpyAsync(&nrm, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  CK(cudaMemsetAsync(h->u, 0, sizeof(double) * h->ldm * h->G, h->s));
+  CK(cudaMemsetAsync(h->su, 0, sizeof(double) * h->ldm * h->G, h->s));
+  return nrm;
+}
+
+// ------------------------------------------------------------------------------------------ solve
+// init scalars after the first pi apply: c = max(r.pr, 0), c1, threshold, pi_gain (pcg.cpp:72-86)
+__global__ void k_init_scalars(const double* partials, int count, SolveState* st, TraceRowD* rows) {
+  __shared__ double res[3];
+  reduce_partials<3>(partials, count, res);
+  if (threadIdx.x == 0) {
+    double c = res[0];
+    if (c < 0.0) c = 0.0;
+    st->c = c;
+    st->c1 = c;
+    st->threshold = st->tol_rel * st->tol_rel * c;
+    st->c_best = c;
+    const double rr = res[1], prn = sqrt(res[2]);
+    if (rr > 0.0) st->pi_gain = dmax_std(st->pi_gain, prn / sqrt(rr));
+    if (st->rows_cap > 0) {
+      rows[0].iter = 0;
+      rows[0].c = c;
+      rows[0].aug = __longlong_as_double(0x7ff8000000000000LL);
+      rows[0].dual = rows[0].aug;
+      rows[0].rmse = rows[0].aug;
+      rows[0].elapsed_ns = (int64_t)(globaltimer() - st->t0);
+    }
+    if (c == 0.0) {
+      st->term = T_CONVERGED;
+      st->active = 0;
+    }
+  }
+}
+
+__global__ void k_set_t0(SolveState* st) { st->t0 = globaltimer(); }
+
+void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int iter_idx) {
+  Geo g = geo_of(h);
+  const int gA = kron_grid(h), gC = rowpass_grid(h);
+  auto ev = [&](int k) {
+    if (timing) CK(cudaEventRecordWithFlags(h->tev[(size_t)iter_idx * 6 + k], h->s, cudaEventRecordExternal));
+  };
+  // pass A: u = pr + mu u, su = Sigma u, d = u.su, uu = u.u
+  ev(0);
+  launch_kron(h, nullptr, h->pr, nullptr, h->u, h->su, h->partA, 2, h->st, nullptr);
+  ev(1);
+  k_scalar_a<<<1, NT, 0, h->s>>>(h->partA, gA, h->st);
+  CKL("k_scalar_a");
+  // pass B
+  ColArgs a = base_args(h);
+  a.vec = h->vs;
+  a.xv_from_x = (xv_mode == GLSGPU_XV_X) ? 1 : 0;
+  a.gate = 1;
+  ev(2);
+  launch_colpass<MODE_B>(h, a, h->st);
+  ev(3);
+  launch_reduce_t(h, h->t, h->st, 1);
+  // pass C
+  ev(4);
+  k_rowpass<<<gC, NT, 0, h->s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, h->st);
+  CKL("k_rowpass");
+  ev(5);
+  k_scalar_c<<<1, NT, 0, h->s>>>(h->partC, gC, h->st, h->rows_d);
+  CKL("k_scalar_c");
+  k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, h->vs, a.xv_from_x, 0, h->st);
+  CKL("k_vupdate");
+  if (diag >= 0) {
+    // est = X*'(y - sw) and the row diagnostics, gated on st->diag_now
+    ColArgs d = base_args(h);
+    d.sel_best = 0;
+    d.gate = 2;
+    launch_colpass<MODE_QT_D>(h, d, h->st);
+    k_reduce_t<<<(unsigned)((h->n + 7) / 8), NT, 0, h->s>>>(h->tpart, h->n, h->nch, h->t2, h->st, 2);
+    CKL("k_reduce_t diag");
+    k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
+    CKL("k_vupdate diag");
+    ColArgs x = base_args(h);
+    x.A = h->X;
+    x.lda = h->ldx;
+    x.avalid = h->M;
+    x.vec = h->t2;
+    x.gate = 2;
+    launch_colpass<MODE_DIAG>(h, x, h->st);
+    k_reduce_t<<<(unsigned)((h->n + 7) / 8), NT, 0, h->s>>>(h->tpart, h->n, h->nch, h->xtw, h->st, 2);
+    CKL("k_reduce_t diag2");
+    k_diag_finalize<<<1, NT, 0, h->s>>>(h->rpart, h->G * h->nch, h->xtw, h->n, h->t2, h->beta_d, h->st,
+                                        h->rows_d, -1);
+    CKL("k_diag_finalize");
+  }
+}
+
+}  // namespace
+
+// ================================================================================ C ABI
+extern "C" {
+
+const char* glsgpu_last_error_message(void) { return g_err.c_str(); }
+const char* glsgpu_version(void) { return "glsgpu 0.1 (sm_100a, fp64, no-FMA)"; }
+
+int glsgpu_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return n > 0 ? GLSGPU_OK : GLSGPU_ERR_NO_DEVICE;
+}
+
+void glsgpu_default_config(glsgpu_pcg_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->tol_rel = 1e-10;
+  c->max_iter = 0;
+  c->breakdown_tol = 1e-14;
+  c->stagnation_window = 5;
+  c->growth_tol = 1e4;
+  c->growth_window = 10;
+  c->record_z_every = 1;
+  c->diag_every = 1;
+  c->xv_mode = GLSGPU_XV_X;
+  c->graph_chunk = 0;
+  c->kernel_timing = 0;
+}
+
+#define API_BEGIN try {
+#define API_END(badp)                          \
+  }                                            \
+  catch (const GErr& e) {                      \
+    g_err = e.msg;                             \
+    if (badp && e.block >= 0) *(badp) = e.block; \
+    return e.code;                             \
+  }                                            \
+  catch (const std::exception& e) {            \
+    g_err = e.what();                          \
+    return GLSGPU_ERR_CUDA;                    \
+  }                                            \
+  return GLSGPU_OK;
+
+int glsgpu_sur_create(int G, int64_t M, const int64_t* n_i, const double* X, const double* Y, const double* omega,
+                      const double* block_scale, int device, glsgpu_sur** out, int* bad_block) {
+  API_BEGIN
+  if (!out || !X || !Y) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create: null argument");
+  *out = nullptr;
+  glsgpu_sur* h = create_common(G, M, n_i, omega, block_scale, device);
+  try {
+    h->X_own = dalloc<double>((size_t)(h->ldm * h->n));
+    h->Y_own = dalloc<double>((size_t)(h->ldm * G));
+    CK(cudaMemsetAsync(h->X_own, 0, sizeof(double) * h->ldm * h->n, h->s));
+    CK(cudaMemsetAsync(h->Y_own, 0, sizeof(double) * h->ldm * G, h->s));
+    CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
+                         cudaMemcpyHostToDevice, h->s));
+    CK(cudaMemcpy2DAsync(h->Y_own, h->ldm * sizeof(double), Y, M * sizeof(double), M * sizeof(double), G,
+                         cudaMemcpyHostToDevice, h->s));
+    h->X = h->X_own;
+    h->ldx = h->ldm;
+    h->Y = h->Y_own;
+    h->ldy = h->ldm;
+    alloc_common(h);
+    run_qr(h);
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  *out = h;
+  API_END(bad_block)
+}
+
+int glsgpu_sur_create_device(int G, int64_t M, const int64_t* n_i, const double* X_dev, int64_t ldx,
+                             const double* Y_dev, int64_t ldy, const double* omega, const double* block_scale,
+                             int device, glsgpu_sur** out, int* bad_block) {
+  API_BEGIN
+  if (!out || !X_dev || !Y_dev) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create_device: null argument");
+  if (ldx < M || ldy < M) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "glsgpu_sur_create_device: leading dimension < M");
+  *out = nullptr;
+  glsgpu_sur* h = create_common(G, M, n_i, omega, block_scale, device);
+  try {
+    h->X = X_dev;
+    h->ldx = ldx;
+    h->Y = Y_dev;
+    h->ldy = ldy;
+    alloc_common(h);
+    run_qr(h);
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  *out = h;
+  API_END(bad_block)
+}
+
+int glsgpu_sur_refactor(glsgpu_sur* h, int* bad_block) {
+  API_BEGIN
+  if (!h) fail(GLSGPU_ERR_INVALID, "null handle");
+  CK(cudaSetDevice(h->dev));
+  run_qr(h);
+  API_END(bad_block)
+}
+
+int glsgpu_sur_destroy(glsgpu_sur* h) {
+  API_BEGIN
+  destroy_impl(h);
+  API_END((int*)nullptr)
+}
+
+int glsgpu_sur_dims(const glsgpu_sur* h, int* G, int64_t* M, int64_t* n) {
+  if (!h) return GLSGPU_ERR_INVALID;
+  if (G) *G = h->G;
+  if (M) *M = h->M;
+  if (n) *n = h->n;
+  return GLSGPU_OK;
+}
+
+void* glsgpu_sur_stream(const glsgpu_sur* h) { return h ? (void*)h->s : nullptr; }
+
+int glsgpu_counters(const glsgpu_sur* h, glsgpu_counters_t* out) {
+  if (!h || !out) return GLSGPU_ERR_INVALID;
+  *out = h->counters;
+  return GLSGPU_OK;
+}
+
+int glsgpu_reset_apply_counters(glsgpu_sur* h) {
+  if (!h) return GLSGPU_ERR_INVALID;
+  h->counters.pi_applies = h->counters.xstar_t_applies = h->counters.xstar_applies = 0;
+  h->counters.apply_multiplies = 0;
+  return GLSGPU_OK;
+}
+
+int glsgpu_apply_pi(glsgpu_sur* h, const double* xi, double* out) {
+  API_BEGIN
+  if (!h || !xi || !out) fail(GLSGPU_ERR_INVALID, "apply_pi: null argument");
+  CK(cudaSetDevice(h->dev));
+  ensure_solver(h, 1);
+  h->counters.pi_applies++;
+  h->counters.apply_multiplies += h->pi_cost;
+  h2d_mvec(h, h->r, xi);
+  qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
+  Geo g = geo_of(h);
+  k_rowpass<<<rowpass_grid(h), NT, 0, h->s>>>(g, h->Q, h->t, h->r, h->pr, nullptr, 0, nullptr);
+  CKL("k_rowpass");
+  d2h_mvec(h, out, h->pr);
+  CK(cudaStreamSynchronize(h->s));
+  API_END((int*)nullptr)
+}
+
+int glsgpu_apply_xstar_t(glsgpu_sur* h, const double* xi, double* out) {
+  API_BEGIN
+  if (!h || !xi || !out) fail(GLSGPU_ERR_INVALID, "apply_xstar_t: null argument");
+  CK(cudaSetDevice(h->dev));
+  ensure_solver(h, 1);
+  h->counters.xstar_t_applies++;
+  h->counters.apply_multiplies += h->xstar_t_cost;
+  h2d_mvec(h, h->r, xi);
+  qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
+  Geo g = geo_of(h);
+  k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, nullptr, 1, 2, nullptr);
+  CKL("k_vupdate");
+  CK(cudaMemcpyAsync(out, h->t, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  API_END((int*)nullptr)
+}
+
+int glsgpu_apply_xstar(glsgpu_sur* h, const double* v, double* out) {
+  API_BEGIN
+  if (!h || !v || !out) fail(GLSGPU_ERR_INVALID, "apply_xstar: null argument");
+  CK(cudaSetDevice(h->dev));
+  ensure_solver(h, 1);
+  h->counters.xstar_applies++;
+  h->counters.apply_multiplies += h->xstar_cost;
+  CK(cudaMemcpyAsync(h->t, v, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
+  Geo g = geo_of(h);
+  k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, nullptr, 1, 3, nullptr);
+  CKL("k_vupdate");
+  k_rowpass<<<rowpass_grid(h), NT, 0, h->s>>>(g, h->Q, h->t, nullptr, h->pr, nullptr, 1, nullptr);
+  CKL("k_rowpass");
+  d2h_mvec(h, out, h->pr);
+  CK(cudaStreamSynchronize(h->s));
+  API_END((int*)nullptr)
+}
+
+int glsgpu_sigma_apply(glsgpu_sur* h, const double* x, double* out) {
+  API_BEGIN
+  if (!h || !x || !out) fail(GLSGPU_ERR_INVALID, "sigma_apply: null argument");
+  CK(cudaSetDevice(h->dev));
+  ensure_solver(h, 1);
+  h2d_mvec(h, h->r, x);
+  launch_kron(h, h->r, nullptr, nullptr, nullptr, h->su, h->partA, 0, nullptr, nullptr);
+  d2h_mvec(h, out, h->su);
+  CK(cudaStreamSynchronize(h->s));
+  API_END((int*)nullptr)
+}
+
+int glsgpu_operator_norm_probe(glsgpu_sur* h, int64_t iters, double* norm) {
+  API_BEGIN
+  if (!h || !norm) fail(GLSGPU_ERR_INVALID, "operator_norm_probe: null argument");
+  CK(cudaSetDevice(h->dev));
+  *norm = norm_probe(h, iters);
+  API_END((int*)nullptr)
+}
+
+int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R) {
+  API_BEGIN
+  if (!h) fail(GLSGPU_ERR_INVALID, "null handle");
+  CK(cudaSetDevice(h->dev));
+  if (Q)
+    CK(cudaMemcpy2D(Q, h->M * sizeof(double), h->Q, h->ldm * sizeof(double), h->M * sizeof(double), h->n,
+                    cudaMemcpyDeviceToHost));
+  if (R) {
+    int64_t rtot = 0;
+    for (int b = 0; b < h->G; ++b) rtot += (int64_t)h->nb[b] * h->nb[b];
+    CK(cudaMemcpy(R, h->R, sizeof(double) * rtot, cudaMemcpyDeviceToHost));
+  }
+  API_END((int*)nullptr)
+}
+
+int glsgpu_kernel_stats(const glsgpu_sur* h, glsgpu_kernel_stat* out, int cap) {
+  if (!h) return 0;
+  const int k = std::min<int>(cap, (int)h->kstats.size());
+  for (int i = 0; i < k; ++i) out[i] = h->kstats[i];
+  return k;
+}
+
+int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const double* w1, const double* z1,
+                     const double* beta_true, double* b_out, double* w_out, glsgpu_trace_row* rows,
+                     int64_t rows_cap, glsgpu_result* res) {
+  API_BEGIN
+  if (!h || !b_out || !res) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_solve: null argument");
+  CK(cudaSetDevice(h->dev));
+  glsgpu_pcg_config cfg;
+  if (cfg_in) cfg = *cfg_in;
+  else glsgpu_default_config(&cfg);
+  const int64_t m = h->M * h->G;
+  const int64_t max_iter = cfg.max_iter ? cfg.max_iter : (m - h->n + 1);
+  const int64_t cap_d = std::max<int64_t>(1, std::min<int64_t>(max_iter + 1, rows ? std::max<int64_t>(rows_cap, 1) : 1));
+  ensure_solver(h, cap_d);
+  const int xv_mode = cfg.xv_mode == GLSGPU_XV_QR ? GLSGPU_XV_QR : GLSGPU_XV_X;
+  const int diag = cfg.diag_every;
+  Geo g = geo_of(h);
+  cudaStream_t s = h->s;
+
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+
+  const double sigma_scale = norm_probe(h, 12);  // pcg.cpp:49
+
+  SolveState hs;
+  std::memset(&hs, 0, sizeof(hs));
+  hs.tol_rel = cfg.tol_rel;
+  hs.breakdown_tol = cfg.breakdown_tol;
+  hs.growth_tol = cfg.growth_tol;
+  hs.sigma_scale = sigma_scale;
+  hs.i = 1;
+  hs.max_iter = max_iter;
+  hs.stride = cfg.record_z_every ? cfg.record_z_every : 1;
+  hs.stagnation_window = cfg.stagnation_window;
+  hs.growth_window = cfg.growth_window;
+  hs.diag_every = diag;
+  hs.rows_cap = cap_d;
+  hs.breakdown_iter = -1;
+  hs.active = 1;
+  hs.term = T_MAXITER;
+  hs.cur = 0;
+  hs.best = 0;
+  hs.nxt = 1;
+  hs.mu_pending = 0;
+  hs.have_beta = beta_true ? 1 : 0;
+  CK(cudaMemcpyAsync(h->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+  k_set_t0<<<1, 1, 0, s>>>(h->st);
+
+  const size_t mvb = sizeof(double) * (size_t)(h->ldm * h->G);
+  // w1 (pcg.cpp:55-66): enforce X'w1 = 0 by projecting along X*
+  int w1_projected = 0;
+  CK(cudaMemsetAsync(h->wb[0], 0, mvb, s));
+  CK(cudaMemsetAsync(h->swb[0], 0, mvb, s));
+  if (w1) {
+    h2d_mvec(h, h->wb[0], w1);
+    ColArgs a = base_args(h);
+    a.A = h->X;
+    a.lda = h->ldx;
+    a.avalid = h->M;
+    a.vec = h->zvec;  // est = 0: only the X'w column part is used here
+    CK(cudaMemsetAsync(h->zvec, 0, sizeof(double) * h->n, s));
+    launch_colpass<MODE_DIAG>(h, a, h->st);
+    launch_reduce_t(h, h->xtw, nullptr, 0);
+    std::vector<double> xtw((size_t)h->n), wv((size_t)m);
+    CK(cudaMemcpyAsync(xtw.data(), h->xtw, sizeof(double) * h->n, cudaMemcpyDeviceToHost, s));
+    if (h->frob_x < 0) {
+      k_sumsq_cols<<<GRID_CAP, NT, 0, s>>>(h->X, h->ldx, h->M, h->n, h->partA);
+      k_sum1<<<1, NT, 0, s>>>(h->partA, GRID_CAP, h->scal + 8);
+      double ss = 0;
+      CK(cudaMemcpyAsync(&ss, h->scal + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      h->frob_x = std::sqrt(ss);
+    }
+    CK(cudaStreamSynchronize(s));
+    double feas = 0.0, wn = 0.0;
+    for (double v : xtw) feas += v * v;
+    feas = std::sqrt(feas);
+    for (int64_t i = 0; i < m; ++i) wn += w1[i] * w1[i];
+    wn = std::sqrt(wn);
+    const double scale = h->frob_x * wn;
+    if (feas > 1e-14 * scale && feas > 0.0) {
+      // corr = X* xtw = Q R^-T xtw per block (xstar_impl); w -= corr
+      CK(cudaMemcpyAsync(h->t, h->xtw, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, s));
+      k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t, nullptr, 1, 3, nullptr);
+      k_rowpass<<<rowpass_grid(h), NT, 0, s>>>(g, h->Q, h->t, nullptr, h->pr, nullptr, 1, nullptr);
+      k_axpy_sub<<<GRID_CAP, NT, 0, s>>>(h->wb[0], h->pr, h->ldm * h->G);
+      CKL("w1 projection");
+      w1_projected = 1;
+    }
+  }
+  if (z1) CK(cudaMemcpyAsync(h->zvec, z1, sizeof(double) * h->n, cudaMemcpyHostToDevice, s));
+  else CK(cudaMemsetAsync(h->zvec, 0, sizeof(double) * h->n, s));
+  if (beta_true) CK(cudaMemcpyAsync(h->beta_d, beta_true, sizeof(double) * h->n, cudaMemcpyHostToDevice, s));
+
+  // sw = Sigma w; r = (sw + X z) - y; pr = Pi r; c
+  launch_kron(h, h->wb[0], nullptr, nullptr, nullptr, h->swb[0], h->partA, 0, nullptr, nullptr);
+  {
+    dim3 grid((unsigned)std::min<int64_t>((h->ldm + NT - 1) / NT, 64), (unsigned)h->G);
+    k_init_residual<<<grid, NT, 0, s>>>(g, h->X, h->ldx, h->zvec, h->swb[0], h->Y, h->ldy, h->r);
+    CKL("k_init_residual");
+  }
+  qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
+  const int gC = rowpass_grid(h);
+  k_rowpass<<<gC, NT, 0, s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, nullptr);
+  CKL("k_rowpass init");
+  k_init_scalars<<<1, NT, 0, s>>>(h->partC, gC, h->st, h->rows_d);
+  CKL("k_init_scalars");
+  // v = X*' r (X mode: R^-1 t; QR mode: s = t); u = pr
+  k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t, h->vs, xv_mode == GLSGPU_XV_X ? 1 : 0, 1, nullptr);
+  CKL("k_vupdate init");
+  CK(cudaMemcpyAsync(h->u, h->pr, mvb, cudaMemcpyDeviceToDevice, s));
+  // row 0 diagnostics: est0 = recover(sw) (pcg.cpp:118-122)
+  if (diag >= 0) {
+    ColArgs d = base_args(h);
+    launch_colpass<MODE_QT_D>(h, d, h->st);
+    launch_reduce_t(h, h->t2, nullptr, 0);
+    k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
+    ColArgs x = base_args(h);
+    x.A = h->X;
+    x.lda = h->ldx;
+    x.avalid = h->M;
+    x.vec = h->t2;
+    launch_colpass<MODE_DIAG>(h, x, h->st);
+    launch_reduce_t(h, h->xtw, nullptr, 0);
+    k_diag_finalize<<<1, NT, 0, s>>>(h->rpart, h->G * h->nch, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d, 0);
+    CKL("row 0 diagnostics");
+  }
+
+  // ---- the iteration loop: CUDA graphs of `chunk` iterations, device-side control
+  int chunk = cfg.graph_chunk;
+  if (chunk <= 0) {
+    const double bytes_iter = 8.0 * (2.0 * (double)h->M * h->n + 14.0 * (double)h->M * h->G);
+    const double t_iter_us = bytes_iter / 6.0e6 + 40.0;
+    chunk = (int)std::clamp(2000.0 / t_iter_us, 2.0, 32.0);
+  }
+  const int timing = cfg.kernel_timing ? 1 : 0;
+  const bool need_graph = !h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
+                          h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing;
+  if (need_graph) {
+    if (h->graph) {
+      CK(cudaGraphExecDestroy(h->graph));
+      h->graph = nullptr;
+    }
+    for (auto e : h->tev) cudaEventDestroy(e);
+    h->tev.clear();
+    if (timing) {
+      h->tev.resize((size_t)chunk * 6);
+      for (auto& e : h->tev) CK(cudaEventCreate(&e));
+    }
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < chunk; ++k) capture_iteration(h, xv_mode, diag >= 0 ? 1 : -1, timing, k);
+    CK(cudaStreamEndCapture(s, &graph));
+    CK(cudaGraphInstantiate(&h->graph, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    h->graph_chunk = chunk;
+    h->graph_xmode = xv_mode;
+    h->graph_diag = diag >= 0 ? 1 : -1;
+    h->graph_timing = timing;
+  }
+  std::vector<double> kt_ms(3, 0.0);
+  std::vector<int64_t> kt_n(3, 0);
+  int64_t prev_i = 1;
+  for (;;) {
+    CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!h->st_host->active) break;
+    prev_i = h->st_host->i;
+    CK(cudaGraphLaunch(h->graph, s));
+    if (timing) {
+      CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      // iterations that executed pass A: prev_i .. last (a pass-A breakdown adds done + 1)
+      const SolveState& q = *h->st_host;
+      const int64_t last = q.active ? q.i - 1 : (q.breakdown_iter == q.done + 1 ? q.done + 1 : q.done);
+      const int64_t ran_a = std::max<int64_t>(0, last - prev_i + 1);
+      const int64_t ran_bc = std::max<int64_t>(0, h->st_host->done - prev_i + 1);
+      for (int64_t k = 0; k < std::min<int64_t>(ran_a, chunk); ++k) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, h->tev[k * 6 + 0], h->tev[k * 6 + 1]));
+        kt_ms[0] += ms;
+        kt_n[0]++;
+      }
+      for (int64_t k = 0; k < std::min<int64_t>(ran_bc, chunk); ++k) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, h->tev[k * 6 + 2], h->tev[k * 6 + 3]));
+        kt_ms[1] += ms;
+        CK(cudaEventElapsedTime(&ms, h->tev[k * 6 + 4], h->tev[k * 6 + 5]));
+        kt_ms[2] += ms;
+        kt_n[1]++;
+        kt_n[2]++;
+      }
+    }
+  }
+  SolveState fin = *h->st_host;
+
+  // exit: b = X*'(y - sw_sel), sel = last if Converged else best (pcg.cpp:215-228)
+  {
+    ColArgs d = base_args(h);
+    d.sel_best = 1;
+    launch_colpass<MODE_QT_D>(h, d, h->st);
+    launch_reduce_t(h, h->t2, nullptr, 0);
+    k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
+    CKL("recover");
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaMemcpyAsync(b_out, h->t2, sizeof(double) * h->n, cudaMemcpyDeviceToHost, s));
+  const int wsel = fin.term == T_CONVERGED ? fin.cur : fin.best;
+  if (w_out) d2h_mvec(h, w_out, h->wb[wsel]);
+  const int64_t nrows = fin.done + 1;
+  std::vector<TraceRowD> rd;
+  if (rows && rows_cap > 0) {
+    const int64_t k = std::min<int64_t>(std::min<int64_t>(nrows, rows_cap), cap_d);
+    rd.resize((size_t)k);
+    CK(cudaMemcpyAsync(rd.data(), h->rows_d, sizeof(TraceRowD) * k, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < rd.size(); ++i) {
+    rows[i].iter = rd[i].iter;
+    rows[i].c = rd[i].c;
+    rows[i].aug_residual_norm = rd[i].aug;
+    rows[i].dual_feas_norm = rd[i].dual;
+    rows[i].rmse = rd[i].rmse;
+    rows[i].elapsed_ns = rd[i].elapsed_ns;
+  }
+  float solve_ms = 0;
+  CK(cudaEventElapsedTime(&solve_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+
+  res->iterations = fin.done;
+  res->termination = fin.term;
+  res->w1_projected = w1_projected;
+  res->breakdown_iteration = fin.term == T_BREAKDOWN ? fin.breakdown_iter : -1;
+  res->residual_seminorm = fin.term == T_CONVERGED ? fin.c : fin.c_best;
+  res->n_rows = nrows;
+  res->sigma_scale = sigma_scale;
+  res->solve_ms = solve_ms;
+
+  // logical operator applies of run_aug (counters as the reference tallies them)
+  {
+    const uint64_t done = (uint64_t)fin.done;
+    const bool c1zero = fin.c1 == 0.0;
+    uint64_t pi = 1 + done;
+    uint64_t xt = 1 /* v */ + 1 /* est0 */ + done /* est_i */ + 1 /* final recover */;
+    // v updates happen after every iteration that passed all termination tests
+    uint64_t cont = done;
+    if (fin.term == T_CONVERGED || fin.term == T_STAGNATION ||
+        (fin.term == T_BREAKDOWN && fin.breakdown_iter == fin.done))
+      cont = done > 0 ? done - 1 : 0;
+    if (c1zero) cont = 0;
+    xt += cont;
+    h->counters.pi_applies += pi;
+    h->counters.xstar_t_applies += xt;
+    h->counters.xstar_applies += (uint64_t)w1_projected;
+    h->counters.apply_multiplies += pi * h->pi_cost + xt * h->xstar_t_cost + (uint64_t)w1_projected * h->xstar_cost;
+  }
+  h->kstats.clear();
+  if (timing) {
+    const double M = (double)h->M, G = (double)h->G, n = (double)h->n;
+    const double bA = 8.0 * 4.0 * M * G;
+    const double bB = 8.0 * (M * n * (xv_mode == GLSGPU_XV_X ? 2.0 : 1.0) + 8.0 * M * G);
+    const double bC = 8.0 * (M * n + 2.0 * M * G);
+    const char* names[3] = {"passA_kron", "passB_update_qtr", "passC_pi"};
+    const double bytes[3] = {bA, bB, bC};
+    for (int k = 0; k < 3; ++k) {
+      glsgpu_kernel_stat ks;
+      std::memset(&ks, 0, sizeof(ks));
+      std::snprintf(ks.name, sizeof(ks.name), "%s", names[k]);
+      ks.launches = kt_n[k];
+      ks.total_ms = kt_ms[k];
+      ks.bytes_per_launch = bytes[k];
+      h->kstats.push_back(ks);
+    }
+  }
+  (void)prev_i;
+  API_END((int*)nullptr)
+}
+
+int glsgpu_synth_normal(double* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t stream,
+                        int device) {
+  API_BEGIN
+  CK(cudaSetDevice(device));
+  k_synth_normal<<<148 * 8, 256>>>(dev, rows, cols, ld, seed, stream);
+  CKL("k_synth_normal");
+  CK(cudaDeviceSynchronize());
+  API_END((int*)nullptr)
+}
+
+int glsgpu_synth_response(int G, int64_t M, const int64_t* n_i, const double* X_dev, int64_t ldx, const double* beta,
+                          const double* omega_half, uint64_t seed, double* Y_dev, int64_t ldy, int device) {
+  API_BEGIN
+  // Y = X beta + Z Omega^1/2 with Z ~ N(0,1) from stream 3 (synth.py's recipe)
+  glsgpu_sur* h = create_common(G, M, n_i, omega_half, nullptr, device);
+  try {
+    ensure_solver(h, 1);
+    k_synth_normal<<<148 * 8, 256, 0, h->s>>>(h->r, M, G, h->ldm, seed, 3);
+    CKL("k_synth_normal");
+    launch_kron(h, h->r, nullptr, nullptr, nullptr, h->su, h->partA, 0, nullptr, nullptr);
+    CK(cudaMemcpy2DAsync(Y_dev, ldy * sizeof(double), h->su, h->ldm * sizeof(double), M * sizeof(double), G,
+                         cudaMemcpyDeviceToDevice, h->s));
+    double* bd = dalloc<double>(h->n);
+    CK(cudaMemcpyAsync(bd, beta, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
+    dim3 grid((unsigned)std::min<int64_t>((M + 255) / 256, 256), (unsigned)G);
+    k_add_xbeta<<<grid, 256, 0, h->s>>>(G, M, h->d_nb, h->d_p0, X_dev, ldx, bd, Y_dev, ldy);
+    CKL("k_add_xbeta");
+    CK(cudaStreamSynchronize(h->s));
+    cudaFree(bd);
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  destroy_impl(h);
+  API_END((int*)nullptr)
+}
+
+}  // extern "C"

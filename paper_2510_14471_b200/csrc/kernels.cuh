@@ -1,0 +1,964 @@
+// kernels.cuh -- sm_100a device code of the B200-native SUR PCG-Aug solver.
+//
+// Compiled with -fmad=false: every a*b+c below is a separately rounded multiply and add, so the
+// element-wise updates, the Kronecker apply (proj/src/operators.cpp:45-50 via dense_matrix.cpp:125-139),
+// the row sums of X v / Q t (dense_matrix.cpp:69-79) and the triangular solves (linalg.cpp:119-145)
+// round exactly as the reference's default x86-64 build does.  The long reductions over rows (dot
+// products and Q'r) are fixed-shape trees: deterministic run to run, not the reference's sequential
+// order (SURVEY.md s0.7 "parity envelope").
+//
+// Data layout in HBM: every M x G state vector and the concatenated Q / X are
+// column-major with a padded leading dimension ldm = round_up(M, 32); padding rows are zero.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace glsgpu {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NT = 256;             // threads per CTA for the streaming passes
+constexpr int GRID_CAP = 148 * 4;   // fixed (device-independent) grid of the grid-stride passes
+
+// ------------------------------------------------------------------------------------------
+// Geometry of one rank's row shard (device-visible, passed by value).
+struct Geo {
+  int G;
+  int nch;          // row chunks per block for the column (Q'x) passes
+  int64_t M;        // rows owned by this rank
+  int64_t ldm;      // padded leading dimension of internal arrays
+  int64_t n;        // total parameters
+  int64_t CH;       // rows per chunk
+  const int* nb;    // [G] widths
+  const int64_t* p0;  // [G] first parameter of block b
+  const int64_t* r0;  // [G] offset of R_b
+  const double* wts;  // [G] w_b = 1/sqrt(block_scale_b)
+};
+
+// Solver state kept on the device; the scalar control of run_aug (proj/src/pcg.cpp:134-211)
+// executes in k_scalar_a / k_scalar_c so no host round trip happens inside an iteration.
+struct SolveState {
+  double c, c1, threshold, c_best, pi_gain, lambda, mu, sigma_scale;
+  double tol_rel, breakdown_tol, growth_tol;
+  double d, uu, c_next, rr, prpr;
+  int64_t i, max_iter, best_iter, stagnant, done, breakdown_iter, stride;
+  int64_t stagnation_window, growth_window, diag_every;
+  int64_t rows_cap;        // device trace capacity
+  unsigned long long t0;   // %globaltimer at solve start
+  int32_t active, term, cur, best, nxt, mu_pending, cont, diag_now, sampled, have_beta;
+  int32_t pad[2];
+};
+
+struct TraceRowD {
+  int64_t iter;
+  double c, aug, dual, rmse;
+  int64_t elapsed_ns;
+};
+
+enum { T_CONVERGED = 0, T_BREAKDOWN = 1, T_STAGNATION = 2, T_MAXITER = 3 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double dmax_std(double a, double b) { return (a < b) ? b : a; }  // std::max
+
+// Deterministic block reduction of K values (fixed shuffle tree, then warps in order).
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* red /* [NT/32][K] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) v[k] += __shfl_xor_sync(FULL, v[k], s);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) red[warp * K + k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double a = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w * K + k];
+      v[k] = a;
+    }
+  }
+}
+
+// Transpose-reduce NB per-lane accumulators across a warp: afterwards lane l holds the warp total
+// of accumulator (l % NB).  Fixed butterfly: deterministic.
+template <int NB>
+__device__ __forceinline__ void warp_transpose_reduce(double (&acc)[NB]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= NB; s >>= 1)
+#pragma unroll
+    for (int i = 0; i < NB; ++i) acc[i] += __shfl_xor_sync(FULL, acc[i], s);
+#pragma unroll
+  for (int s = NB / 2; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = upper ? acc[i] : acc[i + s];
+      const double keep = upper ? acc[i + s] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(FULL, send, s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Kronecker apply out = reshape(x, M, G) * Omega, i.e. (Omega (x) I_M) x   (operators.cpp:45-50).
+// Tile: TR = 8 warps x RW rows, all G columns; lane owns columns c = lane + 32 q.  The p loop runs
+// in ascending order from 0.0 with separate mul/add: bitwise the reference's operator* sum.
+// Modes: in_mode 0: x = src; 1: x = src / (*div) (operator_norm_probe's v[i] /= nrm);
+//        2: pass A: u_new = pr + mu*u when st->mu_pending (pcg.cpp:210) else u; writes u.
+// Partials per CTA: [0] = sum x*out, [1] = sum x*x, [2] = sum out*out.
+template <int CPL, int RW>
+__global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles, const double* __restrict__ omegaT,
+                                             const double* src, const double* pr, const double* div, double* u_io,
+                                             double* out, double* partials, int in_mode, const SolveState* st) {
+  if (st && !st->active) return;
+  extern __shared__ double xs[];  // [G][TR]
+  constexpr int TR = 8 * RW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double mu = 0.0;
+  bool upd = false;
+  if (in_mode == 2) { upd = st->mu_pending != 0; mu = st->mu; }
+  const double dv = (in_mode == 1) ? *div : 1.0;
+  double p_xo = 0.0, p_xx = 0.0, p_oo = 0.0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t k0 = tile * TR;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < G * TR; idx += NT) {
+      const int p = idx / TR, r = idx - p * TR;
+      const int64_t off = (int64_t)p * ldm + k0 + r;
+      double x;
+      if (in_mode == 2) {
+        const double uo = u_io[off];
+        if (upd) { x = pr[off] + mu * uo; u_io[off] = x; }
+        else x = uo;
+      } else if (in_mode == 1) {
+        x = src[off] / dv;
+      } else {
+        x = src[off];
+      }
+      xs[p * TR + r] = x;
+    }
+    __syncthreads();
+    double acc[RW][CPL];
+#pragma unroll
+    for (int i = 0; i < RW; ++i)
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) acc[i][q] = 0.0;
+    const int rbase = warp * RW;
+    for (int p = 0; p < G; ++p) {
+      double o[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int c = lane + 32 * q;
+        o[q] = (c < G) ? __ldg(omegaT + (int64_t)p * G + c) : 0.0;
+      }
+      double xr[RW];
+#pragma unroll
+      for (int i = 0; i < RW; ++i) xr[i] = xs[p * TR + rbase + i];
+#pragma unroll
+      for (int i = 0; i < RW; ++i)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) acc[i][q] = acc[i][q] + xr[i] * o[q];
+    }
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = lane + 32 * q;
+      if (c < G) {
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+          out[(int64_t)c * ldm + k0 + rbase + i] = acc[i][q];
+          const double x = xs[c * TR + rbase + i];
+          p_xo += x * acc[i][q];
+          p_xx += x * x;
+          p_oo += acc[i][q] * acc[i][q];
+        }
+      }
+    }
+  }
+  __shared__ double red[NT / 32 * 3];
+  double v[3] = {p_xo, p_xx, p_oo};
+  block_sum<3>(v, red);
+  if (threadIdx.x == 0 && partials) {
+    partials[blockIdx.x * 3 + 0] = v[0];
+    partials[blockIdx.x * 3 + 1] = v[1];
+    partials[blockIdx.x * 3 + 2] = v[2];
+  }
+}
+
+// Sum K-wide partials of `count` CTAs in fixed order (one CTA); result to out[0..K).
+template <int K>
+__device__ __forceinline__ void reduce_partials(const double* partials, int count, double* out) {
+  double v[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] += partials[i * K + k];
+  __shared__ double red[32 * K];
+  block_sum<K>(v, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = v[k];
+}
+
+__global__ void k_reduce3(const double* partials, int count, double* out) { reduce_partials<3>(partials, count, out); }
+
+// operator_norm_probe step (pcg.cpp:237-242): nrm = norm2(v); if 0 -> result 0 and stop.
+__global__ void k_probe_step(const double* partials, int count, double* nrm, int* stop) {
+  __shared__ double res[3];
+  reduce_partials<3>(partials, count, res);
+  if (threadIdx.x == 0) {
+    if (*stop) return;
+    const double s = sqrt(res[2]);
+    *nrm = s;
+    if (s == 0.0) *stop = 1;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Pass A scalar step (pcg.cpp:144-150): d = u.su, breakdown test, lambda = c/d.
+__global__ void k_scalar_a(const double* partials, int count, SolveState* st) {
+  if (!st->active) return;
+  __shared__ double res[3];
+  reduce_partials<3>(partials, count, res);
+  if (threadIdx.x == 0) {
+    const double d = res[0], uu = res[1];
+    st->d = d;
+    st->uu = uu;
+    if (fabs(d) <= st->breakdown_tol * uu * st->sigma_scale) {
+      st->term = T_BREAKDOWN;
+      st->breakdown_iter = st->i;
+      st->active = 0;
+      st->cont = 0;
+      st->diag_now = 0;
+      return;
+    }
+    st->lambda = st->c / d;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Column passes over (block, chunk) items: acc_j += A[k, j] * x_k for the rows of the chunk, then a
+// deterministic transpose-reduce into tpart[(p0_b + j) * nch + ch].
+//
+// MODE_B   : pass B of an iteration (pcg.cpp:151-155): w -= lambda u, sw -= lambda su (into the
+//            rotation buffer nxt), xv = X v (xv_mode X) or Q s / w_b (xv_mode QR), r -= lambda(su + xv),
+//            x = w_b * r  (gather of the following apply_pi / apply_xstar_t, structured.cpp:347-351).
+// MODE_QT_R: x = w_b * r                    (apply_pi / apply_xstar_t of r)
+// MODE_QT_D: x = w_b * (y - sw[sel])        (recover, pcg.cpp:96-98)
+// MODE_QT_V: x = w_b * v                    (probe apply_xstar_t of a host vector)
+// MODE_DIAG: A = X, x = w[cur] (X'w for dual_feas_norm, pcg.cpp:112); row part: resid = y - (sw + X est),
+//            sum resid^2 -> rpart[b * nch + ch] (aug_residual_norm, pcg.cpp:108-111).
+enum { MODE_B = 0, MODE_QT_R = 1, MODE_QT_D = 2, MODE_QT_V = 3, MODE_DIAG = 4 };
+
+struct ColArgs {
+  const double* A;      // matrix whose transpose is applied (Q, or X for MODE_DIAG)
+  int64_t lda;
+  const double* X;      // X for the X v row sums (xv_mode X) / diag
+  int64_t ldx;
+  const double* u;
+  const double* su;
+  double* wb[3];
+  double* swb[3];
+  double* r;
+  const double* y;
+  int64_t ldy;
+  const double* vec;    // v (xv_mode X) / s (QR) for MODE_B; est for MODE_DIAG; input vector for QT_V
+  const double* vin;    // MODE_QT_V input (m-vector, ld ldm)
+  double* tpart;
+  double* rpart;        // MODE_DIAG residual partials [G * nch]
+  const int* blocks;    // block list of this launch
+  int64_t avalid;       // rows of A that are valid (A = user X: M; internal Q: ldm)
+  int xv_from_x;        // 1: xv = X v; 0: xv = Q s / w_b
+  int sel_best;         // MODE_QT_D: use the selected final buffer (cur or best)
+  int gate;             // 0: always run; 1: only while st->active; 2: only when st->diag_now
+};
+
+template <int MODE, bool FUSED>
+__global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveState* st) {
+  if (a.gate == 1 && !st->active) return;
+  if (a.gate == 2 && !st->diag_now) return;
+  constexpr int NB = 32;
+  extern __shared__ double xsm[];  // !FUSED: [CH] x values of the chunk
+  __shared__ double red[NT / 32][NB];
+  __shared__ double rred[NT / 32];
+  __shared__ double svec_s[512];
+  const int item = blockIdx.x;
+  const int b = a.blocks[item / g.nch];
+  const int ch = item % g.nch;
+  const int nb = g.nb[b];
+  const int64_t p0 = g.p0[b];
+  const double wgt = g.wts[b];
+  const int64_t k0 = (int64_t)ch * g.CH;
+  const int64_t k1 = (k0 + g.CH < g.ldm) ? k0 + g.CH : g.ldm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  double lam = 0.0;
+  int cur = 0, nxt = 0, selb = 0;
+  if (MODE == MODE_B) { lam = st->lambda; cur = st->cur; nxt = st->nxt; }
+  if (MODE == MODE_DIAG) cur = st->cur;
+  if (MODE == MODE_QT_D) {
+    if (a.sel_best) selb = (st->term == T_CONVERGED) ? st->cur : st->best;
+    else selb = st->cur;
+  }
+  if (MODE == MODE_B || MODE == MODE_DIAG) {
+    for (int j = threadIdx.x; j < nb; j += NT) svec_s[j] = a.vec[p0 + j];
+    __syncthreads();
+  }
+  const double* Ab = a.A + p0 * a.lda;
+  const double* Xb = a.X ? a.X + p0 * a.ldx : nullptr;
+  const int64_t vo = (int64_t)b * g.ldm;
+
+  double acc[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) acc[j] = 0.0;
+  double rsum = 0.0;
+
+  // Row phase: compute x_k (and the side effects of the mode).
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += NT) {
+    const int64_t off = vo + k;
+    double x;
+    double qv[NB];
+    if (FUSED) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) qv[j] = (j < nb && k < a.avalid) ? Ab[(int64_t)j * a.lda + k] : 0.0;
+    }
+    if (MODE == MODE_B) {
+      const double uv = a.u[off], suv = a.su[off];
+      const double wv = a.wb[cur][off], swv = a.swb[cur][off], rv = a.r[off];
+      a.wb[nxt][off] = wv + (-lam) * uv;
+      a.swb[nxt][off] = swv + (-lam) * suv;
+      double xv = 0.0;
+      if (a.xv_from_x) {
+        if (k < g.M)
+          for (int j = 0; j < nb; ++j) xv = xv + Xb[(int64_t)j * a.ldx + k] * svec_s[j];
+      } else {
+        if (FUSED) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            if (j < nb) xv = xv + qv[j] * svec_s[j];
+        } else {
+          for (int j = 0; j < nb; ++j) xv = xv + Ab[(int64_t)j * a.lda + k] * svec_s[j];
+        }
+        xv = xv / wgt;
+      }
+      const double rn = rv - lam * (suv + xv);
+      a.r[off] = rn;
+      x = rn * wgt;
+    } else if (MODE == MODE_QT_R) {
+      x = a.r[off] * wgt;
+    } else if (MODE == MODE_QT_D) {
+      const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+      x = (yv - a.swb[selb][off]) * wgt;
+    } else if (MODE == MODE_QT_V) {
+      x = a.vin[off] * wgt;
+    } else {  // MODE_DIAG
+      double xe = 0.0;
+      if (FUSED) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j < nb) xe = xe + qv[j] * svec_s[j];
+      } else {
+        if (k < a.avalid)
+          for (int j = 0; j < nb; ++j) xe = xe + Ab[(int64_t)j * a.lda + k] * svec_s[j];
+      }
+      const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+      const double res = yv - (a.swb[cur][off] + xe);
+      if (k < g.M) rsum += res * res;
+      x = a.wb[cur][off];
+    }
+    if (FUSED) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] += qv[j] * x;
+    } else {
+      xsm[k - k0] = x;
+    }
+  }
+
+  if (MODE == MODE_DIAG) {
+    double v1[1] = {rsum};
+    block_sum<1>(v1, rred);
+    if (threadIdx.x == 0) a.rpart[(int64_t)b * g.nch + ch] = v1[0];
+  }
+
+  auto flush = [&](int j0) {
+    warp_transpose_reduce<NB>(acc);
+    __syncthreads();
+    red[warp][lane] = acc[0];
+    __syncthreads();
+    if (threadIdx.x < NB && j0 + (int)threadIdx.x < nb) {
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += red[w][threadIdx.x];
+      a.tpart[(p0 + j0 + threadIdx.x) * g.nch + ch] = s;
+    }
+  };
+
+  if (FUSED) {
+    flush(0);
+  } else {
+    __syncthreads();
+    for (int j0 = 0; j0 < nb; j0 += NB) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = 0.0;
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += NT) {
+        const double x = xsm[k - k0];
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j0 + j < nb && k < a.avalid) acc[j] += Ab[(int64_t)(j0 + j) * a.lda + k] * x;
+      }
+      flush(j0);
+    }
+  }
+}
+
+// Sum the chunk partials of every parameter (one warp per parameter, fixed order) -> out[n].
+__global__ void k_reduce_t(const double* tpart, int64_t n, int nch, double* out, const SolveState* st,
+                           int gate) {
+  if (gate == 1 && !st->active) return;
+  if (gate == 2 && !st->diag_now) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= n) return;
+  double s = 0.0;
+  for (int c = lane; c < nch; c += 32) s += tpart[j * nch + c];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+  if (lane == 0) out[j] = s;
+}
+
+// Upper-triangular back substitution R x = b per block (linalg.cpp:130-136) or R' x = b
+// (linalg.cpp:137-145), one thread per block, the reference's loop order.
+__device__ __forceinline__ void tri_solve_dev(int n, const double* R, double* x, bool transpose) {
+  if (!transpose) {
+    for (int i = n - 1; i >= 0; --i) {
+      double s = x[i];
+      for (int j = i + 1; j < n; ++j) s -= R[i + (int64_t)j * n] * x[j];
+      x[i] = s / R[i + (int64_t)i * n];
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      double s = x[i];
+      for (int j = 0; j < i; ++j) s -= R[j + (int64_t)i * n] * x[j];
+      x[i] = s / R[i + (int64_t)i * n];
+    }
+  }
+}
+
+// v update (pcg.cpp:208-209): v = R^-1 t + mu v (xv_mode X) or s = t + mu s (QR).
+// mode 0: continue-gated iteration update; mode 1: init v = R^-1 t (X) / s = t (QR);
+// mode 2: plain out = R^-1 t (recover / est / probes); mode 3: out = R'^-1 t (apply_xstar).
+__global__ void k_vupdate(Geo g, const double* R, double* t, double* vs, int xv_from_x, int mode,
+                          const SolveState* st) {
+  if (mode == 0 && (!st->active || !st->cont)) return;
+  if (mode == 2 && st && !st->diag_now) return;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.G) return;
+  const int nb = g.nb[b];
+  const int64_t p0 = g.p0[b];
+  double* tb = t + p0;
+  if (mode == 3) { tri_solve_dev(nb, R + g.r0[b], tb, true); return; }
+  if (mode == 2 || xv_from_x) tri_solve_dev(nb, R + g.r0[b], tb, false);
+  if (mode == 2) return;
+  if (mode == 1) {
+    for (int j = 0; j < nb; ++j) vs[p0 + j] = tb[j];
+  } else {
+    const double mu = st->mu;
+    for (int j = 0; j < nb; ++j) vs[p0 + j] = tb[j] + mu * vs[p0 + j];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Row pass: out_k = w_b (w_b in_k - sum_j Q[k,j] t_j)   (pi_impl, structured.cpp:307-317), or
+// out_k = w_b (sum_j Q[k,j] t_j)                         (xstar_impl, structured.cpp:330-340).
+// Partials per CTA (pi mode): [0] = r.pr, [1] = r.r, [2] = pr.pr   (pcg.cpp:157,165).
+__global__ void __launch_bounds__(NT) k_rowpass(Geo g, const double* Q, const double* t, const double* in,
+                                                double* out, double* partials, int xstar_mode,
+                                                const SolveState* st) {
+  if (st && !st->active) return;
+  __shared__ double ts[512];
+  __shared__ double red[NT / 32 * 3];
+  const int64_t items = (int64_t)g.G * g.nch;
+  double pc = 0.0, prr = 0.0, ppp = 0.0;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = (int)(item / g.nch);
+    const int ch = (int)(item % g.nch);
+    const int nb = g.nb[b];
+    const int64_t p0 = g.p0[b];
+    const double wgt = g.wts[b];
+    __syncthreads();
+    for (int j = threadIdx.x; j < nb; j += NT) ts[j] = t[p0 + j];
+    __syncthreads();
+    const double* Qb = Q + p0 * g.ldm;
+    const int64_t k0 = (int64_t)ch * g.CH;
+    const int64_t k1 = (k0 + g.CH < g.ldm) ? k0 + g.CH : g.ldm;
+    const int64_t vo = (int64_t)b * g.ldm;
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += NT) {
+      double proj = 0.0;
+      int j = 0;
+      for (; j + 4 <= nb; j += 4) {
+        const double q0 = Qb[(int64_t)(j + 0) * g.ldm + k];
+        const double q1 = Qb[(int64_t)(j + 1) * g.ldm + k];
+        const double q2 = Qb[(int64_t)(j + 2) * g.ldm + k];
+        const double q3 = Qb[(int64_t)(j + 3) * g.ldm + k];
+        proj = proj + q0 * ts[j + 0];
+        proj = proj + q1 * ts[j + 1];
+        proj = proj + q2 * ts[j + 2];
+        proj = proj + q3 * ts[j + 3];
+      }
+      for (; j < nb; ++j) proj = proj + Qb[(int64_t)j * g.ldm + k] * ts[j];
+      if (xstar_mode) {
+        out[vo + k] = proj * wgt;
+      } else {
+        const double rv = in[vo + k];
+        const double loc = rv * wgt;
+        const double pv = (loc - proj) * wgt;
+        out[vo + k] = pv;
+        pc += rv * pv;
+        prr += rv * rv;
+        ppp += pv * pv;
+      }
+    }
+  }
+  double v[3] = {pc, prr, ppp};
+  block_sum<3>(v, red);
+  if (threadIdx.x == 0 && partials) {
+    partials[blockIdx.x * 3 + 0] = v[0];
+    partials[blockIdx.x * 3 + 1] = v[1];
+    partials[blockIdx.x * 3 + 2] = v[2];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Pass C scalar step: c_next, the trace row, the roundoff floor, every termination test and the
+// best-iterate bookkeeping of run_aug (pcg.cpp:157-204), in the reference's order.
+__global__ void k_scalar_c(const double* partials, int count, SolveState* st, TraceRowD* rows) {
+  if (!st->active) return;
+  __shared__ double res[3];
+  reduce_partials<3>(partials, count, res);
+  if (threadIdx.x != 0) return;
+  const double kEps = 2.220446049250313e-16;
+  const int64_t i = st->i;
+  double c_next = res[0];
+  const double rr = res[1], prpr = res[2];
+  st->c_next = c_next;
+  st->rr = rr;
+  st->prpr = prpr;
+  st->done = i;
+  st->cur = st->nxt;  // the w / sw written by pass B
+  st->sampled = (i % st->stride == 0) || c_next <= st->threshold || i == st->max_iter;
+  if (i < st->rows_cap) {
+    TraceRowD& row = rows[i];
+    row.iter = i;
+    row.c = c_next;
+    row.aug = __longlong_as_double(0x7ff8000000000000LL);
+    row.dual = row.aug;
+    row.rmse = row.aug;
+    row.elapsed_ns = (int64_t)(globaltimer() - st->t0);
+  }
+  // c_floor (pcg.cpp:81-85)
+  const double pr_norm = sqrt(prpr);
+  if (rr > 0.0) st->pi_gain = dmax_std(st->pi_gain, pr_norm / sqrt(rr));
+  const double floor_c = 16.0 * kEps * dmax_std(st->pi_gain, 1e-3) * rr;
+  const double c = st->c;
+  const bool exhausted = fabs(c_next) <= floor_c / 64.0 || (fabs(c_next) <= floor_c && c_next <= 1e-6 * c);
+  bool stop = false;
+  if (c_next < 0.0 && fabs(c_next) > floor_c) {
+    st->term = T_BREAKDOWN;
+    st->breakdown_iter = i;
+    stop = true;
+  }
+  if (!stop) {
+    if (c_next < 0.0) c_next = 0.0;
+    if (c_next < st->c_best) {
+      st->c_best = c_next;
+      st->best = st->cur;
+      st->best_iter = i;
+    }
+    if (c_next <= st->threshold || exhausted) {
+      st->term = T_CONVERGED;
+      stop = true;
+    }
+  }
+  if (!stop) {
+    if (fabs(c_next - c) <= 1e-15 * c) {
+      if (++st->stagnant >= st->stagnation_window) {
+        st->term = T_STAGNATION;
+        stop = true;
+      }
+    } else {
+      st->stagnant = 0;
+    }
+  }
+  if (!stop && c_next > st->growth_tol * st->c_best && i - st->best_iter >= st->growth_window) {
+    st->term = T_BREAKDOWN;
+    st->breakdown_iter = i;
+    stop = true;
+  }
+  if (!stop) {
+    const double mu = c_next / c;
+    st->mu = mu;
+    st->c = c_next;
+    st->mu_pending = 1;
+    if (i == st->max_iter) stop = true;  // loop exhausted: Termination::MaxIter stays
+  }
+  st->diag_now = (st->diag_every > 0 && (i % st->diag_every) == 0) || stop;
+  if (stop) {
+    st->active = 0;
+    st->cont = 0;
+  } else {
+    st->cont = 1;
+    st->i = i + 1;
+    // next rotation buffer: the one that is neither cur nor best
+    int nx = 0;
+    while (nx == st->cur || nx == st->best) ++nx;
+    st->nxt = nx;
+  }
+}
+
+// Trace diagnostics finalize for the row just computed (pcg.cpp:104-116): aug_residual_norm,
+// dual_feas_norm, rmse against beta_true when the row is sampled.
+__global__ void k_diag_finalize(const double* rpart, int count, const double* xtw, int64_t n, const double* est,
+                                const double* beta, SolveState* st, TraceRowD* rows, int64_t row_override) {
+  if (row_override < 0 && !st->diag_now) return;
+  if (!st->have_beta) beta = nullptr;
+  __shared__ double red[32 * 3];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int i = threadIdx.x; i < count; i += blockDim.x) v[0] += rpart[i];
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    v[1] += xtw[j] * xtw[j];
+    if (beta) {
+      const double d = est[j] - beta[j];
+      v[2] += d * d;
+    }
+  }
+  block_sum<3>(v, red);
+  if (threadIdx.x == 0) {
+    const int64_t i = row_override >= 0 ? row_override : st->done;
+    if (i < st->rows_cap) {
+      TraceRowD& row = rows[i];
+      row.aug = sqrt(v[0]);
+      row.dual = sqrt(v[1]);
+      const bool sampled = row_override >= 0 ? true : (st->sampled != 0);
+      if (sampled && beta) row.rmse = sqrt(v[2] / (double)n);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Setup QR (SurPreconditioner ctor, structured.cpp:427-450 -> householder_factor / form_q_columns,
+// linalg.cpp:24-95) as a TSQR tree per block.  Each work item is one row chunk of one level: the
+// leaf factor applies the reference's Householder recipe (alpha = -sign(x_kk) |x|, unit-head v,
+// beta = -1/(alpha v0)) to the chunk; the chunk's R goes to the next level, whose QR combines them.
+// Q is formed top-down: Q_chunk = H_0 ... H_{n-1} [C; 0] with C the chunk's n x n slice of the
+// parent's explicit Q (the identity at the top), as form_q_columns does.
+struct QrItem {
+  const double* src;   // level matrix (level 0: X_b), column-major ld lds
+  int64_t lds;
+  int64_t r0, rows;    // chunk rows
+  int64_t valid;       // rows >= valid of src read as 0 (level 0: M; padding)
+  double scale;        // level 0: w_b (DenseMatrix *= w, structured.cpp:435-436); else 1
+  double* refl;        // reflector panel / explicit Q destination, ld ldr (same row range)
+  int64_t ldr;
+  double* tau;         // [n] beta of each reflector
+  double* rout;        // R of this chunk: n x n at rout (ld ldo)
+  int64_t ldo;
+  const double* qpar;  // parent explicit-Q slice (n x n, ld ldp); null = identity
+  int64_t ldp;
+  double* rdiag;       // top level only: |R_kk| destination for the rank check (else null)
+  int n;
+  int smem;            // 1: panel in shared memory; 0: in the CTA's global scratch slot
+};
+
+constexpr int QR_NT = 256;
+
+__global__ void __launch_bounds__(QR_NT) k_qr_factor(const QrItem* items, int nitems, double* scratch,
+                                                     int64_t slot) {
+  extern __shared__ double psm[];
+  __shared__ double sh[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = QR_NT / 32;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    double* P = I.smem ? psm : scratch + (int64_t)blockIdx.x * slot;
+    __syncthreads();
+    for (int64_t idx = threadIdx.x; idx < L * n; idx += QR_NT) {
+      const int j = (int)(idx / L);
+      const int64_t i = idx - (int64_t)j * L;
+      const int64_t row = I.r0 + i;
+      P[idx] = (row < I.valid) ? I.src[(int64_t)j * I.lds + row] * I.scale : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+      double* Pk = P + (int64_t)k * L;
+      if (warp == 0) {
+        double amax = 0.0;
+        for (int64_t i = k + lane; i < L; i += 32) amax = fmax(amax, fabs(Pk[i]));
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) amax = fmax(amax, __shfl_xor_sync(FULL, amax, o));
+        double ssq = 0.0;
+        if (amax > 0.0)
+          for (int64_t i = k + lane; i < L; i += 32) {
+            const double t = Pk[i] / amax;
+            ssq += t * t;
+          }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) ssq += __shfl_xor_sync(FULL, ssq, o);
+        const double norm_x = amax * sqrt(ssq);
+        double alpha = 0.0, v0 = 1.0, beta = 0.0;
+        if (norm_x != 0.0) {
+          const double wkk = Pk[k];
+          alpha = wkk >= 0.0 ? -norm_x : norm_x;
+          v0 = wkk - alpha;
+          beta = -1.0 / (alpha * v0);
+        }
+        __syncwarp();
+        if (norm_x != 0.0) {
+          for (int64_t i = k + 1 + lane; i < L; i += 32) Pk[i] /= v0;
+          if (lane == 0) Pk[k] = v0;
+        }
+        if (lane == 0) {
+          sh[0] = alpha;
+          sh[1] = v0;
+          sh[2] = beta;
+          I.tau[k] = beta;
+        }
+      }
+      __syncthreads();
+      const double beta = sh[2];
+      if (beta != 0.0) {
+        const double v0 = sh[1];
+        const double beta_hat = beta * v0 * v0;
+        for (int j = k + 1 + warp; j < n; j += NW) {
+          double* Pj = P + (int64_t)j * L;
+          double s = 0.0;
+          for (int64_t i = k + 1 + lane; i < L; i += 32) s += Pk[i] * Pj[i];
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+          s = (Pj[k] + s) * beta_hat;
+          __syncwarp();
+          if (lane == 0) Pj[k] -= s;
+          for (int64_t i = k + 1 + lane; i < L; i += 32) Pj[i] -= s * Pk[i];
+        }
+      }
+      if (threadIdx.x == 0) {
+        // r_diag[k] = alpha: keep it beside the packed panel (R output below)
+        sh[3] = sh[0];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        I.rout[k + (int64_t)k * I.ldo] = sh[3];
+        if (I.rdiag) I.rdiag[k] = sh[3];
+      }
+    }
+    __syncthreads();
+    // R (strict upper part from the panel; diagonal written above; zeros below)
+    for (int idx = threadIdx.x; idx < n * n; idx += QR_NT) {
+      const int j = idx / n, i = idx - j * n;
+      if (i < j) I.rout[i + (int64_t)j * I.ldo] = P[i + (int64_t)j * L];
+      else if (i > j) I.rout[i + (int64_t)j * I.ldo] = 0.0;
+    }
+    // packed reflectors to the level storage
+    for (int64_t idx = threadIdx.x; idx < L * n; idx += QR_NT) {
+      const int j = (int)(idx / L);
+      const int64_t i = idx - (int64_t)j * L;
+      I.refl[(int64_t)j * I.ldr + I.r0 + i] = P[idx];
+    }
+  }
+}
+
+// Explicit thin Q of a chunk: E = H_0 ... H_{n-1} [C; 0], warp per column, the column held in
+// registers (NQ x 32 rows); reflectors read from the staged panel.
+template <int NQ>
+__global__ void __launch_bounds__(QR_NT) k_qr_formq(const QrItem* items, int nitems, double* scratch, int64_t slot) {
+  extern __shared__ double psm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = QR_NT / 32;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    double* P = I.smem ? psm : scratch + (int64_t)blockIdx.x * slot;
+    __syncthreads();
+    for (int64_t idx = threadIdx.x; idx < L * n; idx += QR_NT) {
+      const int j = (int)(idx / L);
+      const int64_t i = idx - (int64_t)j * L;
+      P[idx] = I.refl[(int64_t)j * I.ldr + I.r0 + i];
+    }
+    __syncthreads();
+    for (int j = warp; j < n; j += NW) {
+      double e[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int64_t i = lane + 32 * q;
+        double v = 0.0;
+        if (i < n) v = I.qpar ? I.qpar[i + (int64_t)j * I.ldp] : (i == j ? 1.0 : 0.0);
+        e[q] = v;
+      }
+      for (int k = n - 1; k >= 0; --k) {
+        const double beta = I.tau[k];
+        if (beta == 0.0) continue;
+        const double* Pk = P + (int64_t)k * L;
+        const double v0 = Pk[k];
+        const double beta_hat = beta * v0 * v0;
+        // s = e[k] + sum_{i>k} P[i,k] e[i]
+        double s = 0.0, ek = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int64_t i = lane + 32 * q;
+          if (i > k && i < L) s += Pk[i] * e[q];
+          if (i == k) ek = e[q];
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+        ek = __shfl_sync(FULL, ek, k & 31);
+        s = (ek + s) * beta_hat;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int64_t i = lane + 32 * q;
+          if (i == k) e[q] -= s;
+          else if (i > k && i < L) e[q] -= s * Pk[i];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int64_t i = lane + 32 * q;
+        if (i < L) I.refl[(int64_t)j * I.ldr + I.r0 + i] = e[q];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Counter-based normal generator for synthetic inputs: Philox4x32-10 on (element, stream) keyed
+// by the seed, Box-Muller on two 53-bit uniforms (u1 in (0,1]).  Element e of a rows x cols
+// matrix is e = col * rows + row, independent of the leading dimension.
+__device__ __forceinline__ void philox(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t h0 = (uint32_t)(p0 >> 32), l0 = (uint32_t)p0;
+    const uint32_t h1 = (uint32_t)(p1 >> 32), l1 = (uint32_t)p1;
+    const uint32_t n0 = h1 ^ c[1] ^ k0, n2 = h0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = l1; c[2] = n2; c[3] = l0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__global__ void k_synth_normal(double* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t stream) {
+  const int64_t total = rows * cols;
+  const int64_t pairs = (total + 1) / 2;
+  for (int64_t pidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pidx < pairs;
+       pidx += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c[4] = {(uint32_t)pidx, (uint32_t)(pidx >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+    philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t a = ((uint64_t)c[0] << 32) | c[1];
+    const uint64_t bb = ((uint64_t)c[2] << 32) | c[3];
+    const double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = (double)(bb >> 11) * 0x1.0p-53;
+    const double rad = sqrt(-2.0 * log(u1));
+    double sv, cv;
+    sincospi(2.0 * u2, &sv, &cv);
+    const int64_t e0 = 2 * pidx, e1 = e0 + 1;
+    {
+      const int64_t col = e0 / rows, row = e0 - col * rows;
+      out[col * ld + row] = rad * cv;
+    }
+    if (e1 < total) {
+      const int64_t col = e1 / rows, row = e1 - col * rows;
+      out[col * ld + row] = rad * sv;
+    }
+  }
+}
+
+// y_b += X_b beta_b (row sums, ascending j) for the synthetic response.
+__global__ void k_add_xbeta(int G, int64_t M, const int* nb, const int64_t* p0, const double* X, int64_t ldx,
+                            const double* beta, double* Y, int64_t ldy) {
+  const int b = blockIdx.y;
+  const int n = nb[b];
+  const int64_t pb = p0[b];
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M; k += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s = s + X[(pb + j) * ldx + k] * beta[pb + j];
+    Y[(int64_t)b * ldy + k] = s + Y[(int64_t)b * ldy + k];
+  }
+}
+
+// Rank check on the final R diagonal (linalg.cpp:55-63): flag[b] = 1 when deficient.
+__global__ void k_rank_check(Geo g, const double* R, int* flags) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.G) return;
+  const int n = g.nb[b];
+  const double* Rb = R + g.r0[b];
+  double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000LL);
+  for (int k = 0; k < n; ++k) {
+    const double d = fabs(Rb[k + (int64_t)k * n]);
+    mx = dmax_std(mx, d);
+    mn = (d < mn) ? d : mn;
+  }
+  flags[b] = (mx == 0.0 || mn <= 1e-10 * mx) ? 1 : 0;
+}
+
+// out[i] = a[i] - b[i] style helpers ---------------------------------------------------------
+// r = (sw + X z) - y   (pcg.cpp:69-70); X z row sums per block in ascending j.
+__global__ void k_init_residual(Geo g, const double* X, int64_t ldx, const double* z, const double* sw,
+                                const double* Y, int64_t ldy, double* r) {
+  const int b = blockIdx.y;
+  const int nb = g.nb[b];
+  const int64_t p0 = g.p0[b];
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.ldm; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t off = (int64_t)b * g.ldm + k;
+    double xz = 0.0;
+    double yv = 0.0;
+    if (k < g.M) {
+      for (int j = 0; j < nb; ++j) xz = xz + X[(p0 + j) * ldx + k] * z[p0 + j];
+      yv = Y[(int64_t)b * ldy + k];
+    }
+    r[off] = (sw[off] + xz) - yv;
+  }
+}
+
+__global__ void k_axpy_sub(double* w, const double* corr, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] -= corr[i];
+}
+
+__global__ void k_fill(double* p, double v, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// Frobenius norm partials of X (storage order of the dense embed: columns, rows; pcg.cpp:60).
+__global__ void k_sumsq_cols(const double* X, int64_t ldx, int64_t M, int64_t ncols, double* partials) {
+  double s = 0.0;
+  for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x)
+    for (int64_t k = threadIdx.x; k < M; k += blockDim.x) {
+      const double v = X[j * ldx + k];
+      s += v * v;
+    }
+  __shared__ double red[NT / 32];
+  double v1[1] = {s};
+  block_sum<1>(v1, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = v1[0];
+}
+
+__global__ void k_sum1(const double* partials, int count, double* out) {
+  double v[1] = {0.0};
+  for (int i = threadIdx.x; i < count; i += blockDim.x) v[0] += partials[i];
+  __shared__ double red[32];
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) *out = v[0];
+}
+
+}  // namespace glsgpu

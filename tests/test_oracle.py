@@ -1,0 +1,144 @@
+"""CPU tests: pin the oracle (C restatement) to the reference itself and to the golden fixtures.
+
+The reference ships no golden vectors; the fixtures in tests/golden/ were produced by the reference
+(tests/golden/make_golden.py).  When oracle/_ref/libglsref.so is present (built here from
+/root/reference; it also travels to the GPU box) the restatement is checked BITWISE against the
+literal reference call on BASELINE-shaped seeded problems.
+"""
+import glob
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_14471_b200 import synth
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _golden_problem(z):
+    p = synth.SurProblem(name="golden", G=int(z["G"]), M=int(z["M"]), nb=z["nb"], X=np.asfortranarray(z["X"]),
+                         Y=np.asfortranarray(z["Y"]), omega=np.asfortranarray(z["omega"]), beta=z["beta"],
+                         tol_rel=float(z["tol_rel"]), max_iter=int(z["max_iter"]))
+    if z["scale"].size:
+        p.scale = z["scale"]
+    w1 = z["w1"] if z["w1"].size else None
+    z1 = z["z1"] if z["z1"].size else None
+    return p, w1, z1
+
+
+def _same(a, b):
+    return np.array_equal(a, b, equal_nan=True)
+
+
+def _assert_bitwise(o, r):
+    assert o.iterations == r.iterations
+    assert o.termination == r.termination
+    assert o.breakdown_iteration == r.breakdown_iteration
+    assert o.w1_projected == r.w1_projected
+    assert o.residual_seminorm == r.residual_seminorm
+    assert _same(o.b, r.b)
+    assert _same(o.w, r.w)
+    for f in ("iter", "c", "aug_residual_norm", "dual_feas_norm", "rmse"):
+        assert _same(o.trace[f], r.trace[f]), f
+    assert o.sigma_scale == r.sigma_scale
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "small_*.npz"))), ids=os.path.basename)
+def test_oracle_matches_reference_golden(oracle_mod, path):
+    z = np.load(path)
+    p, w1, z1 = _golden_problem(z)
+    cfg = oracle.make_config(tol_rel=p.tol_rel, max_iter=p.max_iter)
+    o = oracle.solve(p, "oracle", cfg=cfg, w1=w1, z1=z1, beta_true=p.beta)
+    assert o.iterations == int(z["iterations"])
+    assert o.termination == str(z["termination"])
+    assert _same(o.b, z["b"]) and _same(o.w, z["w"])
+    assert o.residual_seminorm == float(z["residual_seminorm"])
+    tr = z["trace"]
+    for f in ("iter", "c", "aug_residual_norm", "dual_feas_norm", "rmse"):
+        assert _same(o.trace[f], tr[f]), f
+
+
+def test_c0_inputs_reproducible_and_oracle_matches_golden(oracle_mod):
+    z = np.load(os.path.join(GOLDEN, "c0.npz"))
+    p = synth.make_problem(0)
+    h = hashlib.sha256()
+    for a in (p.X, p.Y, p.omega, p.beta):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == str(z["input_sha256"]), "synthetic c0 inputs changed (numpy Philox stream)"
+    o = oracle.solve(p, "oracle", beta_true=p.beta)
+    assert o.iterations == int(z["iterations"]) == 228
+    assert o.termination == "Converged"
+    assert _same(o.b, z["b"]) and _same(o.w, z["w"])
+    assert _same(o.trace["c"], z["trace"]["c"])
+
+
+CASES = [
+    ("c0", lambda: synth.make_problem(0)),
+    ("c1_scaled", lambda: synth.make_problem(1, M=150, G=16)),
+    ("c2_scaled", lambda: synth.make_problem(2, M=120, G=40)),
+    ("c3_scaled", lambda: synth.make_problem(3, M=200, N=16, G=12)),
+    ("c4_scaled", lambda: synth.make_problem(4, M=300, G=24)),
+]
+
+
+@pytest.mark.parametrize("name,mk", CASES, ids=[c[0] for c in CASES])
+def test_oracle_bitwise_equals_reference(oracle_mod, have_ref, name, mk):
+    if not have_ref:
+        pytest.skip("oracle/_ref/libglsref.so not built (needs /root/reference)")
+    p = mk()
+    if p.max_iter == 0 and name == "c4_scaled":
+        p.max_iter = 200
+    o = oracle.solve(p, "oracle", beta_true=p.beta)
+    r = oracle.solve(p, "ref", beta_true=p.beta)
+    _assert_bitwise(o, r)
+
+
+def test_oracle_probes_bitwise(oracle_mod, have_ref):
+    if not have_ref:
+        pytest.skip("reference not built")
+    p = synth.random_sur(4, 25, [3, 6, 2, 5], seed=5)
+    p.scale = np.array([2.0, 0.5, 1.0, 3.0])
+    r = np.random.default_rng(3)
+    xi = r.standard_normal(p.m)
+    v = r.standard_normal(p.n)
+    for kind, vec in (("pi", xi), ("xstar_t", xi), ("xstar", v)):
+        assert _same(oracle.sur_apply(p, kind, vec, "oracle"), oracle.sur_apply(p, kind, vec, "ref")), kind
+    assert _same(oracle.kron_apply(p.omega, xi, p.M, "oracle"), oracle.kron_apply(p.omega, xi, p.M, "ref"))
+    assert oracle.norm_probe(p.omega, p.M, "oracle") == oracle.norm_probe(p.omega, p.M, "ref")
+
+
+def test_oracle_error_paths(oracle_mod):
+    p = synth.random_sur(3, 10, [2, 3, 2], seed=8)
+    # rank-deficient block 1 (duplicate column) -> RankDeficient naming the block
+    X = p.X.copy(order="F")
+    X[:, 3] = X[:, 2]
+    q = synth.SurProblem("bad", p.G, p.M, p.nb, X, p.Y, p.omega, p.beta, 1e-10)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.solve(q, "oracle")
+    assert e.value.kind == "RankDeficient" and "block 1" in str(e.value)
+    q = synth.SurProblem("bad", p.G, p.M, p.nb, p.X, p.Y, p.omega, p.beta, 1e-10, scale=np.array([1.0, 0.0, 1.0]))
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.solve(q, "oracle")
+    assert e.value.kind == "SingularD"
+
+
+def test_oracle_restated_operator_identities(oracle_mod):
+    """Structured-operator pins of proj/tests/test_structured.cpp:177-214 on the restatement."""
+    p = synth.random_sur(3, 8, [2, 3, 2], seed=51)
+    r = np.random.default_rng(1)
+    xi = r.standard_normal(p.m)
+    est = oracle.sur_apply(p, "xstar_t", xi)
+    res = oracle.sur_apply(p, "pi", xi)
+    off = 0
+    for i in range(p.G):
+        Xi = p.X[:, off:off + p.nb[i]]
+        xi_i = xi[i * p.M:(i + 1) * p.M]
+        b_ols = np.linalg.lstsq(Xi, xi_i, rcond=None)[0]
+        assert np.linalg.norm(est[off:off + p.nb[i]] - b_ols) <= 1e-10 * np.linalg.norm(b_ols)
+        assert np.linalg.norm(res[i * p.M:(i + 1) * p.M] - (xi_i - Xi @ b_ols)) <= 1e-10 * np.linalg.norm(xi_i)
+        off += p.nb[i]
+    in_range = np.concatenate([p.X[:, sum(p.nb[:i]):sum(p.nb[:i + 1])] @ np.ones(p.nb[i]) for i in range(p.G)])
+    assert np.linalg.norm(oracle.sur_apply(p, "pi", in_range)) <= 1e-10 * np.linalg.norm(in_range)
