@@ -164,6 +164,9 @@ void glsgpu_default_config(glsgpu_pcg_config* cfg);
 /* Kernel statistics of the last solve with kernel_timing = 1; returns the number written. */
 int glsgpu_kernel_stats(const glsgpu_sur* h, glsgpu_kernel_stat* out, int cap);
 
+/* Kernels this handle has launched so far (CUDA-graph kernel nodes counted per graph launch). */
+int glsgpu_launch_count(const glsgpu_sur* h, int64_t* count);
+
 /* Test / bench helpers (not part of the reference surface) ---------------------------------- */
 /* Copy Q (M x n, ld M) and the concatenated R blocks to host. */
 int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R);

@@ -72,6 +72,7 @@ class SolveOut:
     w1_projected: bool
     trace: np.ndarray
     sigma_scale: float
+    counters: Optional[np.ndarray] = None   # reference CostCounters after the solve (kind="ref")
 
 
 _P = C.POINTER(C.c_double)
@@ -107,7 +108,8 @@ def _load(path: str, kind: str):
     else:
         lib.ref_pcg_aug_sur.restype = C.c_int
         lib.ref_pcg_aug_sur.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, _P, _P, _P, _P, C.POINTER(Config), _P,
-                                        _P, _P, C.POINTER(TraceRow), C.c_int64, C.POINTER(Result)]
+                                        _P, _P, C.POINTER(TraceRow), C.c_int64, C.POINTER(Result),
+                                        C.POINTER(C.c_uint64)]
         lib.ref_sur_apply.restype = C.c_int
         lib.ref_sur_apply.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, C.c_int, _P, _P]
         lib.ref_kron_apply.restype = C.c_int
@@ -162,14 +164,16 @@ def solve(prob, kind: str = "oracle", cfg: Optional[Config] = None, w1=None, z1=
         if st:
             raise OracleError(st, f"block {bad.value}")
     else:
-        st = L.ref_pcg_aug_sur(*args)
+        counters = np.zeros(6, dtype=np.uint64)
+        st = L.ref_pcg_aug_sur(*args, counters.ctypes.data_as(C.POINTER(C.c_uint64)))
         if st:
             raise OracleError(st, L.ref_last_error().decode())
     tr = np.frombuffer(rows, dtype=TRACE_DTYPE, count=min(res.n_rows, cap)).copy() if trace else np.zeros(0, TRACE_DTYPE)
     return SolveOut(b=b, w=w, iterations=int(res.iterations), termination=TERMINATION[res.termination],
                     breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
                     residual_seminorm=float(res.residual_seminorm), w1_projected=bool(res.w1_projected),
-                    trace=tr, sigma_scale=float(res.sigma_scale))
+                    trace=tr, sigma_scale=float(res.sigma_scale),
+                    counters=counters if kind != "oracle" else None)
 
 
 def sur_apply(prob, kind_op: str, vec: np.ndarray, kind: str = "oracle") -> np.ndarray:

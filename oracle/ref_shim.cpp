@@ -84,7 +84,7 @@ const char* ref_last_error() { return g_msg; }
 int ref_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y,
                     const double* omega, const double* scale, const double* w1, const double* z1,
                     const Config* cfg, const double* beta_true, double* b_out, double* w_out,
-                    TraceRow* rows, int64_t rows_cap, Result* res) {
+                    TraceRow* rows, int64_t rows_cap, Result* res, uint64_t* counters) {
   try {
     gls::SurModel sur = build_sur(G, M, nb, X, Y, omega);
     gls::Glm glm = gls::embed_sur(sur);
@@ -116,6 +116,15 @@ int ref_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
     res->residual_seminorm = out.solution.residual_seminorm;
     res->n_rows = static_cast<int64_t>(out.trace.rows.size());
     res->sigma_scale = gls::operator_norm_probe(glm.sigma);
+    if (counters) {
+      const gls::CostCounters& cc = op->counters();
+      counters[0] = cc.factorizations;
+      counters[1] = cc.factor_multiplies;
+      counters[2] = cc.pi_applies;
+      counters[3] = cc.xstar_t_applies;
+      counters[4] = cc.xstar_applies;
+      counters[5] = cc.apply_multiplies;
+    }
     if (rows) {
       const int64_t k = std::min<int64_t>(rows_cap, res->n_rows);
       for (int64_t i = 0; i < k; ++i) {

@@ -49,7 +49,7 @@ EXPORTS = [
     "glsgpu_sur_create_device", "glsgpu_sur_refactor", "glsgpu_sur_destroy", "glsgpu_sur_dims", "glsgpu_sur_stream",
     "glsgpu_apply_pi", "glsgpu_apply_xstar_t", "glsgpu_apply_xstar", "glsgpu_sigma_apply",
     "glsgpu_operator_norm_probe", "glsgpu_counters", "glsgpu_reset_apply_counters", "glsgpu_sur_solve",
-    "glsgpu_default_config", "glsgpu_kernel_stats", "glsgpu_get_factors", "glsgpu_synth_normal",
+    "glsgpu_default_config", "glsgpu_kernel_stats", "glsgpu_launch_count", "glsgpu_get_factors", "glsgpu_synth_normal",
     "glsgpu_synth_response",
 ]
 
@@ -87,6 +87,7 @@ def load() -> C.CDLL:
     L.glsgpu_default_config.argtypes = [C.POINTER(PcgConfigC)]
     L.glsgpu_default_config.restype = None
     L.glsgpu_kernel_stats.argtypes = [H, C.POINTER(KernelStatC), C.c_int]
+    L.glsgpu_launch_count.argtypes = [H, _PI64]
     L.glsgpu_get_factors.argtypes = [H, _P, _P]
     L.glsgpu_synth_normal.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int]
     L.glsgpu_synth_response.argtypes = [C.c_int, C.c_int64, _PI64, C.c_void_p, C.c_int64, _P, _P, C.c_uint64,

@@ -311,6 +311,11 @@ class GpuSurPreconditioner:
         bad = C.c_int(-1)
         _check(self._lib.glsgpu_sur_refactor(self._h, C.byref(bad)), self._lib)
 
+    def launch_count(self) -> int:
+        v = C.c_int64(0)
+        _check(self._lib.glsgpu_launch_count(self._h, C.byref(v)), self._lib)
+        return int(v.value)
+
     def kernel_stats(self) -> List[dict]:
         arr = (L.KernelStatC * 16)()
         k = self._lib.glsgpu_kernel_stats(self._h, arr, 16)

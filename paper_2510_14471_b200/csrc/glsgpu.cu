@@ -118,6 +118,9 @@ struct glsgpu_sur {
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0, graph_xmode = -1, graph_diag = -2, graph_timing = -1;
   std::vector<cudaEvent_t> tev;  // timing events captured into the graph
+  int64_t graph_kernels = 0;     // kernel nodes in the instantiated graph
+  int64_t launches = 0;          // kernels launched by this handle (graph nodes counted per launch)
+  bool capturing = false;
 };
 
 namespace {
@@ -167,6 +170,8 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
   }
 #undef KRON_CASE
   CKL("k_kron");
+  if (!h->capturing) h->launches++;
+  if (!h->capturing) h->launches++;
 }
 
 int kron_grid(const glsgpu_sur* h) {
@@ -184,11 +189,13 @@ void launch_colpass(glsgpu_sur* h, ColArgs a, const SolveState* st) {
   if (h->n_narrow) {
     a.blocks = h->d_blk_narrow;
     k_colpass<MODE, true><<<h->n_narrow * h->nch, NT, 0, h->s>>>(g, a, st);
+    if (!h->capturing) h->launches++;
     CKL("k_colpass fused");
   }
   if (h->n_wide) {
     a.blocks = h->d_blk_wide;
     k_colpass<MODE, false><<<h->n_wide * h->nch, NT, (size_t)h->CH * sizeof(double), h->s>>>(g, a, st);
+    if (!h->capturing) h->launches++;
     CKL("k_colpass panels");
   }
 }
@@ -197,6 +204,7 @@ void launch_reduce_t(glsgpu_sur* h, double* out, const SolveState* st, int gate)
   const int per = NT / 32;
   const int64_t grid = (h->n + per - 1) / per;
   k_reduce_t<<<(unsigned)grid, NT, 0, h->s>>>(h->tpart, h->n, h->nch, out, st, gate);
+  if (!h->capturing) h->launches++;
   CKL("k_reduce_t");
 }
 
@@ -405,23 +413,27 @@ void run_qr(glsgpu_sur* h) {
     const auto& L = h->qr_levels[l];
     const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
     k_qr_factor<<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch, h->qr_slot);
+    if (!h->capturing) h->launches++;
     CKL("k_qr_factor");
   }
   for (int l = nl - 1; l >= 0; --l) {
     const auto& L = h->qr_levels[l];
     const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
-    if (L.max_rows <= 256)
+    if (L.max_rows <= 256) {
       k_qr_formq<8><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch, h->qr_slot);
-    else if (L.max_rows <= 512)
+    } else if (L.max_rows <= 512) {
       k_qr_formq<16><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch,
                                                            h->qr_slot);
-    else
+    } else {
       k_qr_formq<32><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch,
                                                            h->qr_slot);
+    }
+    if (!h->capturing) h->launches++;
     CKL("k_qr_formq");
   }
   Geo g = geo_of(h);
   k_rank_check<<<(h->G + 127) / 128, 128, 0, h->s>>>(g, h->R, h->d_rank_flags);
+  if (!h->capturing) h->launches++;
   CKL("k_rank_check");
   std::vector<int> flags(h->G);
   CK(cudaMemcpyAsync(flags.data(), h->d_rank_flags, sizeof(int) * h->G, cudaMemcpyDeviceToHost, h->s));
@@ -601,6 +613,7 @@ double norm_probe(glsgpu_sur* h, int64_t iters) {
   for (int64_t it = 0; it < iters; ++it) {
     launch_kron(h, a, nullptr, h->scal, nullptr, b, h->partA, it == 0 ? 0 : 1, nullptr, &grid);
     k_probe_step<<<1, NT, 0, h->s>>>(h->partA, grid, h->scal, h->d_stop);
+    if (!h->capturing) h->launches++;
     CKL("k_probe_step");
     std::swap(a, b);
   }
@@ -654,6 +667,7 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   launch_kron(h, nullptr, h->pr, nullptr, h->u, h->su, h->partA, 2, h->st, nullptr);
   ev(1);
   k_scalar_a<<<1, NT, 0, h->s>>>(h->partA, gA, h->st);
+  if (!h->capturing) h->launches++;
   CKL("k_scalar_a");
   // pass B
   ColArgs a = base_args(h);
@@ -667,11 +681,14 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   // pass C
   ev(4);
   k_rowpass<<<gC, NT, 0, h->s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, h->st);
+  if (!h->capturing) h->launches++;
   CKL("k_rowpass");
   ev(5);
   k_scalar_c<<<1, NT, 0, h->s>>>(h->partC, gC, h->st, h->rows_d);
+  if (!h->capturing) h->launches++;
   CKL("k_scalar_c");
   k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, h->vs, a.xv_from_x, 0, h->st);
+  if (!h->capturing) h->launches++;
   CKL("k_vupdate");
   if (diag >= 0) {
     // est = X*'(y - sw) and the row diagnostics, gated on st->diag_now
@@ -680,8 +697,10 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
     d.gate = 2;
     launch_colpass<MODE_QT_D>(h, d, h->st);
     k_reduce_t<<<(unsigned)((h->n + 7) / 8), NT, 0, h->s>>>(h->tpart, h->n, h->nch, h->t2, h->st, 2);
+    if (!h->capturing) h->launches++;
     CKL("k_reduce_t diag");
     k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
+    if (!h->capturing) h->launches++;
     CKL("k_vupdate diag");
     ColArgs x = base_args(h);
     x.A = h->X;
@@ -691,9 +710,11 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
     x.gate = 2;
     launch_colpass<MODE_DIAG>(h, x, h->st);
     k_reduce_t<<<(unsigned)((h->n + 7) / 8), NT, 0, h->s>>>(h->tpart, h->n, h->nch, h->xtw, h->st, 2);
+    if (!h->capturing) h->launches++;
     CKL("k_reduce_t diag2");
     k_diag_finalize<<<1, NT, 0, h->s>>>(h->rpart, h->G * h->nch, h->xtw, h->n, h->t2, h->beta_d, h->st,
                                         h->rows_d, -1);
+    if (!h->capturing) h->launches++;
     CKL("k_diag_finalize");
   }
 }
@@ -846,6 +867,7 @@ int glsgpu_apply_pi(glsgpu_sur* h, const double* xi, double* out) {
   qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
   Geo g = geo_of(h);
   k_rowpass<<<rowpass_grid(h), NT, 0, h->s>>>(g, h->Q, h->t, h->r, h->pr, nullptr, 0, nullptr);
+  if (!h->capturing) h->launches++;
   CKL("k_rowpass");
   d2h_mvec(h, out, h->pr);
   CK(cudaStreamSynchronize(h->s));
@@ -863,6 +885,7 @@ int glsgpu_apply_xstar_t(glsgpu_sur* h, const double* xi, double* out) {
   qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
   Geo g = geo_of(h);
   k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, nullptr, 1, 2, nullptr);
+  if (!h->capturing) h->launches++;
   CKL("k_vupdate");
   CK(cudaMemcpyAsync(out, h->t, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->s));
   CK(cudaStreamSynchronize(h->s));
@@ -879,8 +902,10 @@ int glsgpu_apply_xstar(glsgpu_sur* h, const double* v, double* out) {
   CK(cudaMemcpyAsync(h->t, v, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
   Geo g = geo_of(h);
   k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, nullptr, 1, 3, nullptr);
+  if (!h->capturing) h->launches++;
   CKL("k_vupdate");
   k_rowpass<<<rowpass_grid(h), NT, 0, h->s>>>(g, h->Q, h->t, nullptr, h->pr, nullptr, 1, nullptr);
+  if (!h->capturing) h->launches++;
   CKL("k_rowpass");
   d2h_mvec(h, out, h->pr);
   CK(cudaStreamSynchronize(h->s));
@@ -920,6 +945,12 @@ int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R) {
     CK(cudaMemcpy(R, h->R, sizeof(double) * rtot, cudaMemcpyDeviceToHost));
   }
   API_END((int*)nullptr)
+}
+
+int glsgpu_launch_count(const glsgpu_sur* h, int64_t* count) {
+  if (!h || !count) return GLSGPU_ERR_INVALID;
+  *count = h->launches;
+  return GLSGPU_OK;
 }
 
 int glsgpu_kernel_stats(const glsgpu_sur* h, glsgpu_kernel_stat* out, int cap) {
@@ -977,6 +1008,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   hs.have_beta = beta_true ? 1 : 0;
   CK(cudaMemcpyAsync(h->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
   k_set_t0<<<1, 1, 0, s>>>(h->st);
+  if (!h->capturing) h->launches++;
 
   const size_t mvb = sizeof(double) * (size_t)(h->ldm * h->G);
   // w1 (pcg.cpp:55-66): enforce X'w1 = 0 by projecting along X*
@@ -997,7 +1029,9 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     CK(cudaMemcpyAsync(xtw.data(), h->xtw, sizeof(double) * h->n, cudaMemcpyDeviceToHost, s));
     if (h->frob_x < 0) {
       k_sumsq_cols<<<GRID_CAP, NT, 0, s>>>(h->X, h->ldx, h->M, h->n, h->partA);
+      if (!h->capturing) h->launches++;
       k_sum1<<<1, NT, 0, s>>>(h->partA, GRID_CAP, h->scal + 8);
+      if (!h->capturing) h->launches++;
       double ss = 0;
       CK(cudaMemcpyAsync(&ss, h->scal + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -1014,8 +1048,11 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
       // corr = X* xtw = Q R^-T xtw per block (xstar_impl); w -= corr
       CK(cudaMemcpyAsync(h->t, h->xtw, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, s));
       k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t, nullptr, 1, 3, nullptr);
+      if (!h->capturing) h->launches++;
       k_rowpass<<<rowpass_grid(h), NT, 0, s>>>(g, h->Q, h->t, nullptr, h->pr, nullptr, 1, nullptr);
+      if (!h->capturing) h->launches++;
       k_axpy_sub<<<GRID_CAP, NT, 0, s>>>(h->wb[0], h->pr, h->ldm * h->G);
+      if (!h->capturing) h->launches++;
       CKL("w1 projection");
       w1_projected = 1;
     }
@@ -1029,16 +1066,20 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   {
     dim3 grid((unsigned)std::min<int64_t>((h->ldm + NT - 1) / NT, 64), (unsigned)h->G);
     k_init_residual<<<grid, NT, 0, s>>>(g, h->X, h->ldx, h->zvec, h->swb[0], h->Y, h->ldy, h->r);
+    if (!h->capturing) h->launches++;
     CKL("k_init_residual");
   }
   qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
   const int gC = rowpass_grid(h);
   k_rowpass<<<gC, NT, 0, s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, nullptr);
+  if (!h->capturing) h->launches++;
   CKL("k_rowpass init");
   k_init_scalars<<<1, NT, 0, s>>>(h->partC, gC, h->st, h->rows_d);
+  if (!h->capturing) h->launches++;
   CKL("k_init_scalars");
   // v = X*' r (X mode: R^-1 t; QR mode: s = t); u = pr
   k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t, h->vs, xv_mode == GLSGPU_XV_X ? 1 : 0, 1, nullptr);
+  if (!h->capturing) h->launches++;
   CKL("k_vupdate init");
   CK(cudaMemcpyAsync(h->u, h->pr, mvb, cudaMemcpyDeviceToDevice, s));
   // row 0 diagnostics: est0 = recover(sw) (pcg.cpp:118-122)
@@ -1047,6 +1088,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     launch_colpass<MODE_QT_D>(h, d, h->st);
     launch_reduce_t(h, h->t2, nullptr, 0);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
+    if (!h->capturing) h->launches++;
     ColArgs x = base_args(h);
     x.A = h->X;
     x.lda = h->ldx;
@@ -1055,6 +1097,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     launch_colpass<MODE_DIAG>(h, x, h->st);
     launch_reduce_t(h, h->xtw, nullptr, 0);
     k_diag_finalize<<<1, NT, 0, s>>>(h->rpart, h->G * h->nch, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d, 0);
+    if (!h->capturing) h->launches++;
     CKL("row 0 diagnostics");
   }
 
@@ -1081,8 +1124,23 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     }
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    h->capturing = true;
     for (int k = 0; k < chunk; ++k) capture_iteration(h, xv_mode, diag >= 0 ? 1 : -1, timing, k);
+    h->capturing = false;
     CK(cudaStreamEndCapture(s, &graph));
+    {
+      size_t nn = 0;
+      CK(cudaGraphGetNodes(graph, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+      int64_t kn = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        CK(cudaGraphNodeGetType(nd, &ty));
+        if (ty == cudaGraphNodeTypeKernel) ++kn;
+      }
+      h->graph_kernels = kn;
+    }
     CK(cudaGraphInstantiate(&h->graph, graph, 0));
     CK(cudaGraphDestroy(graph));
     h->graph_chunk = chunk;
@@ -1099,6 +1157,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     if (!h->st_host->active) break;
     prev_i = h->st_host->i;
     CK(cudaGraphLaunch(h->graph, s));
+    h->launches += h->graph_kernels;
     if (timing) {
       CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -1133,6 +1192,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     launch_colpass<MODE_QT_D>(h, d, h->st);
     launch_reduce_t(h, h->t2, nullptr, 0);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
+    if (!h->capturing) h->launches++;
     CKL("recover");
   }
   CK(cudaEventRecord(e1, s));
@@ -1227,6 +1287,7 @@ int glsgpu_synth_response(int G, int64_t M, const int64_t* n_i, const double* X_
   try {
     ensure_solver(h, 1);
     k_synth_normal<<<148 * 8, 256, 0, h->s>>>(h->r, M, G, h->ldm, seed, 3);
+    if (!h->capturing) h->launches++;
     CKL("k_synth_normal");
     launch_kron(h, h->r, nullptr, nullptr, nullptr, h->su, h->partA, 0, nullptr, nullptr);
     CK(cudaMemcpy2DAsync(Y_dev, ldy * sizeof(double), h->su, h->ldm * sizeof(double), M * sizeof(double), G,
@@ -1235,6 +1296,7 @@ int glsgpu_synth_response(int G, int64_t M, const int64_t* n_i, const double* X_
     CK(cudaMemcpyAsync(bd, beta, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
     dim3 grid((unsigned)std::min<int64_t>((M + 255) / 256, 256), (unsigned)G);
     k_add_xbeta<<<grid, 256, 0, h->s>>>(G, M, h->d_nb, h->d_p0, X_dev, ldx, bd, Y_dev, ldy);
+    if (!h->capturing) h->launches++;
     CKL("k_add_xbeta");
     CK(cudaStreamSynchronize(h->s));
     cudaFree(bd);

@@ -1,0 +1,248 @@
+"""GPU parity tests: the sm_100a path through the C-ABI against the oracle and the reference.
+
+Bars (north star, BASELINE.json): same termination and iteration count as the CPU oracle
+(bitwise-equal to the reference, tests/test_oracle.py) and ||b_gpu - b_ref|| / ||b_ref|| <= 1e-10.
+The Kronecker Sigma apply is checked bitwise; operator probes to 1e-12 (the reference's own SUR pins
+use 1e-10 / 1e-11, proj/tests/test_structured.cpp:177-240).  Where the path's long reductions (tree
+order on the GPU, sequential in the reference) can legitimately move the stopping iteration of a slow
+tail (SURVEY.md s0.7, c3-shaped runs), the test states the measured envelope explicitly.
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_14471_b200 import api, synth
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+B_TOL = 1e-10
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def require_device():
+    n = api.device_count()
+    assert n > 0, "no CUDA device: the GPU tests must run on the B200 box (no CPU fallback exists)"
+
+
+def solve_both(p, mode="x", diag=1, cfg_kw=None, w1=None, z1=None):
+    cfg_kw = cfg_kw or {}
+    tol = cfg_kw.get("tol_rel", p.tol_rel)
+    mx = cfg_kw.get("max_iter", p.max_iter)
+    o = oracle.solve(p, "oracle", cfg=oracle.make_config(tol_rel=tol, max_iter=mx), w1=w1, z1=z1, beta_true=p.beta)
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur, block_scale=p.scale)
+    g = api.pcg_aug(sur, op, w1=w1, z1=z1, config=api.PcgConfig(tol_rel=tol, max_iter=mx, xv_mode=mode,
+                                                                 diag_every=diag), true_beta=p.beta)
+    return o, g, op
+
+
+PARITY = [
+    ("c0", lambda: synth.make_problem(0), True),
+    ("c1_M400", lambda: synth.make_problem(1, M=400), True),
+    ("c2_M1000", lambda: synth.make_problem(2, M=1000), True),
+    ("c4_G32_M2000", lambda: synth.make_problem(4, M=2000, G=32), True),
+    ("c4_G256_M300", lambda: synth.make_problem(4, M=300), True),
+    ("c3_M600_N40", lambda: synth.make_problem(3, M=600, N=40), False),
+]
+
+
+@pytest.mark.parametrize("mode", ["x", "qr"])
+@pytest.mark.parametrize("name,mk,strict", PARITY, ids=[c[0] for c in PARITY])
+def test_solve_parity(name, mk, strict, mode):
+    p = mk()
+    o, g, _ = solve_both(p, mode=mode, diag=0)
+    s = g.solution
+    if strict:
+        assert s.iterations == o.iterations, (s.iterations, o.iterations)
+        assert s.termination.name == o.termination
+        assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
+    else:
+        # slow-tail config: the stopping iteration may move by a few (SURVEY.md s0.7 parity envelope)
+        assert s.termination.name == o.termination
+        assert abs(s.iterations - o.iterations) <= 4, (s.iterations, o.iterations)
+        assert rel(s.b, o.b) <= 5e-10, rel(s.b, o.b)
+    # the true coefficients are recovered to statistical accuracy when the solve converged
+    if s.termination == api.Termination.Converged:
+        assert rel(s.b, p.beta) < 0.2
+
+
+@pytest.mark.parametrize("path", sorted(f for f in os.listdir(GOLDEN) if f.startswith("small_")))
+def test_golden_fixtures(path):
+    """GPU vs the reference's own stored outputs (tests/golden/make_golden.py)."""
+    z = np.load(os.path.join(GOLDEN, path))
+    p = synth.SurProblem("g", int(z["G"]), int(z["M"]), z["nb"], np.asfortranarray(z["X"]), np.asfortranarray(z["Y"]),
+                         np.asfortranarray(z["omega"]), z["beta"], float(z["tol_rel"]), int(z["max_iter"]))
+    if z["scale"].size:
+        p.scale = z["scale"]
+    w1 = z["w1"] if z["w1"].size else None
+    z1 = z["z1"] if z["z1"].size else None
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur, block_scale=p.scale)
+    g = api.pcg_aug(sur, op, w1=w1, z1=z1, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=p.max_iter),
+                    true_beta=p.beta)
+    assert g.solution.iterations == int(z["iterations"])
+    assert g.solution.termination.name == str(z["termination"])
+    assert g.trace.w1_projected == bool(z["w1_projected"])
+    bi = int(z["breakdown_iteration"])
+    assert (g.trace.breakdown_iteration or -1) == bi
+    b_ref, b_ex = z["b"], z["b_exact"]
+    if str(z["termination"]) == "Converged" and rel(b_ref, b_ex) > B_TOL:
+        # the reference stopped on its roundoff floor (c never reached tol^2 c1): its own b is only
+        # rel(b_ref, b_exact) accurate, so the bar is "at least as accurate as the reference"
+        assert rel(g.solution.b, b_ex) <= 2.0 * rel(b_ref, b_ex)
+    else:
+        assert rel(g.solution.b, b_ref) <= B_TOL
+    tr = z["trace"]
+    assert len(g.trace.rows) == len(tr)
+    # early trace rows agree tightly (the c sequences drift apart only late); rows at the
+    # roundoff level (c < 1e-8 c1) carry no signal
+    k = min(5, len(tr))
+    sig = tr["c"][:k] > 1e-8 * tr["c"][0]
+    assert np.allclose(g.trace.rows["c"][:k][sig], tr["c"][:k][sig], rtol=1e-9, atol=0)
+    assert np.allclose(g.trace.rows["aug_residual_norm"][:k][sig], tr["aug_residual_norm"][:k][sig], rtol=1e-9)
+    assert np.allclose(g.trace.rows["rmse"][:k], tr["rmse"][:k], rtol=1e-9, equal_nan=True)
+
+
+def test_c0_against_reference_golden():
+    z = np.load(os.path.join(GOLDEN, "c0.npz"))
+    p = synth.make_problem(0)
+    sur = api.sur_from_problem(p)
+    for mode in ("x", "qr"):
+        g = api.pcg_aug(sur, config=api.PcgConfig(tol_rel=1e-12, xv_mode=mode), true_beta=p.beta)
+        assert g.solution.iterations == int(z["iterations"]) == 228
+        assert g.solution.termination == api.Termination.Converged
+        assert rel(g.solution.b, z["b"]) <= 1e-13
+        assert rel(g.solution.w, z["w"]) <= 1e-12
+        assert abs(g.sigma_scale - float(z["sigma_scale"])) <= 1e-12 * float(z["sigma_scale"])
+
+
+def test_operator_probes_and_sigma():
+    for p in (synth.make_problem(1, M=120, G=12), synth.random_sur(4, 25, [3, 6, 2, 5], seed=5)):
+        if p.G == 4:
+            p.scale = np.array([2.0, 0.5, 1.0, 3.0])
+        op = api.sur_preconditioner(api.sur_from_problem(p), block_scale=p.scale)
+        r = np.random.default_rng(3)
+        xi = r.standard_normal(p.m)
+        v = r.standard_normal(p.n)
+        for kind, fn, vec in (("pi", op.apply_pi, xi), ("xstar_t", op.apply_xstar_t, xi), ("xstar", op.apply_xstar, v)):
+            ref = oracle.sur_apply(p, kind, vec)
+            assert np.max(np.abs(fn(vec) - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref))), kind
+        # Kronecker Sigma apply: bitwise the reference's operator* order
+        assert np.array_equal(op.sigma_apply(xi), oracle.kron_apply(p.omega, xi, p.M))
+        nrm = api.operator_norm_probe(op)
+        assert abs(nrm - oracle.norm_probe(p.omega, p.M)) <= 1e-12 * nrm
+
+
+def test_structured_operator_identities():
+    """proj/tests/test_structured.cpp:177-240 on the device operator (OLS per block, annihilation)."""
+    p = synth.random_sur(3, 40, [2, 5, 3], seed=51)
+    op = api.sur_preconditioner(api.sur_from_problem(p))
+    assert op.counters().factorizations == 3
+    xi = np.random.default_rng(1).standard_normal(p.m)
+    est, res = op.apply_xstar_t(xi), op.apply_pi(xi)
+    off = 0
+    for i in range(p.G):
+        Xi = p.X[:, off:off + p.nb[i]]
+        xi_i = xi[i * p.M:(i + 1) * p.M]
+        b = np.linalg.lstsq(Xi, xi_i, rcond=None)[0]
+        assert rel(est[off:off + p.nb[i]], b) < 1e-10
+        assert rel(res[i * p.M:(i + 1) * p.M], xi_i - Xi @ b) < 1e-10
+        off += p.nb[i]
+    in_range = np.concatenate([p.X[:, sum(p.nb[:i]):sum(p.nb[:i + 1])] @ np.ones(p.nb[i]) for i in range(p.G)])
+    assert np.linalg.norm(op.apply_pi(in_range)) <= 1e-10 * np.linalg.norm(in_range)
+    # X' X* v = v
+    v = np.random.default_rng(2).standard_normal(p.n)
+    xs = op.apply_xstar(v)
+    xt = np.concatenate([p.X[:, sum(p.nb[:i]):sum(p.nb[:i + 1])].T @ xs[i * p.M:(i + 1) * p.M] for i in range(p.G)])
+    assert rel(xt, v) < 1e-10
+
+
+@pytest.mark.parametrize("shape", [(3, 5000, [7, 32, 33]), (2, 20000, [100, 16]), (2, 3000, [200, 1]),
+                                   (4, 130, [64, 65, 128, 2])])
+def test_tsqr_factors(shape):
+    """The TSQR tree: Q'Q = I, Q R = X_b, R upper, |diag R| = the reference Householder's |R_kk|."""
+    G, M, nb = shape
+    p = synth.random_sur(G, M, nb, seed=77)
+    op = api.sur_preconditioner(api.sur_from_problem(p))
+    Q, R = op.factors()
+    Qo, Ro = oracle.sur_setup(p)
+    off = roff = 0
+    for i, k in enumerate(nb):
+        Qi, Ri = Q[:, off:off + k], R[roff:roff + k * k].reshape(k, k, order="F")
+        assert np.max(np.abs(Qi.T @ Qi - np.eye(k))) < 1e-13
+        assert np.allclose(np.tril(Ri, -1), 0.0)
+        Xi = p.X[:, off:off + k]
+        assert np.linalg.norm(Qi @ Ri - Xi) <= 1e-13 * np.linalg.norm(Xi)
+        Roi = Ro[roff:roff + k * k].reshape(k, k, order="F")
+        assert np.allclose(np.abs(np.diag(Ri)), np.abs(np.diag(Roi)), rtol=1e-11)
+        off += k
+        roff += k * k
+
+
+def test_error_paths():
+    p = synth.random_sur(3, 10, [2, 3, 2], seed=8)
+    X = p.X.copy(order="F")
+    X[:, 3] = X[:, 2]  # block 1 rank deficient
+    with pytest.raises(api.RankDeficient, match="block 1"):
+        api.sur_preconditioner(api.SurModel(X, p.nb, p.Y, p.omega))
+    with pytest.raises(api.SingularD):
+        api.sur_preconditioner(api.sur_from_problem(p), block_scale=np.array([1.0, -1.0, 1.0]))
+    q = synth.random_sur(2, 5, [2, 6], seed=9)  # M < n_1
+    with pytest.raises(api.DimensionMismatch):
+        api.sur_preconditioner(api.sur_from_problem(q))
+    op = api.sur_preconditioner(api.sur_from_problem(p))
+    with pytest.raises(api.DimensionMismatch):
+        op.apply_pi(np.zeros(3))
+
+
+def test_determinism_and_knob_invariance():
+    """Fixed reduction trees: bitwise reproducible; trace diagnostics do not touch the iterates."""
+    p = synth.make_problem(1, M=300, G=20)
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur)
+    runs = [api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=1e-12, diag_every=d, graph_chunk=c))
+            for d, c in ((1, 0), (1, 0), (0, 3), (-1, 7))]
+    for r in runs[1:]:
+        assert r.solution.iterations == runs[0].solution.iterations
+        assert np.array_equal(r.solution.b, runs[0].solution.b)
+        assert np.array_equal(r.trace.rows["c"], runs[0].trace.rows["c"])
+
+
+def test_counters_match_reference():
+    """CostCounters after pcg_aug equal the reference's own tallies (preconditioner.cpp:9-47)."""
+    if not oracle.have("ref"):
+        pytest.skip("oracle/_ref not shipped")
+    # tol 1e-8: both runs stop on the threshold, well above the roundoff floor, so the iteration
+    # counts (and with them the apply tallies) are the same
+    for p in (synth.random_sur(3, 12, [2, 3, 2], seed=11), synth.random_sur(5, 30, [4, 4, 6, 3, 5], seed=15)):
+        r = oracle.solve(p, "ref", cfg=oracle.make_config(tol_rel=1e-8), beta_true=p.beta)
+        op = api.sur_preconditioner(api.sur_from_problem(p))
+        g = api.pcg_aug(api.sur_from_problem(p), op, config=api.PcgConfig(tol_rel=1e-8))
+        assert g.solution.iterations == r.iterations
+        c = op.counters()
+        got = [c.factorizations, c.factor_multiplies, c.pi_applies, c.xstar_t_applies, c.xstar_applies,
+               c.apply_multiplies]
+        assert got == [int(v) for v in r.counters]
+
+
+def test_trace_diagnostics_every_row():
+    """diag_every = 1: every trace column as the reference computes it (pcg.cpp:104-116)."""
+    p = synth.make_problem(0, M=300)
+    o, g, _ = solve_both(p, diag=1)
+    assert g.solution.iterations == o.iterations
+    tg, to = g.trace.rows, o.trace
+    assert np.array_equal(tg["iter"], to["iter"])
+    big = to["aug_residual_norm"] > 1e-6 * to["aug_residual_norm"][0]
+    assert np.allclose(tg["aug_residual_norm"][big], to["aug_residual_norm"][big], rtol=1e-7)
+    assert np.allclose(tg["rmse"], to["rmse"], rtol=1e-7, equal_nan=True)
+    # X'w vanishes on every iterate (dual feasibility), to roundoff
+    assert np.all(tg["dual_feas_norm"] <= 1e-9 * np.linalg.norm(p.Y))
+    assert np.all(np.diff(tg["elapsed_ns"]) >= 0)
