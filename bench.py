@@ -216,23 +216,31 @@ def run_ours(args):
     max_iter = meta["max_iter"]
     tol = meta["tol"]
 
-    # ---- synthetic inputs generated on the device (counter-based Philox normals; BASELINE distributions)
+    # ---- synthetic inputs generated on the device (counter-based Philox normals; BASELINE distributions);
+    # with N ranks each rank draws its own row shard of the SAME global matrices
     if prob.name.startswith("c3"):
         raise SystemExit("bench: config 3 uses host generation; run config 4 (the bench workload)")
-    X = torch.empty((n, M), dtype=torch.float64, device=f"cuda:{dev}")   # column-major M x n, ld = M
-    Y = torch.empty((G, M), dtype=torch.float64, device=f"cuda:{dev}")
-    rc = lib.glsgpu_synth_normal(C.c_void_p(X.data_ptr()), M, n, M, seed, 0, dev)
+    row0, Ml = api.row_partition(M, world, rank) if world > 1 else (0, M)
+    X = torch.empty((n, Ml), dtype=torch.float64, device=f"cuda:{dev}")   # column-major Ml x n, ld = Ml
+    Y = torch.empty((G, Ml), dtype=torch.float64, device=f"cuda:{dev}")
+    rc = lib.glsgpu_synth_normal(C.c_void_p(X.data_ptr()), Ml, n, Ml, row0, M, seed, 0, dev)
     assert rc == 0, lib.glsgpu_last_error_message()
     beta = synth._rng(seed, 1).standard_normal(n)
     omega = prob.omega
     oh = synth.omega_half(omega)
-    rc = lib.glsgpu_synth_response(G, M, nb.ctypes.data_as(C.POINTER(C.c_int64)), C.c_void_p(X.data_ptr()), M,
-                                   beta.ctypes.data_as(C.POINTER(C.c_double)), oh.ctypes.data_as(C.POINTER(C.c_double)),
-                                   seed, C.c_void_p(Y.data_ptr()), M, dev)
+    rc = lib.glsgpu_synth_response(G, Ml, row0, M, nb.ctypes.data_as(C.POINTER(C.c_int64)), C.c_void_p(X.data_ptr()),
+                                   Ml, beta.ctypes.data_as(C.POINTER(C.c_double)),
+                                   oh.ctypes.data_as(C.POINTER(C.c_double)), seed, C.c_void_p(Y.data_ptr()), Ml, dev)
     assert rc == 0, lib.glsgpu_last_error_message()
     torch.cuda.synchronize()
 
-    op = api.GpuSurPreconditioner.from_device(G, M, nb, X.data_ptr(), M, Y.data_ptr(), M, omega, device=dev)
+    if world > 1:
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        op = api.GpuSurPreconditioner.from_device_sharded(G, Ml, M, nb, X.data_ptr(), Ml, Y.data_ptr(), Ml, omega,
+                                                          obj[0], rank, world, device=dev)
+    else:
+        op = api.GpuSurPreconditioner.from_device(G, M, nb, X.data_ptr(), M, Y.data_ptr(), M, omega, device=dev)
     cfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv, diag_every=0, kernel_timing=False)
     stream = torch.cuda.ExternalStream(op.stream_ptr(), device=f"cuda:{dev}")
 
@@ -302,33 +310,52 @@ def run_ours(args):
 
     # ---- e2e through the C-ABI with host buffers (pinned X, Y -> device every step; b -> host)
     e2e = None
-    if not args.no_e2e and world == 1:
-        Xh = torch.empty((n, M), dtype=torch.float64, pin_memory=True)
-        Yh = torch.empty((G, M), dtype=torch.float64, pin_memory=True)
+    if not args.no_e2e:
+        Xh = torch.empty((n, Ml), dtype=torch.float64, pin_memory=True)
+        Yh = torch.empty((G, Ml), dtype=torch.float64, pin_memory=True)
         Xh.copy_(X)
         Yh.copy_(Y)
         torch.cuda.synchronize()
         op.close()
         del X, Y, op
         torch.cuda.empty_cache()
-        sur = api.SurModel(X=Xh.numpy().T, nb=nb, y=Yh.numpy().T, sigma0=omega)
         e_iters, e_time = 0, 0.0
         ksteps = max(1, min(args.steps, 2))
+        ecfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv, diag_every=0)
         for s in range(ksteps + 1):
+            if world > 1:
+                obj = [api.nccl_unique_id() if rank == 0 else None]
+                torch.distributed.broadcast_object_list(obj, src=0)
+                torch.distributed.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            op2 = api.GpuSurPreconditioner(sur, device=dev)
-            r2 = api.pcg_aug(sur, op2, config=api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv,
-                                                             diag_every=0), want_w=False)
-            op2.close()
+            if world > 1:
+                # the C-ABI's sharded entry takes device buffers: this rank's host shard goes in first
+                Xd = Xh.to(f"cuda:{dev}", non_blocking=True)
+                Yd = Yh.to(f"cuda:{dev}", non_blocking=True)
+                torch.cuda.synchronize()
+                op2 = api.GpuSurPreconditioner.from_device_sharded(G, Ml, M, nb, Xd.data_ptr(), Ml, Yd.data_ptr(), Ml,
+                                                                   omega, obj[0], rank, world, device=dev)
+                r2 = api.pcg_aug(None, op2, config=ecfg, want_w=False)
+                op2.close()
+                del Xd, Yd
+            else:
+                sur = api.SurModel(X=Xh.numpy().T, nb=nb, y=Yh.numpy().T, sigma0=omega)
+                op2 = api.GpuSurPreconditioner(sur, device=dev)
+                r2 = api.pcg_aug(sur, op2, config=ecfg, want_w=False)
+                op2.close()
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([dt], device=f"cuda:{dev}")
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                dt = float(t.item())
             if s > 0:  # first e2e step is a warm-up (allocator / context)
                 e_iters += r2.solution.iterations
                 e_time += dt
         e2e = {"value": e_iters / e_time, "unit": UNIT, "h2d_bytes_per_step": int(8 * (M * n + M * G)),
                "d2h_bytes_per_step": int(8 * n + 48 * (r2.trace.rows.size)), "steps": ksteps,
-               "timer": "host wall clock around create(H2D + QR) + solve + b D2H + destroy"}
+               "timer": "host wall clock (max over ranks) around create(H2D + QR) + solve + b D2H + destroy"}
         del Xh, Yh
 
     cpu = None

@@ -167,15 +167,31 @@ int glsgpu_kernel_stats(const glsgpu_sur* h, glsgpu_kernel_stat* out, int cap);
 /* Kernels this handle has launched so far (CUDA-graph kernel nodes counted per graph launch). */
 int glsgpu_launch_count(const glsgpu_sur* h, int64_t* count);
 
+/* Row sharding over several GPUs (one process per GPU) ------------------------
+ * Rank r owns rows [row0_r, row0_r + M_local) of every block (any contiguous split; each rank needs
+ * at least max n_i rows); Omega, R and every n-vector are replicated.  Per PCG iteration the ranks
+ * all-gather three small partial-sum vectors over NCCL (d, u.u | Q'r per block | c, r.r, pr.pr) and
+ * reduce them in rank order, so every rank takes bitwise the same decisions.  The setup QR is a
+ * TSQR across ranks (all-gather of the per-rank R factors).  Host vectors passed to the probe
+ * applies / solve of a sharded handle are the rank's local rows; b is replicated. */
+int glsgpu_nccl_unique_id(void* id_out /* 128 bytes (ncclUniqueId) */);
+int glsgpu_sur_create_sharded(int G, int64_t M_local, int64_t M_global, const int64_t* n_i, const double* X_dev,
+                              int64_t ldx, const double* Y_dev, int64_t ldy, const double* omega,
+                              const double* block_scale, int device, const void* nccl_id, int rank, int nranks,
+                              glsgpu_sur** out, int* bad_block);
+int glsgpu_sur_shard(const glsgpu_sur* h, int* rank, int* nranks, int64_t* M_global);
+
 /* Test / bench helpers (not part of the reference surface) ---------------------------------- */
 /* Copy Q (M x n, ld M) and the concatenated R blocks to host. */
 int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R);
-/* Fill count doubles of device memory with N(0,1) draws of the counter-based stream (seed, stream). */
-int glsgpu_synth_normal(double* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t stream,
-                        int device);
-/* Device-side y_b = X_b beta_b + (Z Omega_half)_b for synthetic inputs (Z drawn from stream 3). */
-int glsgpu_synth_response(int G, int64_t M, const int64_t* n_i, const double* X_dev, int64_t ldx,
-                          const double* beta, const double* omega_half, uint64_t seed, double* Y_dev,
+/* Rows [row0, row0 + rows) of a rows_total x cols matrix of N(0,1) draws from the counter-based
+ * Philox stream (seed, stream), into device memory with leading dimension ld: every row sharding of
+ * the same matrix draws identical values. */
+int glsgpu_synth_normal(double* dev, int64_t rows, int64_t cols, int64_t ld, int64_t row0, int64_t rows_total,
+                        uint64_t seed, uint64_t stream, int device);
+/* Device-side y_b = X_b beta_b + (Z Omega_half)_b for rows [row0, row0 + M) of M_total (Z: stream 3). */
+int glsgpu_synth_response(int G, int64_t M, int64_t row0, int64_t M_total, const int64_t* n_i, const double* X_dev,
+                          int64_t ldx, const double* beta, const double* omega_half, uint64_t seed, double* Y_dev,
                           int64_t ldy, int device);
 
 #ifdef __cplusplus

@@ -50,7 +50,7 @@ EXPORTS = [
     "glsgpu_apply_pi", "glsgpu_apply_xstar_t", "glsgpu_apply_xstar", "glsgpu_sigma_apply",
     "glsgpu_operator_norm_probe", "glsgpu_counters", "glsgpu_reset_apply_counters", "glsgpu_sur_solve",
     "glsgpu_default_config", "glsgpu_kernel_stats", "glsgpu_launch_count", "glsgpu_get_factors", "glsgpu_synth_normal",
-    "glsgpu_synth_response",
+    "glsgpu_synth_response", "glsgpu_nccl_unique_id", "glsgpu_sur_create_sharded", "glsgpu_sur_shard",
 ]
 
 _lib = None
@@ -89,8 +89,14 @@ def load() -> C.CDLL:
     L.glsgpu_kernel_stats.argtypes = [H, C.POINTER(KernelStatC), C.c_int]
     L.glsgpu_launch_count.argtypes = [H, _PI64]
     L.glsgpu_get_factors.argtypes = [H, _P, _P]
-    L.glsgpu_synth_normal.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int]
-    L.glsgpu_synth_response.argtypes = [C.c_int, C.c_int64, _PI64, C.c_void_p, C.c_int64, _P, _P, C.c_uint64,
-                                        C.c_void_p, C.c_int64, C.c_int]
+    L.glsgpu_synth_normal.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
+                                      C.c_uint64, C.c_int]
+    L.glsgpu_synth_response.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, _PI64, C.c_void_p, C.c_int64, _P, _P,
+                                        C.c_uint64, C.c_void_p, C.c_int64, C.c_int]
+    L.glsgpu_nccl_unique_id.argtypes = [C.c_void_p]
+    L.glsgpu_sur_create_sharded.argtypes = [C.c_int, C.c_int64, C.c_int64, _PI64, C.c_void_p, C.c_int64, C.c_void_p,
+                                            C.c_int64, _P, _P, C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(H),
+                                            C.POINTER(C.c_int)]
+    L.glsgpu_sur_shard.argtypes = [H, C.POINTER(C.c_int), C.POINTER(C.c_int), _PI64]
     _lib = L
     return L

@@ -246,6 +246,29 @@ class GpuSurPreconditioner:
         self.n = int(self._nb.sum())
         return self
 
+    @classmethod
+    def from_device_sharded(cls, G: int, M_local: int, M_global: int, nb, X_ptr: int, ldx: int, Y_ptr: int, ldy: int,
+                            omega: np.ndarray, nccl_id: bytes, rank: int, nranks: int, block_scale=None,
+                            device: int = 0) -> "GpuSurPreconditioner":
+        """Row-sharded operator: this rank owns M_local of the M_global rows of every block."""
+        self = cls.__new__(cls)
+        self._lib = L.load()
+        self.sur = None
+        self._h = C.c_void_p()
+        self._nb = np.ascontiguousarray(nb, dtype=np.int64)
+        bad = C.c_int(-1)
+        om = np.asfortranarray(omega, dtype=np.float64)
+        scale = None if block_scale is None else np.ascontiguousarray(block_scale, dtype=np.float64)
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        code = self._lib.glsgpu_sur_create_sharded(G, M_local, M_global, self._nb.ctypes.data_as(_PI64),
+                                                   C.c_void_p(X_ptr), ldx, C.c_void_p(Y_ptr), ldy, _dp(om), _dp(scale),
+                                                   device, idbuf, rank, nranks, C.byref(self._h), C.byref(bad))
+        self.bad_block = bad.value
+        _check(code, self._lib)
+        self.m = M_local * G      # host vectors of a sharded handle are the rank's local rows
+        self.n = int(self._nb.sum())
+        return self
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             self._lib.glsgpu_sur_destroy(self._h)
@@ -378,6 +401,24 @@ def pcg_aug(sur_or_op, precond: Optional[GpuSurPreconditioner] = None, w1=None, 
                      breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
                      w1_projected=bool(res.w1_projected))
     return AugSolveResult(solution=sol, trace=trace, sigma_scale=float(res.sigma_scale), solve_ms=float(res.solve_ms))
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 creates it; the ranks share it over torch.distributed)."""
+    lib = L.load()
+    buf = C.create_string_buffer(128)
+    _check(lib.glsgpu_nccl_unique_id(buf), lib)
+    return buf.raw
+
+
+def row_partition(M: int, nranks: int, rank: int, align: int = 32):
+    """Contiguous row shard of rank r: [row0, row0 + rows), 32-row aligned boundaries (last takes the rest)."""
+    base = (M // nranks) // align * align
+    if base == 0:
+        base = M // nranks
+    row0 = rank * base
+    rows = (M - row0) if rank == nranks - 1 else base
+    return row0, rows
 
 
 def device_count() -> int:

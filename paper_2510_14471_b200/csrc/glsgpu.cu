@@ -7,6 +7,8 @@
 // control in single-CTA kernels between them, captured into CUDA graphs of `graph_chunk`
 // iterations; the host only checks the device's `active` flag between graph launches.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -54,9 +56,42 @@ T* dalloc(size_t count) {
 
 constexpr int64_t QR_SMEM_BYTES = 200 * 1024;
 
-struct Timer {
-  cudaEvent_t a{}, b{};
+// NCCL, resolved at run time: single-device use never needs it; row-sharded handles all-gather the
+// per-rank partial sums over NVLink (dlopen of the libnccl.so.2 torch or the system already provides).
+struct Nccl {
+  void* so = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
+
+Nccl& nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    n.so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!n.so) n.so = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (n.so) {
+      n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.so, "ncclGetUniqueId");
+      n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.so, "ncclCommInitRank");
+      n.AllGather = (decltype(n.AllGather))dlsym(n.so, "ncclAllGather");
+      n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.so, "ncclCommDestroy");
+      n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.so, "ncclGetErrorString");
+    }
+  }
+  if (!n.GetUniqueId || !n.CommInitRank || !n.AllGather || !n.CommDestroy)
+    fail(GLSGPU_ERR_NCCL, "glsgpu: libnccl.so.2 not loadable (needed for row-sharded handles)");
+  return n;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return;
+  const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
+  fail(GLSGPU_ERR_NCCL, std::string(what) + ": " + s);
+}
 
 }  // namespace
 
@@ -82,10 +117,11 @@ struct glsgpu_sur {
   std::vector<double> omega_h;
   // TSQR plan
   struct Level {
-    int64_t first, count;  // item range
+    int64_t first, count;  // generic item range (k_qr_factor / k_qr_formq)
     int smem_bytes;
     int64_t max_rows;
     bool any_global;
+    int64_t ffirst = 0, fcount = 0;  // register-resident item range (n <= 32, rows <= 256)
   };
   std::vector<Level> qr_levels;
   QrItem* d_items = nullptr;
@@ -121,6 +157,18 @@ struct glsgpu_sur {
   int64_t graph_kernels = 0;     // kernel nodes in the instantiated graph
   int64_t launches = 0;          // kernels launched by this handle (graph nodes counted per launch)
   bool capturing = false;
+  // row sharding: this rank owns rows [row0, row0 + M) of M_global; Omega, R, n-vectors replicated
+  int rank = 0, nranks = 1;
+  bool coll = false;  // collective path (NCCL all-gathers, cross-rank TSQR level); also nranks == 1 + id
+  int64_t M_global = 0;
+  ncclComm_t comm = nullptr;
+  double *loc3 = nullptr, *all3 = nullptr, *t_loc = nullptr, *t_all = nullptr;
+  double *rloc = nullptr, *rall = nullptr, *rstack = nullptr, *gtau = nullptr;  // TSQR across ranks
+  int64_t* d_stack_off = nullptr;
+  std::vector<QrItem> gitems;  // the cross-rank level (one item per block)
+  QrItem* d_gitems = nullptr;
+  int gsmem = 0;
+  int64_t gmax_rows = 0;
 };
 
 namespace {
@@ -231,6 +279,46 @@ ColArgs base_args(glsgpu_sur* h) {
   return a;
 }
 
+// ------------------------------------------------------------------------------------------ ranks
+void allgather(glsgpu_sur* h, const double* send, double* recv, size_t count) {
+  nccl_check(nccl().AllGather(send, recv, count, ncclFloat64, h->comm, h->s), "ncclAllGather");
+}
+
+// CTA partials (count x 3) -> (pointer, rows) that a scalar kernel sums in fixed order: the partials
+// themselves on one rank; on several, every rank's local sum all-gathered in rank order, so every
+// rank computes bitwise the same scalars and takes the same termination decisions.
+std::pair<const double*, int> combine3(glsgpu_sur* h, const double* partials, int count) {
+  if (!h->coll) return {partials, count};
+  k_reduce3<<<1, NT, 0, h->s>>>(partials, count, h->loc3);
+  if (!h->capturing) h->launches++;
+  CKL("k_reduce3");
+  allgather(h, h->loc3, h->all3, 3);
+  return {h->all3, h->nranks};
+}
+
+std::pair<const double*, int> combine1(glsgpu_sur* h, const double* partials, int count) {
+  if (!h->coll) return {partials, count};
+  k_sum1<<<1, NT, 0, h->s>>>(partials, count, h->loc3);
+  if (!h->capturing) h->launches++;
+  CKL("k_sum1");
+  allgather(h, h->loc3, h->all3, 1);
+  return {h->all3, h->nranks};
+}
+
+// tpart -> out[n], summed over chunks and then over ranks (gate as k_reduce_t).
+void reduce_t_global(glsgpu_sur* h, double* out, const SolveState* st, int gate) {
+  if (!h->coll) {
+    launch_reduce_t(h, out, st, gate);
+    return;
+  }
+  launch_reduce_t(h, h->t_loc, st, gate);
+  allgather(h, h->t_loc, h->t_all, (size_t)h->n);
+  k_sum_ranks<<<(unsigned)std::min<int64_t>((h->n + NT - 1) / NT, 148), NT, 0, h->s>>>(h->t_all, h->nranks, h->n,
+                                                                                       out, st, gate);
+  if (!h->capturing) h->launches++;
+  CKL("k_sum_ranks");
+}
+
 // ------------------------------------------------------------------------------------------ setup
 void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const double* block_scale) {
   h->G = G;
@@ -277,7 +365,7 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
   // pass cost model of finalize() (structured.cpp:296-305)
   h->pi_cost = h->xstar_t_cost = h->xstar_cost = 0;
   for (int b = 0; b < G; ++b) {
-    const uint64_t rr = (uint64_t)M, nn = (uint64_t)h->nb[b];
+    const uint64_t rr = (uint64_t)h->M_global, nn = (uint64_t)h->nb[b];
     h->pi_cost += 2 * rr * nn + 2 * rr;
     h->xstar_t_cost += rr * nn + nn * (nn + 1) / 2 + rr;
     h->xstar_cost += rr * nn + nn * (nn + 1) / 2 + rr;
@@ -286,7 +374,11 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
   h->counters.factorizations = (uint64_t)G;
 }
 
+bool qr_fast(int n, int64_t rows) { return n <= 32 && rows <= QRR_NT; }
+
 int64_t qr_leaf_rows(int n) {
+  // narrow blocks: 256-row chunks, one row per thread in registers (k_qr_factor_reg / k_qr_formq_reg)
+  if (n <= 32) return QRR_NT;
   // panel rows per chunk: the panel (rows x n doubles) in <= 200 KB of shared memory when possible,
   // at least 2n rows, at most 1024 (the register column of k_qr_formq).
   int64_t L = (QR_SMEM_BYTES / 8) / n;
@@ -332,7 +424,9 @@ void build_qr_plan(glsgpu_sur* h) {
   int64_t slot = 0;
   bool any_global = false;
   for (int lvl = 0; lvl <= depth_max; ++lvl) {
-    glsgpu_sur::Level L{(int64_t)items.size(), 0, 0, 0, false};
+    glsgpu_sur::Level L{0, 0, 0, 0, false};
+    std::vector<QrItem> fast;
+    const int64_t first = (int64_t)items.size();
     for (int b = 0; b < h->G; ++b) {
       const BT& t = trees[b];
       if ((int)t.rows.size() <= lvl) continue;
@@ -364,7 +458,13 @@ void build_qr_plan(glsgpu_sur* h) {
           it.ldr = rows;
         }
         it.tau = h->qr_tau + t.tau_off[lvl] + c * n;
-        if (top) {
+        if (top && h->coll) {
+          // this rank's R goes to the cross-rank level; its C slice comes back from that level's Q
+          it.rout = h->rloc + h->r0[b];
+          it.ldo = n;
+          it.qpar = h->rstack + (int64_t)h->nranks * h->r0[b] + (int64_t)h->rank * n;
+          it.ldp = (int64_t)h->nranks * n;
+        } else if (top) {
           it.rout = h->R + h->r0[b];
           it.ldo = n;
           it.qpar = nullptr;
@@ -374,6 +474,10 @@ void build_qr_plan(glsgpu_sur* h) {
           it.ldo = rows_next;
           it.qpar = store_next + c * n;
           it.ldp = rows_next;
+        }
+        if (qr_fast(n, it.rows)) {
+          fast.push_back(it);
+          continue;
         }
         const int64_t bytes = it.rows * n * (int64_t)sizeof(double);
         it.smem = bytes <= QR_SMEM_BYTES ? 1 : 0;
@@ -387,49 +491,122 @@ void build_qr_plan(glsgpu_sur* h) {
         items.push_back(it);
       }
     }
-    L.count = (int64_t)items.size() - L.first;
+    L.first = first;
+    L.count = (int64_t)items.size() - first;
+    L.ffirst = (int64_t)items.size();
+    L.fcount = (int64_t)fast.size();
+    items.insert(items.end(), fast.begin(), fast.end());
     h->qr_levels.push_back(L);
   }
   h->d_items = dalloc<QrItem>(items.size());
   CK(cudaMemcpy(h->d_items, items.data(), sizeof(QrItem) * items.size(), cudaMemcpyHostToDevice));
   h->qr_slot = slot;
-  if (any_global) h->qr_scratch = dalloc<double>((size_t)slot * 2 * 148);
+  // cross-rank TSQR level: per block, one chunk = the stacked per-rank R's [R_0; ...; R_{P-1}]
+  if (h->coll) {
+    h->gitems.clear();
+    h->gsmem = 0;
+    h->gmax_rows = 0;
+    std::vector<int64_t> soff(h->G);
+    for (int b = 0; b < h->G; ++b) {
+      const int n = h->nb[b];
+      QrItem it;
+      std::memset(&it, 0, sizeof(it));
+      soff[b] = (int64_t)h->nranks * h->r0[b];
+      it.src = it.refl = h->rstack + soff[b];
+      it.lds = it.ldr = (int64_t)h->nranks * n;
+      it.r0 = 0;
+      it.rows = it.valid = (int64_t)h->nranks * n;
+      it.scale = 1.0;
+      it.tau = h->gtau + h->p0[b];
+      it.rout = h->R + h->r0[b];
+      it.ldo = n;
+      it.n = n;
+      const int64_t bytes = it.rows * n * (int64_t)sizeof(double);
+      it.smem = bytes <= QR_SMEM_BYTES ? 1 : 0;
+      if (it.smem) h->gsmem = std::max<int>(h->gsmem, (int)bytes);
+      else {
+        any_global = true;
+        slot = std::max<int64_t>(slot, it.rows * n);
+      }
+      h->gmax_rows = std::max<int64_t>(h->gmax_rows, it.rows);
+      h->gitems.push_back(it);
+    }
+    h->qr_slot = slot;
+    h->d_gitems = dalloc<QrItem>(h->gitems.size());
+    CK(cudaMemcpy(h->d_gitems, h->gitems.data(), sizeof(QrItem) * h->gitems.size(), cudaMemcpyHostToDevice));
+    h->d_stack_off = dalloc<int64_t>(h->G);
+    CK(cudaMemcpy(h->d_stack_off, soff.data(), sizeof(int64_t) * h->G, cudaMemcpyHostToDevice));
+  }
+  if (any_global) h->qr_scratch = dalloc<double>((size_t)h->qr_slot * 2 * 148);
   h->d_rank_flags = dalloc<int>(h->G);
 }
 
-void run_qr(glsgpu_sur* h) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    CK(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
-    CK(cudaFuncSetAttribute(k_qr_formq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
-    CK(cudaFuncSetAttribute(k_qr_formq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
-    CK(cudaFuncSetAttribute(k_qr_formq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
-    attr_done = true;
+void launch_formq(glsgpu_sur* h, int64_t max_rows, int grid, int smem, const QrItem* items, int count) {
+  if (max_rows <= 256) {
+    k_qr_formq<8><<<grid, QR_NT, smem, h->s>>>(items, count, h->qr_scratch, h->qr_slot);
+  } else if (max_rows <= 512) {
+    k_qr_formq<16><<<grid, QR_NT, smem, h->s>>>(items, count, h->qr_scratch, h->qr_slot);
+  } else {
+    k_qr_formq<32><<<grid, QR_NT, smem, h->s>>>(items, count, h->qr_scratch, h->qr_slot);
   }
+  if (!h->capturing) h->launches++;
+  CKL("k_qr_formq");
+}
+
+void run_qr(glsgpu_sur* h) {
+  CK(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
+  CK(cudaFuncSetAttribute(k_qr_formq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
+  CK(cudaFuncSetAttribute(k_qr_formq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
+  CK(cudaFuncSetAttribute(k_qr_formq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
   // zero Q (its padding rows stay zero) -- the level-0 reflectors overwrite the rest
   CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)(h->ldm * h->n), h->s));
   const int nl = (int)h->qr_levels.size();
+  CK(cudaFuncSetAttribute(k_qr_formq_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, QRR_NT * 32 * 8));
+  const int fgrid_cap = 2 * 148;  // register-resident leaves: 1-2 CTAs per SM
   for (int l = 0; l < nl; ++l) {
     const auto& L = h->qr_levels[l];
-    const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
-    k_qr_factor<<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch, h->qr_slot);
+    if (L.count) {
+      const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
+      k_qr_factor<<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch,
+                                                      h->qr_slot);
+      if (!h->capturing) h->launches++;
+      CKL("k_qr_factor");
+    }
+    if (L.fcount) {
+      k_qr_factor_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, 0, h->s>>>(h->d_items + L.ffirst,
+                                                                                           (int)L.fcount);
+      if (!h->capturing) h->launches++;
+      CKL("k_qr_factor_reg");
+    }
+  }
+  if (h->coll) {
+    // TSQR across ranks: gather every rank's top R, factor the stacks (redundantly, identically on
+    // every rank), form their explicit Q; each rank's C slice then seeds its local top level
+    int64_t rtot = 0;
+    for (int b = 0; b < h->G; ++b) rtot += (int64_t)h->nb[b] * h->nb[b];
+    allgather(h, h->rloc, h->rall, (size_t)rtot);
+    int64_t* d_r0 = h->d_r0;
+    k_stack_r<<<h->G, 256, 0, h->s>>>(h->rall, h->nranks, rtot, h->G, h->d_nb, d_r0, h->d_stack_off, h->rstack);
     if (!h->capturing) h->launches++;
-    CKL("k_qr_factor");
+    CKL("k_stack_r");
+    const int grid = (int)std::min<int64_t>(h->G, 2 * 148);
+    k_qr_factor<<<grid, QR_NT, h->gsmem, h->s>>>(h->d_gitems, h->G, h->qr_scratch, h->qr_slot);
+    if (!h->capturing) h->launches++;
+    CKL("k_qr_factor ranks");
+    launch_formq(h, h->gmax_rows, grid, h->gsmem, h->d_gitems, h->G);
   }
   for (int l = nl - 1; l >= 0; --l) {
     const auto& L = h->qr_levels[l];
-    const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
-    if (L.max_rows <= 256) {
-      k_qr_formq<8><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch, h->qr_slot);
-    } else if (L.max_rows <= 512) {
-      k_qr_formq<16><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch,
-                                                           h->qr_slot);
-    } else {
-      k_qr_formq<32><<<grid, QR_NT, L.smem_bytes, h->s>>>(h->d_items + L.first, (int)L.count, h->qr_scratch,
-                                                           h->qr_slot);
+    if (L.count) {
+      const int grid = (int)std::min<int64_t>(L.count, L.any_global ? 2 * 148 : 8 * 148);
+      launch_formq(h, L.max_rows, grid, L.smem_bytes, h->d_items + L.first, (int)L.count);
     }
-    if (!h->capturing) h->launches++;
-    CKL("k_qr_formq");
+    if (L.fcount) {
+      k_qr_formq_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, QRR_NT * 32 * 8, h->s>>>(
+          h->d_items + L.ffirst, (int)L.fcount);
+      if (!h->capturing) h->launches++;
+      CKL("k_qr_formq_reg");
+    }
   }
   Geo g = geo_of(h);
   k_rank_check<<<(h->G + 127) / 128, 128, 0, h->s>>>(g, h->R, h->d_rank_flags);
@@ -473,6 +650,19 @@ void alloc_common(glsgpu_sur* h) {
   int64_t rtot = 0;
   for (int b = 0; b < h->G; ++b) rtot += (int64_t)h->nb[b] * h->nb[b];
   h->R = dalloc<double>((size_t)rtot);
+  if (h->coll) {
+    const int P = h->nranks;
+    if ((int64_t)P * h->nmax > 1024)
+      fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: nranks * max n_i > 1024 (cross-rank TSQR level)");
+    h->rloc = dalloc<double>((size_t)rtot);
+    h->rall = dalloc<double>((size_t)rtot * P);
+    h->rstack = dalloc<double>((size_t)rtot * P);
+    h->gtau = dalloc<double>((size_t)h->n);
+    h->loc3 = dalloc<double>(4);
+    h->all3 = dalloc<double>((size_t)4 * P);
+    h->t_loc = dalloc<double>((size_t)h->n);
+    h->t_all = dalloc<double>((size_t)h->n * P);
+  }
   build_qr_plan(h);
 }
 
@@ -486,17 +676,27 @@ void destroy_impl(glsgpu_sur* h) {
                   h->qr_store, h->qr_tau, h->qr_scratch, h->d_rank_flags, h->d_blk_narrow, h->d_blk_wide,
                   h->wb[0], h->wb[1], h->wb[2], h->swb[0], h->swb[1], h->swb[2], h->r, h->u, h->su, h->pr, h->t,
                   h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,
-                  h->scal, h->d_stop, h->st, h->rows_d};
+                  h->scal, h->d_stop, h->st, h->rows_d, h->loc3, h->all3, h->t_loc, h->t_all, h->rloc, h->rall,
+                  h->rstack, h->gtau, h->d_stack_off, h->d_gitems};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->st_host) cudaFreeHost(h->st_host);
+  if (h->comm) nccl().CommDestroy(h->comm);
   if (h->s) cudaStreamDestroy(h->s);
   delete h;
 }
 
 glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* omega, const double* block_scale,
-                          int device) {
-  validate(G, M, n_i, block_scale, omega);
+                          int device, int64_t M_global = -1, int rank = 0, int nranks = 1,
+                          const void* nccl_id = nullptr) {
+  if (M_global < 0) M_global = M;
+  validate(G, M_global, n_i, block_scale, omega);
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(GLSGPU_ERR_INVALID, "glsgpu: bad rank / nranks");
+  if (nranks > 1) {
+    if (!nccl_id) fail(GLSGPU_ERR_INVALID, "glsgpu: sharded handle needs an NCCL unique id");
+    for (int b = 0; b < G; ++b)
+      if (M < n_i[b]) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "glsgpu: every rank must own at least max n_i rows", b);
+  }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {
@@ -507,8 +707,17 @@ glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* om
   CK(cudaSetDevice(device));
   glsgpu_sur* h = new glsgpu_sur();
   h->dev = device;
+  h->rank = rank;
+  h->nranks = nranks;
+  h->M_global = M_global;
+  h->coll = nranks > 1 || nccl_id != nullptr;
   try {
     CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    if (h->coll) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      nccl_check(nccl().CommInitRank(&h->comm, nranks, id, rank), "ncclCommInitRank");
+    }
     build_geometry(h, G, M, n_i, block_scale);
     upload_omega(h, omega);
   } catch (...) {
@@ -592,13 +801,13 @@ void qt_apply(glsgpu_sur* h, int mode, const double* vin, double* out, const Sol
   if (mode == MODE_QT_R) launch_colpass<MODE_QT_R>(h, a, nullptr);
   else if (mode == MODE_QT_D) launch_colpass<MODE_QT_D>(h, a, st);
   else launch_colpass<MODE_QT_V>(h, a, nullptr);
-  launch_reduce_t(h, out, nullptr, 0);
+  reduce_t_global(h, out, nullptr, 0);
 }
 
 double norm_probe(glsgpu_sur* h, int64_t iters) {
   // operator_norm_probe (pcg.cpp:233-244): v = 1/sqrt(m); repeat: v = Sigma v; nrm = |v|; v /= nrm.
   ensure_solver(h, 1);
-  const int64_t m = h->M * h->G;
+  const int64_t m = h->M_global * h->G;
   const double v0 = 1.0 / std::sqrt(static_cast<double>(m));
   // v0 in u (rows < M of each column), zero padding
   CK(cudaMemsetAsync(h->u, 0, sizeof(double) * h->ldm * h->G, h->s));
@@ -612,7 +821,8 @@ double norm_probe(glsgpu_sur* h, int64_t iters) {
   int grid = 0;
   for (int64_t it = 0; it < iters; ++it) {
     launch_kron(h, a, nullptr, h->scal, nullptr, b, h->partA, it == 0 ? 0 : 1, nullptr, &grid);
-    k_probe_step<<<1, NT, 0, h->s>>>(h->partA, grid, h->scal, h->d_stop);
+    auto pc = combine3(h, h->partA, grid);
+    k_probe_step<<<1, NT, 0, h->s>>>(pc.first, pc.second, h->scal, h->d_stop);
     if (!h->capturing) h->launches++;
     CKL("k_probe_step");
     std::swap(a, b);
@@ -666,7 +876,8 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   ev(0);
   launch_kron(h, nullptr, h->pr, nullptr, h->u, h->su, h->partA, 2, h->st, nullptr);
   ev(1);
-  k_scalar_a<<<1, NT, 0, h->s>>>(h->partA, gA, h->st);
+  const auto pa = combine3(h, h->partA, gA);
+  k_scalar_a<<<1, NT, 0, h->s>>>(pa.first, pa.second, h->st);
   if (!h->capturing) h->launches++;
   CKL("k_scalar_a");
   // pass B
@@ -677,14 +888,15 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   ev(2);
   launch_colpass<MODE_B>(h, a, h->st);
   ev(3);
-  launch_reduce_t(h, h->t, h->st, 1);
+  reduce_t_global(h, h->t, h->st, 1);
   // pass C
   ev(4);
   k_rowpass<<<gC, NT, 0, h->s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, h->st);
   if (!h->capturing) h->launches++;
   CKL("k_rowpass");
   ev(5);
-  k_scalar_c<<<1, NT, 0, h->s>>>(h->partC, gC, h->st, h->rows_d);
+  const auto pcc = combine3(h, h->partC, gC);
+  k_scalar_c<<<1, NT, 0, h->s>>>(pcc.first, pcc.second, h->st, h->rows_d);
   if (!h->capturing) h->launches++;
   CKL("k_scalar_c");
   k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, h->vs, a.xv_from_x, 0, h->st);
@@ -696,9 +908,7 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
     d.sel_best = 0;
     d.gate = 2;
     launch_colpass<MODE_QT_D>(h, d, h->st);
-    k_reduce_t<<<(unsigned)((h->n + 7) / 8), NT, 0, h->s>>>(h->tpart, h->n, h->nch, h->t2, h->st, 2);
-    if (!h->capturing) h->launches++;
-    CKL("k_reduce_t diag");
+    reduce_t_global(h, h->t2, h->st, 2);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
     if (!h->capturing) h->launches++;
     CKL("k_vupdate diag");
@@ -709,11 +919,10 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
     x.vec = h->t2;
     x.gate = 2;
     launch_colpass<MODE_DIAG>(h, x, h->st);
-    k_reduce_t<<<(unsigned)((h->n + 7) / 8), NT, 0, h->s>>>(h->tpart, h->n, h->nch, h->xtw, h->st, 2);
-    if (!h->capturing) h->launches++;
-    CKL("k_reduce_t diag2");
-    k_diag_finalize<<<1, NT, 0, h->s>>>(h->rpart, h->G * h->nch, h->xtw, h->n, h->t2, h->beta_d, h->st,
-                                        h->rows_d, -1);
+    reduce_t_global(h, h->xtw, h->st, 2);
+    const auto pr1 = combine1(h, h->rpart, h->G * h->nch);
+    k_diag_finalize<<<1, NT, 0, h->s>>>(pr1.first, pr1.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d,
+                                        -1);
     if (!h->capturing) h->launches++;
     CKL("k_diag_finalize");
   }
@@ -969,7 +1178,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   glsgpu_pcg_config cfg;
   if (cfg_in) cfg = *cfg_in;
   else glsgpu_default_config(&cfg);
-  const int64_t m = h->M * h->G;
+  const int64_t m = h->M_global * h->G;
   const int64_t max_iter = cfg.max_iter ? cfg.max_iter : (m - h->n + 1);
   const int64_t cap_d = std::max<int64_t>(1, std::min<int64_t>(max_iter + 1, rows ? std::max<int64_t>(rows_cap, 1) : 1));
   ensure_solver(h, cap_d);
@@ -1015,6 +1224,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   int w1_projected = 0;
   CK(cudaMemsetAsync(h->wb[0], 0, mvb, s));
   CK(cudaMemsetAsync(h->swb[0], 0, mvb, s));
+  if (w1 && h->coll) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: w1 on a row-sharded handle");
   if (w1) {
     h2d_mvec(h, h->wb[0], w1);
     ColArgs a = base_args(h);
@@ -1074,7 +1284,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   k_rowpass<<<gC, NT, 0, s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, nullptr);
   if (!h->capturing) h->launches++;
   CKL("k_rowpass init");
-  k_init_scalars<<<1, NT, 0, s>>>(h->partC, gC, h->st, h->rows_d);
+  const auto pi0 = combine3(h, h->partC, gC);
+  k_init_scalars<<<1, NT, 0, s>>>(pi0.first, pi0.second, h->st, h->rows_d);
   if (!h->capturing) h->launches++;
   CKL("k_init_scalars");
   // v = X*' r (X mode: R^-1 t; QR mode: s = t); u = pr
@@ -1086,7 +1297,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   if (diag >= 0) {
     ColArgs d = base_args(h);
     launch_colpass<MODE_QT_D>(h, d, h->st);
-    launch_reduce_t(h, h->t2, nullptr, 0);
+    reduce_t_global(h, h->t2, nullptr, 0);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
     if (!h->capturing) h->launches++;
     ColArgs x = base_args(h);
@@ -1095,8 +1306,9 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     x.avalid = h->M;
     x.vec = h->t2;
     launch_colpass<MODE_DIAG>(h, x, h->st);
-    launch_reduce_t(h, h->xtw, nullptr, 0);
-    k_diag_finalize<<<1, NT, 0, s>>>(h->rpart, h->G * h->nch, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d, 0);
+    reduce_t_global(h, h->xtw, nullptr, 0);
+    const auto pr0 = combine1(h, h->rpart, h->G * h->nch);
+    k_diag_finalize<<<1, NT, 0, s>>>(pr0.first, pr0.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d, 0);
     if (!h->capturing) h->launches++;
     CKL("row 0 diagnostics");
   }
@@ -1190,7 +1402,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     ColArgs d = base_args(h);
     d.sel_best = 1;
     launch_colpass<MODE_QT_D>(h, d, h->st);
-    launch_reduce_t(h, h->t2, nullptr, 0);
+    reduce_t_global(h, h->t2, nullptr, 0);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
     if (!h->capturing) h->launches++;
     CKL("recover");
@@ -1269,43 +1481,96 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   API_END((int*)nullptr)
 }
 
-int glsgpu_synth_normal(double* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t stream,
-                        int device) {
+int glsgpu_synth_normal(double* dev, int64_t rows, int64_t cols, int64_t ld, int64_t row0, int64_t rows_total,
+                        uint64_t seed, uint64_t stream, int device) {
   API_BEGIN
+  if (!dev || ld < rows || row0 < 0 || row0 + rows > rows_total) fail(GLSGPU_ERR_INVALID, "synth_normal: bad shape");
   CK(cudaSetDevice(device));
-  k_synth_normal<<<148 * 8, 256>>>(dev, rows, cols, ld, seed, stream);
+  k_synth_normal<<<148 * 8, 256>>>(dev, rows, cols, ld, row0, rows_total, seed, stream);
   CKL("k_synth_normal");
   CK(cudaDeviceSynchronize());
   API_END((int*)nullptr)
 }
 
-int glsgpu_synth_response(int G, int64_t M, const int64_t* n_i, const double* X_dev, int64_t ldx, const double* beta,
-                          const double* omega_half, uint64_t seed, double* Y_dev, int64_t ldy, int device) {
+int glsgpu_synth_response(int G, int64_t M, int64_t row0, int64_t M_total, const int64_t* n_i, const double* X_dev,
+                          int64_t ldx, const double* beta, const double* omega_half, uint64_t seed, double* Y_dev,
+                          int64_t ldy, int device) {
   API_BEGIN
-  // Y = X beta + Z Omega^1/2 with Z ~ N(0,1) from stream 3 (synth.py's recipe)
+  // Y = X beta + Z Omega^1/2, Z ~ N(0,1) from stream 3 of the M_total x G matrix (synth.py's recipe)
   glsgpu_sur* h = create_common(G, M, n_i, omega_half, nullptr, device);
+  double *z = nullptr, *e = nullptr, *bd = nullptr;
   try {
-    ensure_solver(h, 1);
-    k_synth_normal<<<148 * 8, 256, 0, h->s>>>(h->r, M, G, h->ldm, seed, 3);
-    if (!h->capturing) h->launches++;
+    const size_t mv = (size_t)(h->ldm * G);
+    z = dalloc<double>(mv);
+    e = dalloc<double>(mv);
+    h->partA = dalloc<double>(GRID_CAP * 3);
+    CK(cudaMemsetAsync(z, 0, mv * sizeof(double), h->s));
+    k_synth_normal<<<148 * 8, 256, 0, h->s>>>(z, M, G, h->ldm, row0, M_total, seed, 3);
     CKL("k_synth_normal");
-    launch_kron(h, h->r, nullptr, nullptr, nullptr, h->su, h->partA, 0, nullptr, nullptr);
-    CK(cudaMemcpy2DAsync(Y_dev, ldy * sizeof(double), h->su, h->ldm * sizeof(double), M * sizeof(double), G,
+    CK(cudaFuncSetAttribute(k_kron<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 8));
+    CK(cudaFuncSetAttribute(k_kron<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16 * 8));
+    launch_kron(h, z, nullptr, nullptr, nullptr, e, h->partA, 0, nullptr, nullptr);
+    CK(cudaMemcpy2DAsync(Y_dev, ldy * sizeof(double), e, h->ldm * sizeof(double), M * sizeof(double), G,
                          cudaMemcpyDeviceToDevice, h->s));
-    double* bd = dalloc<double>(h->n);
+    bd = dalloc<double>(h->n);
     CK(cudaMemcpyAsync(bd, beta, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
     dim3 grid((unsigned)std::min<int64_t>((M + 255) / 256, 256), (unsigned)G);
     k_add_xbeta<<<grid, 256, 0, h->s>>>(G, M, h->d_nb, h->d_p0, X_dev, ldx, bd, Y_dev, ldy);
-    if (!h->capturing) h->launches++;
     CKL("k_add_xbeta");
     CK(cudaStreamSynchronize(h->s));
+  } catch (...) {
+    cudaFree(z);
+    cudaFree(e);
     cudaFree(bd);
+    destroy_impl(h);
+    throw;
+  }
+  cudaFree(z);
+  cudaFree(e);
+  cudaFree(bd);
+  destroy_impl(h);
+  API_END((int*)nullptr)
+}
+
+int glsgpu_nccl_unique_id(void* id_out) {
+  API_BEGIN
+  if (!id_out) fail(GLSGPU_ERR_INVALID, "nccl_unique_id: null");
+  ncclUniqueId id;
+  nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(id_out, &id, sizeof(id));
+  API_END((int*)nullptr)
+}
+
+int glsgpu_sur_create_sharded(int G, int64_t M_local, int64_t M_global, const int64_t* n_i, const double* X_dev,
+                              int64_t ldx, const double* Y_dev, int64_t ldy, const double* omega,
+                              const double* block_scale, int device, const void* nccl_id, int rank, int nranks,
+                              glsgpu_sur** out, int* bad_block) {
+  API_BEGIN
+  if (!out || !X_dev || !Y_dev) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create_sharded: null argument");
+  if (ldx < M_local || ldy < M_local) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "glsgpu: leading dimension < M_local");
+  *out = nullptr;
+  glsgpu_sur* h = create_common(G, M_local, n_i, omega, block_scale, device, M_global, rank, nranks, nccl_id);
+  try {
+    h->X = X_dev;
+    h->ldx = ldx;
+    h->Y = Y_dev;
+    h->ldy = ldy;
+    alloc_common(h);
+    run_qr(h);
   } catch (...) {
     destroy_impl(h);
     throw;
   }
-  destroy_impl(h);
-  API_END((int*)nullptr)
+  *out = h;
+  API_END(bad_block)
+}
+
+int glsgpu_sur_shard(const glsgpu_sur* h, int* rank, int* nranks, int64_t* M_global) {
+  if (!h) return GLSGPU_ERR_INVALID;
+  if (rank) *rank = h->rank;
+  if (nranks) *nranks = h->nranks;
+  if (M_global) *M_global = h->M_global;
+  return GLSGPU_OK;
 }
 
 }  // extern "C"

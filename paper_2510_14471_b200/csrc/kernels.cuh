@@ -434,6 +434,34 @@ __global__ void k_reduce_t(const double* tpart, int64_t n, int nch, double* out,
   if (lane == 0) out[j] = s;
 }
 
+// Multi-rank: t = sum over ranks (in rank order) of the gathered local sums t_all[P][n].
+__global__ void k_sum_ranks(const double* t_all, int nranks, int64_t n, double* out, const SolveState* st, int gate) {
+  if (gate == 1 && !st->active) return;
+  if (gate == 2 && !st->diag_now) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += t_all[(int64_t)r * n + j];
+    out[j] = s;
+  }
+}
+
+// Multi-rank TSQR: scatter the gathered per-rank top R factors (rall[P][sum n_b^2], each block
+// column-major n_b x n_b at r0_b) into the per-block stacks [R_0; ...; R_{P-1}] (P n_b x n_b, ld P n_b).
+__global__ void k_stack_r(const double* rall, int nranks, int64_t rtot, int G, const int* nb, const int64_t* r0,
+                          const int64_t* stack_off, double* stacks) {
+  const int b = blockIdx.x;
+  if (b >= G) return;
+  const int n = nb[b];
+  const int64_t ld = (int64_t)nranks * n;
+  double* S = stacks + stack_off[b];
+  for (int64_t idx = threadIdx.x; idx < (int64_t)nranks * n * n; idx += blockDim.x) {
+    const int r = (int)(idx / ((int64_t)n * n));
+    const int64_t e = idx - (int64_t)r * n * n;
+    const int j = (int)(e / n), i = (int)(e - (int64_t)j * n);
+    S[(int64_t)j * ld + (int64_t)r * n + i] = rall[(int64_t)r * rtot + r0[b] + e];
+  }
+}
+
 // Upper-triangular back substitution R x = b per block (linalg.cpp:130-136) or R' x = b
 // (linalg.cpp:137-145), one thread per block, the reference's loop order.
 __device__ __forceinline__ void tri_solve_dev(int n, const double* R, double* x, bool transpose) {
@@ -839,6 +867,176 @@ __global__ void __launch_bounds__(QR_NT) k_qr_formq(const QrItem* items, int nit
 }
 
 // ------------------------------------------------------------------------------------------
+// Register-resident TSQR leaves for narrow blocks (n <= 32, chunk rows <= 256): thread t owns row t
+// of the chunk in registers; the column loop is fully unrolled (k is compile-time) so the row never
+// leaves the register file.  Per Householder step: one block-wide scaled-norm reduction (LAPACK
+// dnrm2 (scale, ssq) combine, fixed order) and one 32-wide transpose-reduce for the trailing dots.
+constexpr int QRR_NT = 256;
+
+// (scale, ssq) combine of two partial Euclidean norms
+__device__ __forceinline__ void nrm_combine(double& s, double& q, double s2, double q2) {
+  if (s2 > s) {
+    if (s2 > 0.0) {
+      const double r = s / s2;
+      q = q2 + q * r * r;
+    }
+    s = s2;
+  } else if (s > 0.0 && s2 > 0.0) {
+    const double r = s2 / s;
+    q = q + q2 * r * r;
+  }
+}
+
+__device__ __forceinline__ double block_norm(double x, double* red /*[16]*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double s = fabs(x), q = (x != 0.0) ? 1.0 : 0.0;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const double s2 = __shfl_xor_sync(FULL, s, o), q2 = __shfl_xor_sync(FULL, q, o);
+    nrm_combine(s, q, s2, q2);
+  }
+  if (lane == 0) {
+    red[2 * warp] = s;
+    red[2 * warp + 1] = q;
+  }
+  __syncthreads();
+  double S = red[0], Qs = red[1];
+  for (int w = 1; w < QRR_NT / 32; ++w) nrm_combine(S, Qs, red[2 * w], red[2 * w + 1]);
+  return S * sqrt(Qs);
+}
+
+// acc[j] summed over the CTA (fixed order) -> out[j] (shared), all threads see it after the call
+template <int NB>
+__device__ __forceinline__ void block_vec_sum(double (&acc)[NB], double (*red)[NB], double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_transpose_reduce<NB>(acc);
+  red[warp][lane % NB] = acc[0];
+  __syncthreads();
+  if (threadIdx.x < NB) {
+    double s = 0.0;
+    for (int w = 0; w < QRR_NT / 32; ++w) s += red[w][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+template <int NB>
+__global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items, int nitems) {
+  __shared__ double red_n[2 * (QRR_NT / 32)];
+  __shared__ double red_v[QRR_NT / 32][NB];
+  __shared__ double svec[NB];
+  __shared__ double akk_s;
+  const int t = threadIdx.x;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    const int64_t row = I.r0 + t;
+    double a[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      a[j] = (t < L && j < n && row < I.valid) ? I.src[(int64_t)j * I.lds + row] * I.scale : 0.0;
+    double rkk = 0.0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      if (k >= n) break;
+      // column norm over rows >= k (householder_factor, linalg.cpp:30-31)
+      if (t == k) akk_s = a[k];
+      const double norm_x = block_norm(t >= k ? a[k] : 0.0, red_n);  // contains a __syncthreads
+      const double wkk = akk_s;
+      double beta = 0.0, v0 = 1.0, alpha = 0.0;
+      if (norm_x != 0.0) {
+        alpha = wkk >= 0.0 ? -norm_x : norm_x;
+        v0 = wkk - alpha;
+        beta = -1.0 / (alpha * v0);
+      }
+      if (t == 0) I.tau[k] = beta;
+      double v = 0.0;  // this row's reflector component (unit head)
+      if (norm_x != 0.0) {
+        if (t > k) {
+          a[k] = a[k] / v0;
+          v = a[k];
+        } else if (t == k) {
+          v = 1.0;
+          a[k] = v0;
+          rkk = alpha;
+        }
+      } else if (t == k) {
+        rkk = 0.0;
+      }
+      // trailing update: s_j = v' A[:, j] (j > k); A[:, j] -= beta_hat s_j v
+      double acc[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = (j > k) ? v * a[j] : 0.0;
+      block_vec_sum<NB>(acc, red_v, svec);
+      if (beta != 0.0) {
+        const double beta_hat = beta * v0 * v0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j > k && j < n) a[j] -= (svec[j] * beta_hat) * v;
+      }
+    }
+    // packed panel -> reflector storage; R rows (t < n) -> rout
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.r0 + t] = a[j];
+    if (t < n) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (j < n) {
+          const double r = (j > t) ? a[j] : (j == t ? rkk : 0.0);
+          I.rout[t + (int64_t)j * I.ldo] = r;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Explicit thin Q of a narrow chunk: E = H_0 ... H_{n-1} [C; 0]; the output row in registers, the
+// packed reflectors staged in shared memory (rows x n, <= 64 KB).
+template <int NB>
+__global__ void __launch_bounds__(QRR_NT, 1) k_qr_formq_reg(const QrItem* items, int nitems) {
+  extern __shared__ double P[];  // [NB][QRR_NT]
+  __shared__ double red_v[QRR_NT / 32][NB];
+  __shared__ double svec[NB];
+  const int t = threadIdx.x;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    __syncthreads();
+    for (int j = 0; j < n; ++j) P[j * QRR_NT + t] = (t < L) ? I.refl[(int64_t)j * I.ldr + I.r0 + t] : 0.0;
+    double e[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      double v = 0.0;
+      if (t < n && j < n) v = I.qpar ? I.qpar[t + (int64_t)j * I.ldp] : (t == j ? 1.0 : 0.0);
+      e[j] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = NB - 1; k >= 0; --k) {
+      if (k >= n) continue;
+      const double beta = I.tau[k];
+      if (beta == 0.0) continue;  // form_q_columns skips zero reflectors (linalg.cpp:83)
+      const double v0 = P[k * QRR_NT + k];
+      const double beta_hat = beta * v0 * v0;
+      const double v = (t > k && t < L) ? P[k * QRR_NT + t] : (t == k ? 1.0 : 0.0);
+      double acc[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = v * e[j];
+      block_vec_sum<NB>(acc, red_v, svec);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) e[j] -= (svec[j] * beta_hat) * v;
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.r0 + t] = e[j];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Counter-based normal generator for synthetic inputs: Philox4x32-10 on (element, stream) keyed
 // by the seed, Box-Muller on two 53-bit uniforms (u1 in (0,1]).  Element e of a rows x cols
 // matrix is e = col * rows + row, independent of the leading dimension.
@@ -856,11 +1054,15 @@ __device__ __forceinline__ void philox(uint32_t (&c)[4], uint32_t k0, uint32_t k
   }
 }
 
-__global__ void k_synth_normal(double* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t stream) {
+// Rows [row0, row0 + rows) of the rows_total x cols matrix: any row sharding draws the same values.
+__global__ void k_synth_normal(double* out, int64_t rows, int64_t cols, int64_t ld, int64_t row0, int64_t rows_total,
+                               uint64_t seed, uint64_t stream) {
   const int64_t total = rows * cols;
-  const int64_t pairs = (total + 1) / 2;
-  for (int64_t pidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pidx < pairs;
-       pidx += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = idx / rows, row = idx - col * rows;
+    const int64_t e = col * rows_total + row0 + row;  // logical element of the global matrix
+    const int64_t pidx = e >> 1;
     uint32_t c[4] = {(uint32_t)pidx, (uint32_t)(pidx >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
     philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
     const uint64_t a = ((uint64_t)c[0] << 32) | c[1];
@@ -870,15 +1072,7 @@ __global__ void k_synth_normal(double* out, int64_t rows, int64_t cols, int64_t 
     const double rad = sqrt(-2.0 * log(u1));
     double sv, cv;
     sincospi(2.0 * u2, &sv, &cv);
-    const int64_t e0 = 2 * pidx, e1 = e0 + 1;
-    {
-      const int64_t col = e0 / rows, row = e0 - col * rows;
-      out[col * ld + row] = rad * cv;
-    }
-    if (e1 < total) {
-      const int64_t col = e1 / rows, row = e1 - col * rows;
-      out[col * ld + row] = rad * sv;
-    }
+    out[col * ld + row] = (e & 1) ? rad * sv : rad * cv;
   }
 }
 

@@ -220,12 +220,12 @@ def test_counters_match_reference():
     """CostCounters after pcg_aug equal the reference's own tallies (preconditioner.cpp:9-47)."""
     if not oracle.have("ref"):
         pytest.skip("oracle/_ref not shipped")
-    # tol 1e-8: both runs stop on the threshold, well above the roundoff floor, so the iteration
-    # counts (and with them the apply tallies) are the same
-    for p in (synth.random_sur(3, 12, [2, 3, 2], seed=11), synth.random_sur(5, 30, [4, 4, 6, 3, 5], seed=15)):
-        r = oracle.solve(p, "ref", cfg=oracle.make_config(tol_rel=1e-8), beta_true=p.beta)
+    # tol 1e-6 on well-determined problems: both runs stop on the threshold, far above the roundoff
+    # floor, so the iteration counts (and with them the apply tallies) are the same
+    for p in (synth.random_sur(3, 200, [5, 7, 4], seed=21), synth.random_sur(4, 300, [3, 6, 8, 2], seed=22)):
+        r = oracle.solve(p, "ref", cfg=oracle.make_config(tol_rel=1e-6), beta_true=p.beta)
         op = api.sur_preconditioner(api.sur_from_problem(p))
-        g = api.pcg_aug(api.sur_from_problem(p), op, config=api.PcgConfig(tol_rel=1e-8))
+        g = api.pcg_aug(api.sur_from_problem(p), op, config=api.PcgConfig(tol_rel=1e-6))
         assert g.solution.iterations == r.iterations
         c = op.counters()
         got = [c.factorizations, c.factor_multiplies, c.pi_applies, c.xstar_t_applies, c.xstar_applies,
@@ -246,3 +246,58 @@ def test_trace_diagnostics_every_row():
     # X'w vanishes on every iterate (dual feasibility), to roundoff
     assert np.all(tg["dual_feas_norm"] <= 1e-9 * np.linalg.norm(p.Y))
     assert np.all(np.diff(tg["elapsed_ns"]) >= 0)
+
+
+def _device_inputs(p):
+    import torch
+    X = torch.from_numpy(np.ascontiguousarray(p.X.T)).cuda()  # (n, M) row-major == M x n column-major
+    Y = torch.from_numpy(np.ascontiguousarray(p.Y.T)).cuda()
+    return X, Y
+
+
+def test_collective_path_single_rank():
+    """The multi-GPU code path -- NCCL all-gathers of the per-rank partial sums, rank-order sums, the
+    cross-rank TSQR level -- run with ONE rank (no inter-rank waiting on one GPU).  It must agree with
+    the single-device path and with the oracle."""
+    p = synth.make_problem(4, M=3000, G=24)
+    X, Y = _device_inputs(p)
+    op_c = api.GpuSurPreconditioner.from_device_sharded(p.G, p.M, p.M, p.nb, X.data_ptr(), p.M, Y.data_ptr(), p.M,
+                                                        p.omega, api.nccl_unique_id(), 0, 1)
+    op_p = api.GpuSurPreconditioner.from_device(p.G, p.M, p.nb, X.data_ptr(), p.M, Y.data_ptr(), p.M, p.omega)
+    Q, R = op_c.factors()
+    off = 0
+    for k in p.nb:
+        Qi = Q[:, off:off + k]
+        assert np.max(np.abs(Qi.T @ Qi - np.eye(k))) < 1e-13
+        off += k
+    for mode in ("qr", "x"):
+        cfg = api.PcgConfig(tol_rel=p.tol_rel, max_iter=200, xv_mode=mode, diag_every=1)
+        gc = api.pcg_aug(None, op_c, config=cfg, true_beta=p.beta)
+        gp = api.pcg_aug(None, op_p, config=cfg, true_beta=p.beta)
+        assert gc.solution.iterations == gp.solution.iterations
+        assert gc.solution.termination == gp.solution.termination
+        assert rel(gc.solution.b, gp.solution.b) <= 1e-12
+        assert np.allclose(gc.trace.rows["c"][:10], gp.trace.rows["c"][:10], rtol=1e-12)
+    o = oracle.solve(p, "oracle", cfg=oracle.make_config(tol_rel=p.tol_rel, max_iter=200), beta_true=p.beta)
+    assert gc.solution.iterations == o.iterations
+    assert rel(gc.solution.b, o.b) <= B_TOL
+
+
+def test_device_synth_is_shard_invariant():
+    """glsgpu_synth_normal draws the same global matrix for any row split (bench's per-rank inputs)."""
+    import ctypes
+    import torch
+    from paper_2510_14471_b200 import _lib
+    lib = _lib.load()
+    M, n = 1000, 7
+    full = torch.empty((n, M), dtype=torch.float64, device="cuda")
+    assert lib.glsgpu_synth_normal(ctypes.c_void_p(full.data_ptr()), M, n, M, 0, M, 1234, 0, 0) == 0
+    parts = []
+    for r in range(3):
+        row0, rows = api.row_partition(M, 3, r)
+        t = torch.empty((n, rows), dtype=torch.float64, device="cuda")
+        assert lib.glsgpu_synth_normal(ctypes.c_void_p(t.data_ptr()), rows, n, rows, row0, M, 1234, 0, 0) == 0
+        parts.append(t)
+    assert torch.equal(torch.cat(parts, dim=1), full)
+    v = full.cpu().numpy().ravel()
+    assert abs(v.mean()) < 0.1 and abs(v.std() - 1.0) < 0.05
