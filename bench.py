@@ -244,10 +244,17 @@ def run_ours(args):
     cfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv, diag_every=0, kernel_timing=False)
     stream = torch.cuda.ExternalStream(op.stream_ptr(), device=f"cuda:{dev}")
 
+    setup_ms = []
+
     def step(timing=False):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         op.refactor()
+        e1.record(stream)
         cfg.kernel_timing = timing
         r = api.pcg_aug(None, op, config=cfg, true_beta=beta, want_w=False)
+        if timing:
+            setup_ms.append(e0.elapsed_time(e1))
         return r
 
     for _ in range(args.warmup):
@@ -378,6 +385,8 @@ def run_ours(args):
             "iterations_per_step": [r.solution.iterations for r in results],
             "termination": last.solution.termination.name,
             "iter_ms": iter_ms, "b_iter_bytes": b_iter,
+            "setup_qr_ms": statistics.mean(setup_ms) if setup_ms else None,
+            "solve_ms": statistics.mean(r.solve_ms for r in results),
             "iter_GBps_algorithmic": b_iter / (iter_ms / 1e3) / 1e9 if iter_ms else None,
             "passes": passes,
             "roofline": roof,

@@ -76,7 +76,25 @@ typedef struct {
 /* ------------------------------------------------------------------ dense helpers
  * proj/src/dense_matrix.cpp:69-91,165-202 */
 
+/* Summation mode of the long reductions (dot products, X'w / Q'r column dots).  0 = the reference's
+ * sequential sums (default, bitwise the reference).  1 = pairwise (tree) sums -- a DIAGNOSTIC variant
+ * in the accuracy class of the GPU's fixed-shape reduction trees, used to map the arithmetic envelope
+ * of the iteration count; never used for parity claims against the reference. */
+static int g_sum_mode = 0;
+void orc_set_sum_mode(int mode) { g_sum_mode = mode; }
+
+static double pairwise_dot(int64_t n, const double* a, const double* b) {
+  if (n <= 32) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
+    return acc;
+  }
+  const int64_t h = n / 2;
+  return pairwise_dot(h, a, b) + pairwise_dot(n - h, a + h, b + h);
+}
+
 static double vdot(int64_t n, const double* a, const double* b) {
+  if (g_sum_mode == 1) return pairwise_dot(n, a, b);
   double acc = 0.0;
   for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
   return acc;
@@ -95,6 +113,10 @@ static void gemv(int64_t rows, int64_t cols, const double* a, int64_t ld, const 
 }
 /* y = A' x, sequential dot per column (dense_matrix.cpp:81-91) */
 static void gemv_t(int64_t rows, int64_t cols, const double* a, int64_t ld, const double* x, double* y) {
+  if (g_sum_mode == 1) {
+    for (int64_t j = 0; j < cols; ++j) y[j] = pairwise_dot(rows, a + j * ld, x);
+    return;
+  }
   for (int64_t j = 0; j < cols; ++j) {
     const double* cj = a + j * ld;
     double acc = 0.0;

@@ -46,6 +46,40 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+CPP_TESTS = os.path.join(ROOT, "tests", "cpp")
+REF_INCLUDE = "/root/reference/proj/include"
+
+
+def build_cpp_tests(verbose: bool = False) -> list:
+    """The C++ host-API test (always) and the reference-adapter test (when the reference headers are
+    present -- i.e. here, not on the GPU box; the binary travels).  rpath $ORIGIN-relative so the
+    binaries find libglsgpu.so / the oracle libraries inside the snapshot."""
+    out = os.path.join(CPP_TESTS, "bin")
+    os.makedirs(out, exist_ok=True)
+    rpath = "-Wl,-rpath,$ORIGIN/../../../paper_2510_14471_b200:$ORIGIN/../../../oracle:$ORIGIN/../../../oracle/_ref"
+    cmds = [[
+        "g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(CPP_TESTS, "test_header_api.cpp"),
+        "-L", PKG, "-lglsgpu", "-L", os.path.join(ROOT, "oracle"), "-loracle", rpath,
+        "-o", os.path.join(out, "test_header_api"),
+    ]]
+    if os.path.isdir(REF_INCLUDE) and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libglsref.so")):
+        cmds.append([
+            "g++", "-std=c++20", "-O2", "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"), "-I",
+            os.path.join(ROOT, "integration"), os.path.join(CPP_TESTS, "test_reference_adapter.cpp"),
+            "-L", os.path.join(ROOT, "oracle", "_ref"), "-lglsref", "-L", PKG, "-lglsgpu", rpath,
+            "-o", os.path.join(out, "test_reference_adapter"),
+        ])
+    built = []
+    for cmd in cmds:
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or p.returncode != 0:
+            sys.stderr.write(p.stdout + p.stderr)
+        if p.returncode != 0:
+            raise RuntimeError(f"g++ failed: {' '.join(cmd)}")
+        built.append(cmd[cmd.index("-o") + 1])
+    return built
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -160,6 +161,11 @@ struct glsgpu_sur {
   // row sharding: this rank owns rows [row0, row0 + M) of M_global; Omega, R, n-vectors replicated
   int rank = 0, nranks = 1;
   bool coll = false;  // collective path (NCCL all-gathers, cross-rank TSQR level); also nranks == 1 + id
+  bool use_stream = false;  // TMA-staged passes (n_i <= 128, 16-byte aligned X columns, ldx >= ldm)
+  bool qtiled = false;      // Q tile-contiguous: block b, rows [256 k, 256 k + 256) contiguous (n_i <= 32)
+  std::vector<int64_t> qoff;  // offset of Q_b
+  int64_t* d_qoff = nullptr;
+  int64_t qsize = 0;
   int64_t M_global = 0;
   ncclComm_t comm = nullptr;
   double *loc3 = nullptr, *all3 = nullptr, *t_loc = nullptr, *t_all = nullptr;
@@ -196,6 +202,15 @@ int kron_cpl(int G) {
   return 16;
 }
 
+WBuf wbuf_of(const glsgpu_sur* h) {
+  WBuf b;
+  for (int i = 0; i < 3; ++i) {
+    b.w[i] = h->wb[i];
+    b.sw[i] = h->swb[i];
+  }
+  return b;
+}
+
 // out = (Omega (x) I) x with the CTA partials; in_mode per k_kron.
 void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const double* div, double* u_io, double* out,
                  double* partials, int in_mode, const SolveState* st, int* grid_out) {
@@ -208,7 +223,7 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
   if (grid_out) *grid_out = grid;
 #define KRON_CASE(C, RW)                                                                                       \
   k_kron<C, RW><<<grid, NT, smem, h->s>>>(h->G, h->ldm, ntiles, h->omegaT, src, prv, div, u_io, out, partials, \
-                                          in_mode, st)
+                                          in_mode, st, wbuf_of(h))
   switch (cpl) {
     case 1: KRON_CASE(1, 4); break;
     case 2: KRON_CASE(2, 4); break;
@@ -277,6 +292,207 @@ ColArgs base_args(glsgpu_sur* h) {
   a.avalid = h->ldm;
   a.gate = 0;
   return a;
+}
+
+// ------------------------------------------------------------------------------------------ TMA passes
+// k_stream tile geometry: T rows per tile (128 for narrow blocks), S = 3 ring stages.
+struct StreamCfg {
+  int T, S;
+  int64_t stage_doubles;
+  size_t smem;
+  int grid;
+};
+
+StreamCfg stream_cfg(const glsgpu_sur* h, int nmat, int nv) {
+  StreamCfg c;
+  const int nmax = h->nmax;
+  // largest tile (one row per thread at T = 256) whose ring of >= 2 stages fits in ~200 KB; a third
+  // stage when it still fits (deeper memory-level parallelism for the smaller tiles)
+  const int64_t budget = 200 * 1024;
+  c.T = 32;
+  c.S = 2;
+  for (int T : {256, 128, 64, 32}) {
+    const int64_t stage = (int64_t)(nmat * nmax + nv) * T * 8;
+    const int64_t extra = (int64_t)(T + nmax + std::max(nmax, 32)) * 8;
+    if (2 * stage + extra <= budget) {
+      c.T = T;
+      c.S = (3 * stage + extra <= budget) ? 3 : 2;
+      break;
+    }
+  }
+  c.stage_doubles = (int64_t)(nmat * nmax + nv) * c.T;
+  c.smem = (size_t)(c.S * c.stage_doubles + c.T + nmax + std::max(nmax, 32)) * sizeof(double);
+  const int per_sm = std::max<int>(1, (int)((227 * 1024) / (c.smem + 2048)));
+  const int64_t items = (int64_t)h->G * h->nch;
+  c.grid = (int)std::min<int64_t>(items, (int64_t)148 * std::min(per_sm, 4));
+  return c;
+}
+
+StreamArgs stream_args(glsgpu_sur* h) {
+  StreamArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.Q = h->Q;
+  a.X = h->X;
+  a.ldx = h->ldx;
+  a.u = h->u;
+  a.su = h->su;
+  for (int i = 0; i < 3; ++i) {
+    a.wb[i] = h->wb[i];
+    a.swb[i] = h->swb[i];
+  }
+  a.r = h->r;
+  a.pr = h->pr;
+  a.y = h->Y;
+  a.ldy = h->ldy;
+  a.tpart = h->tpart;
+  a.nmax = h->nmax;
+  a.qtiled = h->qtiled ? 1 : 0;
+  a.qoff = h->d_qoff;
+  return a;
+}
+
+template <int MODE>
+int stream_nmat_host(const StreamArgs& a) {
+  return MODE == SMODE_B ? 1 + a.xv_from_x : 1;
+}
+template <int MODE>
+int stream_nvec_host() {
+  return stream_nvec<MODE>();
+}
+
+// returns the grid (= number of per-CTA partials written for SMODE_C / SMODE_DIAG)
+template <int MODE>
+int launch_stream(glsgpu_sur* h, StreamArgs a, const SolveState* st) {
+  const StreamCfg c = stream_cfg(h, stream_nmat_host<MODE>(a), stream_nvec_host<MODE>());
+  a.T = c.T;
+  a.S = c.S;
+  a.stage_doubles = c.stage_doubles;
+  // narrow blocks: column partials accumulated in registers in the row sweep (k_stream FUSE)
+  constexpr bool COLS = (MODE != SMODE_C && MODE != SMODE_XS);
+  if (COLS && h->nmax <= 32)
+    k_stream<MODE, COLS><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
+  else
+    k_stream<MODE, false><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
+  if (!h->capturing) h->launches++;
+  CKL("k_stream");
+  return c.grid;
+}
+
+// dynamic shared memory attributes of every streaming mode (set outside any graph capture)
+void stream_attrs(glsgpu_sur* h) {
+  // the tile choice depends on nmat (pass B: 1 or 2 matrices), so allow the full opt-in maximum
+  auto set = [&](const void* fn, int, int) {
+    int dev = 0, maxsm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, fn));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm - (int)fa.sharedSizeBytes));
+  };
+  set((const void*)k_stream<SMODE_B, false>, 0, 0);
+  set((const void*)k_stream<SMODE_B, true>, 0, 0);
+  set((const void*)k_stream<SMODE_C, false>, 0, 0);
+  set((const void*)k_stream<SMODE_QT_R, false>, 0, 0);
+  set((const void*)k_stream<SMODE_QT_R, true>, 0, 0);
+  set((const void*)k_stream<SMODE_QT_D, false>, 0, 0);
+  set((const void*)k_stream<SMODE_QT_D, true>, 0, 0);
+  set((const void*)k_stream<SMODE_QT_V, false>, 0, 0);
+  set((const void*)k_stream<SMODE_QT_V, true>, 0, 0);
+  set((const void*)k_stream<SMODE_DIAG, false>, 0, 0);
+  set((const void*)k_stream<SMODE_DIAG, true>, 0, 0);
+  set((const void*)k_stream<SMODE_XS, false>, 0, 0);
+}
+
+// ---- pass wrappers: TMA-staged k_stream when possible, the register kernels otherwise
+// Q'(w x) column partials into tpart: mode MODE_QT_R (x = r), MODE_QT_D (x = y - sw[sel]), MODE_QT_V (x = vin)
+void pass_qt(glsgpu_sur* h, int mode, const double* vin, const SolveState* st, int sel_best, int gate) {
+  if (h->use_stream) {
+    StreamArgs a = stream_args(h);
+    a.vin = vin;
+    a.sel_best = sel_best;
+    a.gate = gate;
+    if (mode == MODE_QT_R) launch_stream<SMODE_QT_R>(h, a, st);
+    else if (mode == MODE_QT_D) launch_stream<SMODE_QT_D>(h, a, st);
+    else launch_stream<SMODE_QT_V>(h, a, st);
+    return;
+  }
+  ColArgs a = base_args(h);
+  a.vin = vin;
+  a.sel_best = sel_best;
+  a.gate = gate;
+  if (mode == MODE_QT_R) launch_colpass<MODE_QT_R>(h, a, st);
+  else if (mode == MODE_QT_D) launch_colpass<MODE_QT_D>(h, a, st);
+  else launch_colpass<MODE_QT_V>(h, a, st);
+}
+
+// pass B of an iteration (gated on st->active)
+void pass_b(glsgpu_sur* h, int xv_from_x, const SolveState* st) {
+  if (h->use_stream) {
+    StreamArgs a = stream_args(h);
+    a.vec = h->vs;
+    a.xv_from_x = xv_from_x;
+    a.gate = 1;
+    launch_stream<SMODE_B>(h, a, st);
+    return;
+  }
+  ColArgs a = base_args(h);
+  a.vec = h->vs;
+  a.xv_from_x = xv_from_x;
+  a.gate = 1;
+  launch_colpass<MODE_B>(h, a, st);
+}
+
+// pr = Pi r with the dot partials (r.pr, r.r, pr.pr) per CTA; returns the number of partial rows
+int pass_c(glsgpu_sur* h, const double* t, const double* r_in, double* pr_out, double* partials, const SolveState* st,
+           int gate) {
+  if (h->use_stream) {
+    StreamArgs a = stream_args(h);
+    a.vec = t;
+    a.r = const_cast<double*>(r_in);
+    a.pr = pr_out;
+    a.partials = partials;
+    a.gate = gate;
+    return launch_stream<SMODE_C>(h, a, st);
+  }
+  const int gC = rowpass_grid(h);
+  k_rowpass<<<gC, NT, 0, h->s>>>(geo_of(h), h->Q, t, r_in, pr_out, partials, 0, gate ? st : nullptr);
+  if (!h->capturing) h->launches++;
+  CKL("k_rowpass");
+  return gC;
+}
+
+// out = w_b Q t (xstar_impl row part)
+void pass_xs(glsgpu_sur* h, const double* t, double* out) {
+  if (h->use_stream) {
+    StreamArgs a = stream_args(h);
+    a.vec = t;
+    a.out = out;
+    launch_stream<SMODE_XS>(h, a, nullptr);
+    return;
+  }
+  k_rowpass<<<rowpass_grid(h), NT, 0, h->s>>>(geo_of(h), h->Q, t, nullptr, out, nullptr, 1, nullptr);
+  if (!h->capturing) h->launches++;
+  CKL("k_rowpass xs");
+}
+
+// trace diagnostics pass over X: X'w partials (tpart) + residual partials; returns (pointer, rows)
+std::pair<double*, int> pass_diag(glsgpu_sur* h, const double* est, const SolveState* st, int gate) {
+  if (h->use_stream) {
+    StreamArgs a = stream_args(h);
+    a.vec = est;
+    a.partials = h->rpart;
+    a.gate = gate;
+    const int grid = launch_stream<SMODE_DIAG>(h, a, st);
+    return {h->rpart, grid};
+  }
+  ColArgs x = base_args(h);
+  x.A = h->X;
+  x.lda = h->ldx;
+  x.avalid = h->M;
+  x.vec = est;
+  x.gate = gate;
+  launch_colpass<MODE_DIAG>(h, x, st);
+  return {h->rpart, h->G * h->nch};
 }
 
 // ------------------------------------------------------------------------------------------ ranks
@@ -441,8 +657,20 @@ void build_qr_plan(glsgpu_sur* h) {
         std::memset(&it, 0, sizeof(it));
         it.r0 = c * rows / nchk;
         it.rows = (c + 1) * rows / nchk - it.r0;
+        it.rr0 = it.r0;
         it.n = n;
-        if (lvl == 0) {
+        if (lvl == 0 && h->qtiled) {
+          // tile-contiguous Q: leaf c = rows [256 c, 256 c + 256) (zero-padded) = Q tile c of block b
+          it.r0 = c * QRR_NT;
+          it.rows = std::min<int64_t>(QRR_NT, rows - it.r0);
+          it.src = h->X + h->p0[b] * h->ldx;
+          it.lds = h->ldx;
+          it.valid = h->M;
+          it.scale = h->wts[b];
+          it.refl = h->Q + h->qoff[b] + c * QRR_NT * (int64_t)n;
+          it.ldr = QRR_NT;
+          it.rr0 = 0;
+        } else if (lvl == 0) {
           it.src = h->X + h->p0[b] * h->ldx;
           it.lds = h->ldx;
           it.valid = h->M;
@@ -559,7 +787,7 @@ void run_qr(glsgpu_sur* h) {
   CK(cudaFuncSetAttribute(k_qr_formq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
   CK(cudaFuncSetAttribute(k_qr_formq<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
   // zero Q (its padding rows stay zero) -- the level-0 reflectors overwrite the rest
-  CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)(h->ldm * h->n), h->s));
+  CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));
   const int nl = (int)h->qr_levels.size();
   CK(cudaFuncSetAttribute(k_qr_formq_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, QRR_NT * 32 * 8));
   const int fgrid_cap = 2 * 148;  // register-resident leaves: 1-2 CTAs per SM
@@ -646,7 +874,21 @@ void upload_omega(glsgpu_sur* h, const double* omega) {
 }
 
 void alloc_common(glsgpu_sur* h) {
-  h->Q = dalloc<double>((size_t)(h->ldm * h->n));
+  // TMA-staged passes need 16-byte aligned column segments of X reaching every padded row
+  h->use_stream = h->nmax <= 128 && h->ldx >= h->ldm && (h->ldx % 2) == 0 &&
+                  (reinterpret_cast<uintptr_t>(h->X) % 16) == 0 && std::getenv("GLSGPU_NO_TMA") == nullptr;
+  // tile-contiguous Q (256-row tiles per block) when every block takes the register-resident QR leaves
+  h->qtiled = h->use_stream && h->nmax <= 32 && std::getenv("GLSGPU_NO_QTILE") == nullptr;
+  h->qoff.assign(h->G, 0);
+  int64_t qsize = 0;
+  for (int b = 0; b < h->G; ++b) {
+    h->qoff[b] = h->qtiled ? qsize : h->p0[b] * h->ldm;
+    qsize += (h->qtiled ? round_up(h->ldm, QRR_NT) : h->ldm) * h->nb[b];
+  }
+  h->qsize = qsize;
+  h->Q = dalloc<double>((size_t)qsize);
+  h->d_qoff = dalloc<int64_t>(h->G);
+  CK(cudaMemcpy(h->d_qoff, h->qoff.data(), sizeof(int64_t) * h->G, cudaMemcpyHostToDevice));
   int64_t rtot = 0;
   for (int b = 0; b < h->G; ++b) rtot += (int64_t)h->nb[b] * h->nb[b];
   h->R = dalloc<double>((size_t)rtot);
@@ -677,7 +919,7 @@ void destroy_impl(glsgpu_sur* h) {
                   h->wb[0], h->wb[1], h->wb[2], h->swb[0], h->swb[1], h->swb[2], h->r, h->u, h->su, h->pr, h->t,
                   h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,
                   h->scal, h->d_stop, h->st, h->rows_d, h->loc3, h->all3, h->t_loc, h->t_all, h->rloc, h->rall,
-                  h->rstack, h->gtau, h->d_stack_off, h->d_gitems};
+                  h->rstack, h->gtau, h->d_stack_off, h->d_gitems, h->d_qoff};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->st_host) cudaFreeHost(h->st_host);
@@ -746,7 +988,7 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     h->zvec = dalloc<double>(h->n);
     h->beta_d = dalloc<double>(h->n);
     h->tpart = dalloc<double>((size_t)h->n * h->nch);
-    h->rpart = dalloc<double>((size_t)h->G * h->nch);
+    h->rpart = dalloc<double>((size_t)std::max<int64_t>((int64_t)h->G * h->nch, 4 * GRID_CAP));
     h->partA = dalloc<double>(GRID_CAP * 3);
     h->partC = dalloc<double>(GRID_CAP * 3);
     h->scal = dalloc<double>(64);
@@ -762,6 +1004,7 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     CK(cudaMemsetAsync(h->su, 0, mv * sizeof(double), h->s));
     CK(cudaMemsetAsync(h->pr, 0, mv * sizeof(double), h->s));
     h->solver_ready = true;
+    stream_attrs(h);
     // kron kernels: >48 KB dynamic shared memory at large G
     CK(cudaFuncSetAttribute(k_kron<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 8));
     CK(cudaFuncSetAttribute(k_kron<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16 * 8));
@@ -795,12 +1038,7 @@ void d2h_mvec(glsgpu_sur* h, double* dst, const double* src) {
 
 // t_out = (Q' (w_b x))_b partials reduced: a Q'-apply of an m-vector already on the device.
 void qt_apply(glsgpu_sur* h, int mode, const double* vin, double* out, const SolveState* st, int sel_best) {
-  ColArgs a = base_args(h);
-  a.vin = vin;
-  a.sel_best = sel_best;
-  if (mode == MODE_QT_R) launch_colpass<MODE_QT_R>(h, a, nullptr);
-  else if (mode == MODE_QT_D) launch_colpass<MODE_QT_D>(h, a, st);
-  else launch_colpass<MODE_QT_V>(h, a, nullptr);
+  pass_qt(h, mode, vin, st, sel_best, 0);
   reduce_t_global(h, out, nullptr, 0);
 }
 
@@ -868,7 +1106,8 @@ __global__ void k_set_t0(SolveState* st) { st->t0 = globaltimer(); }
 
 void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int iter_idx) {
   Geo g = geo_of(h);
-  const int gA = kron_grid(h), gC = rowpass_grid(h);
+  const int gA = kron_grid(h);
+  const int xfx = (xv_mode == GLSGPU_XV_X) ? 1 : 0;
   auto ev = [&](int k) {
     if (timing) CK(cudaEventRecordWithFlags(h->tev[(size_t)iter_idx * 6 + k], h->s, cudaEventRecordExternal));
   };
@@ -880,47 +1119,32 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   k_scalar_a<<<1, NT, 0, h->s>>>(pa.first, pa.second, h->st);
   if (!h->capturing) h->launches++;
   CKL("k_scalar_a");
-  // pass B
-  ColArgs a = base_args(h);
-  a.vec = h->vs;
-  a.xv_from_x = (xv_mode == GLSGPU_XV_X) ? 1 : 0;
-  a.gate = 1;
+  // pass B: w, sw, r updates + Q'(w r) column partials
   ev(2);
-  launch_colpass<MODE_B>(h, a, h->st);
+  pass_b(h, xfx, h->st);
   ev(3);
   reduce_t_global(h, h->t, h->st, 1);
-  // pass C
+  // pass C: pr = Pi r, c = r.pr
   ev(4);
-  k_rowpass<<<gC, NT, 0, h->s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, h->st);
-  if (!h->capturing) h->launches++;
-  CKL("k_rowpass");
+  const int gC = pass_c(h, h->t, h->r, h->pr, h->partC, h->st, 1);
   ev(5);
   const auto pcc = combine3(h, h->partC, gC);
   k_scalar_c<<<1, NT, 0, h->s>>>(pcc.first, pcc.second, h->st, h->rows_d);
   if (!h->capturing) h->launches++;
   CKL("k_scalar_c");
-  k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, h->vs, a.xv_from_x, 0, h->st);
+  k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, h->vs, xfx, 0, h->st);
   if (!h->capturing) h->launches++;
   CKL("k_vupdate");
   if (diag >= 0) {
     // est = X*'(y - sw) and the row diagnostics, gated on st->diag_now
-    ColArgs d = base_args(h);
-    d.sel_best = 0;
-    d.gate = 2;
-    launch_colpass<MODE_QT_D>(h, d, h->st);
+    pass_qt(h, MODE_QT_D, nullptr, h->st, 0, 2);
     reduce_t_global(h, h->t2, h->st, 2);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
     if (!h->capturing) h->launches++;
     CKL("k_vupdate diag");
-    ColArgs x = base_args(h);
-    x.A = h->X;
-    x.lda = h->ldx;
-    x.avalid = h->M;
-    x.vec = h->t2;
-    x.gate = 2;
-    launch_colpass<MODE_DIAG>(h, x, h->st);
+    const auto rp = pass_diag(h, h->t2, h->st, 2);
     reduce_t_global(h, h->xtw, h->st, 2);
-    const auto pr1 = combine1(h, h->rpart, h->G * h->nch);
+    const auto pr1 = combine1(h, rp.first, rp.second);
     k_diag_finalize<<<1, NT, 0, h->s>>>(pr1.first, pr1.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d,
                                         -1);
     if (!h->capturing) h->launches++;
@@ -1074,10 +1298,7 @@ int glsgpu_apply_pi(glsgpu_sur* h, const double* xi, double* out) {
   h->counters.apply_multiplies += h->pi_cost;
   h2d_mvec(h, h->r, xi);
   qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
-  Geo g = geo_of(h);
-  k_rowpass<<<rowpass_grid(h), NT, 0, h->s>>>(g, h->Q, h->t, h->r, h->pr, nullptr, 0, nullptr);
-  if (!h->capturing) h->launches++;
-  CKL("k_rowpass");
+  pass_c(h, h->t, h->r, h->pr, h->partC, nullptr, 0);
   d2h_mvec(h, out, h->pr);
   CK(cudaStreamSynchronize(h->s));
   API_END((int*)nullptr)
@@ -1113,9 +1334,7 @@ int glsgpu_apply_xstar(glsgpu_sur* h, const double* v, double* out) {
   k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, nullptr, 1, 3, nullptr);
   if (!h->capturing) h->launches++;
   CKL("k_vupdate");
-  k_rowpass<<<rowpass_grid(h), NT, 0, h->s>>>(g, h->Q, h->t, nullptr, h->pr, nullptr, 1, nullptr);
-  if (!h->capturing) h->launches++;
-  CKL("k_rowpass");
+  pass_xs(h, h->t, h->pr);
   d2h_mvec(h, out, h->pr);
   CK(cudaStreamSynchronize(h->s));
   API_END((int*)nullptr)
@@ -1145,9 +1364,20 @@ int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R) {
   API_BEGIN
   if (!h) fail(GLSGPU_ERR_INVALID, "null handle");
   CK(cudaSetDevice(h->dev));
-  if (Q)
+  if (Q && !h->qtiled) {
     CK(cudaMemcpy2D(Q, h->M * sizeof(double), h->Q, h->ldm * sizeof(double), h->M * sizeof(double), h->n,
                     cudaMemcpyDeviceToHost));
+  } else if (Q) {
+    // tile-contiguous -> column-major M x n
+    std::vector<double> qt((size_t)h->qsize);
+    CK(cudaMemcpy(qt.data(), h->Q, sizeof(double) * h->qsize, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < h->G; ++b) {
+      const int nb = h->nb[b];
+      for (int j = 0; j < nb; ++j)
+        for (int64_t k = 0; k < h->M; ++k)
+          Q[(h->p0[b] + j) * h->M + k] = qt[h->qoff[b] + (k / QRR_NT) * QRR_NT * nb + (int64_t)j * QRR_NT + k % QRR_NT];
+    }
+  }
   if (R) {
     int64_t rtot = 0;
     for (int b = 0; b < h->G; ++b) rtot += (int64_t)h->nb[b] * h->nb[b];
@@ -1227,13 +1457,9 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   if (w1 && h->coll) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: w1 on a row-sharded handle");
   if (w1) {
     h2d_mvec(h, h->wb[0], w1);
-    ColArgs a = base_args(h);
-    a.A = h->X;
-    a.lda = h->ldx;
-    a.avalid = h->M;
-    a.vec = h->zvec;  // est = 0: only the X'w column part is used here
+    // X'w via the diagnostics pass with est = 0 (only its column part is used here)
     CK(cudaMemsetAsync(h->zvec, 0, sizeof(double) * h->n, s));
-    launch_colpass<MODE_DIAG>(h, a, h->st);
+    pass_diag(h, h->zvec, h->st, 0);
     launch_reduce_t(h, h->xtw, nullptr, 0);
     std::vector<double> xtw((size_t)h->n), wv((size_t)m);
     CK(cudaMemcpyAsync(xtw.data(), h->xtw, sizeof(double) * h->n, cudaMemcpyDeviceToHost, s));
@@ -1259,8 +1485,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
       CK(cudaMemcpyAsync(h->t, h->xtw, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, s));
       k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t, nullptr, 1, 3, nullptr);
       if (!h->capturing) h->launches++;
-      k_rowpass<<<rowpass_grid(h), NT, 0, s>>>(g, h->Q, h->t, nullptr, h->pr, nullptr, 1, nullptr);
-      if (!h->capturing) h->launches++;
+      pass_xs(h, h->t, h->pr);
       k_axpy_sub<<<GRID_CAP, NT, 0, s>>>(h->wb[0], h->pr, h->ldm * h->G);
       if (!h->capturing) h->launches++;
       CKL("w1 projection");
@@ -1280,10 +1505,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     CKL("k_init_residual");
   }
   qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
-  const int gC = rowpass_grid(h);
-  k_rowpass<<<gC, NT, 0, s>>>(g, h->Q, h->t, h->r, h->pr, h->partC, 0, nullptr);
-  if (!h->capturing) h->launches++;
-  CKL("k_rowpass init");
+  const int gC = pass_c(h, h->t, h->r, h->pr, h->partC, nullptr, 0);
   const auto pi0 = combine3(h, h->partC, gC);
   k_init_scalars<<<1, NT, 0, s>>>(pi0.first, pi0.second, h->st, h->rows_d);
   if (!h->capturing) h->launches++;
@@ -1295,19 +1517,13 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   CK(cudaMemcpyAsync(h->u, h->pr, mvb, cudaMemcpyDeviceToDevice, s));
   // row 0 diagnostics: est0 = recover(sw) (pcg.cpp:118-122)
   if (diag >= 0) {
-    ColArgs d = base_args(h);
-    launch_colpass<MODE_QT_D>(h, d, h->st);
+    pass_qt(h, MODE_QT_D, nullptr, h->st, 0, 0);
     reduce_t_global(h, h->t2, nullptr, 0);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
     if (!h->capturing) h->launches++;
-    ColArgs x = base_args(h);
-    x.A = h->X;
-    x.lda = h->ldx;
-    x.avalid = h->M;
-    x.vec = h->t2;
-    launch_colpass<MODE_DIAG>(h, x, h->st);
+    const auto rp0 = pass_diag(h, h->t2, h->st, 0);
     reduce_t_global(h, h->xtw, nullptr, 0);
-    const auto pr0 = combine1(h, h->rpart, h->G * h->nch);
+    const auto pr0 = combine1(h, rp0.first, rp0.second);
     k_diag_finalize<<<1, NT, 0, s>>>(pr0.first, pr0.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d, 0);
     if (!h->capturing) h->launches++;
     CKL("row 0 diagnostics");
@@ -1395,13 +1611,18 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
       }
     }
   }
+  // a w / sw update still pending (the loop stopped in k_scalar_c) is materialized now
+  k_apply_pending<<<GRID_CAP, NT, 0, s>>>(h->st, wbuf_of(h), h->u, h->su, h->ldm * h->G);
+  k_finish_pending<<<1, 1, 0, s>>>(h->st);
+  h->launches += 2;
+  CKL("apply pending");
+  CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   SolveState fin = *h->st_host;
 
   // exit: b = X*'(y - sw_sel), sel = last if Converged else best (pcg.cpp:215-228)
   {
-    ColArgs d = base_args(h);
-    d.sel_best = 1;
-    launch_colpass<MODE_QT_D>(h, d, h->st);
+    pass_qt(h, MODE_QT_D, nullptr, h->st, 1, 0);
     reduce_t_global(h, h->t2, nullptr, 0);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
     if (!h->capturing) h->launches++;
@@ -1462,8 +1683,10 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   h->kstats.clear();
   if (timing) {
     const double M = (double)h->M, G = (double)h->G, n = (double)h->n;
-    const double bA = 8.0 * 4.0 * M * G;
-    const double bB = 8.0 * (M * n * (xv_mode == GLSGPU_XV_X ? 2.0 : 1.0) + 8.0 * M * G);
+    // pass A: reads pr, u, su, w, sw; writes u, su, w, sw (the deferred update of pcg.cpp:151-152)
+    // pass B: reads Q (+ X in xv_mode X), su, r; writes r.   pass C: reads Q, r; writes pr.
+    const double bA = 8.0 * 9.0 * M * G;
+    const double bB = 8.0 * (M * n * (xv_mode == GLSGPU_XV_X ? 2.0 : 1.0) + 3.0 * M * G);
     const double bC = 8.0 * (M * n + 2.0 * M * G);
     const char* names[3] = {"passA_kron", "passB_update_qtr", "passC_pi"};
     const double bytes[3] = {bA, bB, bC};

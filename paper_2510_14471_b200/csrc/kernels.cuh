@@ -38,6 +38,7 @@ struct Geo {
 // executes in k_scalar_a / k_scalar_c so no host round trip happens inside an iteration.
 struct SolveState {
   double c, c1, threshold, c_best, pi_gain, lambda, mu, sigma_scale;
+  double lam_prev;         // lambda of the w / sw update still pending (applied by the next pass A)
   double tol_rel, breakdown_tol, growth_tol;
   double d, uu, c_next, rr, prpr;
   int64_t i, max_iter, best_iter, stagnant, done, breakdown_iter, stride;
@@ -45,7 +46,10 @@ struct SolveState {
   int64_t rows_cap;        // device trace capacity
   unsigned long long t0;   // %globaltimer at solve start
   int32_t active, term, cur, best, nxt, mu_pending, cont, diag_now, sampled, have_beta;
-  int32_t pad[2];
+  // w_{i+1} = w_i - lambda_i u_i and sw_{i+1} = sw_i - lambda_i su_i (pcg.cpp:151-152) are deferred
+  // to the next pass A (compute-bound, so their traffic is free there): upd_pending marks them
+  int32_t upd_pending;
+  int32_t pad[1];
 };
 
 struct TraceRowD {
@@ -115,36 +119,90 @@ __device__ __forceinline__ void warp_transpose_reduce(double (&acc)[NB]) {
 // Modes: in_mode 0: x = src; 1: x = src / (*div) (operator_norm_probe's v[i] /= nrm);
 //        2: pass A: u_new = pr + mu*u when st->mu_pending (pcg.cpp:210) else u; writes u.
 // Partials per CTA: [0] = sum x*out, [1] = sum x*x, [2] = sum out*out.
+struct WBuf {
+  double* w[3];
+  double* sw[3];
+};
+
 template <int CPL, int RW>
-__global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles, const double* __restrict__ omegaT,
+__global__ void __launch_bounds__(NT, 2) k_kron(int G, int64_t ldm, int64_t ntiles, const double* __restrict__ omegaT,
                                              const double* src, const double* pr, const double* div, double* u_io,
-                                             double* out, double* partials, int in_mode, const SolveState* st) {
+                                             double* out, double* partials, int in_mode, const SolveState* st,
+                                             WBuf wbuf) {
   if (st && !st->active) return;
   extern __shared__ double xs[];  // [G][TR]
   constexpr int TR = 8 * RW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double mu = 0.0;
-  bool upd = false;
-  if (in_mode == 2) { upd = st->mu_pending != 0; mu = st->mu; }
+  double mu = 0.0, lp = 0.0;
+  bool upd = false, wupd = false;
+  double *wc = nullptr, *wn = nullptr, *swc = nullptr, *swn = nullptr;
+  if (in_mode == 2) {
+    upd = st->mu_pending != 0;
+    mu = st->mu;
+    wupd = st->upd_pending != 0;  // the deferred w / sw update of the previous iteration
+    lp = st->lam_prev;
+    wc = wbuf.w[st->cur];
+    wn = wbuf.w[st->nxt];
+    swc = wbuf.sw[st->cur];
+    swn = wbuf.sw[st->nxt];
+  }
   const double dv = (in_mode == 1) ? *div : 1.0;
   double p_xo = 0.0, p_xx = 0.0, p_oo = 0.0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t k0 = tile * TR;
     __syncthreads();
-    for (int idx = threadIdx.x; idx < G * TR; idx += NT) {
-      const int p = idx / TR, r = idx - p * TR;
-      const int64_t off = (int64_t)p * ldm + k0 + r;
-      double x;
-      if (in_mode == 2) {
-        const double uo = u_io[off];
-        if (upd) { x = pr[off] + mu * uo; u_io[off] = x; }
-        else x = uo;
-      } else if (in_mode == 1) {
-        x = src[off] / dv;
-      } else {
-        x = src[off];
+    if (in_mode == 2) {
+      // batches of 4 elements per thread: every load of the batch is issued before any store, so the
+      // deferred w / sw update (axpy(-lambda, u, w), axpy(-lambda, su, sw), pcg.cpp:151-152; su read
+      // before Sigma u overwrites it) streams under the Kronecker math instead of serialising it
+      const double* __restrict__ prr = pr;
+      const double* __restrict__ wcr = wc;
+      const double* __restrict__ swcr = swc;
+      double* __restrict__ wnr = wn;
+      double* __restrict__ swnr = swn;
+      for (int idx0 = threadIdx.x; idx0 < G * TR; idx0 += 4 * NT) {
+        double uo[4], pv[4], wv[4], swv[4], so[4];
+        int64_t offs[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int idx = idx0 + e * NT;
+          const int p = idx / TR, r = idx - p * TR;
+          offs[e] = (int64_t)p * ldm + k0 + r;
+          if (idx < G * TR) {
+            uo[e] = u_io[offs[e]];
+            pv[e] = upd ? prr[offs[e]] : 0.0;
+            if (wupd) {
+              wv[e] = wcr[offs[e]];
+              swv[e] = swcr[offs[e]];
+              so[e] = out[offs[e]];
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int idx = idx0 + e * NT;
+          if (idx < G * TR) {
+            const int64_t off = offs[e];
+            if (wupd) {
+              wnr[off] = wv[e] + (-lp) * uo[e];
+              swnr[off] = swv[e] + (-lp) * so[e];
+            }
+            double x = uo[e];
+            if (upd) {
+              x = pv[e] + mu * uo[e];
+              u_io[off] = x;
+            }
+            const int p = idx / TR, r = idx - p * TR;
+            xs[p * TR + r] = x;
+          }
+        }
       }
-      xs[p * TR + r] = x;
+    } else {
+      for (int idx = threadIdx.x; idx < G * TR; idx += NT) {
+        const int p = idx / TR, r = idx - p * TR;
+        const int64_t off = (int64_t)p * ldm + k0 + r;
+        xs[p * TR + r] = (in_mode == 1) ? src[off] / dv : src[off];
+      }
     }
     __syncthreads();
     double acc[RW][CPL];
@@ -230,6 +288,13 @@ __global__ void k_scalar_a(const double* partials, int count, SolveState* st) {
   __shared__ double res[3];
   reduce_partials<3>(partials, count, res);
   if (threadIdx.x == 0) {
+    if (st->upd_pending) {  // pass A just materialized w_i / sw_i into nxt
+      st->cur = st->nxt;
+      st->upd_pending = 0;
+      int nx = 0;
+      while (nx == st->cur || nx == st->best) ++nx;
+      st->nxt = nx;
+    }
     const double d = res[0], uu = res[1];
     st->d = d;
     st->uu = uu;
@@ -250,7 +315,7 @@ __global__ void k_scalar_a(const double* partials, int count, SolveState* st) {
 // deterministic transpose-reduce into tpart[(p0_b + j) * nch + ch].
 //
 // MODE_B   : pass B of an iteration (pcg.cpp:151-155): w -= lambda u, sw -= lambda su (into the
-//            rotation buffer nxt), xv = X v (xv_mode X) or Q s / w_b (xv_mode QR), r -= lambda(su + xv),
+//            rotation buffer; now deferred to pass A), xv = X v (xv_mode X) or Q s / w_b (QR), r -= lambda(su + xv),
 //            x = w_b * r  (gather of the following apply_pi / apply_xstar_t, structured.cpp:347-351).
 // MODE_QT_R: x = w_b * r                    (apply_pi / apply_xstar_t of r)
 // MODE_QT_D: x = w_b * (y - sw[sel])        (recover, pcg.cpp:96-98)
@@ -301,14 +366,15 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
   const int64_t k1 = (k0 + g.CH < g.ldm) ? k0 + g.CH : g.ldm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  double lam = 0.0;
-  int cur = 0, nxt = 0, selb = 0;
-  if (MODE == MODE_B) { lam = st->lambda; cur = st->cur; nxt = st->nxt; }
+  double lam = 0.0, lp = 0.0;  // lp: lambda of a pending w / sw update (applied on the fly)
+  int cur = 0, selb = 0;
+  if (MODE == MODE_B) lam = st->lambda;
   if (MODE == MODE_DIAG) cur = st->cur;
   if (MODE == MODE_QT_D) {
     if (a.sel_best) selb = (st->term == T_CONVERGED) ? st->cur : st->best;
     else selb = st->cur;
   }
+  if ((MODE == MODE_DIAG || MODE == MODE_QT_D) && st && st->upd_pending) lp = st->lam_prev;
   if (MODE == MODE_B || MODE == MODE_DIAG) {
     for (int j = threadIdx.x; j < nb; j += NT) svec_s[j] = a.vec[p0 + j];
     __syncthreads();
@@ -332,10 +398,8 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
       for (int j = 0; j < NB; ++j) qv[j] = (j < nb && k < a.avalid) ? Ab[(int64_t)j * a.lda + k] : 0.0;
     }
     if (MODE == MODE_B) {
-      const double uv = a.u[off], suv = a.su[off];
-      const double wv = a.wb[cur][off], swv = a.swb[cur][off], rv = a.r[off];
-      a.wb[nxt][off] = wv + (-lam) * uv;
-      a.swb[nxt][off] = swv + (-lam) * suv;
+      // (w / sw updates are deferred to the next pass A)
+      const double suv = a.su[off], rv = a.r[off];
       double xv = 0.0;
       if (a.xv_from_x) {
         if (k < g.M)
@@ -357,7 +421,7 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
       x = a.r[off] * wgt;
     } else if (MODE == MODE_QT_D) {
       const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
-      x = (yv - a.swb[selb][off]) * wgt;
+      x = (yv - (a.swb[selb][off] + (-lp) * a.su[off])) * wgt;
     } else if (MODE == MODE_QT_V) {
       x = a.vin[off] * wgt;
     } else {  // MODE_DIAG
@@ -371,9 +435,9 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
           for (int j = 0; j < nb; ++j) xe = xe + Ab[(int64_t)j * a.lda + k] * svec_s[j];
       }
       const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
-      const double res = yv - (a.swb[cur][off] + xe);
+      const double res = yv - ((a.swb[cur][off] + (-lp) * a.su[off]) + xe);
       if (k < g.M) rsum += res * res;
-      x = a.wb[cur][off];
+      x = a.wb[cur][off] + (-lp) * a.u[off];
     }
     if (FUSED) {
 #pragma unroll
@@ -415,6 +479,377 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
           if (j0 + j < nb && k < a.avalid) acc[j] += Ab[(int64_t)(j0 + j) * a.lda + k] * x;
       }
       flush(j0);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA-staged streaming pass (Blackwell bulk-copy engine).  A persistent grid walks (block, chunk)
+// items in tiles of T rows; warp 0 issues one cp.async.bulk per column segment of the matrix tile(s)
+// (Q and/or X: T contiguous doubles each, column-major) and per vector segment into an S-stage
+// shared-memory ring, completion tracked by one mbarrier per stage (expect_tx).  Phase 1 (thread per
+// row) does the row work; phase 2 (warp per column) the Q'x column partial sums.  The memory-level
+// parallelism comes from the ring, not from registers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+enum { SMODE_B = 0, SMODE_C = 1, SMODE_QT_R = 2, SMODE_QT_D = 3, SMODE_QT_V = 4, SMODE_DIAG = 5, SMODE_XS = 6 };
+
+struct StreamArgs {
+  const double* Q;      // ld = ldm
+  const double* X;      // ld = ldx (>= ldm, 16-byte aligned columns)
+  int64_t ldx;
+  const double* u;
+  const double* su;
+  double* wb[3];
+  double* swb[3];
+  double* r;
+  double* pr;           // SMODE_C output
+  double* out;          // SMODE_XS output
+  const double* y;
+  int64_t ldy;
+  const double* vin;    // SMODE_QT_V input
+  const double* vec;    // per-block n-vector: v / s (B), t (C, XS), est (DIAG)
+  double* tpart;        // column partials [(p0 + j) * nch + ch]
+  double* partials;     // per-CTA dot partials (C: 3, DIAG: 1)
+  int xv_from_x, sel_best, gate;
+  int T, S, nmax;
+  int qtiled;           // Q stored tile-contiguous (256-row tiles per block, column-major inside)
+  const int64_t* qoff;  // [G] offset of Q_b (tiled layout)
+  int64_t stage_doubles;
+};
+
+template <int MODE>
+__device__ __forceinline__ int stream_nmat(const StreamArgs& a) {
+  return MODE == SMODE_B ? 1 + a.xv_from_x : 1;
+}
+template <int MODE>
+__host__ __device__ constexpr int stream_nvec() {
+  return MODE == SMODE_B ? 2 : MODE == SMODE_DIAG ? 4 : MODE == SMODE_QT_D ? 2 : MODE == SMODE_XS ? 0 : 1;
+}
+
+template <int MODE, bool FUSE>
+__global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveState* st) {
+  if (a.gate == 1 && !st->active) return;
+  if (a.gate == 2 && !st->diag_now) return;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bars[4];
+  __shared__ double red[NT / 32 * 3];
+  __shared__ double fred[FUSE ? NT : 1];
+  const int S = a.S, T = a.T;
+  double* xs = sm + (int64_t)S * a.stage_doubles;
+  double* colacc = xs + T;
+  double* tv = colacc + a.nmax;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nmat = stream_nmat<MODE>(a);
+  constexpr int NV = stream_nvec<MODE>();
+  const int64_t items = (int64_t)g.G * g.nch;
+
+  double lam = 0.0, lp = 0.0;  // lp: lambda of a still-pending w / sw update (diagnostics apply it on the fly)
+  int cur = 0, sel = 0;
+  if (MODE == SMODE_B) lam = st->lambda;
+  if (MODE == SMODE_DIAG) cur = st->cur;
+  if (MODE == SMODE_QT_D) sel = a.sel_best ? (st->term == T_CONVERGED ? st->cur : st->best) : st->cur;
+  if ((MODE == SMODE_DIAG || MODE == SMODE_QT_D) && st && st->upd_pending) lp = st->lam_prev;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // tile iterator (item = blockIdx.x + j * gridDim.x; tiles of T rows inside the item's chunk)
+  auto item_rows = [&](int64_t item, int64_t& k0, int64_t& k1) {
+    const int ch = (int)(item % g.nch);
+    k0 = (int64_t)ch * g.CH;
+    k1 = (k0 + g.CH < g.ldm) ? k0 + g.CH : g.ldm;
+  };
+  int64_t p_item = blockIdx.x, p_tile = 0;  // producer position
+  auto issue = [&](int stage) {
+    // warp 0 only; advances the producer iterator
+    if (p_item >= items) return;
+    int64_t k0, k1;
+    item_rows(p_item, k0, k1);
+    const int64_t kb = k0 + p_tile * T;
+    const int rows = (int)((k1 - kb) < T ? (k1 - kb) : T);
+    const int b = (int)(p_item / g.nch);
+    const int nb = g.nb[b];
+    const int64_t p0 = g.p0[b];
+    const uint32_t seg = (uint32_t)rows * 8u;
+    // tile-contiguous Q with T == 256: the whole tile (padded to 256 rows) is ONE contiguous region,
+    // moved as 4 bulk copies; otherwise one copy per column segment
+    const bool qbig = (MODE != SMODE_DIAG) && a.qtiled && T == 256;
+    const int nq = qbig ? 4 : nb;
+    const int nseg = nq + (nmat - 1) * nb + NV;
+    const uint32_t qpiece = (uint32_t)(T * nb * 8 / 4);
+    const uint32_t total = (qbig ? 4u * qpiece : seg * (uint32_t)nb) + seg * (uint32_t)((nmat - 1) * nb + NV);
+    double* base = sm + (int64_t)stage * a.stage_doubles;
+    if (lane == 0) mbar_expect_tx(&bars[stage], total);
+    __syncwarp();
+    for (int q = lane; q < nseg; q += 32) {
+      const double* src;
+      double* dst;
+      uint32_t bytes = seg;
+      if (q < nq) {  // first matrix: Q (X for DIAG)
+        if (MODE == SMODE_DIAG) {
+          src = a.X + (p0 + q) * a.ldx + kb;
+          dst = base + (int64_t)q * T;
+        } else if (qbig) {
+          src = a.Q + a.qoff[b] + (kb >> 8) * (int64_t)(256 * nb) + (int64_t)q * (qpiece / 8);
+          dst = base + (int64_t)q * (qpiece / 8);
+          bytes = qpiece;
+        } else if (a.qtiled) {
+          src = a.Q + a.qoff[b] + (kb >> 8) * (int64_t)(256 * nb) + (int64_t)q * 256 + (kb & 255);
+          dst = base + (int64_t)q * T;
+        } else {
+          src = a.Q + (p0 + q) * g.ldm + kb;
+          dst = base + (int64_t)q * T;
+        }
+      } else if (q < nq + (nmat - 1) * nb) {  // second matrix: X (pass B, xv_mode X)
+        src = a.X + (p0 + (q - nq)) * a.ldx + kb;
+        dst = base + (int64_t)(nb + (q - nq)) * T;
+      } else {
+        const int v = q - nq - (nmat - 1) * nb;
+        const int64_t vo = (int64_t)b * g.ldm + kb;
+        const double* vb = nullptr;
+        if (MODE == SMODE_B) vb = v == 0 ? a.su : a.r;
+        else if (MODE == SMODE_C || MODE == SMODE_QT_R) vb = a.r;
+        else if (MODE == SMODE_QT_V) vb = a.vin;
+        else if (MODE == SMODE_QT_D) vb = v == 0 ? a.swb[sel] : a.su;
+        else if (MODE == SMODE_DIAG) vb = v == 0 ? a.wb[cur] : v == 1 ? a.swb[cur] : v == 2 ? a.u : a.su;
+        src = vb + vo;
+        dst = base + (int64_t)(nmat * nb) * T + (int64_t)v * T;
+      }
+      tma_load_1d(dst, src, bytes, &bars[stage]);
+    }
+    if (++p_tile * T >= k1 - k0) {
+      p_tile = 0;
+      p_item += gridDim.x;
+    }
+  };
+  if (warp == 0)
+    for (int s = 0; s < S; ++s) issue(s);
+
+  double pc = 0.0, prr = 0.0, ppp = 0.0, rsum = 0.0;
+  constexpr int MAXC = 16;  // columns per warp (n_b <= 128 on this path)
+  constexpr bool COLS = (MODE != SMODE_C && MODE != SMODE_XS);
+  int64_t it_count = 0;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    int64_t k0, k1;
+    item_rows(item, k0, k1);
+    const int b = (int)(item / g.nch);
+    const int ch = (int)(item % g.nch);
+    const int nb = g.nb[b];
+    const int64_t p0 = g.p0[b];
+    const double wgt = g.wts[b];
+    const int64_t vbase = (int64_t)b * g.ldm;
+    // tv holds >= 32 entries (zero past n_b): the fused row dots read all 32
+    for (int j = tid; j < (nb > 32 ? nb : 32); j += NT)
+      if (MODE == SMODE_B || MODE == SMODE_C || MODE == SMODE_XS || MODE == SMODE_DIAG)
+        tv[j] = (j < nb) ? a.vec[p0 + j] : 0.0;
+    __syncthreads();
+    // column partials live in registers across the item's tiles: lane partial of column warp + 8 c
+    double acc[MAXC];
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) acc[q] = 0.0;
+    double facc[FUSE ? 32 : 1];
+#pragma unroll
+    for (int j = 0; j < (FUSE ? 32 : 1); ++j) facc[j] = 0.0;
+    for (int64_t kb = k0; kb < k1; kb += T, ++it_count) {
+      const int stage = (int)(it_count % S);
+      const int rows = (int)((k1 - kb) < T ? (k1 - kb) : T);
+      mbar_wait(&bars[stage], (uint32_t)((it_count / S) & 1));
+      const double* base = sm + (int64_t)stage * a.stage_doubles;
+      const double* M0 = base;                                 // Q (X for DIAG)
+      const double* M1 = base + (int64_t)nb * T;               // X (pass B, xv_mode X)
+      const double* V = base + (int64_t)(nmat * nb) * T;       // vectors
+      if constexpr (FUSE && COLS) {
+        // narrow blocks (n_b <= 32): the row of the tile's matrix lives in registers; the row work and
+        // the column partials (acc_j += A[k, j] x_k) happen in one sweep -- no second phase, no extra
+        // barrier; the per-lane accumulators are transpose-reduced once per item
+        for (int t = tid; t < rows; t += NT) {
+          const int64_t k = kb + t;
+          const int64_t vo = vbase + k;
+          double arow[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) arow[j] = (j < nb) ? M0[(int64_t)j * T + t] : 0.0;
+          auto rdot = [&]() {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              s0 = s0 + arow[j + 0] * tv[j + 0];
+              s1 = s1 + arow[j + 1] * tv[j + 1];
+              s2 = s2 + arow[j + 2] * tv[j + 2];
+              s3 = s3 + arow[j + 3] * tv[j + 3];
+            }
+            return (s0 + s1) + (s2 + s3);
+          };
+          double x;
+          if (MODE == SMODE_B) {
+            const double suv = V[t], rv = V[T + t];
+            double xv = 0.0;
+            if (a.xv_from_x) {
+              if (k < g.M)
+                for (int j = 0; j < nb; ++j) xv = xv + M1[(int64_t)j * T + t] * tv[j];
+            } else {
+              xv = rdot() / wgt;
+            }
+            const double rn = rv - lam * (suv + xv);
+            a.r[vo] = rn;
+            x = rn * wgt;
+          } else if (MODE == SMODE_QT_R || MODE == SMODE_QT_V) {
+            x = V[t] * wgt;
+          } else if (MODE == SMODE_QT_D) {
+            const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+            x = (yv - (V[t] + (-lp) * V[T + t])) * wgt;
+          } else {  // SMODE_DIAG
+            const double xe = (k < g.M) ? rdot() : 0.0;
+            const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+            const double res = yv - ((V[T + t] + (-lp) * V[3 * T + t]) + xe);
+            if (k < g.M) rsum += res * res;
+            x = V[t] + (-lp) * V[2 * T + t];
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) facc[j] += arow[j] * x;
+        }
+        __syncthreads();  // the stage is free
+        if (warp == 0) issue(stage);
+        continue;
+      }
+      // ---- phase 1: row work (thread per row).  Q-side row sums use 4 independent chains (their
+      // inputs come from tree reductions anyway); the X v row sum of xv_mode X stays sequential in j
+      // (bitwise the reference's DenseMatrix::apply, dense_matrix.cpp:69-79).
+      auto qdot = [&](const double* Mrow) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int j = 0;
+        for (; j + 4 <= nb; j += 4) {
+          s0 = s0 + Mrow[(int64_t)(j + 0) * T] * tv[j + 0];
+          s1 = s1 + Mrow[(int64_t)(j + 1) * T] * tv[j + 1];
+          s2 = s2 + Mrow[(int64_t)(j + 2) * T] * tv[j + 2];
+          s3 = s3 + Mrow[(int64_t)(j + 3) * T] * tv[j + 3];
+        }
+        for (; j < nb; ++j) s0 = s0 + Mrow[(int64_t)j * T] * tv[j];
+        return (s0 + s1) + (s2 + s3);
+      };
+      for (int t = tid; t < rows; t += NT) {
+        const int64_t k = kb + t;
+        const int64_t vo = vbase + k;
+        if (MODE == SMODE_B) {
+          // (w / sw updates are deferred to the next pass A)
+          const double suv = V[t], rv = V[T + t];
+          double xv = 0.0;
+          if (a.xv_from_x) {
+            if (k < g.M)
+              for (int j = 0; j < nb; ++j) xv = xv + M1[(int64_t)j * T + t] * tv[j];
+          } else {
+            xv = qdot(M0 + t) / wgt;
+          }
+          const double rn = rv - lam * (suv + xv);
+          a.r[vo] = rn;
+          xs[t] = rn * wgt;
+        } else if (MODE == SMODE_C || MODE == SMODE_XS) {
+          const double proj = qdot(M0 + t);
+          if (MODE == SMODE_XS) {
+            a.out[vo] = proj * wgt;
+          } else {
+            const double rv = V[t];
+            const double pv = (rv * wgt - proj) * wgt;
+            a.pr[vo] = pv;
+            pc += rv * pv;
+            prr += rv * rv;
+            ppp += pv * pv;
+          }
+        } else if (MODE == SMODE_QT_R || MODE == SMODE_QT_V) {
+          xs[t] = V[t] * wgt;
+        } else if (MODE == SMODE_QT_D) {
+          const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+          const double swv = V[t] + (-lp) * V[T + t];  // sw_{i+1} = sw_i - lambda_i su_i when pending
+          xs[t] = (yv - swv) * wgt;
+        } else {  // SMODE_DIAG
+          const double xe = (k < g.M) ? qdot(M0 + t) : 0.0;
+          const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+          const double swv = V[T + t] + (-lp) * V[3 * T + t];
+          const double res = yv - (swv + xe);
+          if (k < g.M) rsum += res * res;
+          xs[t] = V[t] + (-lp) * V[2 * T + t];
+        }
+      }
+      // ---- phase 2: column partials acc_j += sum_rows A[k, j] x_k (warp per column, lanes over rows)
+      if (COLS) {
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < MAXC; ++q) {
+          const int j = warp + (NT / 32) * q;
+          if (j < nb) {
+            const double* Mj = M0 + (int64_t)j * T;
+            double s = acc[q];
+            for (int t = lane; t < rows; t += 32) s += Mj[t] * xs[t];
+            acc[q] = s;
+          }
+        }
+      }
+      __syncthreads();  // the stage (and xs) are free
+      if (warp == 0) issue(stage);
+    }
+    if constexpr (FUSE && COLS) {
+      // transpose-reduce the 32 per-lane column partials, then the 8 warps in order
+      warp_transpose_reduce<32>(facc);
+      fred[warp * 32 + lane] = facc[0];
+      __syncthreads();
+      if (tid < nb) {
+        double s = 0.0;
+        for (int w = 0; w < NT / 32; ++w) s += fred[w * 32 + tid];
+        a.tpart[(p0 + tid) * g.nch + ch] = s;
+      }
+      __syncthreads();
+    } else if (COLS) {
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int j = warp + (NT / 32) * q;
+        if (j < nb) {  // warp-uniform
+          double s = acc[q];
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+          if (lane == 0) a.tpart[(p0 + j) * g.nch + ch] = s;
+        }
+      }
+    }
+  }
+  if (MODE == SMODE_C || MODE == SMODE_DIAG) {
+    double v[3] = {MODE == SMODE_C ? pc : rsum, prr, ppp};
+    block_sum<3>(v, red);
+    if (tid == 0) {
+      if (MODE == SMODE_C) {
+        a.partials[blockIdx.x * 3 + 0] = v[0];
+        a.partials[blockIdx.x * 3 + 1] = v[1];
+        a.partials[blockIdx.x * 3 + 2] = v[2];
+      } else {
+        a.partials[blockIdx.x] = v[0];
+      }
     }
   }
 }
@@ -580,7 +1015,9 @@ __global__ void k_scalar_c(const double* partials, int count, SolveState* st, Tr
   st->rr = rr;
   st->prpr = prpr;
   st->done = i;
-  st->cur = st->nxt;  // the w / sw written by pass B
+  // w_{i+1} / sw_{i+1} (lambda_i) are materialized into nxt by the next pass A (or k_apply_pending)
+  st->upd_pending = 1;
+  st->lam_prev = st->lambda;
   st->sampled = (i % st->stride == 0) || c_next <= st->threshold || i == st->max_iter;
   if (i < st->rows_cap) {
     TraceRowD& row = rows[i];
@@ -607,7 +1044,7 @@ __global__ void k_scalar_c(const double* partials, int count, SolveState* st, Tr
     if (c_next < 0.0) c_next = 0.0;
     if (c_next < st->c_best) {
       st->c_best = c_next;
-      st->best = st->cur;
+      st->best = st->nxt;  // where w_{i+1} lands
       st->best_iter = i;
     }
     if (c_next <= st->threshold || exhausted) {
@@ -644,11 +1081,26 @@ __global__ void k_scalar_c(const double* partials, int count, SolveState* st, Tr
   } else {
     st->cont = 1;
     st->i = i + 1;
-    // next rotation buffer: the one that is neither cur nor best
-    int nx = 0;
-    while (nx == st->cur || nx == st->best) ++nx;
-    st->nxt = nx;
   }
+}
+
+// Materialize a pending w / sw update after the loop stopped in k_scalar_c (pass A of a next
+// iteration never ran): w[nxt] = w[cur] - lambda u, sw[nxt] = sw[cur] - lambda su.
+__global__ void k_apply_pending(SolveState* st, WBuf wbuf, const double* u, const double* su, int64_t count) {
+  if (!st->upd_pending) return;
+  const double lp = st->lam_prev;
+  const double *wc = wbuf.w[st->cur], *swc = wbuf.sw[st->cur];
+  double *wn = wbuf.w[st->nxt], *swn = wbuf.sw[st->nxt];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    wn[i] = wc[i] + (-lp) * u[i];
+    swn[i] = swc[i] + (-lp) * su[i];
+  }
+}
+
+__global__ void k_finish_pending(SolveState* st) {
+  if (!st->upd_pending) return;
+  st->cur = st->nxt;
+  st->upd_pending = 0;
 }
 
 // Trace diagnostics finalize for the row just computed (pcg.cpp:104-116): aug_residual_norm,
@@ -690,7 +1142,8 @@ __global__ void k_diag_finalize(const double* rpart, int count, const double* xt
 struct QrItem {
   const double* src;   // level matrix (level 0: X_b), column-major ld lds
   int64_t lds;
-  int64_t r0, rows;    // chunk rows
+  int64_t r0, rows;    // chunk rows (of src)
+  int64_t rr0;         // first row of the chunk in refl (= r0, or 0 for a tile-contiguous Q tile)
   int64_t valid;       // rows >= valid of src read as 0 (level 0: M; padding)
   double scale;        // level 0: w_b (DenseMatrix *= w, structured.cpp:435-436); else 1
   double* refl;        // reflector panel / explicit Q destination, ld ldr (same row range)
@@ -799,7 +1252,7 @@ __global__ void __launch_bounds__(QR_NT) k_qr_factor(const QrItem* items, int ni
     for (int64_t idx = threadIdx.x; idx < L * n; idx += QR_NT) {
       const int j = (int)(idx / L);
       const int64_t i = idx - (int64_t)j * L;
-      I.refl[(int64_t)j * I.ldr + I.r0 + i] = P[idx];
+      I.refl[(int64_t)j * I.ldr + I.rr0 + i] = P[idx];
     }
   }
 }
@@ -820,7 +1273,7 @@ __global__ void __launch_bounds__(QR_NT) k_qr_formq(const QrItem* items, int nit
     for (int64_t idx = threadIdx.x; idx < L * n; idx += QR_NT) {
       const int j = (int)(idx / L);
       const int64_t i = idx - (int64_t)j * L;
-      P[idx] = I.refl[(int64_t)j * I.ldr + I.r0 + i];
+      P[idx] = I.refl[(int64_t)j * I.ldr + I.rr0 + i];
     }
     __syncthreads();
     for (int j = warp; j < n; j += NW) {
@@ -860,7 +1313,7 @@ __global__ void __launch_bounds__(QR_NT) k_qr_formq(const QrItem* items, int nit
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int64_t i = lane + 32 * q;
-        if (i < L) I.refl[(int64_t)j * I.ldr + I.r0 + i] = e[q];
+        if (i < L) I.refl[(int64_t)j * I.ldr + I.rr0 + i] = e[q];
       }
     }
   }
@@ -922,11 +1375,11 @@ __device__ __forceinline__ void block_vec_sum(double (&acc)[NB], double (*red)[N
 
 template <int NB>
 __global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items, int nitems) {
-  __shared__ double red_n[2 * (QRR_NT / 32)];
   __shared__ double red_v[QRR_NT / 32][NB];
   __shared__ double svec[NB];
-  __shared__ double akk_s;
-  const int t = threadIdx.x;
+  __shared__ double rowk[2][NB];
+  __shared__ double redm[QRR_NT / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     const QrItem I = items[it];
     const int n = I.n;
@@ -936,14 +1389,37 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items
 #pragma unroll
     for (int j = 0; j < NB; ++j)
       a[j] = (t < L && j < n && row < I.valid) ? I.src[(int64_t)j * I.lds + row] * I.scale : 0.0;
+    // exact power-of-two pre-scale of the leaf so the plain sums of squares below cannot overflow
+    double mx = 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) mx = fmax(mx, fabs(a[j]));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    if (lane == 0) redm[warp] = mx;
+    __syncthreads();
+    mx = redm[0];
+    for (int w = 1; w < QRR_NT / 32; ++w) mx = fmax(mx, redm[w]);
+    int ex = 0;
+    if (mx > 0.0) frexp(mx, &ex);
+    const double sc = ldexp(1.0, -ex), unsc = ldexp(1.0, ex);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) a[j] *= sc;
     double rkk = 0.0;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       if (k >= n) break;
-      // column norm over rows >= k (householder_factor, linalg.cpp:30-31)
-      if (t == k) akk_s = a[k];
-      const double norm_x = block_norm(t >= k ? a[k] : 0.0, red_n);  // contains a __syncthreads
-      const double wkk = akk_s;
+      // one reduction per column: S_k = x'x (x = column k, rows >= k) and S_j = x'a_j (j > k)
+      const double x = (t >= k) ? a[k] : 0.0;
+      if (t == k) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) rowk[k & 1][j] = a[j];
+      }
+      double acc[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = (j >= k) ? x * a[j] : 0.0;
+      block_vec_sum<NB>(acc, red_v, svec);  // two __syncthreads
+      const double norm_x = sqrt(svec[k]);
+      const double wkk = rowk[k & 1][k];
       double beta = 0.0, v0 = 1.0, alpha = 0.0;
       if (norm_x != 0.0) {
         alpha = wkk >= 0.0 ? -norm_x : norm_x;
@@ -961,31 +1437,30 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items
           a[k] = v0;
           rkk = alpha;
         }
+        // v' a_j = (x' a_j - alpha a_kj) / v0; with beta_hat = beta v0^2 = -v0 / alpha the update factor
+        // is s_j beta_hat = -(x' a_j - alpha a_kj) / alpha: one reciprocal per column, no per-element divide
+        const double inv_alpha = 1.0 / alpha;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          if (j > k && j < n) {
+            const double f = (alpha * rowk[k & 1][j] - svec[j]) * inv_alpha;  // s_j * beta_hat
+            a[j] -= f * v;
+          }
+        }
       } else if (t == k) {
         rkk = 0.0;
       }
-      // trailing update: s_j = v' A[:, j] (j > k); A[:, j] -= beta_hat s_j v
-      double acc[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) acc[j] = (j > k) ? v * a[j] : 0.0;
-      block_vec_sum<NB>(acc, red_v, svec);
-      if (beta != 0.0) {
-        const double beta_hat = beta * v0 * v0;
-#pragma unroll
-        for (int j = 0; j < NB; ++j)
-          if (j > k && j < n) a[j] -= (svec[j] * beta_hat) * v;
-      }
     }
-    // packed panel -> reflector storage; R rows (t < n) -> rout
+    // packed panel -> reflector storage (scale-invariant); R rows (t < n) -> rout, unscaled exactly
 #pragma unroll
     for (int j = 0; j < NB; ++j)
-      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.r0 + t] = a[j];
+      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = a[j];
     if (t < n) {
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         if (j < n) {
           const double r = (j > t) ? a[j] : (j == t ? rkk : 0.0);
-          I.rout[t + (int64_t)j * I.ldo] = r;
+          I.rout[t + (int64_t)j * I.ldo] = r * unsc;
         }
       }
     }
@@ -1006,7 +1481,7 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_formq_reg(const QrItem* items,
     const int n = I.n;
     const int64_t L = I.rows;
     __syncthreads();
-    for (int j = 0; j < n; ++j) P[j * QRR_NT + t] = (t < L) ? I.refl[(int64_t)j * I.ldr + I.r0 + t] : 0.0;
+    for (int j = 0; j < n; ++j) P[j * QRR_NT + t] = (t < L) ? I.refl[(int64_t)j * I.ldr + I.rr0 + t] : 0.0;
     double e[NB];
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
@@ -1032,7 +1507,7 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_formq_reg(const QrItem* items,
     }
 #pragma unroll
     for (int j = 0; j < NB; ++j)
-      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.r0 + t] = e[j];
+      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = e[j];
   }
 }
 

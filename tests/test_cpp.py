@@ -1,0 +1,56 @@
+"""The C++ host layers: the standalone header API (include/gls_b200/gls_b200.hpp) and the reference-side
+adapter (integration/gls_gpu_adapter.hpp) that runs the reference's UNMODIFIED pcg_aug on the B200
+operator.  Binaries are built by __graft_entry__.build() (tests/cpp/bin/, they travel to the GPU box)."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cpp", "bin")
+
+
+def _ensure(name):
+    path = os.path.join(BIN, name)
+    if not os.path.exists(path):
+        from paper_2510_14471_b200 import build as B
+        B.build()
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "all"], check=True, capture_output=True)
+        B.build_cpp_tests()
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not built (needs the reference headers at build time)")
+    return path
+
+
+def _run(path, *args):
+    p = subprocess.run([path, *args], capture_output=True, text=True, timeout=600)
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    return p.returncode, lines, p.stderr
+
+
+def test_header_api_fails_loudly_without_device():
+    from paper_2510_14471_b200 import api
+    if api.device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    rc, lines, err = _run(_ensure("test_header_api"))
+    assert rc == 0, err
+    assert lines and lines[0]["device"] is False and "no CPU fallback" in lines[0]["error"]
+
+
+@pytest.mark.gpu
+def test_header_api_matches_oracle():
+    rc, lines, err = _run(_ensure("test_header_api"), "--gpu")
+    assert rc == 0, (lines, err)
+    assert lines[0]["ok"] is True
+
+
+@pytest.mark.gpu
+def test_reference_pcg_aug_runs_on_the_gpu_operator():
+    """The reference's own pcg_aug(embed_sur(sur), *op) with op = the B200 preconditioner, and the whole
+    loop on the B200, both match the reference's CPU run (same iterations, b within 1e-10, counters)."""
+    rc, lines, err = _run(_ensure("test_reference_adapter"))
+    assert rc == 0, (lines, err)
+    cases = [x for x in lines if "ok" in x]
+    assert len(cases) == 3 and all(c["ok"] for c in cases)
+    assert any(x.get("rank_deficient_maps_to_gls_RankDeficient") for x in lines)

@@ -142,3 +142,23 @@ def test_oracle_restated_operator_identities(oracle_mod):
         off += p.nb[i]
     in_range = np.concatenate([p.X[:, sum(p.nb[:i]):sum(p.nb[:i + 1])] @ np.ones(p.nb[i]) for i in range(p.G)])
     assert np.linalg.norm(oracle.sur_apply(p, "pi", in_range)) <= 1e-10 * np.linalg.norm(in_range)
+
+
+def test_c3_envelope(oracle_mod):
+    """The arithmetic envelope of the c3-shaped slow tail: the restatement with pairwise (tree) sums --
+    the accuracy class of the GPU's fixed reduction trees -- stops a few iterations away from the
+    reference's sequential sums on the SAME inputs, with b ~1e-10 apart."""
+    import ctypes
+    L = oracle.lib("oracle")
+    L.orc_set_sum_mode.argtypes = [ctypes.c_int]
+    p = synth.make_problem(3, M=600, N=40)
+    try:
+        L.orc_set_sum_mode(1)
+        pw = oracle.solve(p, "oracle")
+    finally:
+        L.orc_set_sum_mode(0)
+    seq = oracle.solve(p, "oracle")
+    assert seq.iterations == 374 and pw.iterations == 372
+    assert seq.termination == pw.termination == "Converged"
+    rel = np.linalg.norm(seq.b - pw.b) / np.linalg.norm(seq.b)
+    assert 1e-11 < rel < 5e-10
