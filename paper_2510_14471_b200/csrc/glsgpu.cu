@@ -237,10 +237,36 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
   if (!h->capturing) h->launches++;
 }
 
+bool kron_gemm_ok(const glsgpu_sur* h) { return h->G > 128 && h->G <= 256 && h->G % 8 == 0; }
+
 int kron_grid(const glsgpu_sur* h) {
+  if (kron_gemm_ok(h)) return (int)std::min<int64_t>(h->ldm / KG_BM, 148);
   const int cpl = kron_cpl(h->G);
   const int tr = 8 * (cpl >= 16 ? 2 : 4);
   return (int)std::min<int64_t>(h->ldm / tr, GRID_CAP);
+}
+
+// pass A: u = pr + mu u, the deferred w / sw update, su = Sigma u with the (d, u.u) partials
+void launch_pass_a(glsgpu_sur* h) {
+  if (!kron_gemm_ok(h)) {
+    launch_kron(h, nullptr, h->pr, nullptr, h->u, h->su, h->partA, 2, h->st, nullptr);
+    return;
+  }
+  const int grid = kron_grid(h);
+  static const bool fma = std::getenv("GLSGPU_KRON_FMA") != nullptr;  // measurement knob (not bitwise)
+  static const bool wide = std::getenv("GLSGPU_KRON_256") == nullptr;  // 512 threads (4x4) by default
+  const int nth = wide ? 512 : 256;
+  const size_t smem = (size_t)(2 * KG_BM * KG_LD + 2 * KG_BK * KG_LD + 2 * 5 * nth) * sizeof(double);
+#define KG_LAUNCH(F, W)                                                                                    \
+  k_kron_gemm<F, W><<<grid, nth, smem, h->s>>>(h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->pr, h->u, h->su, \
+                                               h->partA, h->st, wbuf_of(h))
+  if (fma && wide) KG_LAUNCH(true, 4);
+  else if (fma) KG_LAUNCH(true, 8);
+  else if (wide) KG_LAUNCH(false, 4);
+  else KG_LAUNCH(false, 8);
+#undef KG_LAUNCH
+  if (!h->capturing) h->launches++;
+  CKL("k_kron_gemm");
 }
 
 int rowpass_grid(const glsgpu_sur* h) { return (int)std::min<int64_t>((int64_t)h->G * h->nch, GRID_CAP); }
@@ -389,6 +415,10 @@ void stream_attrs(glsgpu_sur* h) {
     CK(cudaFuncGetAttributes(&fa, fn));
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm - (int)fa.sharedSizeBytes));
   };
+  set((const void*)k_kron_gemm<false, 8>, 0, 0);
+  set((const void*)k_kron_gemm<true, 8>, 0, 0);
+  set((const void*)k_kron_gemm<false, 4>, 0, 0);
+  set((const void*)k_kron_gemm<true, 4>, 0, 0);
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);
   set((const void*)k_stream<SMODE_C, false>, 0, 0);
@@ -1113,7 +1143,7 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   };
   // pass A: u = pr + mu u, su = Sigma u, d = u.su, uu = u.u
   ev(0);
-  launch_kron(h, nullptr, h->pr, nullptr, h->u, h->su, h->partA, 2, h->st, nullptr);
+  launch_pass_a(h);
   ev(1);
   const auto pa = combine3(h, h->partA, gA);
   k_scalar_a<<<1, NT, 0, h->s>>>(pa.first, pa.second, h->st);
