@@ -620,11 +620,11 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
   h->counters.factorizations = (uint64_t)G;
 }
 
-bool qr_fast(int n, int64_t rows) { return n <= 32 && rows <= QRR_NT; }
+bool qr_fast(int n, int64_t rows) { return n <= 32 && rows <= QRR_ROWS; }
 
 int64_t qr_leaf_rows(int n) {
   // narrow blocks: 256-row chunks, one row per thread in registers (k_qr_factor_reg / k_qr_formq_reg)
-  if (n <= 32) return QRR_NT;
+  if (n <= 32) return QRR_ROWS;
   // panel rows per chunk: the panel (rows x n doubles) in <= 200 KB of shared memory when possible,
   // at least 2n rows, at most 1024 (the register column of k_qr_formq).
   int64_t L = (QR_SMEM_BYTES / 8) / n;
@@ -688,18 +688,20 @@ void build_qr_plan(glsgpu_sur* h) {
         it.r0 = c * rows / nchk;
         it.rows = (c + 1) * rows / nchk - it.r0;
         it.rr0 = it.r0;
+        it.rhalf = QRR_NT;
         it.n = n;
         if (lvl == 0 && h->qtiled) {
           // tile-contiguous Q: leaf c = rows [256 c, 256 c + 256) (zero-padded) = Q tile c of block b
-          it.r0 = c * QRR_NT;
-          it.rows = std::min<int64_t>(QRR_NT, rows - it.r0);
+          it.r0 = c * QRR_ROWS;
+          it.rows = std::min<int64_t>(QRR_ROWS, rows - it.r0);
           it.src = h->X + h->p0[b] * h->ldx;
           it.lds = h->ldx;
           it.valid = h->M;
           it.scale = h->wts[b];
-          it.refl = h->Q + h->qoff[b] + c * QRR_NT * (int64_t)n;
+          it.refl = h->Q + h->qoff[b] + c * QRR_ROWS * (int64_t)n;  // tiles 2c and 2c + 1
           it.ldr = QRR_NT;
           it.rr0 = 0;
+          it.rhalf = (int64_t)QRR_NT * n;
         } else if (lvl == 0) {
           it.src = h->X + h->p0[b] * h->ldx;
           it.lds = h->ldx;
@@ -819,7 +821,7 @@ void run_qr(glsgpu_sur* h) {
   // zero Q (its padding rows stay zero) -- the level-0 reflectors overwrite the rest
   CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));
   const int nl = (int)h->qr_levels.size();
-  CK(cudaFuncSetAttribute(k_qr_formq_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, QRR_NT * 32 * 8));
+  CK(cudaFuncSetAttribute(k_qr_formq_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, QRR_ROWS * 32 * 8));
   const int fgrid_cap = 2 * 148;  // register-resident leaves: 1-2 CTAs per SM
   for (int l = 0; l < nl; ++l) {
     const auto& L = h->qr_levels[l];
@@ -860,7 +862,7 @@ void run_qr(glsgpu_sur* h) {
       launch_formq(h, L.max_rows, grid, L.smem_bytes, h->d_items + L.first, (int)L.count);
     }
     if (L.fcount) {
-      k_qr_formq_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, QRR_NT * 32 * 8, h->s>>>(
+      k_qr_formq_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, QRR_ROWS * 32 * 8, h->s>>>(
           h->d_items + L.ffirst, (int)L.fcount);
       if (!h->capturing) h->launches++;
       CKL("k_qr_formq_reg");
@@ -1073,33 +1075,32 @@ void qt_apply(glsgpu_sur* h, int mode, const double* vin, double* out, const Sol
 }
 
 double norm_probe(glsgpu_sur* h, int64_t iters) {
-  // operator_norm_probe (pcg.cpp:233-244): v = 1/sqrt(m); repeat: v = Sigma v; nrm = |v|; v /= nrm.
-  ensure_solver(h, 1);
-  const int64_t m = h->M_global * h->G;
-  const double v0 = 1.0 / std::sqrt(static_cast<double>(m));
-  // v0 in u (rows < M of each column), zero padding
-  CK(cudaMemsetAsync(h->u, 0, sizeof(double) * h->ldm * h->G, h->s));
-  std::vector<double> ones((size_t)h->M, v0);
-  for (int b = 0; b < h->G; ++b)
-    CK(cudaMemcpyAsync(h->u + (int64_t)b * h->ldm, ones.data(), sizeof(double) * h->M, cudaMemcpyHostToDevice, h->s));
-  CK(cudaMemsetAsync(h->d_stop, 0, sizeof(int), h->s));
-  CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->s));
-  double* a = h->u;
-  double* b = h->su;
-  int grid = 0;
-  for (int64_t it = 0; it < iters; ++it) {
-    launch_kron(h, a, nullptr, h->scal, nullptr, b, h->partA, it == 0 ? 0 : 1, nullptr, &grid);
-    auto pc = combine3(h, h->partA, grid);
-    k_probe_step<<<1, NT, 0, h->s>>>(pc.first, pc.second, h->scal, h->d_stop);
-    if (!h->capturing) h->launches++;
-    CKL("k_probe_step");
-    std::swap(a, b);
-  }
+  // operator_norm_probe (pcg.cpp:233-244) starts from v = 1/sqrt(m) 1.  For Sigma = Omega (x) I_M every
+  // row of reshape(v, M, G) then stays equal: v = 1_M x' and Sigma v = 1_M (x' Omega) (operators.cpp:45-50),
+  // so the power iteration is exactly an iteration on the G-vector x with |v| = sqrt(M |x|^2).  Each
+  // entry of Sigma v is the reference's own p-ascending sum; only the norm's summation order differs.
+  // O(iters G^2) on the host instead of iters full Kronecker passes over M x G.
+  const int G = h->G;
+  const double Mg = static_cast<double>(h->M_global);
+  const double m = Mg * G;
+  std::vector<double> x((size_t)G, 1.0 / std::sqrt(m)), y((size_t)G);
   double nrm = 0.0;
-  CK(cudaMemcpyAsync(&nrm, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->s));
-  CK(cudaStreamSynchronize(h->s));
-  CK(cudaMemsetAsync(h->u, 0, sizeof(double) * h->ldm * h->G, h->s));
-  CK(cudaMemsetAsync(h->su, 0, sizeof(double) * h->ldm * h->G, h->s));
+  for (int64_t it = 0; it < iters; ++it) {
+    for (int j = 0; j < G; ++j) {
+      double s = 0.0;
+      for (int p = 0; p < G; ++p) {
+        const double o = h->omega_h[(size_t)p + (size_t)j * G];
+        if (o == 0.0) continue;
+        s += x[(size_t)p] * o;
+      }
+      y[(size_t)j] = s;
+    }
+    double ss = 0.0;
+    for (int j = 0; j < G; ++j) ss += y[(size_t)j] * y[(size_t)j];
+    nrm = std::sqrt(Mg * ss);
+    if (nrm == 0.0) return 0.0;
+    for (int j = 0; j < G; ++j) x[(size_t)j] = y[(size_t)j] / nrm;
+  }
   return nrm;
 }
 

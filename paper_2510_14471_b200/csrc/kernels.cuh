@@ -1351,6 +1351,7 @@ struct QrItem {
   int64_t lds;
   int64_t r0, rows;    // chunk rows (of src)
   int64_t rr0;         // first row of the chunk in refl (= r0, or 0 for a tile-contiguous Q tile)
+  int64_t rhalf;       // register leaves: offset of row t + 256 from row t in refl (256, or a Q tile)
   int64_t valid;       // rows >= valid of src read as 0 (level 0: M; padding)
   double scale;        // level 0: w_b (DenseMatrix *= w, structured.cpp:435-436); else 1
   double* refl;        // reflector panel / explicit Q destination, ld ldr (same row range)
@@ -1527,43 +1528,13 @@ __global__ void __launch_bounds__(QR_NT) k_qr_formq(const QrItem* items, int nit
 }
 
 // ------------------------------------------------------------------------------------------
-// Register-resident TSQR leaves for narrow blocks (n <= 32, chunk rows <= 256): thread t owns row t
-// of the chunk in registers; the column loop is fully unrolled (k is compile-time) so the row never
-// leaves the register file.  Per Householder step: one block-wide scaled-norm reduction (LAPACK
-// dnrm2 (scale, ssq) combine, fixed order) and one 32-wide transpose-reduce for the trailing dots.
+// Register-resident TSQR leaves for narrow blocks (n <= 32, chunk rows <= RPT * 256): thread t owns
+// rows t + 256 h (h < RPT) of the chunk in registers.  Per Householder step one block reduction of 32
+// values (the column norm and every trailing dot at once); the k loop stays rolled (the factor rotates
+// its rows left one column per step) so the code stays in the instruction cache.
 constexpr int QRR_NT = 256;
-
-// (scale, ssq) combine of two partial Euclidean norms
-__device__ __forceinline__ void nrm_combine(double& s, double& q, double s2, double q2) {
-  if (s2 > s) {
-    if (s2 > 0.0) {
-      const double r = s / s2;
-      q = q2 + q * r * r;
-    }
-    s = s2;
-  } else if (s > 0.0 && s2 > 0.0) {
-    const double r = s2 / s;
-    q = q + q2 * r * r;
-  }
-}
-
-__device__ __forceinline__ double block_norm(double x, double* red /*[16]*/) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double s = fabs(x), q = (x != 0.0) ? 1.0 : 0.0;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const double s2 = __shfl_xor_sync(FULL, s, o), q2 = __shfl_xor_sync(FULL, q, o);
-    nrm_combine(s, q, s2, q2);
-  }
-  if (lane == 0) {
-    red[2 * warp] = s;
-    red[2 * warp + 1] = q;
-  }
-  __syncthreads();
-  double S = red[0], Qs = red[1];
-  for (int w = 1; w < QRR_NT / 32; ++w) nrm_combine(S, Qs, red[2 * w], red[2 * w + 1]);
-  return S * sqrt(Qs);
-}
+constexpr int QRR_RPT = 2;                 // rows per thread
+constexpr int QRR_ROWS = QRR_NT * QRR_RPT;  // leaf rows
 
 // acc[j] summed over the CTA (fixed order) -> out[j] (shared), all threads see it after the call
 template <int NB>
@@ -1580,6 +1551,12 @@ __device__ __forceinline__ void block_vec_sum(double (&acc)[NB], double (*red)[N
   __syncthreads();
 }
 
+// row (t + 256 h) of a chunk in the reflector / Q storage: column-major (ld ldr) or, for a level-0
+// leaf of tile-contiguous Q, two 256-row tiles rhalf doubles apart
+__device__ __forceinline__ int64_t qr_row_off(const QrItem& I, int j, int t, int h) {
+  return (int64_t)j * I.ldr + I.rr0 + t + (int64_t)h * I.rhalf;
+}
+
 template <int NB>
 __global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items, int nitems) {
   __shared__ double red_v[QRR_NT / 32][NB];
@@ -1591,15 +1568,21 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items
     const QrItem I = items[it];
     const int n = I.n;
     const int64_t L = I.rows;
-    const int64_t row = I.r0 + t;
-    double a[NB];
+    double a[QRR_RPT][NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j)
-      a[j] = (t < L && j < n && row < I.valid) ? I.src[(int64_t)j * I.lds + row] * I.scale : 0.0;
+    for (int h = 0; h < QRR_RPT; ++h) {
+      const int64_t rl = t + h * QRR_NT;
+      const int64_t row = I.r0 + rl;
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        a[h][j] = (rl < L && j < n && row < I.valid) ? I.src[(int64_t)j * I.lds + row] * I.scale : 0.0;
+    }
     // exact power-of-two pre-scale of the leaf so the plain sums of squares below cannot overflow
     double mx = 0.0;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) mx = fmax(mx, fabs(a[j]));
+    for (int h = 0; h < QRR_RPT; ++h)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) mx = fmax(mx, fabs(a[h][j]));
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
     if (lane == 0) redm[warp] = mx;
@@ -1610,23 +1593,36 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items
     if (mx > 0.0) frexp(mx, &ex);
     const double sc = ldexp(1.0, -ex), unsc = ldexp(1.0, ex);
 #pragma unroll
-    for (int j = 0; j < NB; ++j) a[j] *= sc;
-    double rkk = 0.0;
+    for (int h = 0; h < QRR_RPT; ++h)
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      if (k >= n) break;
-      // one reduction per column: S_k = x'x (x = column k, rows >= k) and S_j = x'a_j (j > k)
-      const double x = (t >= k) ? a[k] : 0.0;
-      if (t == k) {
+      for (int j = 0; j < NB; ++j) a[h][j] *= sc;
+    // Row rotation: at step k, a[h][0] is column k and a[h][j] column k + j.
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+      const int ntr = n - k;
+      // one reduction per column: S_0 = x'x (x = column k, rows >= k) and S_j = x'a_{k+j}
+      double x[QRR_RPT];
 #pragma unroll
-        for (int j = 0; j < NB; ++j) rowk[k & 1][j] = a[j];
+      for (int h = 0; h < QRR_RPT; ++h) x[h] = (t + h * QRR_NT >= k) ? a[h][0] : 0.0;
+      if (t == (k & (QRR_NT - 1))) {  // the owner of row k (h = k / 256)
+        const int hk = k / QRR_NT;
+#pragma unroll
+        for (int h = 0; h < QRR_RPT; ++h)
+          if (h == hk)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) rowk[k & 1][j] = a[h][j];
       }
       double acc[NB];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) acc[j] = (j >= k) ? x * a[j] : 0.0;
+      for (int j = 0; j < NB; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int h = 0; h < QRR_RPT; ++h) s += x[h] * a[h][j];
+        acc[j] = (j < ntr) ? s : 0.0;
+      }
       block_vec_sum<NB>(acc, red_v, svec);  // two __syncthreads
-      const double norm_x = sqrt(svec[k]);
-      const double wkk = rowk[k & 1][k];
+      const double norm_x = sqrt(svec[0]);
+      const double wkk = rowk[k & 1][0];
       double beta = 0.0, v0 = 1.0, alpha = 0.0;
       if (norm_x != 0.0) {
         alpha = wkk >= 0.0 ? -norm_x : norm_x;
@@ -1634,52 +1630,45 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_factor_reg(const QrItem* items
         beta = -1.0 / (alpha * v0);
       }
       if (t == 0) I.tau[k] = beta;
-      double v = 0.0;  // this row's reflector component (unit head)
-      if (norm_x != 0.0) {
-        if (t > k) {
-          a[k] = a[k] / v0;
-          v = a[k];
-        } else if (t == k) {
-          v = 1.0;
-          a[k] = v0;
-          rkk = alpha;
-        }
-        // v' a_j = (x' a_j - alpha a_kj) / v0; with beta_hat = beta v0^2 = -v0 / alpha the update factor
-        // is s_j beta_hat = -(x' a_j - alpha a_kj) / alpha: one reciprocal per column, no per-element divide
-        const double inv_alpha = 1.0 / alpha;
+      const double inv_v0 = 1.0 / v0, inv_alpha = (alpha != 0.0) ? 1.0 / alpha : 0.0;
+      // update factor s_j beta_hat = -(x'a_j - alpha a_kj) / alpha   (beta_hat = -v0 / alpha)
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          if (j > k && j < n) {
-            const double f = (alpha * rowk[k & 1][j] - svec[j]) * inv_alpha;  // s_j * beta_hat
-            a[j] -= f * v;
+      for (int h = 0; h < QRR_RPT; ++h) {
+        const int rl = t + h * QRR_NT;
+        double v = 0.0;       // this row's reflector component (unit head)
+        double col = a[h][0]; // final packed-panel entry of column k for this row
+        if (norm_x != 0.0) {
+          if (rl > k) {
+            col = a[h][0] * inv_v0;
+            v = col;
+          } else if (rl == k) {
+            v = 1.0;
+            col = v0;
           }
-        }
-      } else if (t == k) {
-        rkk = 0.0;
-      }
-    }
-    // packed panel -> reflector storage (scale-invariant); R rows (t < n) -> rout, unscaled exactly
 #pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = a[j];
-    if (t < n) {
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        if (j < n) {
-          const double r = (j > t) ? a[j] : (j == t ? rkk : 0.0);
-          I.rout[t + (int64_t)j * I.ldo] = r * unsc;
+          for (int j = 1; j < NB; ++j)
+            if (j < ntr) a[h][j] -= ((alpha * rowk[k & 1][j] - svec[j]) * inv_alpha) * v;
         }
+        if (rl < L) I.refl[qr_row_off(I, k, t, h)] = col;
+        if (rl < n) {  // R column k: R(rl, k) for rl < k, alpha on the diagonal, zero below
+          const double r = (rl < k) ? a[h][0] : (rl == k ? alpha : 0.0);
+          I.rout[rl + (int64_t)k * I.ldo] = r * unsc;
+        }
+        // rotate the row left by one column
+#pragma unroll
+        for (int j = 0; j < NB - 1; ++j) a[h][j] = a[h][j + 1];
+        a[h][NB - 1] = 0.0;
       }
     }
     __syncthreads();
   }
 }
 
-// Explicit thin Q of a narrow chunk: E = H_0 ... H_{n-1} [C; 0]; the output row in registers, the
-// packed reflectors staged in shared memory (rows x n, <= 64 KB).
+// Explicit thin Q of a narrow chunk: E = H_0 ... H_{n-1} [C; 0]; the output rows in registers, the
+// packed reflectors staged in shared memory (rows x n, <= 128 KB).
 template <int NB>
 __global__ void __launch_bounds__(QRR_NT, 1) k_qr_formq_reg(const QrItem* items, int nitems) {
-  extern __shared__ double P[];  // [NB][QRR_NT]
+  extern __shared__ double P[];  // [NB][QRR_ROWS]
   __shared__ double red_v[QRR_NT / 32][NB];
   __shared__ double svec[NB];
   const int t = threadIdx.x;
@@ -1688,33 +1677,56 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_formq_reg(const QrItem* items,
     const int n = I.n;
     const int64_t L = I.rows;
     __syncthreads();
-    for (int j = 0; j < n; ++j) P[j * QRR_NT + t] = (t < L) ? I.refl[(int64_t)j * I.ldr + I.rr0 + t] : 0.0;
-    double e[NB];
+    for (int j = 0; j < n; ++j)
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      double v = 0.0;
-      if (t < n && j < n) v = I.qpar ? I.qpar[t + (int64_t)j * I.ldp] : (t == j ? 1.0 : 0.0);
-      e[j] = v;
-    }
+      for (int h = 0; h < QRR_RPT; ++h) {
+        const int rl = t + h * QRR_NT;
+        P[j * QRR_ROWS + rl] = (rl < L) ? I.refl[qr_row_off(I, j, t, h)] : 0.0;
+      }
+    double e[QRR_RPT][NB];
+#pragma unroll
+    for (int h = 0; h < QRR_RPT; ++h)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int rl = t + h * QRR_NT;
+        double v = 0.0;
+        if (rl < n && j < n) v = I.qpar ? I.qpar[rl + (int64_t)j * I.ldp] : (rl == j ? 1.0 : 0.0);
+        e[h][j] = v;
+      }
     __syncthreads();
-#pragma unroll
-    for (int k = NB - 1; k >= 0; --k) {
-      if (k >= n) continue;
+#pragma unroll 1
+    for (int k = n - 1; k >= 0; --k) {
       const double beta = I.tau[k];
       if (beta == 0.0) continue;  // form_q_columns skips zero reflectors (linalg.cpp:83)
-      const double v0 = P[k * QRR_NT + k];
+      const double v0 = P[k * QRR_ROWS + k];
       const double beta_hat = beta * v0 * v0;
-      const double v = (t > k && t < L) ? P[k * QRR_NT + t] : (t == k ? 1.0 : 0.0);
+      double v[QRR_RPT];
+#pragma unroll
+      for (int h = 0; h < QRR_RPT; ++h) {
+        const int rl = t + h * QRR_NT;
+        v[h] = (rl > k && rl < L) ? P[k * QRR_ROWS + rl] : (rl == k ? 1.0 : 0.0);
+      }
       double acc[NB];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) acc[j] = v * e[j];
+      for (int j = 0; j < NB; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int h = 0; h < QRR_RPT; ++h) s += v[h] * e[h][j];
+        acc[j] = s;
+      }
       block_vec_sum<NB>(acc, red_v, svec);
 #pragma unroll
-      for (int j = 0; j < NB; ++j) e[j] -= (svec[j] * beta_hat) * v;
+      for (int h = 0; h < QRR_RPT; ++h)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) e[h][j] -= (svec[j] * beta_hat) * v[h];
     }
 #pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (j < n && t < L) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = e[j];
+    for (int h = 0; h < QRR_RPT; ++h) {
+      const int rl = t + h * QRR_NT;
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (j < n && rl < L) I.refl[qr_row_off(I, j, t, h)] = e[h][j];
+    }
   }
 }
 

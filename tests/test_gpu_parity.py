@@ -227,12 +227,17 @@ def test_counters_match_reference():
     """CostCounters after pcg_aug equal the reference's own tallies (preconditioner.cpp:9-47)."""
     if not oracle.have("ref"):
         pytest.skip("oracle/_ref not shipped")
-    # tol 1e-6 on well-determined problems: both runs stop on the threshold, far above the roundoff
-    # floor, so the iteration counts (and with them the apply tallies) are the same
+    # tol 1e-5: both runs stop on the threshold with a clear margin on either side of the crossing and
+    # far above the roundoff floor (at tol 1e-6 the first problem reaches its floor, where the stop
+    # depends on the last bits of c), so the iteration counts and the apply tallies are the same
+    tol = 1e-5
     for p in (synth.random_sur(3, 200, [5, 7, 4], seed=21), synth.random_sur(4, 300, [3, 6, 8, 2], seed=22)):
-        r = oracle.solve(p, "ref", cfg=oracle.make_config(tol_rel=1e-6), beta_true=p.beta)
+        r = oracle.solve(p, "ref", cfg=oracle.make_config(tol_rel=tol), beta_true=p.beta)
+        c = np.asarray(r.trace["c"])
+        thr = tol * tol * c[0]
+        assert r.termination == "Converged" and c[-2] > 2 * thr and c[-1] < 0.8 * thr
         op = api.sur_preconditioner(api.sur_from_problem(p))
-        g = api.pcg_aug(api.sur_from_problem(p), op, config=api.PcgConfig(tol_rel=1e-6))
+        g = api.pcg_aug(api.sur_from_problem(p), op, config=api.PcgConfig(tol_rel=tol))
         assert g.solution.iterations == r.iterations
         c = op.counters()
         got = [c.factorizations, c.factor_multiplies, c.pi_applies, c.xstar_t_applies, c.xstar_applies,
