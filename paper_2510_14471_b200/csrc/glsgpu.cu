@@ -6,6 +6,8 @@
 // (A: u update + Kronecker Sigma u + d; B: w/sw/r updates + Q'r; C: Pi r + c) with the scalar
 // control in single-CTA kernels between them, captured into CUDA graphs of `graph_chunk`
 // iterations; the host only checks the device's `active` flag between graph launches.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -137,6 +139,11 @@ struct glsgpu_sur {
   int n_narrow = 0, n_wide = 0;
   // solver buffers
   bool solver_ready = false;
+  // the ten M x G iteration vectors live in one slab (column blocks of G columns, ld = ldm) so that one
+  // 2-D tensor map reaches all of them: w[0..2], sw[0..2], r, u, su, pr (MV_* column-block indices)
+  double* mvec = nullptr;
+  CUtensorMap vmap;
+  bool vmap_ok = false;
   double *wb[3] = {nullptr, nullptr, nullptr}, *swb[3] = {nullptr, nullptr, nullptr};
   double *r = nullptr, *u = nullptr, *su = nullptr, *pr = nullptr;
   double *t = nullptr, *vs = nullptr, *est = nullptr, *t2 = nullptr, *xtw = nullptr, *zvec = nullptr,
@@ -238,6 +245,7 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
 }
 
 bool kron_gemm_ok(const glsgpu_sur* h) { return h->G > 128 && h->G <= 256 && h->G % 8 == 0; }
+bool kron_ws_ok(const glsgpu_sur* h) { return kron_gemm_ok(h) && h->vmap_ok && std::getenv("GLSGPU_KRON_OLD") == nullptr; }
 
 int kron_grid(const glsgpu_sur* h) {
   if (kron_gemm_ok(h)) return (int)std::min<int64_t>(h->ldm / KG_BM, 148);
@@ -253,10 +261,17 @@ void launch_pass_a(glsgpu_sur* h) {
     return;
   }
   const int grid = kron_grid(h);
+  if (kron_ws_ok(h)) {
+    k_kron_ws<<<grid, KW_NT, kw_smem_bytes(), h->s>>>(h->vmap, h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->u,
+                                                      h->su, h->partA, h->st, wbuf_of(h));
+    if (!h->capturing) h->launches++;
+    CKL("k_kron_ws");
+    return;
+  }
   static const bool fma = std::getenv("GLSGPU_KRON_FMA") != nullptr;  // measurement knob (not bitwise)
   static const bool wide = std::getenv("GLSGPU_KRON_256") == nullptr;  // 512 threads (4x4) by default
   const int nth = wide ? 512 : 256;
-  const size_t smem = (size_t)(2 * KG_BM * KG_LD + 2 * KG_BK * KG_LD + 2 * 5 * nth) * sizeof(double);
+  const size_t smem = (size_t)(2 * KG_XT + 2 * KG_BK * KG_LD + 2 * 5 * nth) * sizeof(double);
 #define KG_LAUNCH(F, W)                                                                                    \
   k_kron_gemm<F, W><<<grid, nth, smem, h->s>>>(h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->pr, h->u, h->su, \
                                                h->partA, h->st, wbuf_of(h))
@@ -415,6 +430,7 @@ void stream_attrs(glsgpu_sur* h) {
     CK(cudaFuncGetAttributes(&fa, fn));
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm - (int)fa.sharedSizeBytes));
   };
+  set((const void*)k_kron_ws, 0, 0);
   set((const void*)k_kron_gemm<false, 8>, 0, 0);
   set((const void*)k_kron_gemm<true, 8>, 0, 0);
   set((const void*)k_kron_gemm<false, 4>, 0, 0);
@@ -948,7 +964,7 @@ void destroy_impl(glsgpu_sur* h) {
   for (auto e : h->tev) cudaEventDestroy(e);
   void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
                   h->qr_store, h->qr_tau, h->qr_scratch, h->d_rank_flags, h->d_blk_narrow, h->d_blk_wide,
-                  h->wb[0], h->wb[1], h->wb[2], h->swb[0], h->swb[1], h->swb[2], h->r, h->u, h->su, h->pr, h->t,
+                  h->mvec, h->t,
                   h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,
                   h->scal, h->d_stop, h->st, h->rows_d, h->loc3, h->all3, h->t_loc, h->t_all, h->rloc, h->rall,
                   h->rstack, h->gtau, h->d_stack_off, h->d_gitems, h->d_qoff};
@@ -1001,17 +1017,42 @@ glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* om
   return h;
 }
 
+// 2-D tensor map over the vector slab: rows = ldm (inner), columns = MV_COUNT * G; boxes of 32 rows x
+// 8 columns (one pass-A element chunk of one vector).  cuTensorMapEncodeTiled comes from the driver
+// through the runtime's entry-point query (no libcuda link).
+bool make_vmap(glsgpu_sur* h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)h->ldm, (cuuint64_t)MV_COUNT * h->G};
+  const cuuint64_t strides[1] = {(cuuint64_t)h->ldm * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)KG_BM, (cuuint32_t)KG_BK};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = encode(&h->vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->mvec, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return rc == CUDA_SUCCESS;
+}
+
 void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
   if (!h->solver_ready) {
     const size_t mv = (size_t)(h->ldm * h->G);
+    h->mvec = dalloc<double>(mv * MV_COUNT);
     for (int i = 0; i < 3; ++i) {
-      h->wb[i] = dalloc<double>(mv);
-      h->swb[i] = dalloc<double>(mv);
+      h->wb[i] = h->mvec + (MV_W + i) * mv;
+      h->swb[i] = h->mvec + (MV_SW + i) * mv;
     }
-    h->r = dalloc<double>(mv);
-    h->u = dalloc<double>(mv);
-    h->su = dalloc<double>(mv);
-    h->pr = dalloc<double>(mv);
+    h->r = h->mvec + MV_R * mv;
+    h->u = h->mvec + MV_U * mv;
+    h->su = h->mvec + MV_SU * mv;
+    h->pr = h->mvec + MV_PR * mv;
+    h->vmap_ok = make_vmap(h);
     h->t = dalloc<double>(h->n);
     h->vs = dalloc<double>(h->n);
     h->est = dalloc<double>(h->n);

@@ -10,6 +10,7 @@
 // Data layout in HBM: every M x G state vector and the concatenated Q / X are
 // column-major with a padded leading dimension ldm = round_up(M, 32); padding rows are zero.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -119,6 +120,9 @@ __device__ __forceinline__ void warp_transpose_reduce(double (&acc)[NB]) {
 // Modes: in_mode 0: x = src; 1: x = src / (*div) (operator_norm_probe's v[i] /= nrm);
 //        2: pass A: u_new = pr + mu*u when st->mu_pending (pcg.cpp:210) else u; writes u.
 // Partials per CTA: [0] = sum x*out, [1] = sum x*x, [2] = sum out*out.
+// column-block indices of the iteration vectors in the vector slab (glsgpu_sur::mvec)
+enum { MV_W = 0, MV_SW = 3, MV_R = 6, MV_U = 7, MV_SU = 8, MV_PR = 9, MV_COUNT = 10 };
+
 struct WBuf {
   double* w[3];
   double* sw[3];
@@ -262,6 +266,8 @@ __global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles,
 constexpr int KG_BM = 32;   // rows per tile
 constexpr int KG_BK = 8;    // Omega rows per slab
 constexpr int KG_LD = 256;  // padded Omega row stride in shared memory
+constexpr int KG_XS = 34;   // U tile: row stride of one p (32 rows + 2 pad: conflict-light epilogue reads)
+constexpr int KG_XT = KG_LD * KG_XS;  // U tile doubles
 
 __device__ __forceinline__ uint32_t smem_u32_k(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -282,15 +288,15 @@ __global__ void __launch_bounds__(256 * (8 / WN), 1) k_kron_gemm(int G, int64_t 
   if (!st->active) return;
   extern __shared__ __align__(16) double ksm[];
   // layout (direct offsets off the extern array keep every access in the shared state space):
-  //   U tiles [p][r]          ksm + buf * KG_BM * KG_LD                     (2 buffers)
+  //   U tiles [p][r]          ksm + buf * KG_XT (row stride KG_XS)          (2 buffers)
   //   Omega slabs [p][c]      ksm + 2 KG_BM KG_LD + b * KG_BK * KG_LD         (2 buffers)
   //   element stages [v][tid] ksm + 2 KG_BM KG_LD + 2 KG_BK KG_LD + e * 5 NT  (2 buffers, 5 vectors)
-#define XSB(buf) (ksm + (buf) * (KG_BM * KG_LD))
-#define OSB(buf) (ksm + 2 * KG_BM * KG_LD + (buf) * (KG_BK * KG_LD))
+#define XSB(buf) (ksm + (buf) * KG_XT)
+#define OSB(buf) (ksm + 2 * KG_XT + (buf) * (KG_BK * KG_LD))
   constexpr int NTH = 256 * (8 / WN);        // threads
   constexpr int CS = 8 / WN;                  // column splits across warps
   constexpr int NP = WN / 2;                  // column pairs per thread
-#define ESB(buf) (ksm + 2 * KG_BM * KG_LD + 2 * KG_BK * KG_LD + (buf) * (5 * NTH))
+#define ESB(buf) (ksm + 2 * KG_XT + 2 * KG_BK * KG_LD + (buf) * (5 * NTH))
   const int tid = threadIdx.x, tx = tid & 31, w = tid >> 5;
   const int ty = w % 8, cbase = (w / 8) * (KG_LD / CS);  // rows 4 ty .. 4 ty + 3; columns cbase + 2 tx + 64 q
   const bool upd = st->mu_pending != 0, wupd = st->upd_pending != 0;
@@ -353,7 +359,7 @@ __global__ void __launch_bounds__(256 * (8 / WN), 1) k_kron_gemm(int G, int64_t 
     }
     const int idx = tid + e * NTH;
     const int p = idx / KG_BM, r = idx - p * KG_BM;
-    xs_next[p * KG_BM + r] = v;
+    xs_next[p * KG_XS + r] = v;
   };
 
   double p_xo = 0.0, p_xx = 0.0;
@@ -389,29 +395,44 @@ __global__ void __launch_bounds__(256 * (8 / WN), 1) k_kron_gemm(int G, int64_t 
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // slab s and element s - 1 landed
       __syncthreads();
       if (has_next && s >= 1 && s - 1 < per_thread) finish_elt(next * KG_BM, s - 1, (s - 1) & 1, xs_next);
+      // G % KG_BK == 0 (kron_gemm_ok): every slab is full, so the p loop is branch-free and the
+      // operands of step pp + 1 are loaded while step pp's products issue (register double buffer)
       const double* os = OSB(s & 1);
-      const int pmax = (s + 1) * KG_BK < G ? KG_BK : G - s * KG_BK;
+      const double* xp = xs + s * KG_BK * KG_XS + 4 * ty;
+      const double* op = os + cbase + 2 * tx;
+      double2 xa[2], oa[NP];
+      xa[0] = *reinterpret_cast<const double2*>(xp);
+      xa[1] = *reinterpret_cast<const double2*>(xp + 2);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) oa[q] = *reinterpret_cast<const double2*>(op + 64 * q);
 #pragma unroll
       for (int pp = 0; pp < KG_BK; ++pp) {
-        if (pp < pmax) {
-          const int p = s * KG_BK + pp;
-          const double2 x01 = *reinterpret_cast<const double2*>(xs + p * KG_BM + 4 * ty);
-          const double2 x23 = *reinterpret_cast<const double2*>(xs + p * KG_BM + 4 * ty + 2);
-          const double xr[4] = {x01.x, x01.y, x23.x, x23.y};
-          double o[WN];
+        double2 xb[2], ob[NP];
+        if (pp + 1 < KG_BK) {
+          xb[0] = *reinterpret_cast<const double2*>(xp + (pp + 1) * KG_XS);
+          xb[1] = *reinterpret_cast<const double2*>(xp + (pp + 1) * KG_XS + 2);
 #pragma unroll
-          for (int q = 0; q < NP; ++q) {
-            const double2 t2 = *reinterpret_cast<const double2*>(os + pp * KG_LD + cbase + 2 * tx + 64 * q);
-            o[2 * q] = t2.x;
-            o[2 * q + 1] = t2.y;
+          for (int q = 0; q < NP; ++q) ob[q] = *reinterpret_cast<const double2*>(op + (pp + 1) * KG_LD + 64 * q);
+        }
+        const double xr[4] = {xa[0].x, xa[0].y, xa[1].x, xa[1].y};
+        double o[WN];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          o[2 * q] = oa[q].x;
+          o[2 * q + 1] = oa[q].y;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < WN; ++q) {
+            if (FMA) acc[i][q] = fma(xr[i], o[q], acc[i][q]);
+            else acc[i][q] = acc[i][q] + xr[i] * o[q];
           }
+        if (pp + 1 < KG_BK) {
+          xa[0] = xb[0];
+          xa[1] = xb[1];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int q = 0; q < WN; ++q) {
-              if (FMA) acc[i][q] = fma(xr[i], o[q], acc[i][q]);
-              else acc[i][q] = acc[i][q] + xr[i] * o[q];
-            }
+          for (int q = 0; q < NP; ++q) oa[q] = ob[q];
         }
       }
       __syncthreads();  // slab buffer (s & 1) and element stage ((s - 1) & 1) free for reuse
@@ -436,7 +457,7 @@ __global__ void __launch_bounds__(256 * (8 / WN), 1) k_kron_gemm(int G, int64_t 
         for (int i = 0; i < 4; ++i) {
           const int r = 4 * ty + i;
           out[(int64_t)c * ldm + k0 + r] = acc[i][q];
-          const double x = xs[c * KG_BM + r];
+          const double x = xs[c * KG_XS + r];
           p_xo += x * acc[i][q];
           p_xx += x * x;
         }
@@ -722,6 +743,239 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// 2-D tensor-map load of one box (coordinates: inner = row, outer = column)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// Pass A, warp-specialised (128 < G <= 256, G % 8 == 0): the Kronecker apply Sigma u = U Omega
+// (operators.cpp:45-50) as an FP64 register-blocked product over 32-row tiles, with
+//   * 8 math warps: 8 rows x 4 columns per thread (4 row groups x 2 column halves), operands of step
+//     p + 1 loaded while step p's separate multiplies / adds issue (bitwise the reference's order:
+//     every output accumulated p-ascending from 0.0, no FMA contraction);
+//   * 1 loader warp: Omega' in 8-row slabs (8 G contiguous doubles each) by one cp.async.bulk per slab
+//     into a KW_OS-stage ring (full: tx bytes; empty: one arrival per math warp);
+//   * 1 element warp: builds the NEXT tile's U while the math warps run the current one.  Per 8-column
+//     chunk it loads the 32 x 8 boxes of u, pr, w, sw, su (one 2-D TMA each, through the tensor map of
+//     the vector slab; KW_ES-stage ring), then per element: the deferred w / sw update
+//     (pcg.cpp:151-152), u = pr + mu u (pcg.cpp:210), u.u.
+// The math warps write Sigma u and the u . Sigma u partials.  No CTA-wide barrier inside the tile loop.
+constexpr int KW_MATH = 8;                 // math warps
+constexpr int KW_NT = (KW_MATH + 2) * 32;  // + loader warp + element warp
+constexpr int KW_OS = 3;                   // Omega slab stages
+constexpr int KW_ES = 4;                   // element chunk stages
+constexpr int KW_XS = 32;                  // U tile row stride (doubles per p)
+constexpr int KW_XT = KG_LD * KW_XS;       // U tile doubles
+constexpr int KW_EC = 5 * KG_BK * KG_BM;   // element chunk doubles: 5 vectors x 8 columns x 32 rows
+constexpr size_t kw_smem_bytes() { return (size_t)(2 * KW_XT + KW_OS * KG_BK * KG_LD + KW_ES * KW_EC) * sizeof(double); }
+
+__global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CUtensorMap vmap, int G, int64_t ldm,
+                                                     int64_t ntiles, const double* __restrict__ omegaT,
+                                                     double* __restrict__ u_io, double* __restrict__ out,
+                                                     double* partials, const SolveState* st, WBuf wbuf) {
+  if (!st->active) return;
+  extern __shared__ __align__(128) double ksm[];
+  __shared__ __align__(8) uint64_t om_full[KW_OS], om_empty[KW_OS], el_full[KW_ES], xs_full[2], xs_empty[2];
+  __shared__ double red[KW_NT / 32][2];
+  double* const xsb = ksm;                                // [2][KG_LD][KW_XS]
+  double* const omb = ksm + 2 * KW_XT;                    // [KW_OS][KG_BK][G]
+  double* const elb = omb + KW_OS * KG_BK * KG_LD;        // [KW_ES][5][KG_BK][KG_BM]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nslab = G / KG_BK;
+  const int64_t ntl = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA
+  if (tid == 0) {
+    for (int i = 0; i < KW_OS; ++i) {
+      mbar_init(&om_full[i], 1);
+      mbar_init(&om_empty[i], KW_MATH);
+    }
+    for (int i = 0; i < KW_ES; ++i) mbar_init(&el_full[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&xs_full[i], 32);
+      mbar_init(&xs_empty[i], KW_MATH);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  double p_a = 0.0, p_b = 0.0;  // math warps: u . Sigma u; element warp: u . u
+  if (warp == KW_MATH) {
+    // ---------------- Omega loader
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(KG_BK * G * sizeof(double));
+      const int64_t total = ntl * nslab;
+      for (int64_t g = 0; g < total; ++g) {
+        const int sl = (int)(g % KW_OS);
+        if (g >= KW_OS) mbar_wait(&om_empty[sl], (uint32_t)(((g / KW_OS) & 1) ^ 1));
+        mbar_expect_tx(&om_full[sl], bytes);
+        tma_load_1d(omb + sl * KG_BK * KG_LD, omegaT + (int64_t)(g % nslab) * KG_BK * G, bytes, &om_full[sl]);
+      }
+    }
+  } else if (warp == KW_MATH + 1) {
+    // ---------------- element warp
+    const bool upd = st->mu_pending != 0, wupd = st->upd_pending != 0;
+    const double mu = st->mu, lp = st->lam_prev;
+    // column-block bases of u, pr, w_cur, sw_cur, su in the vector slab
+    const int cur = st->cur;
+    const int base[5] = {MV_U * G, MV_PR * G, (MV_W + cur) * G, (MV_SW + cur) * G, MV_SU * G};
+    double* __restrict__ wn = wbuf.w[st->nxt];
+    double* __restrict__ swn = wbuf.sw[st->nxt];
+    const uint32_t chunk_bytes = (uint32_t)((1 + (upd ? 1 : 0) + (wupd ? 3 : 0)) * KG_BK * KG_BM * sizeof(double));
+    const int64_t total = ntl * nslab;
+    auto issue = [&](int64_t e) {
+      const int sl = (int)(e % KW_ES);
+      const int64_t tile = blockIdx.x + (e / nslab) * gridDim.x;
+      const int c0 = (int)(e % nslab) * KG_BK;
+      double* E = elb + sl * KW_EC;
+      __syncwarp();
+      fence_proxy_async_smem();
+      if (lane == 0) {
+        mbar_expect_tx(&el_full[sl], chunk_bytes);
+        const int row = (int)(tile * KG_BM);
+        tma_load_2d(E, &vmap, row, base[0] + c0, &el_full[sl]);
+        if (upd) tma_load_2d(E + 1 * KG_BK * KG_BM, &vmap, row, base[1] + c0, &el_full[sl]);
+        if (wupd) {
+          tma_load_2d(E + 2 * KG_BK * KG_BM, &vmap, row, base[2] + c0, &el_full[sl]);
+          tma_load_2d(E + 3 * KG_BK * KG_BM, &vmap, row, base[3] + c0, &el_full[sl]);
+          tma_load_2d(E + 4 * KG_BK * KG_BM, &vmap, row, base[4] + c0, &el_full[sl]);
+        }
+      }
+      __syncwarp();
+    };
+    int64_t e_issue = 0;
+    for (; e_issue < KW_ES - 1 && e_issue < total; ++e_issue) issue(e_issue);
+    int64_t e = 0;
+    for (int64_t jl = 0; jl < ntl; ++jl) {
+      const int b = (int)(jl & 1);
+      if (jl >= 2) mbar_wait(&xs_empty[b], (uint32_t)(((jl >> 1) & 1) ^ 1));
+      double* xs = xsb + b * KW_XT;
+      const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KG_BM;
+      for (int k = 0; k < nslab; ++k, ++e) {
+        if (e_issue < total) issue(e_issue++);
+        const int sl = (int)(e % KW_ES);
+        mbar_wait(&el_full[sl], (uint32_t)((e / KW_ES) & 1));
+        const double* E = elb + sl * KW_EC;
+#pragma unroll
+        for (int cc = 0; cc < KG_BK; ++cc) {
+          const int c = k * KG_BK + cc;
+          const int64_t off = (int64_t)c * ldm + k0 + lane;
+          const double uo = E[(0 * KG_BK + cc) * KG_BM + lane];
+          if (wupd) {
+            wn[off] = E[(2 * KG_BK + cc) * KG_BM + lane] + (-lp) * uo;
+            swn[off] = E[(3 * KG_BK + cc) * KG_BM + lane] + (-lp) * E[(4 * KG_BK + cc) * KG_BM + lane];
+          }
+          double v = uo;
+          if (upd) {
+            v = E[(1 * KG_BK + cc) * KG_BM + lane] + mu * uo;
+            u_io[off] = v;
+          }
+          xs[c * KW_XS + lane] = v;
+          p_b += v * v;
+        }
+      }
+      __syncwarp();
+      mbar_arrive(&xs_full[b]);
+    }
+  } else {
+    // ---------------- math warps
+    const int rg = warp & 3, chf = warp >> 2;
+    const int cb = 128 * chf + 2 * lane;  // columns cb, cb + 1, cb + 64, cb + 65
+    int64_t g = 0;
+    for (int64_t jl = 0; jl < ntl; ++jl) {
+      const int b = (int)(jl & 1);
+      mbar_wait(&xs_full[b], (uint32_t)((jl >> 1) & 1));
+      const double* xs = xsb + b * KW_XT;
+      const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KG_BM;
+      double acc[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+      for (int s = 0; s < nslab; ++s, ++g) {
+        const int sl = (int)(g % KW_OS);
+        mbar_wait(&om_full[sl], (uint32_t)((g / KW_OS) & 1));
+        const double* xp = xs + s * KG_BK * KW_XS + 8 * rg;
+        const double* op = omb + sl * KG_BK * KG_LD + cb;
+        double2 xa[4], oa[2];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) xa[h] = *reinterpret_cast<const double2*>(xp + 2 * h);
+        oa[0] = *reinterpret_cast<const double2*>(op);
+        oa[1] = *reinterpret_cast<const double2*>(op + 64);
+#pragma unroll
+        for (int pp = 0; pp < KG_BK; ++pp) {
+          double2 xb[4], ob[2];
+          if (pp + 1 < KG_BK) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) xb[h] = *reinterpret_cast<const double2*>(xp + (pp + 1) * KW_XS + 2 * h);
+            ob[0] = *reinterpret_cast<const double2*>(op + (pp + 1) * G);
+            ob[1] = *reinterpret_cast<const double2*>(op + (pp + 1) * G + 64);
+          }
+          const double xr[8] = {xa[0].x, xa[0].y, xa[1].x, xa[1].y, xa[2].x, xa[2].y, xa[3].x, xa[3].y};
+          const double o[4] = {oa[0].x, oa[0].y, oa[1].x, oa[1].y};
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][q] = acc[i][q] + xr[i] * o[q];
+          if (pp + 1 < KG_BK) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) xa[h] = xb[h];
+            oa[0] = ob[0];
+            oa[1] = ob[1];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&om_empty[sl]);
+      }
+      // outputs (8 consecutive rows per column: 4 x 16-byte stores) + u . Sigma u partials
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = cb + 64 * (q >> 1) + (q & 1);
+        if (c < G) {
+          double* dst = out + (int64_t)c * ldm + k0 + 8 * rg;
+          const double* xc = xs + c * KW_XS + 8 * rg;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            *reinterpret_cast<double2*>(dst + 2 * h) = make_double2(acc[2 * h][q], acc[2 * h + 1][q]);
+            const double2 x2 = *reinterpret_cast<const double2*>(xc + 2 * h);
+            p_a += x2.x * acc[2 * h][q];
+            p_a += x2.y * acc[2 * h + 1][q];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xs_empty[b]);
+    }
+  }
+  // (d, u.u) partials of this CTA, fixed order (pcg.cpp:144-145)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    p_a += __shfl_xor_sync(FULL, p_a, o);
+    p_b += __shfl_xor_sync(FULL, p_b, o);
+  }
+  if (lane == 0) {
+    red[warp][0] = p_a;
+    red[warp][1] = p_b;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, bb = 0.0;
+    for (int w = 0; w < KW_NT / 32; ++w) {
+      a += red[w][0];
+      bb += red[w][1];
+    }
+    partials[blockIdx.x * 3 + 0] = a;
+    partials[blockIdx.x * 3 + 1] = bb;
+    partials[blockIdx.x * 3 + 2] = 0.0;
+  }
 }
 
 enum { SMODE_B = 0, SMODE_C = 1, SMODE_QT_R = 2, SMODE_QT_D = 3, SMODE_QT_V = 4, SMODE_DIAG = 5, SMODE_XS = 6 };
