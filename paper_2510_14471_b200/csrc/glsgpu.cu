@@ -347,9 +347,11 @@ struct StreamCfg {
 StreamCfg stream_cfg(const glsgpu_sur* h, int nmat, int nv) {
   StreamCfg c;
   const int nmax = h->nmax;
-  // largest tile (one row per thread at T = 256) whose ring of >= 2 stages fits in ~200 KB; a third
-  // stage when it still fits (deeper memory-level parallelism for the smaller tiles)
-  const int64_t budget = 200 * 1024;
+  // largest tile (one row per thread at T = 256) whose ring of >= 2 stages fits in ~220 KB (the opt-in
+  // 227 KB less the static buffers); a third stage when it still fits: with two stages only one tile
+  // is in flight while the other is consumed, too little memory-level parallelism for HBM3e
+  static const char* kb_env = std::getenv("GLSGPU_STREAM_KB");  // development knob
+  const int64_t budget = (kb_env ? std::atoi(kb_env) : 220) * 1024;
   c.T = 32;
   c.S = 2;
   for (int T : {256, 128, 64, 32}) {

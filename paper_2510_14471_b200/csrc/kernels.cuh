@@ -771,14 +771,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 //     the vector slab; KW_ES-stage ring), then per element: the deferred w / sw update
 //     (pcg.cpp:151-152), u = pr + mu u (pcg.cpp:210), u.u.
 // The math warps write Sigma u and the u . Sigma u partials.  No CTA-wide barrier inside the tile loop.
-constexpr int KW_MATH = 8;                 // math warps
-constexpr int KW_NT = (KW_MATH + 2) * 32;  // + loader warp + element warp
-constexpr int KW_OS = 3;                   // Omega slab stages
-constexpr int KW_ES = 4;                   // element chunk stages
-constexpr int KW_XS = 32;                  // U tile row stride (doubles per p)
-constexpr int KW_XT = KG_LD * KW_XS;       // U tile doubles
-constexpr int KW_EC = 5 * KG_BK * KG_BM;   // element chunk doubles: 5 vectors x 8 columns x 32 rows
+constexpr int KW_MATH = 8;                          // math warps
+constexpr int KW_EW = 2;                            // element warps (4 of each chunk's 8 columns each)
+constexpr int KW_NT = (KW_MATH + 1 + KW_EW) * 32;   // + loader warp
+constexpr int KW_OS = 3;                            // Omega slab stages
+constexpr int KW_ES = 4;                            // element chunk stages
+constexpr int KW_XS = 32;                           // U tile row stride (doubles per p)
+constexpr int KW_XT = KG_LD * KW_XS;                // U tile doubles
+constexpr int KW_EC = 5 * KG_BK * KG_BM;            // element chunk doubles: 5 vectors x 8 columns x 32 rows
 constexpr size_t kw_smem_bytes() { return (size_t)(2 * KW_XT + KW_OS * KG_BK * KG_LD + KW_ES * KW_EC) * sizeof(double); }
+
+// ring position: slot and phase parity advanced together (no division in the loops)
+struct RingPos {
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int stages) {
+    if (++slot == stages) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
 
 __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CUtensorMap vmap, int G, int64_t ldm,
                                                      int64_t ntiles, const double* __restrict__ omegaT,
@@ -786,7 +799,8 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
                                                      double* partials, const SolveState* st, WBuf wbuf) {
   if (!st->active) return;
   extern __shared__ __align__(128) double ksm[];
-  __shared__ __align__(8) uint64_t om_full[KW_OS], om_empty[KW_OS], el_full[KW_ES], xs_full[2], xs_empty[2];
+  __shared__ __align__(8) uint64_t om_full[KW_OS], om_empty[KW_OS], el_full[KW_ES], el_empty[KW_ES], xs_full[2],
+      xs_empty[2];
   __shared__ double red[KW_NT / 32][2];
   double* const xsb = ksm;                                // [2][KG_LD][KW_XS]
   double* const omb = ksm + 2 * KW_XT;                    // [KW_OS][KG_BK][G]
@@ -799,73 +813,85 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
       mbar_init(&om_full[i], 1);
       mbar_init(&om_empty[i], KW_MATH);
     }
-    for (int i = 0; i < KW_ES; ++i) mbar_init(&el_full[i], 1);
+    for (int i = 0; i < KW_ES; ++i) {
+      mbar_init(&el_full[i], 1);
+      mbar_init(&el_empty[i], KW_EW);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&xs_full[i], 32);
+      mbar_init(&xs_full[i], KW_EW * 32);
       mbar_init(&xs_empty[i], KW_MATH);
     }
     mbar_fence_init();
   }
   __syncthreads();
-  double p_a = 0.0, p_b = 0.0;  // math warps: u . Sigma u; element warp: u . u
+  double p_a = 0.0, p_b = 0.0;  // math warps: u . Sigma u; element warps: u . u
   if (warp == KW_MATH) {
     // ---------------- Omega loader
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)(KG_BK * G * sizeof(double));
-      const int64_t total = ntl * nslab;
-      for (int64_t g = 0; g < total; ++g) {
-        const int sl = (int)(g % KW_OS);
-        if (g >= KW_OS) mbar_wait(&om_empty[sl], (uint32_t)(((g / KW_OS) & 1) ^ 1));
-        mbar_expect_tx(&om_full[sl], bytes);
-        tma_load_1d(omb + sl * KG_BK * KG_LD, omegaT + (int64_t)(g % nslab) * KG_BK * G, bytes, &om_full[sl]);
+      RingPos w;
+      int s = 0;
+      for (int64_t g = 0; g < ntl * nslab; ++g) {
+        if (g >= KW_OS) mbar_wait(&om_empty[w.slot], w.phase ^ 1u);
+        mbar_expect_tx(&om_full[w.slot], bytes);
+        tma_load_1d(omb + w.slot * KG_BK * KG_LD, omegaT + (int64_t)s * KG_BK * G, bytes, &om_full[w.slot]);
+        w.next(KW_OS);
+        if (++s == nslab) s = 0;
       }
     }
-  } else if (warp == KW_MATH + 1) {
-    // ---------------- element warp
+  } else if (warp > KW_MATH) {
+    // ---------------- element warps: warp ew owns columns [4 ew, 4 ew + 4) of every chunk; element
+    // warp 0 lane 0 issues the chunk loads
+    const int ew = warp - KW_MATH - 1;
     const bool upd = st->mu_pending != 0, wupd = st->upd_pending != 0;
     const double mu = st->mu, lp = st->lam_prev;
     // column-block bases of u, pr, w_cur, sw_cur, su in the vector slab
     const int cur = st->cur;
-    const int base[5] = {MV_U * G, MV_PR * G, (MV_W + cur) * G, (MV_SW + cur) * G, MV_SU * G};
+    const int bu = MV_U * G, bp = MV_PR * G, bw = (MV_W + cur) * G, bsw = (MV_SW + cur) * G, bsu = MV_SU * G;
     double* __restrict__ wn = wbuf.w[st->nxt];
     double* __restrict__ swn = wbuf.sw[st->nxt];
     const uint32_t chunk_bytes = (uint32_t)((1 + (upd ? 1 : 0) + (wupd ? 3 : 0)) * KG_BK * KG_BM * sizeof(double));
     const int64_t total = ntl * nslab;
-    auto issue = [&](int64_t e) {
-      const int sl = (int)(e % KW_ES);
-      const int64_t tile = blockIdx.x + (e / nslab) * gridDim.x;
-      const int c0 = (int)(e % nslab) * KG_BK;
-      double* E = elb + sl * KW_EC;
-      __syncwarp();
-      fence_proxy_async_smem();
-      if (lane == 0) {
-        mbar_expect_tx(&el_full[sl], chunk_bytes);
-        const int row = (int)(tile * KG_BM);
-        tma_load_2d(E, &vmap, row, base[0] + c0, &el_full[sl]);
-        if (upd) tma_load_2d(E + 1 * KG_BK * KG_BM, &vmap, row, base[1] + c0, &el_full[sl]);
-        if (wupd) {
-          tma_load_2d(E + 2 * KG_BK * KG_BM, &vmap, row, base[2] + c0, &el_full[sl]);
-          tma_load_2d(E + 3 * KG_BK * KG_BM, &vmap, row, base[3] + c0, &el_full[sl]);
-          tma_load_2d(E + 4 * KG_BK * KG_BM, &vmap, row, base[4] + c0, &el_full[sl]);
-        }
+    const bool issuer = (ew == 0 && lane == 0);
+    RingPos ip;               // issue position
+    int64_t e_issue = 0, it_tile = blockIdx.x;
+    int it_c0 = 0;
+    auto issue = [&]() {
+      if (e_issue >= KW_ES) mbar_wait(&el_empty[ip.slot], ip.phase ^ 1u);
+      double* E = elb + ip.slot * KW_EC;
+      uint64_t* bar = &el_full[ip.slot];
+      mbar_expect_tx(bar, chunk_bytes);
+      const int row = (int)(it_tile * KG_BM);
+      tma_load_2d(E, &vmap, row, bu + it_c0, bar);
+      if (upd) tma_load_2d(E + 1 * KG_BK * KG_BM, &vmap, row, bp + it_c0, bar);
+      if (wupd) {
+        tma_load_2d(E + 2 * KG_BK * KG_BM, &vmap, row, bw + it_c0, bar);
+        tma_load_2d(E + 3 * KG_BK * KG_BM, &vmap, row, bsw + it_c0, bar);
+        tma_load_2d(E + 4 * KG_BK * KG_BM, &vmap, row, bsu + it_c0, bar);
       }
-      __syncwarp();
+      ip.next(KW_ES);
+      ++e_issue;
+      it_c0 += KG_BK;
+      if (it_c0 == G) {
+        it_c0 = 0;
+        it_tile += gridDim.x;
+      }
     };
-    int64_t e_issue = 0;
-    for (; e_issue < KW_ES - 1 && e_issue < total; ++e_issue) issue(e_issue);
-    int64_t e = 0;
+    if (issuer)
+      while (e_issue < KW_ES - 1 && e_issue < total) issue();
+    RingPos cp;               // consume position
     for (int64_t jl = 0; jl < ntl; ++jl) {
       const int b = (int)(jl & 1);
       if (jl >= 2) mbar_wait(&xs_empty[b], (uint32_t)(((jl >> 1) & 1) ^ 1));
       double* xs = xsb + b * KW_XT;
       const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KG_BM;
-      for (int k = 0; k < nslab; ++k, ++e) {
-        if (e_issue < total) issue(e_issue++);
-        const int sl = (int)(e % KW_ES);
-        mbar_wait(&el_full[sl], (uint32_t)((e / KW_ES) & 1));
-        const double* E = elb + sl * KW_EC;
+      for (int k = 0; k < nslab; ++k) {
+        if (issuer && e_issue < total) issue();
+        mbar_wait(&el_full[cp.slot], cp.phase);
+        const double* E = elb + cp.slot * KW_EC;
 #pragma unroll
-        for (int cc = 0; cc < KG_BK; ++cc) {
+        for (int ci = 0; ci < KG_BK / KW_EW; ++ci) {
+          const int cc = ew * (KG_BK / KW_EW) + ci;
           const int c = k * KG_BK + cc;
           const int64_t off = (int64_t)c * ldm + k0 + lane;
           const double uo = E[(0 * KG_BK + cc) * KG_BM + lane];
@@ -881,6 +907,12 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
           xs[c * KW_XS + lane] = v;
           p_b += v * v;
         }
+        // this warp's reads of the slot are done: release it to the issuer (generic reads before the
+        // next async-proxy write into it)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&el_empty[cp.slot]);
+        cp.next(KW_ES);
       }
       __syncwarp();
       mbar_arrive(&xs_full[b]);
@@ -889,7 +921,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
     // ---------------- math warps
     const int rg = warp & 3, chf = warp >> 2;
     const int cb = 128 * chf + 2 * lane;  // columns cb, cb + 1, cb + 64, cb + 65
-    int64_t g = 0;
+    RingPos rp;
     for (int64_t jl = 0; jl < ntl; ++jl) {
       const int b = (int)(jl & 1);
       mbar_wait(&xs_full[b], (uint32_t)((jl >> 1) & 1));
@@ -900,11 +932,10 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
-      for (int s = 0; s < nslab; ++s, ++g) {
-        const int sl = (int)(g % KW_OS);
-        mbar_wait(&om_full[sl], (uint32_t)((g / KW_OS) & 1));
+      for (int s = 0; s < nslab; ++s) {
+        mbar_wait(&om_full[rp.slot], rp.phase);
         const double* xp = xs + s * KG_BK * KW_XS + 8 * rg;
-        const double* op = omb + sl * KG_BK * KG_LD + cb;
+        const double* op = omb + rp.slot * KG_BK * KG_LD + cb;
         double2 xa[4], oa[2];
 #pragma unroll
         for (int h = 0; h < 4; ++h) xa[h] = *reinterpret_cast<const double2*>(xp + 2 * h);
@@ -933,7 +964,8 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&om_empty[sl]);
+        if (lane == 0) mbar_arrive(&om_empty[rp.slot]);
+        rp.next(KW_OS);
       }
       // outputs (8 consecutive rows per column: 4 x 16-byte stores) + u . Sigma u partials
 #pragma unroll
@@ -1023,8 +1055,9 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
   __shared__ double fred[FUSE ? NT : 1];
   const int S = a.S, T = a.T;
   double* xs = sm + (int64_t)S * a.stage_doubles;
-  double* colacc = xs + T;
-  double* tv = colacc + a.nmax;
+  // per-item n-vector slice (nmax <= 128 on this path): a static shared array, so the row dots read it
+  // with immediate shared-memory offsets
+  __shared__ double tv[128];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmat = stream_nmat<MODE>(a);
   constexpr int NV = stream_nvec<MODE>();
@@ -1049,17 +1082,26 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     k0 = (int64_t)ch * g.CH;
     k1 = (k0 + g.CH < g.ldm) ? k0 + g.CH : g.ldm;
   };
-  int64_t p_item = blockIdx.x, p_tile = 0;  // producer position
+  // producer position: the current item's block / rows are cached (one division per item, not per tile)
+  int64_t p_item = blockIdx.x, p_tile = 0, p_k0 = 0, p_k1 = 0, p_p0 = 0;
+  int p_b = 0, p_nb = 0;
+  auto p_load = [&]() {
+    if (p_item >= items) return;
+    item_rows(p_item, p_k0, p_k1);
+    p_b = (int)(p_item / g.nch);
+    p_nb = g.nb[p_b];
+    p_p0 = g.p0[p_b];
+  };
+  p_load();
   auto issue = [&](int stage) {
     // warp 0 only; advances the producer iterator
     if (p_item >= items) return;
-    int64_t k0, k1;
-    item_rows(p_item, k0, k1);
+    const int64_t k0 = p_k0, k1 = p_k1;
     const int64_t kb = k0 + p_tile * T;
     const int rows = (int)((k1 - kb) < T ? (k1 - kb) : T);
-    const int b = (int)(p_item / g.nch);
-    const int nb = g.nb[b];
-    const int64_t p0 = g.p0[b];
+    const int b = p_b;
+    const int nb = p_nb;
+    const int64_t p0 = p_p0;
     const uint32_t seg = (uint32_t)rows * 8u;
     // tile-contiguous Q with T == 256: the whole tile (padded to 256 rows) is ONE contiguous region,
     // moved as 4 bulk copies; otherwise one copy per column segment
@@ -1110,6 +1152,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     if (++p_tile * T >= k1 - k0) {
       p_tile = 0;
       p_item += gridDim.x;
+      p_load();
     }
   };
   if (warp == 0)
@@ -1127,6 +1170,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     const int nb = g.nb[b];
     const int64_t p0 = g.p0[b];
     const double wgt = g.wts[b];
+    const double iwgt = 1.0 / wgt;  // Q-side X v = Q (R v) / w (exact when w = 1)
     const int64_t vbase = (int64_t)b * g.ldm;
     // tv holds >= 32 entries (zero past n_b): the fused row dots read all 32
     for (int j = tid; j < (nb > 32 ? nb : 32); j += NT)
@@ -1177,7 +1221,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
               if (k < g.M)
                 for (int j = 0; j < nb; ++j) xv = xv + M1[(int64_t)j * T + t] * tv[j];
             } else {
-              xv = rdot() / wgt;
+              xv = rdot() * iwgt;
             }
             const double rn = rv - lam * (suv + xv);
             a.r[vo] = rn;
@@ -1227,7 +1271,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
             if (k < g.M)
               for (int j = 0; j < nb; ++j) xv = xv + M1[(int64_t)j * T + t] * tv[j];
           } else {
-            xv = qdot(M0 + t) / wgt;
+            xv = qdot(M0 + t) * iwgt;
           }
           const double rn = rv - lam * (suv + xv);
           a.r[vo] = rn;
