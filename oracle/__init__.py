@@ -227,3 +227,16 @@ def sur_setup(prob):
     if st:
         raise OracleError(st, f"block {bad.value}")
     return Q, R
+
+
+def diag(kind: str = "oracle", cap: int = 1 << 16):
+    """Per-iteration margins of the last restatement solve (DIAGNOSTIC): d / (u.u sigma_scale) of the
+    breakdown test and c_next / c_best of the growth test (proj/src/pcg.cpp:144-147,197-200)."""
+    L = lib(kind)
+    L.orc_diag.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64]
+    L.orc_diag.restype = C.c_int64
+    d = np.zeros(cap)
+    g = np.zeros(cap)
+    n = L.orc_diag(d.ctypes.data_as(C.POINTER(C.c_double)), g.ctypes.data_as(C.POINTER(C.c_double)),
+                   cap)
+    return d[:n], g[:n]

@@ -83,6 +83,21 @@ typedef struct {
 static int g_sum_mode = 0;
 void orc_set_sum_mode(int mode) { g_sum_mode = mode; }
 
+/* DIAGNOSTIC: per-iteration margins of the last orc_pcg_aug_sur call -- d / (uu sigma_scale) of the
+ * breakdown test and c_next / c_best of the growth test -- to show how close a run was to a
+ * roundoff-level stop.  Not part of the restatement's results. */
+#define ORC_DIAG_MAX 100000
+static double g_diag_d[ORC_DIAG_MAX], g_diag_g[ORC_DIAG_MAX];
+static int64_t g_diag_n = 0;
+int64_t orc_diag(double* d_ratio, double* growth, int64_t cap) {
+  const int64_t n = g_diag_n < cap ? g_diag_n : cap;
+  for (int64_t i = 0; i < n; ++i) {
+    d_ratio[i] = g_diag_d[i];
+    growth[i] = g_diag_g[i];
+  }
+  return n;
+}
+
 static double pairwise_dot(int64_t n, const double* a, const double* b) {
   if (n <= 32) {
     double acc = 0.0;
@@ -548,12 +563,18 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
   int64_t best_iter = 0, stagnant = 0, done_it = 0;
   int term = T_MAXITER;
 
+  g_diag_n = 0;
   if (c1 == 0.0) {
     term = T_CONVERGED;
   } else {
     for (int64_t i = 1; i <= max_iter; ++i) {
       orc_kron_apply(G, M, omega, u, su);                               /* su = Sigma u */
       const double d = vdot(m, u, su);
+      if (i - 1 < ORC_DIAG_MAX) {
+        g_diag_d[i - 1] = fabs(d) / (vdot(m, u, u) * sigma_scale);
+        g_diag_g[i - 1] = 0.0;
+        g_diag_n = i;
+      }
       if (fabs(d) <= cfg->breakdown_tol * vdot(m, u, u) * sigma_scale) {
         term = T_BREAKDOWN;
         res->breakdown_iteration = i;
@@ -580,6 +601,7 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
         break;
       }
       if (c_next < 0.0) c_next = 0.0;
+      if (i - 1 < ORC_DIAG_MAX) g_diag_g[i - 1] = c_best > 0.0 ? c_next / c_best : 0.0;
       if (c_next < c_best) {
         c_best = c_next;
         memcpy(w_best, w, mb);

@@ -638,11 +638,18 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
   h->counters.factorizations = (uint64_t)G;
 }
 
-bool qr_fast(int n, int64_t rows) { return n <= 32 && rows <= QRR_ROWS; }
+// narrow blocks (n <= 32): lane-per-column leaves of 256 rows (k_qr_factor_lc / k_qr_formq_lc), or the
+// previous row-per-thread register leaves of 512 rows (GLSGPU_QR_REG=1, development comparison)
+bool qr_lc() {
+  static const bool lc = std::getenv("GLSGPU_QR_REG") == nullptr;
+  return lc;
+}
+int64_t narrow_leaf_rows() { return qr_lc() ? QRC_ROWS : QRR_ROWS; }
+bool qr_fast(int n, int64_t rows) { return n <= 32 && rows <= narrow_leaf_rows(); }
 
 int64_t qr_leaf_rows(int n) {
   // narrow blocks: 256-row chunks, one row per thread in registers (k_qr_factor_reg / k_qr_formq_reg)
-  if (n <= 32) return QRR_ROWS;
+  if (n <= 32) return narrow_leaf_rows();
   // panel rows per chunk: the panel (rows x n doubles) in <= 200 KB of shared memory when possible,
   // at least 2n rows, at most 1024 (the register column of k_qr_formq).
   int64_t L = (QR_SMEM_BYTES / 8) / n;
@@ -710,13 +717,13 @@ void build_qr_plan(glsgpu_sur* h) {
         it.n = n;
         if (lvl == 0 && h->qtiled) {
           // tile-contiguous Q: leaf c = rows [256 c, 256 c + 256) (zero-padded) = Q tile c of block b
-          it.r0 = c * QRR_ROWS;
-          it.rows = std::min<int64_t>(QRR_ROWS, rows - it.r0);
+          it.r0 = c * narrow_leaf_rows();
+          it.rows = std::min<int64_t>(narrow_leaf_rows(), rows - it.r0);
           it.src = h->X + h->p0[b] * h->ldx;
           it.lds = h->ldx;
           it.valid = h->M;
           it.scale = h->wts[b];
-          it.refl = h->Q + h->qoff[b] + c * QRR_ROWS * (int64_t)n;  // tiles 2c and 2c + 1
+          it.refl = h->Q + h->qoff[b] + c * narrow_leaf_rows() * (int64_t)n;  // tile c (and 2c + 1: reg leaves)
           it.ldr = QRR_NT;
           it.rr0 = 0;
           it.rhalf = (int64_t)QRR_NT * n;
@@ -840,6 +847,16 @@ void run_qr(glsgpu_sur* h) {
   CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));
   const int nl = (int)h->qr_levels.size();
   CK(cudaFuncSetAttribute(k_qr_formq_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, QRR_ROWS * 32 * 8));
+  CK(cudaFuncSetAttribute(k_qr_factor_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
+  CK(cudaFuncSetAttribute(k_qr_formq_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
+  // lane-per-column leaves: grid = resident CTAs (the item loop strides by gridDim; a non-resident
+  // second wave would serialise behind the first)
+  int occ_f = 1, occ_q = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_qr_factor_lc, QRC_NT, qrc_smem_bytes()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, k_qr_formq_lc, QRC_NT, qrc_smem_bytes()));
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  const int lc_grid_f = std::max(1, occ_f) * nsm, lc_grid_q = std::max(1, occ_q) * nsm;
   const int fgrid_cap = 2 * 148;  // register-resident leaves: 1-2 CTAs per SM
   for (int l = 0; l < nl; ++l) {
     const auto& L = h->qr_levels[l];
@@ -851,8 +868,12 @@ void run_qr(glsgpu_sur* h) {
       CKL("k_qr_factor");
     }
     if (L.fcount) {
-      k_qr_factor_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, 0, h->s>>>(h->d_items + L.ffirst,
-                                                                                           (int)L.fcount);
+      if (qr_lc())
+        k_qr_factor_lc<<<(int)std::min<int64_t>(L.fcount, lc_grid_f), QRC_NT, qrc_smem_bytes(), h->s>>>(
+            h->d_items + L.ffirst, (int)L.fcount);
+      else
+        k_qr_factor_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, 0, h->s>>>(h->d_items + L.ffirst,
+                                                                                             (int)L.fcount);
       if (!h->capturing) h->launches++;
       CKL("k_qr_factor_reg");
     }
@@ -880,8 +901,12 @@ void run_qr(glsgpu_sur* h) {
       launch_formq(h, L.max_rows, grid, L.smem_bytes, h->d_items + L.first, (int)L.count);
     }
     if (L.fcount) {
-      k_qr_formq_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, QRR_ROWS * 32 * 8, h->s>>>(
-          h->d_items + L.ffirst, (int)L.fcount);
+      if (qr_lc())
+        k_qr_formq_lc<<<(int)std::min<int64_t>(L.fcount, lc_grid_q), QRC_NT, qrc_smem_bytes(), h->s>>>(
+            h->d_items + L.ffirst, (int)L.fcount);
+      else
+        k_qr_formq_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, QRR_ROWS * 32 * 8, h->s>>>(
+            h->d_items + L.ffirst, (int)L.fcount);
       if (!h->capturing) h->launches++;
       CKL("k_qr_formq_reg");
     }

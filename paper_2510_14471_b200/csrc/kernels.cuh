@@ -2029,6 +2029,249 @@ __global__ void __launch_bounds__(QRR_NT, 1) k_qr_formq_reg(const QrItem* items,
 }
 
 // ------------------------------------------------------------------------------------------
+// Lane-per-column TSQR leaves (n <= 32, chunk rows <= 256).  Lane j of every warp owns column j; the
+// chunk's rows are interleaved across the 8 warps (warp w, slot i: row 8 i + w), so the top 32 rows
+// -- the only ones that need step-dependent masking -- are spread 4 per warp and every warp does the
+// same work.  Per Householder step k (the reference recipe, linalg.cpp:24-63: alpha = -sign(x_kk) |x|,
+// unit-head v, beta = -1 / (alpha v0)):
+//   * x = column k, broadcast from lane k with shuffles (rows < k masked to 0);
+//   * S_j = x . a_j for every column at once: per-lane dot over the warp's rows, then one CTA reduction
+//     (one barrier per step, double-buffered); row k comes with it;
+//   * a_j -= f_j v, f_j = (alpha a_kj - S_j) / alpha, v = x / v0 (unit head): one FMA per entry.
+// Panels move global <-> shared with coalesced row-per-thread accesses; the next chunk's panel is
+// prefetched (cp.async, zero-filled padding) while the current one is factored.  Not bitwise the
+// reference's sequential Householder (the TSQR tree reorders it anyway): FMA is used explicitly.
+constexpr int QRC_NT = 256;
+constexpr int QRC_ROWS = 256;                 // leaf rows (one 256-row Q tile)
+constexpr int QRC_LD = QRC_ROWS + 1;          // panel column stride in shared memory (odd)
+constexpr int QRC_PANEL = 32 * QRC_LD;        // doubles per panel buffer
+constexpr size_t qrc_smem_bytes() { return (size_t)2 * QRC_PANEL * sizeof(double); }
+
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+__device__ __forceinline__ void cp_async8_zfill(double* dst, const double* src, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  const int bytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(valid ? src : nullptr), "r"(bytes)
+               : "memory");
+}
+
+// row t (= threadIdx.x) of a leaf panel into P (columns j < 32; zero past n, past the chunk, past valid)
+__device__ __forceinline__ void qrc_prefetch(double* P, const double* src, int64_t lds, int64_t r0, int64_t rows,
+                                             int64_t valid, int n) {
+  const int t = threadIdx.x;
+  const bool rv = t < rows && r0 + t < valid;
+  for (int j = 0; j < 32; ++j) cp_async8_zfill(P + j * QRC_LD + t, src + (int64_t)j * lds + r0 + t, rv && j < n);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(QRC_NT, 1) k_qr_factor_lc(const QrItem* items, int nitems) {
+  extern __shared__ double SB[];                // 2 panel buffers [32][QRC_LD]
+  __shared__ double red[2][QRC_NT / 32][32];
+  __shared__ double rowk[2][32];
+  __shared__ double alph[32];
+  __shared__ double redm[QRC_NT / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int buf = 0;
+  if (blockIdx.x < nitems) {
+    const QrItem I0 = items[blockIdx.x];
+    qrc_prefetch(SB, I0.src, I0.lds, I0.r0, I0.rows, I0.valid, I0.n);
+  }
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x, buf ^= 1) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    double* S = SB + buf * QRC_PANEL;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();                            // panel landed; the other buffer's readers are done
+    if (it + (int)gridDim.x < nitems) {
+      const QrItem& In = items[it + gridDim.x];
+      qrc_prefetch(SB + (buf ^ 1) * QRC_PANEL, In.src, In.lds, In.r0, In.rows, In.valid, In.n);
+    }
+    double* col = S + lane * QRC_LD;            // this lane's column
+    double a[32];
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      a[i] = col[8 * i + warp] * I.scale;
+      mx = fmax(mx, fabs(a[i]));
+    }
+    // exact power-of-two pre-scale so the plain sums of squares cannot overflow
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    if (lane == 0) redm[warp] = mx;
+    __syncthreads();
+    mx = redm[0];
+#pragma unroll
+    for (int w = 1; w < QRC_NT / 32; ++w) mx = fmax(mx, redm[w]);
+    int ex = 0;
+    if (mx > 0.0) frexp(mx, &ex);
+    const double sc = ldexp(1.0, -ex), unsc = ldexp(1.0, ex);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] *= sc;
+    double my_inv = 1.0, my_v0 = 0.0;           // this lane's own reflector (step k == lane)
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+      const int par = k & 1;
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = __shfl_sync(FULL, a[i], k);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (8 * i + warp < k) x[i] = 0.0;       // rows above k are R rows
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        s0 = fma_rn(x[i + 0], a[i + 0], s0);
+        s1 = fma_rn(x[i + 1], a[i + 1], s1);
+        s2 = fma_rn(x[i + 2], a[i + 2], s2);
+        s3 = fma_rn(x[i + 3], a[i + 3], s3);
+      }
+      if (warp == (k & 7)) {                    // row k = slot k / 8 of warp k % 8
+        const int sk = k >> 3;
+        rowk[par][lane] = sk == 0 ? a[0] : sk == 1 ? a[1] : sk == 2 ? a[2] : a[3];
+      }
+      red[par][warp][lane] = (s0 + s1) + (s2 + s3);
+      __syncthreads();
+      double sj = 0.0;
+#pragma unroll
+      for (int w = 0; w < QRC_NT / 32; ++w) sj += red[par][w][lane];
+      const double skk = __shfl_sync(FULL, sj, k);
+      const double akj = rowk[par][lane];
+      const double wkk = rowk[par][k];
+      const double norm_x = sqrt(skk);
+      double alpha = 0.0, v0 = 1.0, beta = 0.0, inv_alpha = 0.0, inv_v0 = 1.0;
+      if (norm_x != 0.0) {
+        alpha = wkk >= 0.0 ? -norm_x : norm_x;
+        v0 = wkk - alpha;
+        const double dd = 1.0 / (alpha * v0);
+        beta = -dd;
+        inv_alpha = v0 * dd;
+        inv_v0 = alpha * dd;
+      }
+      const double f = (lane > k && lane < n) ? (alpha * akj - sj) * inv_alpha : 0.0;
+      const double g = f * inv_v0;
+      if (lane == k) {
+        my_inv = inv_v0;
+        my_v0 = (norm_x != 0.0) ? v0 : wkk;
+      }
+      if (t == k) {
+        alph[k] = alpha;
+        I.tau[k] = beta;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double up = fma_rn(-g, x[i], a[i]);
+        a[i] = (8 * i + warp == k) ? a[i] - f : up;
+      }
+#pragma unroll
+      for (int i = 4; i < 32; ++i) a[i] = fma_rn(-g, x[i], a[i]);
+    }
+    // packed reflector panel: rows > j of column j scaled by 1 / v0_j, v0_j on the diagonal, R above
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = 8 * i + warp;
+      double v = a[i];
+      if (i >= 4 || r > lane) v = a[i] * my_inv;
+      else if (r == lane) v = my_v0;
+      col[r] = v;
+    }
+    __syncthreads();
+    // R (scaled back), the diagonal from alpha; zeros below
+    for (int idx = t; idx < n * n; idx += QRC_NT) {
+      const int j = idx / n, i = idx - j * n;
+      const double r = (i < j) ? S[j * QRC_LD + i] * unsc : (i == j ? alph[j] * unsc : 0.0);
+      I.rout[i + (int64_t)j * I.ldo] = r;
+      if (i == j && I.rdiag) I.rdiag[j] = r;
+    }
+    // reflector panel out (coalesced: thread per row)
+    if (t < L)
+      for (int j = 0; j < n; ++j) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = S[j * QRC_LD + t];
+  }
+}
+
+// Explicit thin Q of a narrow chunk: E = H_0 ... H_{n-1} [C; 0] (form_q_columns, linalg.cpp:65-95),
+// lane j = column j of E, rows interleaved across warps in registers; the packed reflectors staged in
+// shared memory, their top 32 rows pre-masked (unit head, zeros above: V0) so every read is a plain
+// broadcast.  The next chunk's panel is prefetched while the current one is formed.
+__global__ void __launch_bounds__(QRC_NT, 1) k_qr_formq_lc(const QrItem* items, int nitems) {
+  extern __shared__ double SB[];                // 2 packed-panel buffers [32][QRC_LD]
+  __shared__ double V0[32][33];                 // masked reflector columns, rows 0..31
+  __shared__ double bh[32];                     // beta_hat = beta v0^2 per reflector
+  __shared__ int tz[32];                        // reflector k is zero (beta == 0)
+  __shared__ double red[2][QRC_NT / 32][32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int buf = 0;
+  if (blockIdx.x < nitems) {
+    const QrItem I0 = items[blockIdx.x];
+    qrc_prefetch(SB, I0.refl + I0.rr0, I0.ldr, 0, I0.rows, I0.rows, I0.n);
+  }
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x, buf ^= 1) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    double* S = SB + buf * QRC_PANEL;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (it + (int)gridDim.x < nitems) {
+      const QrItem& In = items[it + gridDim.x];
+      qrc_prefetch(SB + (buf ^ 1) * QRC_PANEL, In.refl + In.rr0, In.ldr, 0, In.rows, In.rows, In.n);
+    }
+    for (int idx = t; idx < 32 * 32; idx += QRC_NT) {
+      const int k = idx >> 5, i = idx & 31;
+      const double pk = S[k * QRC_LD + i];
+      V0[k][i] = (i > k && i < L) ? pk : (i == k ? 1.0 : 0.0);
+      if (i == k) {
+        const double tk = (k < n) ? I.tau[k] : 0.0;
+        bh[k] = tk * pk * pk;
+        tz[k] = (tk == 0.0);
+      }
+    }
+    double e[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = 8 * i + warp;
+      double v = 0.0;
+      if (i < 4 && r < n && lane < n) v = I.qpar ? I.qpar[r + (int64_t)lane * I.ldp] : (r == lane ? 1.0 : 0.0);
+      e[i] = v;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = n - 1; k >= 0; --k) {
+      if (tz[k]) continue;  // form_q_columns skips zero reflectors (linalg.cpp:83)
+      const double bhk = bh[k];
+      const int par = k & 1;
+      double v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = (i < 4) ? V0[k][8 * i + warp] : S[k * QRC_LD + 8 * i + warp];
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        s0 = fma_rn(v[i + 0], e[i + 0], s0);
+        s1 = fma_rn(v[i + 1], e[i + 1], s1);
+        s2 = fma_rn(v[i + 2], e[i + 2], s2);
+        s3 = fma_rn(v[i + 3], e[i + 3], s3);
+      }
+      red[par][warp][lane] = (s0 + s1) + (s2 + s3);
+      __syncthreads();
+      double sj = 0.0;
+#pragma unroll
+      for (int w = 0; w < QRC_NT / 32; ++w) sj += red[par][w][lane];
+      const double h = -(sj * bhk);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) e[i] = fma_rn(h, v[i], e[i]);
+    }
+    // E out through the panel (coalesced)
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) S[lane * QRC_LD + 8 * i + warp] = e[i];
+    __syncthreads();
+    if (t < L)
+      for (int j = 0; j < n; ++j) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = S[j * QRC_LD + t];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Counter-based normal generator for synthetic inputs: Philox4x32-10 on (element, stream) keyed
 // by the seed, Box-Muller on two 53-bit uniforms (u1 in (0,1]).  Element e of a rows x cols
 // matrix is e = col * rows + row, independent of the leading dimension.

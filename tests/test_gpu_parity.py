@@ -44,25 +44,38 @@ def solve_both(p, mode="x", diag=1, cfg_kw=None, w1=None, z1=None):
     return o, g, op
 
 
+# kind: "strict" -- same termination and iteration, b to 1e-10;
+#       "growth" -- singular Omega: c falls to its roundoff floor (best iterate 50) and the run stops on the
+#                   growth test (c_next > 1e4 c_best, pcg.cpp:197-200) when that floor NOISE has grown
+#                   1e4-fold: the oracle's ratio is 8073 at iteration 66 and 12378 at 67
+#                   (oracle.orc_diag), so any rounding difference in Q moves the stop by one.  The
+#                   result is the best iterate: the same iterate must be selected and b agree to 1e-10;
+#       "tail"   -- slow tail (c3), see below.
 PARITY = [
-    ("c0", lambda: synth.make_problem(0), True),
-    ("c1_M400", lambda: synth.make_problem(1, M=400), True),
-    ("c2_M1000", lambda: synth.make_problem(2, M=1000), True),
-    ("c4_G32_M2000", lambda: synth.make_problem(4, M=2000, G=32), True),
-    ("c4_G256_M300", lambda: synth.make_problem(4, M=300), True),
-    ("c3_M600_N40", lambda: synth.make_problem(3, M=600, N=40), False),
+    ("c0", lambda: synth.make_problem(0), "strict"),
+    ("c1_M400", lambda: synth.make_problem(1, M=400), "strict"),
+    ("c2_M1000", lambda: synth.make_problem(2, M=1000), "growth"),
+    ("c4_G32_M2000", lambda: synth.make_problem(4, M=2000, G=32), "strict"),
+    ("c4_G256_M300", lambda: synth.make_problem(4, M=300), "strict"),
+    ("c3_M600_N40", lambda: synth.make_problem(3, M=600, N=40), "tail"),
 ]
 
 
 @pytest.mark.parametrize("mode", ["x", "qr"])
-@pytest.mark.parametrize("name,mk,strict", PARITY, ids=[c[0] for c in PARITY])
-def test_solve_parity(name, mk, strict, mode):
+@pytest.mark.parametrize("name,mk,kind", PARITY, ids=[c[0] for c in PARITY])
+def test_solve_parity(name, mk, kind, mode):
     p = mk()
     o, g, _ = solve_both(p, mode=mode, diag=0)
     s = g.solution
-    if strict:
+    if kind == "strict":
         assert s.iterations == o.iterations, (s.iterations, o.iterations)
         assert s.termination.name == o.termination
+        assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
+    elif kind == "growth":
+        assert s.termination.name == o.termination == "Breakdown"
+        assert abs(s.iterations - o.iterations) <= 2, (s.iterations, o.iterations)
+        cg, co = np.asarray(g.trace.rows["c"])[1:], np.asarray(o.trace["c"])[1:]
+        assert int(np.argmin(cg)) == int(np.argmin(co))  # the same best iterate is returned
         assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
     else:
         # slow-tail config: c crosses tol^2 c1 so gradually that ANY change of summation order moves the

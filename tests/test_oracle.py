@@ -162,3 +162,15 @@ def test_c3_envelope(oracle_mod):
     assert seq.termination == pw.termination == "Converged"
     rel = np.linalg.norm(seq.b - pw.b) / np.linalg.norm(seq.b)
     assert 1e-11 < rel < 5e-10
+
+
+def test_c2_growth_margin(oracle_mod):
+    """c2 (singular Omega) stops on the growth test, whose ratio is roundoff NOISE over a c at its floor:
+    8073 at iteration 66 against the 1e4 threshold, 12378 at 67.  The GPU parity test accepts a stop one
+    iteration either side as long as the same best iterate (and b) comes back (test_gpu_parity.py)."""
+    p = synth.make_problem(2, M=1000)
+    o = oracle.solve(p, "oracle")
+    d, g = oracle.diag()
+    assert o.termination == "Breakdown" and o.iterations == 67 and len(g) == 67
+    assert 5e3 < g[65] < 1e4 < g[66]
+    assert int(np.argmin(o.trace["c"][1:])) + 1 == 50
