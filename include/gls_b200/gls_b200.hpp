@@ -94,6 +94,7 @@ struct PcgConfig {
   int diag_every = 1;
   int xv_mode = GLSGPU_XV_X;
   int graph_chunk = 0;
+  int kron_fma = 0;
 };
 
 struct PcgTraceRow {
@@ -253,6 +254,7 @@ inline AugSolveResult pcg_aug(const SurModel& sur, const SurOperator& op, const 
   c.diag_every = config.diag_every;
   c.xv_mode = config.xv_mode;
   c.graph_chunk = config.graph_chunk;
+  c.kron_fma = config.kron_fma;
   bool w1_zero = true, z1_zero = true;
   for (double v : w1) w1_zero = w1_zero && v == 0.0;
   for (double v : z1) z1_zero = z1_zero && v == 0.0;

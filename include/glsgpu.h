@@ -75,6 +75,10 @@ typedef struct {
   int32_t xv_mode;           /* GLSGPU_XV_X or GLSGPU_XV_QR */
   int32_t graph_chunk;       /* PCG iterations per CUDA-graph launch (0 = auto) */
   int32_t kernel_timing;     /* 1 = record CUDA events around every streaming pass (glsgpu_kernel_stats) */
+  int32_t kron_fma;          /* Kronecker pass of the FP64-bound shapes (128 < G <= 256): 0 = separate
+                                multiply and add, bitwise the reference's operator* (default); 1 = one
+                                fused multiply-add per term (half the FP64 instructions; one rounding per
+                                term instead of two) */
 } glsgpu_pcg_config;
 
 /* gls::PcgTraceRow (proj/include/gls/pcg.hpp:32-39).  Diagnostics not computed are NaN. */

@@ -19,7 +19,8 @@ class PcgConfigC(C.Structure):
     _fields_ = [("tol_rel", C.c_double), ("max_iter", C.c_int64), ("breakdown_tol", C.c_double),
                 ("stagnation_window", C.c_int64), ("growth_tol", C.c_double), ("growth_window", C.c_int64),
                 ("record_z_every", C.c_int64), ("diag_every", C.c_int32), ("xv_mode", C.c_int32),
-                ("graph_chunk", C.c_int32), ("kernel_timing", C.c_int32)]
+                ("graph_chunk", C.c_int32), ("kernel_timing", C.c_int32),
+                ("kron_fma", C.c_int32)]
 
 
 class TraceRowC(C.Structure):

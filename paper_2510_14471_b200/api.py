@@ -97,11 +97,13 @@ class PcgConfig:
     xv_mode: str = "x"         # "x": X v with the original X (reference); "qr": Q (R v) by recurrence
     graph_chunk: int = 0
     kernel_timing: bool = False
+    kron_fma: bool = False     # FP64-bound Kronecker pass (128 < G <= 256) with fused multiply-adds
 
     def to_c(self) -> L.PcgConfigC:
         return L.PcgConfigC(self.tol_rel, self.max_iter, self.breakdown_tol, self.stagnation_window, self.growth_tol,
                             self.growth_window, self.record_z_every, self.diag_every,
-                            1 if self.xv_mode == "qr" else 0, self.graph_chunk, 1 if self.kernel_timing else 0)
+                            1 if self.xv_mode == "qr" else 0, self.graph_chunk, 1 if self.kernel_timing else 0,
+                            1 if self.kron_fma else 0)
 
 
 TRACE_DTYPE = np.dtype([("iter", np.int64), ("c", np.float64), ("aug_residual_norm", np.float64),

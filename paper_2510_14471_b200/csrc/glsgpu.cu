@@ -160,7 +160,8 @@ struct glsgpu_sur {
   std::vector<glsgpu_kernel_stat> kstats;
   // graphs
   cudaGraphExec_t graph = nullptr;
-  int graph_chunk = 0, graph_xmode = -1, graph_diag = -2, graph_timing = -1;
+  int graph_chunk = 0, graph_xmode = -1, graph_diag = -2, graph_timing = -1, graph_fma = -1;
+  int kron_fma = 0;  // glsgpu_pcg_config::kron_fma of the current solve
   std::vector<cudaEvent_t> tev;  // timing events captured into the graph
   int64_t graph_kernels = 0;     // kernel nodes in the instantiated graph
   int64_t launches = 0;          // kernels launched by this handle (graph nodes counted per launch)
@@ -244,8 +245,8 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
   if (!h->capturing) h->launches++;
 }
 
-bool kron_gemm_ok(const glsgpu_sur* h) { return h->G > 128 && h->G <= 256 && h->G % 8 == 0; }
-bool kron_ws_ok(const glsgpu_sur* h) { return kron_gemm_ok(h) && h->vmap_ok && std::getenv("GLSGPU_KRON_OLD") == nullptr; }
+// the warp-specialised FP64 kernel serves the compute-bound shapes; the generic k_kron the rest
+bool kron_gemm_ok(const glsgpu_sur* h) { return h->G > 128 && h->G <= 256 && h->G % 8 == 0 && h->vmap_ok; }
 
 int kron_grid(const glsgpu_sur* h) {
   if (kron_gemm_ok(h)) return (int)std::min<int64_t>(h->ldm / KG_BM, 148);
@@ -261,27 +262,14 @@ void launch_pass_a(glsgpu_sur* h) {
     return;
   }
   const int grid = kron_grid(h);
-  if (kron_ws_ok(h)) {
-    k_kron_ws<<<grid, KW_NT, kw_smem_bytes(), h->s>>>(h->vmap, h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->u,
-                                                      h->su, h->partA, h->st, wbuf_of(h));
-    if (!h->capturing) h->launches++;
-    CKL("k_kron_ws");
-    return;
-  }
-  static const bool fma = std::getenv("GLSGPU_KRON_FMA") != nullptr;  // measurement knob (not bitwise)
-  static const bool wide = std::getenv("GLSGPU_KRON_256") == nullptr;  // 512 threads (4x4) by default
-  const int nth = wide ? 512 : 256;
-  const size_t smem = (size_t)(2 * KG_XT + 2 * KG_BK * KG_LD + 2 * 5 * nth) * sizeof(double);
-#define KG_LAUNCH(F, W)                                                                                    \
-  k_kron_gemm<F, W><<<grid, nth, smem, h->s>>>(h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->pr, h->u, h->su, \
-                                               h->partA, h->st, wbuf_of(h))
-  if (fma && wide) KG_LAUNCH(true, 4);
-  else if (fma) KG_LAUNCH(true, 8);
-  else if (wide) KG_LAUNCH(false, 4);
-  else KG_LAUNCH(false, 8);
-#undef KG_LAUNCH
+  if (h->kron_fma)
+    k_kron_ws<true><<<grid, KW_NT, kw_smem_bytes(), h->s>>>(h->vmap, h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->u,
+                                                            h->su, h->partA, h->st, wbuf_of(h));
+  else
+    k_kron_ws<false><<<grid, KW_NT, kw_smem_bytes(), h->s>>>(h->vmap, h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->u,
+                                                             h->su, h->partA, h->st, wbuf_of(h));
   if (!h->capturing) h->launches++;
-  CKL("k_kron_gemm");
+  CKL("k_kron_ws");
 }
 
 int rowpass_grid(const glsgpu_sur* h) { return (int)std::min<int64_t>((int64_t)h->G * h->nch, GRID_CAP); }
@@ -432,11 +420,8 @@ void stream_attrs(glsgpu_sur* h) {
     CK(cudaFuncGetAttributes(&fa, fn));
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm - (int)fa.sharedSizeBytes));
   };
-  set((const void*)k_kron_ws, 0, 0);
-  set((const void*)k_kron_gemm<false, 8>, 0, 0);
-  set((const void*)k_kron_gemm<true, 8>, 0, 0);
-  set((const void*)k_kron_gemm<false, 4>, 0, 0);
-  set((const void*)k_kron_gemm<true, 4>, 0, 0);
+  set((const void*)k_kron_ws<false>, 0, 0);
+  set((const void*)k_kron_ws<true>, 0, 0);
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);
   set((const void*)k_stream<SMODE_C, false>, 0, 0);
@@ -1283,6 +1268,7 @@ void glsgpu_default_config(glsgpu_pcg_config* c) {
   c->xv_mode = GLSGPU_XV_X;
   c->graph_chunk = 0;
   c->kernel_timing = 0;
+  c->kron_fma = 0;
 }
 
 #define API_BEGIN try {
@@ -1513,6 +1499,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   ensure_solver(h, cap_d);
   const int xv_mode = cfg.xv_mode == GLSGPU_XV_QR ? GLSGPU_XV_QR : GLSGPU_XV_X;
   const int diag = cfg.diag_every;
+  h->kron_fma = cfg.kron_fma ? 1 : 0;
   Geo g = geo_of(h);
   cudaStream_t s = h->s;
 
@@ -1637,7 +1624,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   }
   const int timing = cfg.kernel_timing ? 1 : 0;
   const bool need_graph = !h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
-                          h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing;
+                          h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing ||
+                          h->graph_fma != h->kron_fma;
   if (need_graph) {
     if (h->graph) {
       CK(cudaGraphExecDestroy(h->graph));
@@ -1674,6 +1662,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     h->graph_xmode = xv_mode;
     h->graph_diag = diag >= 0 ? 1 : -1;
     h->graph_timing = timing;
+    h->graph_fma = h->kron_fma;
   }
   std::vector<double> kt_ms(3, 0.0);
   std::vector<int64_t> kt_n(3, 0);

@@ -256,228 +256,10 @@ __global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles,
 }
 
 // ------------------------------------------------------------------------------------------
-// Pass A for 128 < G <= 256 (BASELINE config 4): register-blocked FP64 "GEMM" su = U Omega on the
-// CUDA cores.  CTA tile 32 rows x all G columns; thread micro-tile 4 rows x 8 columns (columns
-// 2 tx + 64 q + {0,1}); Omega streamed in 8-row slabs through a double-buffered shared-memory ring
-// (cp.async); the U tile double-buffered in shared memory.  The elementwise memory work of the NEXT
-// tile (u = pr + mu u and the deferred w / sw update) is software-pipelined into the slab loop of the
-// current tile, one element per thread per slab, so it streams under the FP64 math.  Every output is
-// accumulated p-ascending from 0.0 with separate mul / add: bitwise the reference's operator*.
+// Tile constants of the FP64-bound pass A (k_kron_ws, 128 < G <= 256).
 constexpr int KG_BM = 32;   // rows per tile
 constexpr int KG_BK = 8;    // Omega rows per slab
-constexpr int KG_LD = 256;  // padded Omega row stride in shared memory
-constexpr int KG_XS = 34;   // U tile: row stride of one p (32 rows + 2 pad: conflict-light epilogue reads)
-constexpr int KG_XT = KG_LD * KG_XS;  // U tile doubles
-
-__device__ __forceinline__ uint32_t smem_u32_k(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32_k(dst)), "l"(src) : "memory");
-}
-
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32_k(dst)), "l"(src) : "memory");
-}
-
-// WN = columns per thread: 8 -> 256 threads (4 x 8 micro-tile); 4 -> 512 threads (4 x 4 micro-tile)
-template <bool FMA, int WN>
-__global__ void __launch_bounds__(256 * (8 / WN), 1) k_kron_gemm(int G, int64_t ldm, int64_t ntiles, const double* __restrict__ omegaT,
-                                                     const double* __restrict__ pr, double* __restrict__ u_io,
-                                                     double* __restrict__ out, double* partials, const SolveState* st,
-                                                     WBuf wbuf) {
-  if (!st->active) return;
-  extern __shared__ __align__(16) double ksm[];
-  // layout (direct offsets off the extern array keep every access in the shared state space):
-  //   U tiles [p][r]          ksm + buf * KG_XT (row stride KG_XS)          (2 buffers)
-  //   Omega slabs [p][c]      ksm + 2 KG_BM KG_LD + b * KG_BK * KG_LD         (2 buffers)
-  //   element stages [v][tid] ksm + 2 KG_BM KG_LD + 2 KG_BK KG_LD + e * 5 NT  (2 buffers, 5 vectors)
-#define XSB(buf) (ksm + (buf) * KG_XT)
-#define OSB(buf) (ksm + 2 * KG_XT + (buf) * (KG_BK * KG_LD))
-  constexpr int NTH = 256 * (8 / WN);        // threads
-  constexpr int CS = 8 / WN;                  // column splits across warps
-  constexpr int NP = WN / 2;                  // column pairs per thread
-#define ESB(buf) (ksm + 2 * KG_XT + 2 * KG_BK * KG_LD + (buf) * (5 * NTH))
-  const int tid = threadIdx.x, tx = tid & 31, w = tid >> 5;
-  const int ty = w % 8, cbase = (w / 8) * (KG_LD / CS);  // rows 4 ty .. 4 ty + 3; columns cbase + 2 tx + 64 q
-  const bool upd = st->mu_pending != 0, wupd = st->upd_pending != 0;
-  const double mu = st->mu, lp = st->lam_prev;
-  const double* __restrict__ wc = wbuf.w[st->cur];
-  const double* __restrict__ swc = wbuf.sw[st->cur];
-  double* __restrict__ wn = wbuf.w[st->nxt];
-  double* __restrict__ swn = wbuf.sw[st->nxt];
-  const int nslab = (G + KG_BK - 1) / KG_BK;
-  const int per_thread = (G * KG_BM + NTH - 1) / NTH;  // elements of a U tile per thread
-
-  // zero the padded Omega columns once (cp.async only ever writes columns < G)
-  for (int i = tid; i < 2 * KG_BK * KG_LD; i += NTH) OSB(0)[i] = 0.0;
-  __syncthreads();
-
-  auto issue_slab = [&](int s, int buf) {  // Omega rows [8 s, 8 s + 8), 16-byte pieces
-    const int p0 = s * KG_BK;
-    const int per_row = G / 2;
-    for (int i = tid; i < KG_BK * per_row; i += NTH) {
-      const int pr_ = i / per_row, c2 = i - pr_ * per_row;
-      const int p = p0 + pr_;
-      if (p < G) cp_async16(OSB(buf) + pr_ * KG_LD + 2 * c2, omegaT + (int64_t)p * G + 2 * c2);
-    }
-  };
-  // element e of a tile: its u, pr, w, sw, su staged (cp.async, 8 bytes each) into stage buffer eb
-  auto elt_off = [&](int64_t k0, int e, int64_t& off) {
-    const int idx = tid + e * NTH;
-    if (idx >= G * KG_BM) return false;
-    const int p = idx / KG_BM, r = idx - p * KG_BM;
-    off = (int64_t)p * ldm + k0 + r;
-    return true;
-  };
-  auto issue_elt = [&](int64_t k0, int e, int eb) {
-    int64_t off;
-    if (!elt_off(k0, e, off)) return;
-    double* E = ESB(eb);
-    cp_async8(E + 0 * NTH + tid, u_io + off);
-    if (upd) cp_async8(E + 1 * NTH + tid, pr + off);
-    if (wupd) {
-      cp_async8(E + 2 * NTH + tid, wc + off);
-      cp_async8(E + 3 * NTH + tid, swc + off);
-      cp_async8(E + 4 * NTH + tid, out + off);
-    }
-  };
-  // u_new = pr + mu u (pcg.cpp:210) and the deferred w / sw update (pcg.cpp:151-152; su read before
-  // Sigma u overwrites it); u_new also goes to the next tile's shared U tile
-  auto finish_elt = [&](int64_t k0, int e, int eb, double* xs_next) {
-    int64_t off;
-    if (!elt_off(k0, e, off)) return;
-    const double* E = ESB(eb);
-    const double uo = E[tid];
-    if (wupd) {
-      wn[off] = E[2 * NTH + tid] + (-lp) * uo;
-      swn[off] = E[3 * NTH + tid] + (-lp) * E[4 * NTH + tid];
-    }
-    double v = uo;
-    if (upd) {
-      v = E[NTH + tid] + mu * uo;
-      u_io[off] = v;
-    }
-    const int idx = tid + e * NTH;
-    const int p = idx / KG_BM, r = idx - p * KG_BM;
-    xs_next[p * KG_XS + r] = v;
-  };
-
-  double p_xo = 0.0, p_xx = 0.0;
-  int buf = 0;
-  int64_t tile = blockIdx.x;
-  if (tile < ntiles) {  // first tile: plain (non-overlapped) staging
-    for (int e = 0; e < per_thread; ++e) {
-      issue_elt(tile * KG_BM, e, 0);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      finish_elt(tile * KG_BM, e, 0, XSB(0));
-    }
-  }
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int64_t k0 = tile * KG_BM;
-    const int64_t next = tile + gridDim.x;
-    const bool has_next = next < ntiles;
-    double* xs = XSB(buf);
-    double* xs_next = XSB(buf ^ 1);
-    double acc[4][WN];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < WN; ++q) acc[i][q] = 0.0;
-    // group g_s = {Omega slab s, element s - 1 of the next tile}; g_0 = {slab 0}
-    issue_slab(0, 0);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    for (int s = 0; s < nslab; ++s) {
-      // group s + 1: slab s + 1 and element s of the next tile
-      if (s + 1 < nslab) issue_slab(s + 1, (s + 1) & 1);
-      if (has_next && s < per_thread) issue_elt(next * KG_BM, s, s & 1);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // slab s and element s - 1 landed
-      __syncthreads();
-      if (has_next && s >= 1 && s - 1 < per_thread) finish_elt(next * KG_BM, s - 1, (s - 1) & 1, xs_next);
-      // G % KG_BK == 0 (kron_gemm_ok): every slab is full, so the p loop is branch-free and the
-      // operands of step pp + 1 are loaded while step pp's products issue (register double buffer)
-      const double* os = OSB(s & 1);
-      const double* xp = xs + s * KG_BK * KG_XS + 4 * ty;
-      const double* op = os + cbase + 2 * tx;
-      double2 xa[2], oa[NP];
-      xa[0] = *reinterpret_cast<const double2*>(xp);
-      xa[1] = *reinterpret_cast<const double2*>(xp + 2);
-#pragma unroll
-      for (int q = 0; q < NP; ++q) oa[q] = *reinterpret_cast<const double2*>(op + 64 * q);
-#pragma unroll
-      for (int pp = 0; pp < KG_BK; ++pp) {
-        double2 xb[2], ob[NP];
-        if (pp + 1 < KG_BK) {
-          xb[0] = *reinterpret_cast<const double2*>(xp + (pp + 1) * KG_XS);
-          xb[1] = *reinterpret_cast<const double2*>(xp + (pp + 1) * KG_XS + 2);
-#pragma unroll
-          for (int q = 0; q < NP; ++q) ob[q] = *reinterpret_cast<const double2*>(op + (pp + 1) * KG_LD + 64 * q);
-        }
-        const double xr[4] = {xa[0].x, xa[0].y, xa[1].x, xa[1].y};
-        double o[WN];
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          o[2 * q] = oa[q].x;
-          o[2 * q + 1] = oa[q].y;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int q = 0; q < WN; ++q) {
-            if (FMA) acc[i][q] = fma(xr[i], o[q], acc[i][q]);
-            else acc[i][q] = acc[i][q] + xr[i] * o[q];
-          }
-        if (pp + 1 < KG_BK) {
-          xa[0] = xb[0];
-          xa[1] = xb[1];
-#pragma unroll
-          for (int q = 0; q < NP; ++q) oa[q] = ob[q];
-        }
-      }
-      __syncthreads();  // slab buffer (s & 1) and element stage ((s - 1) & 1) free for reuse
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (has_next) {  // elements nslab - 1, ... of the next tile
-      for (int e = nslab - 1; e < per_thread; ++e) {
-        if (e >= nslab) {
-          issue_elt(next * KG_BM, e, e & 1);
-          asm volatile("cp.async.commit_group;" ::: "memory");
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        finish_elt(next * KG_BM, e, e & 1, xs_next);
-      }
-    }
-    // outputs + d / u.u partials (pcg.cpp:144-145)
-#pragma unroll
-    for (int q = 0; q < WN; ++q) {
-      const int c = cbase + 2 * tx + 64 * (q >> 1) + (q & 1);
-      if (c < G) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = 4 * ty + i;
-          out[(int64_t)c * ldm + k0 + r] = acc[i][q];
-          const double x = xs[c * KG_XS + r];
-          p_xo += x * acc[i][q];
-          p_xx += x * x;
-        }
-      }
-    }
-    __syncthreads();  // xs (this buffer) no longer read; the next tile's buffer is complete
-    buf ^= 1;
-  }
-#undef XSB
-#undef OSB
-#undef ESB
-  __shared__ double red[NTH / 32 * 3];
-  double v[3] = {p_xo, p_xx, 0.0};
-  block_sum<3>(v, red);
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x * 3 + 0] = v[0];
-    partials[blockIdx.x * 3 + 1] = v[1];
-    partials[blockIdx.x * 3 + 2] = v[2];
-  }
-}
+constexpr int KG_LD = 256;  // Omega row stride in shared memory
 
 // Sum K-wide partials of `count` CTAs in fixed order (one CTA); result to out[0..K).
 template <int K>
@@ -793,6 +575,7 @@ struct RingPos {
   }
 };
 
+template <bool FMA>
 __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CUtensorMap vmap, int G, int64_t ldm,
                                                      int64_t ntiles, const double* __restrict__ omegaT,
                                                      double* __restrict__ u_io, double* __restrict__ out,
@@ -955,7 +738,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
 #pragma unroll
           for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[i][q] = acc[i][q] + xr[i] * o[q];
+            for (int q = 0; q < 4; ++q) acc[i][q] = FMA ? __fma_rn(xr[i], o[q], acc[i][q]) : acc[i][q] + xr[i] * o[q];
           if (pp + 1 < KG_BK) {
 #pragma unroll
             for (int h = 0; h < 4; ++h) xa[h] = xb[h];

@@ -236,6 +236,31 @@ def test_determinism_and_knob_invariance():
         assert np.array_equal(r.trace.rows["c"], runs[0].trace.rows["c"])
 
 
+KRON_FMA_CASES = [
+    ("c4_G256_M300", lambda: synth.make_problem(4, M=300)),          # MaxIter 200, the bench shape
+    ("G160_M600_conv", lambda: synth.random_sur(160, 600, [8] * 160, seed=7)),   # converges, ~700 it
+]
+
+
+@pytest.mark.parametrize("fma", [False, True])
+@pytest.mark.parametrize("name,mk", KRON_FMA_CASES, ids=[c[0] for c in KRON_FMA_CASES])
+def test_kron_fma_parity(name, mk, fma):
+    """The FP64-bound Kronecker pass (128 < G <= 256) with kron_fma: one rounding per term instead of
+    two changes Sigma u in the last bit only, and the solve still meets the north-star bar against
+    the oracle (same termination and iteration count, b to 1e-10).  kron_fma = False stays bitwise in
+    Sigma u (pass A writes exactly the reference's operator* sums)."""
+    p = mk()
+    o = oracle.solve(p, "oracle", cfg=oracle.make_config(tol_rel=p.tol_rel, max_iter=p.max_iter), beta_true=p.beta)
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur)
+    g = api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=p.max_iter, xv_mode="qr",
+                                                  diag_every=0, kron_fma=fma), true_beta=p.beta)
+    s = g.solution
+    assert s.termination.name == o.termination
+    assert s.iterations == o.iterations, (s.iterations, o.iterations)
+    assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
+
+
 def test_counters_match_reference():
     """CostCounters after pcg_aug equal the reference's own tallies (preconditioner.cpp:9-47)."""
     if not oracle.have("ref"):
