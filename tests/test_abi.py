@@ -29,9 +29,28 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in lib.glsgpu_version()
 
 
+def _c_layout(struct, fields):
+    """sizeof / offsetof as the C compiler lays out include/glsgpu.h."""
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    body = "".join(f'printf("%zu\\n", offsetof({struct}, {f}));' for f in fields)
+    src = ("#include <stdio.h>\n#include <stddef.h>\n#include \"glsgpu.h\"\n"
+           f'int main(void){{printf("%zu\\n", sizeof({struct}));{body}return 0;}}\n')
+    with tempfile.TemporaryDirectory() as d:
+        open(os.path.join(d, "l.c"), "w").write(src)
+        subprocess.run(["gcc", "-I", os.path.join(root, "include"), "-o", os.path.join(d, "l"),
+                        os.path.join(d, "l.c")], check=True)
+        out = subprocess.run([os.path.join(d, "l")], check=True, capture_output=True, text=True).stdout.split()
+    return [int(x) for x in out]
+
+
 def test_config_struct_layout_matches_header():
-    # glsgpu_pcg_config: 7 reference fields (8 bytes each) + 4 int32 knobs
-    assert ctypes.sizeof(_lib.PcgConfigC) == 7 * 8 + 4 * 4
+    # glsgpu_pcg_config: the ctypes mirror matches the C compiler's layout field by field
+    names = [f for f, _ in _lib.PcgConfigC._fields_]
+    lay = _c_layout("glsgpu_pcg_config", names)
+    assert ctypes.sizeof(_lib.PcgConfigC) == lay[0]
+    assert [getattr(_lib.PcgConfigC, f).offset for f in names] == lay[1:]
     assert ctypes.sizeof(_lib.TraceRowC) == 48
     assert ctypes.sizeof(_lib.ResultC) == 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8
     c = _lib.PcgConfigC()
