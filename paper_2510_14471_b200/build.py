@@ -50,6 +50,20 @@ CPP_TESTS = os.path.join(ROOT, "tests", "cpp")
 REF_INCLUDE = "/root/reference/proj/include"
 
 
+CPP_DEPS = [os.path.join(ROOT, "include", "glsgpu.h"), os.path.join(ROOT, "include", "gls_b200", "gls_b200.hpp"),
+            os.path.join(ROOT, "integration", "gls_gpu_adapter.hpp"), os.path.join(CPP_TESTS, "test_header_api.cpp"),
+            os.path.join(CPP_TESTS, "test_reference_adapter.cpp")]
+
+
+def cpp_deps_digest() -> str:
+    """Content hash of the headers / sources the C++ test binaries are compiled from."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in CPP_DEPS:
+        h.update(open(d, "rb").read() if os.path.exists(d) else b"-")
+    return h.hexdigest()
+
+
 def build_cpp_tests(verbose: bool = False) -> list:
     """The C++ host-API test (always) and the reference-adapter test (when the reference headers are
     present -- i.e. here, not on the GPU box; the binary travels).  rpath $ORIGIN-relative so the
@@ -77,6 +91,8 @@ def build_cpp_tests(verbose: bool = False) -> list:
         if p.returncode != 0:
             raise RuntimeError(f"g++ failed: {' '.join(cmd)}")
         built.append(cmd[cmd.index("-o") + 1])
+    with open(os.path.join(out, "deps.sha256"), "w") as f:
+        f.write(cpp_deps_digest())
     return built
 
 

@@ -342,8 +342,10 @@ StreamCfg stream_cfg(const glsgpu_sur* h, int nmat, int nv) {
   const int64_t budget = (kb_env ? std::atoi(kb_env) : 220) * 1024;
   c.T = 32;
   c.S = 2;
+  // narrow blocks (nmax <= 32, k_stream<MODE, true>) read 32 column slots per stage
+  const int64_t slots = nmax <= 32 ? std::max<int64_t>(nmat * nmax + nv, 32) : nmat * nmax + nv;
   for (int T : {256, 128, 64, 32}) {
-    const int64_t stage = (int64_t)(nmat * nmax + nv) * T * 8;
+    const int64_t stage = slots * T * 8;
     const int64_t extra = (int64_t)(T + nmax + std::max(nmax, 32)) * 8;
     if (2 * stage + extra <= budget) {
       c.T = T;
@@ -351,7 +353,7 @@ StreamCfg stream_cfg(const glsgpu_sur* h, int nmat, int nv) {
       break;
     }
   }
-  c.stage_doubles = (int64_t)(nmat * nmax + nv) * c.T;
+  c.stage_doubles = slots * c.T;
   c.smem = (size_t)(c.S * c.stage_doubles + c.T + nmax + std::max(nmax, 32)) * sizeof(double);
   const int per_sm = std::max<int>(1, (int)((227 * 1024) / (c.smem + 2048)));
   const int64_t items = (int64_t)h->G * h->nch;
@@ -398,10 +400,9 @@ int launch_stream(glsgpu_sur* h, StreamArgs a, const SolveState* st) {
   a.T = c.T;
   a.S = c.S;
   a.stage_doubles = c.stage_doubles;
-  // narrow blocks: column partials accumulated in registers in the row sweep (k_stream FUSE)
-  constexpr bool COLS = (MODE != SMODE_C && MODE != SMODE_XS);
-  if (COLS && h->nmax <= 32)
-    k_stream<MODE, COLS><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
+  // narrow blocks: one register-resident row sweep, column partials accumulated in it (k_stream FUSE)
+  if (h->nmax <= 32)
+    k_stream<MODE, true><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
   else
     k_stream<MODE, false><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
   if (!h->capturing) h->launches++;
@@ -425,6 +426,8 @@ void stream_attrs(glsgpu_sur* h) {
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);
   set((const void*)k_stream<SMODE_C, false>, 0, 0);
+  set((const void*)k_stream<SMODE_C, true>, 0, 0);
+  set((const void*)k_stream<SMODE_XS, true>, 0, 0);
   set((const void*)k_stream<SMODE_QT_R, false>, 0, 0);
   set((const void*)k_stream<SMODE_QT_R, true>, 0, 0);
   set((const void*)k_stream<SMODE_QT_D, false>, 0, 0);

@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[4];
   __shared__ double red[NT / 32 * 3];
-  __shared__ double fred[FUSE ? NT : 1];
+  __shared__ double fred[(FUSE && (MODE != SMODE_C && MODE != SMODE_XS)) ? NT : 1];
   const int S = a.S, T = a.T;
   double* xs = sm + (int64_t)S * a.stage_doubles;
   // per-item n-vector slice (nmax <= 128 on this path): a static shared array, so the row dots read it
@@ -856,6 +856,11 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     mbar_fence_init();
+  }
+  if (FUSE) {
+    // the narrow-block sweep reads all 32 column slots of a stage: start from finite contents
+    for (int64_t i = tid; i < (int64_t)S * a.stage_doubles; i += NT) sm[i] = 0.0;
+    fence_proxy_async_smem();  // generic writes ordered before the first TMA writes into the ring
   }
   __syncthreads();
 
@@ -964,9 +969,9 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     double acc[MAXC];
 #pragma unroll
     for (int q = 0; q < MAXC; ++q) acc[q] = 0.0;
-    double facc[FUSE ? 32 : 1];
+    double facc[(FUSE && COLS) ? 32 : 1];
 #pragma unroll
-    for (int j = 0; j < (FUSE ? 32 : 1); ++j) facc[j] = 0.0;
+    for (int j = 0; j < ((FUSE && COLS) ? 32 : 1); ++j) facc[j] = 0.0;
     for (int64_t kb = k0; kb < k1; kb += T, ++it_count) {
       const int stage = (int)(it_count % S);
       const int rows = (int)((k1 - kb) < T ? (k1 - kb) : T);
@@ -975,28 +980,33 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
       const double* M0 = base;                                 // Q (X for DIAG)
       const double* M1 = base + (int64_t)nb * T;               // X (pass B, xv_mode X)
       const double* V = base + (int64_t)(nmat * nb) * T;       // vectors
-      if constexpr (FUSE && COLS) {
+      if constexpr (FUSE) {
         // narrow blocks (n_b <= 32): the row of the tile's matrix lives in registers; the row work and
         // the column partials (acc_j += A[k, j] x_k) happen in one sweep -- no second phase, no extra
-        // barrier; the per-lane accumulators are transpose-reduced once per item
+        // barrier; the per-lane accumulators are transpose-reduced once per item.  All 32 columns are
+        // read unconditionally (immediate shared-memory offsets, no per-column branch): columns past
+        // n_b hold finite stale data (the ring is zero-filled at launch and only ever receives finite
+        // Q / vector tiles) and meet tv[j] = 0 in the row dot, and their column partials are dropped.
+        // Row dots and column partials are fixed-shape sums (not the reference's order anyway), so
+        // they use fused multiply-adds.
         for (int t = tid; t < rows; t += NT) {
           const int64_t k = kb + t;
           const int64_t vo = vbase + k;
           double arow[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) arow[j] = (j < nb) ? M0[(int64_t)j * T + t] : 0.0;
+          for (int j = 0; j < 32; ++j) arow[j] = M0[(int64_t)j * T + t];
           auto rdot = [&]() {
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
-              s0 = s0 + arow[j + 0] * tv[j + 0];
-              s1 = s1 + arow[j + 1] * tv[j + 1];
-              s2 = s2 + arow[j + 2] * tv[j + 2];
-              s3 = s3 + arow[j + 3] * tv[j + 3];
+              s0 = __fma_rn(arow[j + 0], tv[j + 0], s0);
+              s1 = __fma_rn(arow[j + 1], tv[j + 1], s1);
+              s2 = __fma_rn(arow[j + 2], tv[j + 2], s2);
+              s3 = __fma_rn(arow[j + 3], tv[j + 3], s3);
             }
             return (s0 + s1) + (s2 + s3);
           };
-          double x;
+          double x = 0.0;
           if (MODE == SMODE_B) {
             const double suv = V[t], rv = V[T + t];
             double xv = 0.0;
@@ -1009,6 +1019,18 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
             const double rn = rv - lam * (suv + xv);
             a.r[vo] = rn;
             x = rn * wgt;
+          } else if (MODE == SMODE_C || MODE == SMODE_XS) {
+            const double proj = rdot();
+            if (MODE == SMODE_XS) {
+              a.out[vo] = proj * wgt;
+            } else {
+              const double rv = V[t];
+              const double pv = (rv * wgt - proj) * wgt;
+              a.pr[vo] = pv;
+              pc += rv * pv;
+              prr += rv * rv;
+              ppp += pv * pv;
+            }
           } else if (MODE == SMODE_QT_R || MODE == SMODE_QT_V) {
             x = V[t] * wgt;
           } else if (MODE == SMODE_QT_D) {
@@ -1021,8 +1043,10 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
             if (k < g.M) rsum += res * res;
             x = V[t] + (-lp) * V[2 * T + t];
           }
+          if constexpr (COLS) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) facc[j] += arow[j] * x;
+            for (int j = 0; j < 32; ++j) facc[j] = __fma_rn(arow[j], x, facc[j]);
+          }
         }
         __syncthreads();  // the stage is free
         if (warp == 0) issue(stage);

@@ -11,8 +11,20 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "cpp", "bin")
 
 
+def _stale(path):
+    """True when the binary was compiled from other headers than the current ones (content hash)."""
+    from paper_2510_14471_b200 import build as B
+    stamp = os.path.join(BIN, "deps.sha256")
+    return not os.path.exists(stamp) or open(stamp).read().strip() != B.cpp_deps_digest()
+
+
 def _ensure(name):
     path = os.path.join(BIN, name)
+    if os.path.exists(path) and _stale(path):
+        # a binary older than the ABI header would corrupt memory through a stale struct layout
+        if name == "test_reference_adapter" and not os.path.isdir("/root/reference/proj/include"):
+            pytest.fail(f"{name} is older than its headers; rebuild it with __graft_entry__.build()")
+        os.remove(path)
     if not os.path.exists(path):
         from paper_2510_14471_b200 import build as B
         B.build()
