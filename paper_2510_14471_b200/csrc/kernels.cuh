@@ -531,6 +531,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// explicit global-space streaming stores (no generic-address path; evict-first: the data is next
+// read by a later pass, long after this one has streamed the rest of the vectors through L2)
+__device__ __forceinline__ void stg_cs(double* p, double v) {
+  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void stg_cs2(double* p, double a, double b) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
 // 2-D tensor-map load of one box (coordinates: inner = row, outer = column)
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
@@ -546,22 +554,24 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 //   * 8 math warps: 8 rows x 4 columns per thread (4 row groups x 2 column halves), operands of step
 //     p + 1 loaded while step p's separate multiplies / adds issue (bitwise the reference's order:
 //     every output accumulated p-ascending from 0.0, no FMA contraction);
-//   * 1 loader warp: Omega' in 8-row slabs (8 G contiguous doubles each) by one cp.async.bulk per slab
+//   * 1 loader warp: Omega' in KW_OK-row slabs (KW_OK G contiguous doubles each), one cp.async.bulk per slab
 //     into a KW_OS-stage ring (full: tx bytes; empty: one arrival per math warp);
-//   * 1 element warp: builds the NEXT tile's U while the math warps run the current one.  Per 8-column
+//   * KW_EW element warps: build the NEXT tile's U while the math warps run the current one.  Per 8-column
 //     chunk it loads the 32 x 8 boxes of u, pr, w, sw, su (one 2-D TMA each, through the tensor map of
 //     the vector slab; KW_ES-stage ring), then per element: the deferred w / sw update
 //     (pcg.cpp:151-152), u = pr + mu u (pcg.cpp:210), u.u.
 // The math warps write Sigma u and the u . Sigma u partials.  No CTA-wide barrier inside the tile loop.
 constexpr int KW_MATH = 8;                          // math warps
-constexpr int KW_EW = 2;                            // element warps (4 of each chunk's 8 columns each)
+constexpr int KW_EW = 3;                            // element warps (columns ew, ew + 3, ew + 6 of each 8-column chunk)
 constexpr int KW_NT = (KW_MATH + 1 + KW_EW) * 32;   // + loader warp
+constexpr int KW_OK = 8;                            // Omega rows per slab
 constexpr int KW_OS = 3;                            // Omega slab stages
 constexpr int KW_ES = 4;                            // element chunk stages
-constexpr int KW_XS = 32;                           // U tile row stride (doubles per p)
+constexpr int KW_XS = 34;                           // U tile row stride (doubles per p; +2 pad: 8-way instead of
+                                                    // 32-way bank conflicts in the epilogue's per-column reads)
 constexpr int KW_XT = KG_LD * KW_XS;                // U tile doubles
 constexpr int KW_EC = 5 * KG_BK * KG_BM;            // element chunk doubles: 5 vectors x 8 columns x 32 rows
-constexpr size_t kw_smem_bytes() { return (size_t)(2 * KW_XT + KW_OS * KG_BK * KG_LD + KW_ES * KW_EC) * sizeof(double); }
+constexpr size_t kw_smem_bytes() { return (size_t)(2 * KW_XT + KW_OS * KW_OK * KG_LD + KW_ES * KW_EC) * sizeof(double); }
 
 // ring position: slot and phase parity advanced together (no division in the loops)
 struct RingPos {
@@ -586,10 +596,11 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
       xs_empty[2];
   __shared__ double red[KW_NT / 32][2];
   double* const xsb = ksm;                                // [2][KG_LD][KW_XS]
-  double* const omb = ksm + 2 * KW_XT;                    // [KW_OS][KG_BK][G]
-  double* const elb = omb + KW_OS * KG_BK * KG_LD;        // [KW_ES][5][KG_BK][KG_BM]
+  double* const omb = ksm + 2 * KW_XT;                    // [KW_OS][KW_OK][G]
+  double* const elb = omb + KW_OS * KW_OK * KG_LD;        // [KW_ES][5][KG_BK][KG_BM]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nslab = G / KG_BK;
+  const int nslab = G / KG_BK;   // element chunks per tile
+  const int nslab_o = G / KW_OK;  // Omega slabs per tile
   const int64_t ntl = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA
   if (tid == 0) {
     for (int i = 0; i < KW_OS; ++i) {
@@ -611,19 +622,19 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
   if (warp == KW_MATH) {
     // ---------------- Omega loader
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(KG_BK * G * sizeof(double));
+      const uint32_t bytes = (uint32_t)(KW_OK * G * sizeof(double));
       RingPos w;
       int s = 0;
-      for (int64_t g = 0; g < ntl * nslab; ++g) {
+      for (int64_t g = 0; g < ntl * nslab_o; ++g) {
         if (g >= KW_OS) mbar_wait(&om_empty[w.slot], w.phase ^ 1u);
         mbar_expect_tx(&om_full[w.slot], bytes);
-        tma_load_1d(omb + w.slot * KG_BK * KG_LD, omegaT + (int64_t)s * KG_BK * G, bytes, &om_full[w.slot]);
+        tma_load_1d(omb + w.slot * KW_OK * KG_LD, omegaT + (int64_t)s * KW_OK * G, bytes, &om_full[w.slot]);
         w.next(KW_OS);
-        if (++s == nslab) s = 0;
+        if (++s == nslab_o) s = 0;
       }
     }
   } else if (warp > KW_MATH) {
-    // ---------------- element warps: warp ew owns columns [4 ew, 4 ew + 4) of every chunk; element
+    // ---------------- element warps: warp ew owns columns ew, ew + KW_EW, ... of every chunk; element
     // warp 0 lane 0 issues the chunk loads
     const int ew = warp - KW_MATH - 1;
     const bool upd = st->mu_pending != 0, wupd = st->upd_pending != 0;
@@ -673,19 +684,18 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
         mbar_wait(&el_full[cp.slot], cp.phase);
         const double* E = elb + cp.slot * KW_EC;
 #pragma unroll
-        for (int ci = 0; ci < KG_BK / KW_EW; ++ci) {
-          const int cc = ew * (KG_BK / KW_EW) + ci;
+        for (int cc = ew; cc < KG_BK; cc += KW_EW) {
           const int c = k * KG_BK + cc;
           const int64_t off = (int64_t)c * ldm + k0 + lane;
           const double uo = E[(0 * KG_BK + cc) * KG_BM + lane];
           if (wupd) {
-            wn[off] = E[(2 * KG_BK + cc) * KG_BM + lane] + (-lp) * uo;
-            swn[off] = E[(3 * KG_BK + cc) * KG_BM + lane] + (-lp) * E[(4 * KG_BK + cc) * KG_BM + lane];
+            stg_cs(wn + off, E[(2 * KG_BK + cc) * KG_BM + lane] + (-lp) * uo);
+            stg_cs(swn + off, E[(3 * KG_BK + cc) * KG_BM + lane] + (-lp) * E[(4 * KG_BK + cc) * KG_BM + lane]);
           }
           double v = uo;
           if (upd) {
             v = E[(1 * KG_BK + cc) * KG_BM + lane] + mu * uo;
-            u_io[off] = v;
+            stg_cs(u_io + off, v);
           }
           xs[c * KW_XS + lane] = v;
           p_b += v * v;
@@ -715,19 +725,19 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
-      for (int s = 0; s < nslab; ++s) {
+      for (int s = 0; s < nslab_o; ++s) {
         mbar_wait(&om_full[rp.slot], rp.phase);
-        const double* xp = xs + s * KG_BK * KW_XS + 8 * rg;
-        const double* op = omb + rp.slot * KG_BK * KG_LD + cb;
+        const double* xp = xs + s * KW_OK * KW_XS + 8 * rg;
+        const double* op = omb + rp.slot * KW_OK * KG_LD + cb;
         double2 xa[4], oa[2];
 #pragma unroll
         for (int h = 0; h < 4; ++h) xa[h] = *reinterpret_cast<const double2*>(xp + 2 * h);
         oa[0] = *reinterpret_cast<const double2*>(op);
         oa[1] = *reinterpret_cast<const double2*>(op + 64);
 #pragma unroll
-        for (int pp = 0; pp < KG_BK; ++pp) {
+        for (int pp = 0; pp < KW_OK; ++pp) {
           double2 xb[4], ob[2];
-          if (pp + 1 < KG_BK) {
+          if (pp + 1 < KW_OK) {
 #pragma unroll
             for (int h = 0; h < 4; ++h) xb[h] = *reinterpret_cast<const double2*>(xp + (pp + 1) * KW_XS + 2 * h);
             ob[0] = *reinterpret_cast<const double2*>(op + (pp + 1) * G);
@@ -739,7 +749,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
           for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[i][q] = FMA ? __fma_rn(xr[i], o[q], acc[i][q]) : acc[i][q] + xr[i] * o[q];
-          if (pp + 1 < KG_BK) {
+          if (pp + 1 < KW_OK) {
 #pragma unroll
             for (int h = 0; h < 4; ++h) xa[h] = xb[h];
             oa[0] = ob[0];
@@ -759,7 +769,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
           const double* xc = xs + c * KW_XS + 8 * rg;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            *reinterpret_cast<double2*>(dst + 2 * h) = make_double2(acc[2 * h][q], acc[2 * h + 1][q]);
+            stg_cs2(dst + 2 * h, acc[2 * h][q], acc[2 * h + 1][q]);
             const double2 x2 = *reinterpret_cast<const double2*>(xc + 2 * h);
             p_a += x2.x * acc[2 * h][q];
             p_a += x2.y * acc[2 * h + 1][q];
