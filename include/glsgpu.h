@@ -17,6 +17,10 @@
  *                                        true_beta)  proj/include/gls/pcg.hpp:80-83; proj/src/pcg.cpp:36-229,346-350
  *   glsgpu_counters / _reset_counters    IndefinitePreconditioner::counters / reset_apply_counters
  *                                        proj/include/gls/preconditioner.hpp:40-41; preconditioner.cpp:30-35
+ *   glsgpu_mvrglm_create                 make_mvrglm + mvrglm_preconditioner (+ embed_mvrglm's operator layout)
+ *                                        proj/include/gls/structured.hpp:33-50,96-100;
+ *                                        proj/src/structured.cpp:63-95,365-414,468-477
+ *   glsgpu_mv_reduce                     mv_reduce  proj/include/gls/structured.hpp:76; structured.cpp:121-130
  *
  * Errors: every call returns a status code; the codes map 1:1 onto the reference's gls::Error
  * subclasses (proj/include/gls/errors.hpp:10-88) and glsgpu_last_error_message() holds the text.
@@ -184,6 +188,24 @@ int glsgpu_sur_create_sharded(int G, int64_t M_local, int64_t M_global, const in
                               const double* block_scale, int device, const void* nccl_id, int rank, int nranks,
                               glsgpu_sur** out, int* bad_block);
 int glsgpu_sur_shard(const glsgpu_sur* h, int* rank, int* nranks, int64_t* M_global);
+
+/* Multivariate model with exclusion restrictions (gls::MvRglm) ------------------------------------
+ * Y = Z0 B + U, restriction list i = the zero-forced rows of B[:, i] as CSR: equation i restricts parameters
+ * ridx[roff[i] .. roff[i + 1]) (strictly increasing, < N0; roff[0] = 0).  The handle is the operator of
+ * pcg_aug(embed_mvrglm(mv), *mvrglm_preconditioner(mv[, z_scale, c_scale]), ...): every entry point above
+ * (applies, sigma_apply, norm probe, solve, counters) works on it with m = G M0 + k rows in the reference's
+ * order -- the G M0 observation rows (equation-major), then the k constraint rows (equation 0's first) --
+ * and n = G N0 parameters.  z_scale / c_scale (G each) may be NULL (identity auxiliary). */
+int glsgpu_mvrglm_create(int G, int64_t M0, int64_t N0, const double* Z0 /* M0 x N0 */, const double* Y /* M0 x G */,
+                         const double* omega /* G x G */, const int64_t* roff, const int64_t* ridx,
+                         const double* z_scale, const double* c_scale, int device, glsgpu_sur** out, int* bad_block);
+/* mv_reduce: the thin QR Z0 = Q0 R0 on the device; R0 (N0 x N0) and Q0' Y (N0 x G), column-major.  R0 equals
+ * the reference's up to the signs of its rows (a TSQR tree instead of one Householder sweep); the reduced
+ * model is the same up to that orthogonal diagonal, which the GLS estimate does not see. */
+int glsgpu_mv_reduce(int G, int64_t M0, int64_t N0, const double* Z0, const double* Y, double* R0, double* QtY,
+                     int device);
+/* m (rows of the reference's embedded GLM) and n of a handle. */
+int glsgpu_model_dims(const glsgpu_sur* h, int64_t* m, int64_t* n);
 
 /* Test / bench helpers (not part of the reference surface) ---------------------------------- */
 /* Copy Q (M x n, ld M) and the concatenated R blocks to host. */

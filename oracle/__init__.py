@@ -105,6 +105,16 @@ def _load(path: str, kind: str):
         lib.orc_norm_probe.argtypes = [C.c_int, C.c_int64, _P, C.c_int64]
         lib.orc_qr_thin.restype = C.c_int
         lib.orc_qr_thin.argtypes = [C.c_int64, C.c_int64, _P, C.c_int64, C.c_double, _P, C.c_int64, _P]
+        lib.orc_pcg_aug_mvrglm.restype = C.c_int
+        lib.orc_pcg_aug_mvrglm.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _PI, _PI, _P, _P, _P, _P,
+                                           C.POINTER(Config), _P, _P, _P, C.POINTER(TraceRow), C.c_int64,
+                                           C.POINTER(Result), C.POINTER(C.c_int)]
+        lib.orc_mvrglm_apply.restype = C.c_int
+        lib.orc_mvrglm_apply.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _PI, _PI, _P, _P, C.c_int, _P, _P]
+        lib.orc_mvrglm_norm_probe.restype = C.c_double
+        lib.orc_mvrglm_norm_probe.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _PI, _PI]
+        lib.orc_mv_reduce.restype = C.c_int
+        lib.orc_mv_reduce.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _P]
     else:
         lib.ref_pcg_aug_sur.restype = C.c_int
         lib.ref_pcg_aug_sur.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, _P, _P, _P, _P, C.POINTER(Config), _P,
@@ -119,6 +129,14 @@ def _load(path: str, kind: str):
         lib.ref_qr_thin.restype = C.c_int
         lib.ref_qr_thin.argtypes = [C.c_int64, C.c_int64, _P, _P, _P]
         lib.ref_last_error.restype = C.c_char_p
+        lib.ref_pcg_aug_mvrglm.restype = C.c_int
+        lib.ref_pcg_aug_mvrglm.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _PI, _PI, _P, _P, _P, _P,
+                                           C.POINTER(Config), _P, _P, _P, C.POINTER(TraceRow), C.c_int64,
+                                           C.POINTER(Result), C.POINTER(C.c_uint64)]
+        lib.ref_mvrglm_apply.restype = C.c_int
+        lib.ref_mvrglm_apply.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _PI, _PI, _P, _P, C.c_int, _P, _P]
+        lib.ref_mv_reduce.restype = C.c_int
+        lib.ref_mv_reduce.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _P]
     return lib
 
 
@@ -240,3 +258,95 @@ def diag(kind: str = "oracle", cap: int = 1 << 16):
     n = L.orc_diag(d.ctypes.data_as(C.POINTER(C.c_double)), g.ctypes.data_as(C.POINTER(C.c_double)),
                    cap)
     return d[:n], g[:n]
+
+
+# ------------------------------------------------------------------ MVRGLM (structured.cpp:77-95,121-130,365-414)
+def _f(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def solve_mv(prob, kind: str = "oracle", cfg: Optional[Config] = None, w1=None, z1=None, trace: bool = True,
+             beta_true: Optional[np.ndarray] = None) -> SolveOut:
+    """pcg_aug(embed_mvrglm(mv), *mvrglm_preconditioner(mv[, z_scale, c_scale]), w1, z1, cfg).
+
+    kind="oracle": the restatement; kind="ref": the literal reference (dense embed; small sizes only).
+    Vectors use the reference's embedded row order (observation rows per equation, then constraints)."""
+    L = lib(kind)
+    if cfg is None:
+        cfg = make_config(tol_rel=prob.tol_rel, max_iter=prob.max_iter)
+    roff, ridx = prob.csr()
+    m, n = prob.m, prob.n
+    max_iter = cfg.max_iter if cfg.max_iter else m - n + 1
+    cap = max_iter + 1 if trace else 0
+    rows = (TraceRow * max(cap, 1))()
+    b = np.zeros(n)
+    w = np.zeros(m)
+    res = Result()
+    Z0 = np.asfortranarray(prob.Z0, dtype=np.float64)
+    Y = np.asfortranarray(prob.Y, dtype=np.float64)
+    om = np.asfortranarray(prob.omega, dtype=np.float64)
+    args = [prob.G, prob.M0, prob.N0, _dp(Z0), _dp(Y), _dp(om), roff.ctypes.data_as(_PI), ridx.ctypes.data_as(_PI),
+            _dp(_f(prob.z_scale)), _dp(_f(prob.c_scale)), _dp(_f(w1)), _dp(_f(z1)), C.byref(cfg),
+            _dp(_f(beta_true)), _dp(b), _dp(w), rows if trace else None, cap, C.byref(res)]
+    counters = None
+    if kind == "oracle":
+        bad = C.c_int(-1)
+        st = L.orc_pcg_aug_mvrglm(*args, C.byref(bad))
+        if st:
+            raise OracleError(st, f"block {bad.value}")
+    else:
+        counters = np.zeros(6, dtype=np.uint64)
+        st = L.ref_pcg_aug_mvrglm(*args, counters.ctypes.data_as(C.POINTER(C.c_uint64)))
+        if st:
+            raise OracleError(st, L.ref_last_error().decode())
+    tr = np.frombuffer(rows, dtype=TRACE_DTYPE, count=min(res.n_rows, cap)).copy() if trace else np.zeros(0, TRACE_DTYPE)
+    return SolveOut(b=b, w=w, iterations=int(res.iterations), termination=TERMINATION[res.termination],
+                    breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
+                    residual_seminorm=float(res.residual_seminorm), w1_projected=bool(res.w1_projected),
+                    trace=tr, sigma_scale=float(res.sigma_scale), counters=counters)
+
+
+MV_OPS = {"pi": 0, "xstar_t": 1, "xstar": 2, "sigma": 3, "x": 4, "xt": 5}
+
+
+def mv_apply(prob, kind_op: str, vec: np.ndarray, kind: str = "oracle") -> np.ndarray:
+    """mvrglm_preconditioner applies (and, oracle only, the embedded Sigma / X / X' applies)."""
+    L = lib(kind)
+    op = MV_OPS[kind_op]
+    roff, ridx = prob.csr()
+    out = np.zeros(prob.n if op in (1, 5) else prob.m)
+    v = np.ascontiguousarray(vec, dtype=np.float64)
+    Z0 = np.asfortranarray(prob.Z0, dtype=np.float64)
+    if kind == "oracle":
+        om = np.asfortranarray(prob.omega, dtype=np.float64)
+        st = L.orc_mvrglm_apply(prob.G, prob.M0, prob.N0, _dp(Z0), _dp(om), roff.ctypes.data_as(_PI),
+                                ridx.ctypes.data_as(_PI), _dp(_f(prob.z_scale)), _dp(_f(prob.c_scale)), op, _dp(v),
+                                _dp(out))
+    else:
+        assert op <= 2
+        st = L.ref_mvrglm_apply(prob.G, prob.M0, prob.N0, _dp(Z0), roff.ctypes.data_as(_PI),
+                                ridx.ctypes.data_as(_PI), _dp(_f(prob.z_scale)), _dp(_f(prob.c_scale)), op, _dp(v),
+                                _dp(out))
+    if st:
+        raise OracleError(st)
+    return out
+
+
+def mv_norm_probe(prob) -> float:
+    roff, ridx = prob.csr()
+    return lib("oracle").orc_mvrglm_norm_probe(prob.G, prob.M0, prob.N0, _dp(np.asfortranarray(prob.Z0)),
+                                               _dp(np.asfortranarray(prob.omega)), roff.ctypes.data_as(_PI),
+                                               ridx.ctypes.data_as(_PI))
+
+
+def mv_reduce(prob, kind: str = "oracle"):
+    """mv_reduce: (R0 (N0 x N0), Q0'Y (N0 x G)) of the thin QR Z0 = Q0 R0."""
+    L = lib(kind)
+    R = np.zeros((prob.N0, prob.N0), order="F")
+    QtY = np.zeros((prob.N0, prob.G), order="F")
+    fn = L.orc_mv_reduce if kind == "oracle" else L.ref_mv_reduce
+    st = fn(prob.G, prob.M0, prob.N0, _dp(np.asfortranarray(prob.Z0)), _dp(np.asfortranarray(prob.Y)), _dp(R),
+            _dp(QtY))
+    if st:
+        raise OracleError(st)
+    return R, QtY

@@ -453,26 +453,55 @@ static int64_t now_ns(void) {
   return (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
 }
 
+/* ------------------------------------------------------------------ the model behind run_aug
+ * run_aug only touches the GLM through X, X', |X|_F, Sigma and operator_norm_probe(Sigma), and the
+ * preconditioner through pi / xstar_t / xstar: these hooks restate them per model class. */
+typedef struct {
+  int64_t m, n;
+  const void* ctx;
+  void (*x_apply)(const void*, const double* v, double* y);
+  void (*x_apply_t)(const void*, const double* w, double* out);
+  double (*x_frob)(const void*);
+  void (*sigma)(const void*, const double* x, double* out);
+  void (*pi)(const void*, const double* xi, double* out);
+  int (*xstar_t)(const void*, const double* xi, double* out);
+  int (*xstar)(const void*, const double* v, double* out);
+} orc_model;
+
+/* operator_norm_probe(glm.sigma) (pcg.cpp:233-244) through the model's Sigma hook */
+static double model_norm_probe(const orc_model* mo, int64_t iters) {
+  const int64_t m = mo->m;
+  double* v = (double*)malloc(sizeof(double) * (size_t)m);
+  double* t = (double*)malloc(sizeof(double) * (size_t)m);
+  for (int64_t i = 0; i < m; ++i) v[i] = 1.0 / sqrt((double)m);
+  double nrm = 0.0;
+  for (int64_t it = 0; it < iters; ++it) {
+    mo->sigma(mo->ctx, v, t);
+    memcpy(v, t, sizeof(double) * (size_t)m);
+    nrm = vnorm2(m, v);
+    if (nrm == 0.0) break;
+    for (int64_t i = 0; i < m; ++i) v[i] /= nrm;
+  }
+  free(v); free(t);
+  return nrm;
+}
+
 /* ------------------------------------------------------------------ run_aug, Recovery variant
- * proj/src/pcg.cpp:36-229 (entered through pcg_aug, pcg.cpp:346-350), with
- * glm = embed_sur(sur) and precond = sur_preconditioner(sur[, block_scale]).
+ * proj/src/pcg.cpp:36-229 (entered through pcg_aug, pcg.cpp:346-350) on a model (hooks above).
  *
  * w1 / z1 may be NULL (zeros); beta_true may be NULL (rmse = NaN).  rows may be NULL (trace not
  * returned); otherwise it must hold max_iter + 1 rows.  b_out: n, w_out: m (may be NULL). */
-int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y, const double* omega,
-                    const double* scale, const double* w1, const double* z1, const orc_config* cfg,
-                    const double* beta_true, double* b_out, double* w_out, orc_trace_row* rows,
-                    int64_t rows_cap, orc_result* res, int* bad_block) {
-  const int64_t m = M * G;
-  orc_sur* s = NULL;
-  int st = orc_sur_build(G, M, nb, X, scale, &s, bad_block);
-  if (st) return st;
-  const int64_t n = s->n;
-  if (m < n) { orc_sur_free(s); return ORC_DIMENSION_MISMATCH; } /* make_glm: m > n (glm.cpp:10-16) */
+static int run_aug(const orc_model* mo, const double* Y, const double* w1, const double* z1,
+                   const orc_config* cfg, const double* beta_true, double* b_out, double* w_out,
+                   orc_trace_row* rows, int64_t rows_cap, orc_result* res) {
+  const int64_t m = mo->m, n = mo->n;
+  const void* s = mo->ctx;
+  int st = ORC_OK;
+  if (m < n) return ORC_DIMENSION_MISMATCH; /* make_glm: m > n (glm.cpp:10-16) */
 
   const int64_t max_iter = cfg->max_iter ? cfg->max_iter : (m - n + 1); /* pcg.cpp:34,46-47 */
   const int64_t stride = cfg->record_z_every ? cfg->record_z_every : 1;
-  const double sigma_scale = orc_norm_probe(G, M, omega, 12);
+  const double sigma_scale = model_norm_probe(mo, 12);
   const int64_t start = now_ns();
 
   size_t mb = sizeof(double) * (size_t)m, nbytes = sizeof(double) * (size_t)(n > 0 ? n : 1);
@@ -492,21 +521,21 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
   /* Enforce X'w1 = 0 (pcg.cpp:55-66) */
   if (w1) memcpy(w, w1, mb); else memset(w, 0, mb);
   {
-    x_apply_t(G, M, nb, X, w, xtw);
+    mo->x_apply_t(s, w, xtw);
     const double feas = vnorm2(n, xtw);
-    const double sc = x_frobenius(G, M, nb, X) * vnorm2(m, w);
+    const double sc = mo->x_frob(s) * vnorm2(m, w);
     if (feas > 1e-14 * sc && feas > 0.0) {
-      st = sur_xstar(s, xtw, tmp);
+      st = mo->xstar(s, xtw, tmp);
       if (st) goto done;
       for (int64_t i = 0; i < m; ++i) w[i] -= tmp[i];
       res->w1_projected = 1;
     }
   }
   if (z1) memcpy(z, z1, nbytes); else memset(z, 0, nbytes);
-  orc_kron_apply(G, M, omega, w, sw);                                   /* sw = Sigma w */
-  x_apply(G, M, nb, X, z, xv);
+  mo->sigma(s, w, sw);                                                  /* sw = Sigma w */
+  mo->x_apply(s, z, xv);
   for (int64_t i = 0; i < m; ++i) r[i] = (sw[i] + xv[i]) - Y[i];         /* sub(add(sw, Xz), y) */
-  sur_pi(s, r, pr);
+  mo->pi(s, r, pr);
   double c = vdot(m, r, pr);
   if (c < 0.0) c = 0.0;                                                  /* max(dot, 0) */
   const double c1 = c;
@@ -521,14 +550,14 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
   (void)C_FLOOR(vdot(m, r, r), vnorm2(m, pr));
 
   memcpy(u, pr, mb);
-  st = sur_xstar_t(s, r, v);
+  st = mo->xstar_t(s, r, v);
   if (st) goto done;
 
   /* recover(sw) = X*'(y - sw) and push_row (pcg.cpp:96-116) */
 #define RECOVER(swsel, outv)                                           \
   do {                                                                 \
     for (int64_t i_ = 0; i_ < m; ++i_) tmp[i_] = Y[i_] - (swsel)[i_];  \
-    st = sur_xstar_t(s, tmp, (outv));                                  \
+    st = mo->xstar_t(s, tmp, (outv));                                  \
     if (st) goto done;                                                 \
   } while (0)
 #define PUSH_ROW(iter_, cval_, sampled_)                                                       \
@@ -537,10 +566,10 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
       orc_trace_row* row_ = &rows[nrows];                                                      \
       row_->iter = (iter_);                                                                    \
       row_->c = (cval_);                                                                       \
-      x_apply(G, M, nb, X, est, tmp);                                                          \
+      mo->x_apply(s, est, tmp);                                                                \
       for (int64_t i_ = 0; i_ < m; ++i_) tmp[i_] = Y[i_] - (sw[i_] + tmp[i_]);                 \
       row_->aug_residual_norm = vnorm2(m, tmp);                                                \
-      x_apply_t(G, M, nb, X, w, xtw);                                                          \
+      mo->x_apply_t(s, w, xtw);                                                                \
       row_->dual_feas_norm = vnorm2(n, xtw);                                                   \
       if ((sampled_) && beta_true) {                                                           \
         double acc_ = 0.0;                                                                     \
@@ -568,7 +597,7 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
     term = T_CONVERGED;
   } else {
     for (int64_t i = 1; i <= max_iter; ++i) {
-      orc_kron_apply(G, M, omega, u, su);                               /* su = Sigma u */
+      mo->sigma(s, u, su);                                              /* su = Sigma u */
       const double d = vdot(m, u, su);
       if (i - 1 < ORC_DIAG_MAX) {
         g_diag_d[i - 1] = fabs(d) / (vdot(m, u, u) * sigma_scale);
@@ -583,9 +612,9 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
       const double lambda = c / d;
       for (int64_t k = 0; k < m; ++k) w[k] += -lambda * u[k];          /* axpy(-lambda, u, w) */
       for (int64_t k = 0; k < m; ++k) sw[k] += -lambda * su[k];        /* axpy(-lambda, su, sw) */
-      x_apply(G, M, nb, X, v, xv);
+      mo->x_apply(s, v, xv);
       for (int64_t k = 0; k < m; ++k) r[k] -= lambda * (su[k] + xv[k]);
-      sur_pi(s, r, pr);
+      mo->pi(s, r, pr);
       double c_next = vdot(m, r, pr);
       done_it = i;
 
@@ -627,7 +656,7 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
       }
       const double mu = c_next / c;
       c = c_next;
-      st = sur_xstar_t(s, r, xr);
+      st = mo->xstar_t(s, r, xr);
       if (st) goto done;
       for (int64_t k = 0; k < n; ++k) v[k] = xr[k] + mu * v[k];
       for (int64_t k = 0; k < m; ++k) u[k] = pr[k] + mu * u[k];
@@ -652,6 +681,304 @@ int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const 
 done:
   free(w); free(sw); free(r); free(pr); free(u); free(su); free(xv); free(tmp); free(w_best); free(sw_best);
   free(z); free(v); free(xtw); free(est); free(xr);
+  return st;
+}
+
+/* ------------------------------------------------------------------ SUR: embed_sur + sur_preconditioner */
+typedef struct {
+  int G;
+  int64_t M;
+  const int64_t* nb;
+  const double* X;
+  const double* omega;
+  const orc_sur* op;
+} sur_model;
+
+static void sur_h_x(const void* c, const double* v, double* y) {
+  const sur_model* q = (const sur_model*)c;
+  x_apply(q->G, q->M, q->nb, q->X, v, y);
+}
+static void sur_h_xt(const void* c, const double* w, double* out) {
+  const sur_model* q = (const sur_model*)c;
+  x_apply_t(q->G, q->M, q->nb, q->X, w, out);
+}
+static double sur_h_frob(const void* c) {
+  const sur_model* q = (const sur_model*)c;
+  return x_frobenius(q->G, q->M, q->nb, q->X);
+}
+static void sur_h_sigma(const void* c, const double* x, double* out) {
+  const sur_model* q = (const sur_model*)c;
+  orc_kron_apply(q->G, q->M, q->omega, x, out);
+}
+static void sur_h_pi(const void* c, const double* xi, double* out) { sur_pi(((const sur_model*)c)->op, xi, out); }
+static int sur_h_xt_star(const void* c, const double* xi, double* out) {
+  return sur_xstar_t(((const sur_model*)c)->op, xi, out);
+}
+static int sur_h_xstar(const void* c, const double* v, double* out) { return sur_xstar(((const sur_model*)c)->op, v, out); }
+
+/* pcg_aug(embed_sur(sur), *sur_preconditioner(sur[, block_scale]), w1, z1, cfg, beta_true) */
+int orc_pcg_aug_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y, const double* omega,
+                    const double* scale, const double* w1, const double* z1, const orc_config* cfg,
+                    const double* beta_true, double* b_out, double* w_out, orc_trace_row* rows,
+                    int64_t rows_cap, orc_result* res, int* bad_block) {
+  orc_sur* s = NULL;
+  int st = orc_sur_build(G, M, nb, X, scale, &s, bad_block);
+  if (st) return st;
+  sur_model q = {G, M, nb, X, omega, s};
+  orc_model mo = {M * G, s->n, &q, sur_h_x, sur_h_xt, sur_h_frob, sur_h_sigma, sur_h_pi, sur_h_xt_star, sur_h_xstar};
+  st = run_aug(&mo, Y, w1, z1, cfg, beta_true, b_out, w_out, rows, rows_cap, res);
   orc_sur_free(s);
   return st;
+}
+
+/* ------------------------------------------------------------------ MVRGLM
+ * The multivariate model with exclusion restrictions (proj/include/gls/structured.hpp:37-52):
+ *   glm  = embed_mvrglm(mv)          (structured.cpp:77-95): X = [I_G (x) Z0 ; C], y = [vec Y ; 0_k],
+ *                                     Sigma = diag(Omega0 (x) I_M0, 0_k) (SymmetricOperator Padded)
+ *   op   = mvrglm_preconditioner(mv[, z_scale, c_scale])  (structured.cpp:365-414)
+ * The embedded row order is the reference's: rows [i M0, (i + 1) M0) are equation i's observations,
+ * then the k constraint rows, equation 0's first.  Restrictions come as CSR: equation i restricts the
+ * parameters ridx[roff[i] .. roff[i + 1]) (strictly increasing, < N0).  Nothing dense is formed: every
+ * X / X' / |X|_F / Sigma apply visits the non-zeros in the dense routine's order (off-pattern entries
+ * add exact +-0, as for SUR). */
+typedef struct {
+  int G;
+  int64_t M0, N0, m, k, n;
+  const double* Z0;     /* M0 x N0 */
+  const double* omega;  /* G x G */
+  const int64_t* roff;
+  const int64_t* ridx;
+  double* wz;           /* 1/sqrt(z_scale_i) */
+  double* wc;           /* 1/sqrt(c_scale_i) */
+  int64_t* qoff;        /* Q_i: (M0 + k_i) x N0 at qoff[i] */
+  double* Q;
+  double* R;            /* G x (N0 x N0) */
+  double* local;
+  double* tvec;
+} orc_mv;
+
+static void orc_mv_free(orc_mv* s) {
+  if (!s) return;
+  free(s->wz); free(s->wc); free(s->qoff); free(s->Q); free(s->R); free(s->local); free(s->tvec);
+  free(s);
+}
+
+/* MvRglmPreconditioner ctor (structured.cpp:367-411): per equation, qr_thin of the stacked
+ * [Z0 w_z ; C_i w_c] with C_i(r, restr_i[r]) = 1 */
+static int orc_mv_build(int G, int64_t M0, int64_t N0, const double* Z0, const double* omega, const int64_t* roff,
+                        const int64_t* ridx, const double* z_scale, const double* c_scale, orc_mv** out,
+                        int* bad_block) {
+  *out = NULL;
+  if (G < 1 || M0 < N0 || N0 < 1) return ORC_DIMENSION_MISMATCH; /* make_mvrglm: Z0 tall */
+  for (int i = 0; i < G; ++i)
+    for (int64_t q = roff[i]; q < roff[i + 1]; ++q)
+      if (ridx[q] < 0 || ridx[q] >= N0 || (q > roff[i] && ridx[q] <= ridx[q - 1])) return ORC_DIMENSION_MISMATCH;
+  orc_mv* s = (orc_mv*)calloc(1, sizeof(orc_mv));
+  if (!s) return ORC_NO_MEMORY;
+  s->G = G; s->M0 = M0; s->N0 = N0; s->Z0 = Z0; s->omega = omega; s->roff = roff; s->ridx = ridx;
+  s->k = roff[G];
+  s->m = (int64_t)G * M0;
+  s->n = (int64_t)G * N0;
+  int64_t kmax = 0, qtot = 0;
+  for (int i = 0; i < G; ++i) {
+    const int64_t ki = roff[i + 1] - roff[i];
+    if (ki > kmax) kmax = ki;
+    qtot += (M0 + ki) * N0;
+  }
+  s->wz = (double*)malloc(sizeof(double) * G);
+  s->wc = (double*)malloc(sizeof(double) * G);
+  s->qoff = (int64_t*)malloc(sizeof(int64_t) * G);
+  s->Q = (double*)malloc(sizeof(double) * (size_t)qtot);
+  s->R = (double*)malloc(sizeof(double) * (size_t)(G * N0 * N0));
+  s->local = (double*)malloc(sizeof(double) * (size_t)(M0 + kmax));
+  s->tvec = (double*)malloc(sizeof(double) * (size_t)N0);
+  double* stacked = (double*)malloc(sizeof(double) * (size_t)((M0 + kmax) * N0));
+  if (!s->wz || !s->wc || !s->qoff || !s->Q || !s->R || !s->local || !s->tvec || !stacked) {
+    free(stacked); orc_mv_free(s); return ORC_NO_MEMORY;
+  }
+  for (int i = 0; i < G; ++i) {
+    const double zs = z_scale ? z_scale[i] : 1.0, cs = c_scale ? c_scale[i] : 1.0;
+    if (zs <= 0.0 || cs <= 0.0) { if (bad_block) *bad_block = i; free(stacked); orc_mv_free(s); return ORC_SINGULAR_D; }
+  }
+  int64_t q0 = 0;
+  for (int i = 0; i < G; ++i) {
+    const int64_t ki = roff[i + 1] - roff[i], rows = M0 + ki;
+    const double wz = 1.0 / sqrt(z_scale ? z_scale[i] : 1.0);
+    const double wc = 1.0 / sqrt(c_scale ? c_scale[i] : 1.0);
+    s->wz[i] = wz; s->wc[i] = wc;
+    memset(stacked, 0, sizeof(double) * (size_t)(rows * N0));
+    for (int64_t j = 0; j < N0; ++j)
+      for (int64_t r = 0; r < M0; ++r) stacked[r + j * rows] = Z0[r + j * M0] * wz;
+    for (int64_t r = 0; r < ki; ++r) stacked[M0 + r + ridx[roff[i] + r] * rows] = wc;
+    s->qoff[i] = q0;
+    int st = orc_qr_thin(rows, N0, stacked, rows, 1.0, s->Q + q0, rows, s->R + (int64_t)i * N0 * N0);
+    if (st != ORC_OK) { if (bad_block) *bad_block = i; free(stacked); orc_mv_free(s); return st; }
+    q0 += rows * N0;
+  }
+  free(stacked);
+  *out = s;
+  return ORC_OK;
+}
+
+/* embedded row of local row r of equation i (Block::row_index, structured.cpp:392-400) */
+static int64_t mv_row(const orc_mv* s, int i, int64_t r) {
+  return r < s->M0 ? (int64_t)i * s->M0 + r : s->m + s->roff[i] + (r - s->M0);
+}
+static double mv_isd(const orc_mv* s, int i, int64_t r) { return r < s->M0 ? s->wz[i] : s->wc[i]; }
+
+/* BlockQrPreconditioner::pi_impl / xstar_t_impl / xstar_impl (structured.cpp:307-340) */
+static void mv_pi(const void* c, const double* xi, double* out) {
+  const orc_mv* s = (const orc_mv*)c;
+  const int64_t N0 = s->N0;
+  for (int64_t i = 0; i < s->m + s->k; ++i) out[i] = 0.0;
+  double* proj = (double*)malloc(sizeof(double) * (size_t)(s->M0 + s->k + 1));
+  for (int i = 0; i < s->G; ++i) {
+    const int64_t rows = s->M0 + (s->roff[i + 1] - s->roff[i]);
+    const double* Qi = s->Q + s->qoff[i];
+    for (int64_t r = 0; r < rows; ++r) s->local[r] = xi[mv_row(s, i, r)] * mv_isd(s, i, r);
+    gemv_t(rows, N0, Qi, rows, s->local, s->tvec);
+    gemv(rows, N0, Qi, rows, s->tvec, proj);
+    for (int64_t r = 0; r < rows; ++r) s->local[r] -= proj[r];
+    for (int64_t r = 0; r < rows; ++r) out[mv_row(s, i, r)] = s->local[r] * mv_isd(s, i, r);
+  }
+  free(proj);
+}
+static int mv_xstar_t(const void* c, const double* xi, double* out) {
+  const orc_mv* s = (const orc_mv*)c;
+  const int64_t N0 = s->N0;
+  for (int i = 0; i < s->G; ++i) {
+    const int64_t rows = s->M0 + (s->roff[i + 1] - s->roff[i]);
+    for (int64_t r = 0; r < rows; ++r) s->local[r] = xi[mv_row(s, i, r)] * mv_isd(s, i, r);
+    gemv_t(rows, N0, s->Q + s->qoff[i], rows, s->local, out + (int64_t)i * N0);
+    int st = tri_solve(N0, s->R + (int64_t)i * N0 * N0, out + (int64_t)i * N0, 0);
+    if (st) return st;
+  }
+  return ORC_OK;
+}
+static int mv_xstar(const void* c, const double* v, double* out) {
+  const orc_mv* s = (const orc_mv*)c;
+  const int64_t N0 = s->N0;
+  for (int64_t i = 0; i < s->m + s->k; ++i) out[i] = 0.0;
+  for (int i = 0; i < s->G; ++i) {
+    const int64_t rows = s->M0 + (s->roff[i + 1] - s->roff[i]);
+    memcpy(s->tvec, v + (int64_t)i * N0, sizeof(double) * (size_t)N0);
+    int st = tri_solve(N0, s->R + (int64_t)i * N0 * N0, s->tvec, 1);
+    if (st) return st;
+    gemv(rows, N0, s->Q + s->qoff[i], rows, s->tvec, s->local);
+    for (int64_t r = 0; r < rows; ++r) out[mv_row(s, i, r)] = s->local[r] * mv_isd(s, i, r);
+  }
+  return ORC_OK;
+}
+
+/* X v with X = embed_mvrglm's dense matrix (dense_matrix.cpp:69-79): column i N0 + j holds Z0(:, j) on
+ * equation i's rows and a 1 on the constraint row of (i, j) when j is restricted. */
+static void mv_x(const void* c, const double* v, double* y) {
+  const orc_mv* s = (const orc_mv*)c;
+  for (int i = 0; i < s->G; ++i) gemv(s->M0, s->N0, s->Z0, s->M0, v + (int64_t)i * s->N0, y + (int64_t)i * s->M0);
+  for (int i = 0; i < s->G; ++i)
+    for (int64_t q = s->roff[i]; q < s->roff[i + 1]; ++q) {
+      const double vj = v[(int64_t)i * s->N0 + s->ridx[q]];
+      y[s->m + q] = (vj == 0.0) ? 0.0 : 0.0 + 1.0 * vj;
+    }
+}
+/* X' w: per column, the sequential dot over every row (dense_matrix.cpp:81-91): the observation rows,
+ * then the one constraint row */
+static void mv_xt(const void* c, const double* w, double* out) {
+  const orc_mv* s = (const orc_mv*)c;
+  for (int i = 0; i < s->G; ++i) {
+    double* oi = out + (int64_t)i * s->N0;
+    gemv_t(s->M0, s->N0, s->Z0, s->M0, w + (int64_t)i * s->M0, oi);
+    for (int64_t q = s->roff[i]; q < s->roff[i + 1]; ++q) oi[s->ridx[q]] += 1.0 * w[s->m + q];
+  }
+}
+/* |X|_F in storage order (dense_matrix.cpp:93-97) */
+static double mv_frob(const void* c) {
+  const orc_mv* s = (const orc_mv*)c;
+  double acc = 0.0;
+  for (int i = 0; i < s->G; ++i) {
+    int64_t q = s->roff[i];
+    for (int64_t j = 0; j < s->N0; ++j) {
+      for (int64_t r = 0; r < s->M0; ++r) acc += s->Z0[r + j * s->M0] * s->Z0[r + j * s->M0];
+      if (q < s->roff[i + 1] && s->ridx[q] == j) { acc += 1.0 * 1.0; ++q; }
+    }
+  }
+  return sqrt(acc);
+}
+/* Sigma = block_zero_padded(kronecker(Omega0, I_M0), k) (operators.cpp:51-57): the top is the dense
+ * Kronecker matrix, whose row (a M0 + r) sums Omega0(a, b) x[b M0 + r] in ascending b -- the Kronecker
+ * apply's order for a symmetric Omega0; the k constraint rows are zero. */
+static void mv_sigma(const void* c, const double* x, double* out) {
+  const orc_mv* s = (const orc_mv*)c;
+  orc_kron_apply(s->G, s->M0, s->omega, x, out);
+  for (int64_t q = 0; q < s->k; ++q) out[s->m + q] = 0.0;
+}
+
+int orc_pcg_aug_mvrglm(int G, int64_t M0, int64_t N0, const double* Z0, const double* Y, const double* omega,
+                       const int64_t* roff, const int64_t* ridx, const double* z_scale, const double* c_scale,
+                       const double* w1, const double* z1, const orc_config* cfg, const double* beta_true,
+                       double* b_out, double* w_out, orc_trace_row* rows, int64_t rows_cap, orc_result* res,
+                       int* bad_block) {
+  orc_mv* s = NULL;
+  int st = orc_mv_build(G, M0, N0, Z0, omega, roff, ridx, z_scale, c_scale, &s, bad_block);
+  if (st) return st;
+  const int64_t mt = s->m + s->k;
+  double* y = (double*)calloc((size_t)mt, sizeof(double));
+  if (!y) { orc_mv_free(s); return ORC_NO_MEMORY; }
+  memcpy(y, Y, sizeof(double) * (size_t)s->m); /* y = [vec Y ; 0_k] (structured.cpp:89-90) */
+  orc_model mo = {mt, s->n, s, mv_x, mv_xt, mv_frob, mv_sigma, mv_pi, mv_xstar_t, mv_xstar};
+  st = run_aug(&mo, y, w1, z1, cfg, beta_true, b_out, w_out, rows, rows_cap, res);
+  free(y);
+  orc_mv_free(s);
+  return st;
+}
+
+/* kind: 0 = apply_pi (m + k -> m + k), 1 = apply_xstar_t (-> G N0), 2 = apply_xstar (G N0 -> m + k);
+ * 3 = Sigma apply, 4 = X apply (G N0 -> m + k), 5 = X' apply (m + k -> G N0) */
+int orc_mvrglm_apply(int G, int64_t M0, int64_t N0, const double* Z0, const double* omega, const int64_t* roff,
+                     const int64_t* ridx, const double* z_scale, const double* c_scale, int kind, const double* in,
+                     double* out) {
+  orc_mv* s = NULL;
+  int bad = -1;
+  int st = orc_mv_build(G, M0, N0, Z0, omega, roff, ridx, z_scale, c_scale, &s, &bad);
+  if (st) return st;
+  if (kind == 0) mv_pi(s, in, out);
+  else if (kind == 1) st = mv_xstar_t(s, in, out);
+  else if (kind == 2) st = mv_xstar(s, in, out);
+  else if (kind == 3) mv_sigma(s, in, out);
+  else if (kind == 4) mv_x(s, in, out);
+  else mv_xt(s, in, out);
+  orc_mv_free(s);
+  return st;
+}
+
+double orc_mvrglm_norm_probe(int G, int64_t M0, int64_t N0, const double* Z0, const double* omega,
+                             const int64_t* roff, const int64_t* ridx) {
+  orc_mv* s = NULL;
+  int bad = -1;
+  if (orc_mv_build(G, M0, N0, Z0, omega, roff, ridx, NULL, NULL, &s, &bad)) return -1.0;
+  orc_model mo = {s->m + s->k, s->n, s, mv_x, mv_xt, mv_frob, mv_sigma, mv_pi, mv_xstar_t, mv_xstar};
+  const double r = model_norm_probe(&mo, 12);
+  orc_mv_free(s);
+  return r;
+}
+
+/* mv_reduce (structured.cpp:121-130): Z0 = Q0 R0; reduced Z0 = R0 (N0 x N0), reduced Y = Q0' Y via
+ * DenseMatrix operator* (dense_matrix.cpp:125-139: out(:, j) += A(:, p) B(p, j), p ascending, skipping
+ * B(p, j) == 0) with A = Q0' */
+int orc_mv_reduce(int G, int64_t M0, int64_t N0, const double* Z0, const double* Y, double* r_out, double* qty_out) {
+  double* q = (double*)malloc(sizeof(double) * (size_t)(M0 * N0));
+  if (!q) return ORC_NO_MEMORY;
+  int st = orc_qr_thin(M0, N0, Z0, M0, 1.0, q, M0, r_out);
+  if (st) { free(q); return st; }
+  for (int64_t k = 0; k < N0 * G; ++k) qty_out[k] = 0.0;
+  for (int j = 0; j < G; ++j) {
+    double* cj = qty_out + (int64_t)j * N0;
+    for (int64_t p = 0; p < M0; ++p) {
+      const double bpj = Y[p + (int64_t)j * M0];
+      if (bpj == 0.0) continue;
+      for (int64_t i = 0; i < N0; ++i) cj[i] += q[p + i * M0] * bpj; /* Q0'(i, p) = Q0(p, i) */
+    }
+  }
+  free(q);
+  return ORC_OK;
 }

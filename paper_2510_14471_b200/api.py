@@ -372,11 +372,17 @@ def pcg_aug(sur_or_op, precond: Optional[GpuSurPreconditioner] = None, w1=None, 
             want_trace: bool = True) -> AugSolveResult:
     """pcg_aug (pcg.cpp:346-350 -> run_aug, Recovery variant) on the SUR model, on the device.
 
-    `sur_or_op` is the SurModel (the reference passes embed_sur(sur)); `precond` its
-    sur_preconditioner (built here when None).
+    `sur_or_op` is the SurModel (the reference passes embed_sur(sur)) or the MvRglm (embed_mvrglm(mv));
+    `precond` its sur_preconditioner / mvrglm_preconditioner (built here when None).
     """
-    op = precond if precond is not None else (sur_or_op if isinstance(sur_or_op, GpuSurPreconditioner)
-                                              else sur_preconditioner(sur_or_op))
+    if precond is not None:
+        op = precond
+    elif isinstance(sur_or_op, GpuSurPreconditioner):
+        op = sur_or_op
+    elif isinstance(sur_or_op, MvRglm):
+        op = mvrglm_preconditioner(sur_or_op)  # pcg_aug(embed_mvrglm(mv), *mvrglm_preconditioner(mv))
+    else:
+        op = sur_preconditioner(sur_or_op)
     cfg = config or PcgConfig()
     m, n = op.m, op.n
     if w1 is not None and np.asarray(w1).size != m or z1 is not None and np.asarray(z1).size != n:
@@ -403,6 +409,150 @@ def pcg_aug(sur_or_op, precond: Optional[GpuSurPreconditioner] = None, w1=None, 
                      breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
                      w1_projected=bool(res.w1_projected))
     return AugSolveResult(solution=sol, trace=trace, sigma_scale=float(res.sigma_scale), solve_ms=float(res.solve_ms))
+
+
+# ------------------------------------------------------------------------------------------ MVRGLM
+@dataclasses.dataclass
+class MvRglm:
+    """gls::MvRglm (structured.hpp:33-43): Y = Z0 B + U, restrictions[i] = zero-forced rows of B[:, i]."""
+    z0: np.ndarray
+    y: np.ndarray
+    omega0: np.ndarray
+    restrictions: List[np.ndarray]
+
+    def obs(self) -> int:
+        return int(self.z0.shape[0])
+
+    def params_per_eq(self) -> int:
+        return int(self.z0.shape[1])
+
+    def equations(self) -> int:
+        return int(self.y.shape[1])
+
+    def total_restrictions(self) -> int:
+        return int(sum(len(r) for r in self.restrictions))
+
+    def csr(self):
+        roff = np.zeros(self.equations() + 1, dtype=np.int64)
+        roff[1:] = np.cumsum([len(r) for r in self.restrictions])
+        ridx = (np.concatenate([np.asarray(r, dtype=np.int64) for r in self.restrictions])
+                if roff[-1] else np.zeros(1, dtype=np.int64))
+        return roff, np.ascontiguousarray(ridx, dtype=np.int64)
+
+
+@dataclasses.dataclass
+class ReductionRecord:
+    """gls::ReductionRecord (structured.hpp:67-72)."""
+    original_rows: int
+    reduced_rows: int
+    rank: int
+
+
+def make_mvrglm(z0: np.ndarray, y: np.ndarray, omega0: np.ndarray, restrictions) -> MvRglm:
+    """make_mvrglm (structured.cpp:63-74): same checks, same messages."""
+    z0 = np.asfortranarray(z0, dtype=np.float64)
+    y = np.asfortranarray(y, dtype=np.float64)
+    omega0 = np.asfortranarray(omega0, dtype=np.float64)
+    if z0.shape[0] < z0.shape[1]:
+        raise DimensionMismatch("make_mvrglm: Z0 must be tall")
+    if y.shape[0] != z0.shape[0]:
+        raise DimensionMismatch("make_mvrglm: Y/Z0 row mismatch")
+    if omega0.shape != (y.shape[1], y.shape[1]):
+        raise DimensionMismatch("make_mvrglm: Omega0 must be G x G")
+    if len(restrictions) != y.shape[1]:
+        raise DimensionMismatch("restrictions: need one list per equation")
+    out = []
+    for lst in restrictions:
+        a = np.asarray(lst, dtype=np.int64).reshape(-1)
+        if a.size and (a.min() < 0 or a.max() >= z0.shape[1]):
+            raise DimensionMismatch("restrictions: index out of range")
+        if a.size > 1 and np.any(np.diff(a) <= 0):
+            raise DimensionMismatch("restrictions: indices must be strictly increasing")
+        out.append(a)
+    return MvRglm(z0=z0, y=y, omega0=omega0, restrictions=out)
+
+
+def mv_from_problem(prob) -> MvRglm:
+    return make_mvrglm(prob.Z0, prob.Y, prob.omega, prob.restrictions)
+
+
+class GpuMvRglmPreconditioner(GpuSurPreconditioner):
+    """MvRglmPreconditioner (structured.cpp:365-414) on the B200, with the embed_mvrglm operator
+    (structured.cpp:77-95) behind the same handle: per-equation QR of the stacked [Z0 w_z; C_i w_c].
+    Host m-vectors use the reference's embedded order (G M0 observation rows, then the k constraint rows)."""
+
+    def __init__(self, mv: MvRglm, z_scale=None, c_scale=None, device: int = 0):
+        self._lib = L.load()
+        self.sur = None
+        self.mv = mv
+        self._h = C.c_void_p()
+        G = mv.equations()
+        self._nb = np.full(G, mv.params_per_eq(), dtype=np.int64)
+        zs = None if z_scale is None else np.ascontiguousarray(z_scale, dtype=np.float64)
+        cs = None if c_scale is None else np.ascontiguousarray(c_scale, dtype=np.float64)
+        for v in (zs, cs):
+            if v is not None and v.shape != (G,):
+                raise DimensionMismatch("mvrglm_preconditioner: need one scale per equation")
+        roff, ridx = mv.csr()
+        bad = C.c_int(-1)
+        code = self._lib.glsgpu_mvrglm_create(G, mv.obs(), mv.params_per_eq(), _dp(mv.z0), _dp(mv.y), _dp(mv.omega0),
+                                              roff.ctypes.data_as(_PI64), ridx.ctypes.data_as(_PI64), _dp(zs), _dp(cs),
+                                              device, C.byref(self._h), C.byref(bad))
+        self.bad_block = bad.value
+        _check(code, self._lib)
+        m, n = C.c_int64(0), C.c_int64(0)
+        _check(self._lib.glsgpu_model_dims(self._h, C.byref(m), C.byref(n)), self._lib)
+        self.m, self.n = int(m.value), int(n.value)
+
+    def factors(self):
+        raise NotImplementedError("factors(): SUR handles only")
+
+
+def mvrglm_preconditioner(mv: MvRglm, z_scale=None, c_scale=None, device: int = 0) -> GpuMvRglmPreconditioner:
+    """mvrglm_preconditioner (structured.cpp:468-477); identity auxiliary when no scales are given."""
+    return GpuMvRglmPreconditioner(mv, z_scale, c_scale, device)
+
+
+def mv_reduce(mv: MvRglm, device: int = 0):
+    """mv_reduce (structured.cpp:121-130) on the device: (reduced MvRglm with Z0 -> R0, Y -> Q0'Y, record).
+
+    R0 is the reference's up to row signs (TSQR instead of one Householder sweep); the GLS estimate of the
+    reduced model does not depend on them."""
+    lib = L.load()
+    G, M0, N0 = mv.equations(), mv.obs(), mv.params_per_eq()
+    R = np.zeros((N0, N0), order="F")
+    QtY = np.zeros((N0, G), order="F")
+    _check(lib.glsgpu_mv_reduce(G, M0, N0, _dp(mv.z0), _dp(mv.y), _dp(R), _dp(QtY), device), lib)
+    red = MvRglm(z0=R, y=QtY, omega0=mv.omega0, restrictions=list(mv.restrictions))
+    return red, ReductionRecord(original_rows=M0, reduced_rows=N0, rank=N0)
+
+
+def _frobenius(a: np.ndarray) -> float:
+    """DenseMatrix::frobenius_norm (dense_matrix.cpp:93-97): sequential sum of squares in storage order."""
+    v = np.asarray(a, dtype=np.float64).reshape(-1, order="F")
+    return float(np.sqrt(np.cumsum(v * v)[-1])) if v.size else 0.0
+
+
+def auxiliary_scales(omega0: np.ndarray, rule: str, z0: Optional[np.ndarray] = None):
+    """The harness's scaled-D choices (experiments.cpp:826-851): K1 = alpha I with alpha = max_i Omega_ii,
+    K2 = diag(Omega).  Returns the SUR block scales, or with z0 (the reduced multivariate regressor) the
+    (z_scale, c_scale) pair of mvrglm_preconditioner: the constraint rows' auxiliary variance is matched to
+    the data scale |Z0|_F^2 / N0."""
+    d = np.array([float(omega0[i, i]) for i in range(omega0.shape[0])])
+    alpha = 0.0
+    for v in d:  # std::max in the reference's loop order
+        alpha = max(alpha, v)
+    if rule == "k1":
+        z = np.full(len(d), alpha)
+    elif rule == "k2":
+        z = d.copy()
+    else:
+        raise ValueError(rule)
+    if z0 is None:
+        return z
+    f = _frobenius(z0)
+    z_scale2 = f * f / float(z0.shape[1])
+    return z, z / z_scale2
 
 
 def nccl_unique_id() -> bytes:

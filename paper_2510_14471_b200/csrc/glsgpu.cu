@@ -106,10 +106,20 @@ struct glsgpu_sur {
   int nch = 0, nmax = 0;
   std::vector<int> nb;
   std::vector<int64_t> p0, r0;
-  std::vector<double> wts;
+  std::vector<double> wts, wtc;
   int* d_nb = nullptr;
   int64_t *d_p0 = nullptr, *d_r0 = nullptr;
-  double* d_wts = nullptr;
+  double *d_wts = nullptr, *d_wtc = nullptr;
+  // MVRGLM embedding (glsgpu_mvrglm_create): block b = [Z0 (M0 rows); C_b (k_b selector rows); 0], M = M0 + max k_b.
+  // For SUR: msig = ldm (every row under Sigma), m_ref = M_global G, wtc = wts.
+  bool mv = false;
+  int64_t msig = 0;                 // rows of every block under Sigma
+  int64_t m_ref = 0;                // rows of the reference's embedded GLM (host m-vectors)
+  int64_t M0 = 0;                   // MVRGLM observation rows per equation
+  std::vector<int64_t> kb, kofs;    // MVRGLM constraint rows of block b and their offset in the reference order
+  std::vector<int64_t> rows_b;      // rows of block b in the reference's operator (cost model)
+  double* Xqr = nullptr;            // pre-scaled QR source D^-1/2 X (two weights per block); null: X * w_b
+  int rank_msg = 0;                 // 1: plain qr_thin (mv_reduce) wording of RankDeficient
   const double* X = nullptr;
   int64_t ldx = 0;
   double* X_own = nullptr;
@@ -199,6 +209,8 @@ Geo geo_of(const glsgpu_sur* h) {
   g.p0 = h->d_p0;
   g.r0 = h->d_r0;
   g.wts = h->d_wts;
+  g.wtc = h->d_wtc;
+  g.msig = h->msig;
   return g;
 }
 
@@ -231,7 +243,7 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
   if (grid_out) *grid_out = grid;
 #define KRON_CASE(C, RW)                                                                                       \
   k_kron<C, RW><<<grid, NT, smem, h->s>>>(h->G, h->ldm, ntiles, h->omegaT, src, prv, div, u_io, out, partials, \
-                                          in_mode, st, wbuf_of(h))
+                                          in_mode, st, wbuf_of(h), h->msig)
   switch (cpl) {
     case 1: KRON_CASE(1, 4); break;
     case 2: KRON_CASE(2, 4); break;
@@ -264,10 +276,10 @@ void launch_pass_a(glsgpu_sur* h) {
   const int grid = kron_grid(h);
   if (h->kron_fma)
     k_kron_ws<true><<<grid, KW_NT, kw_smem_bytes(), h->s>>>(h->vmap, h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->u,
-                                                            h->su, h->partA, h->st, wbuf_of(h));
+                                                            h->su, h->partA, h->st, wbuf_of(h), h->msig);
   else
     k_kron_ws<false><<<grid, KW_NT, kw_smem_bytes(), h->s>>>(h->vmap, h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->u,
-                                                             h->su, h->partA, h->st, wbuf_of(h));
+                                                             h->su, h->partA, h->st, wbuf_of(h), h->msig);
   if (!h->capturing) h->launches++;
   CKL("k_kron_ws");
 }
@@ -572,14 +584,21 @@ void reduce_t_global(glsgpu_sur* h, double* out, const SolveState* st, int gate)
 }
 
 // ------------------------------------------------------------------------------------------ setup
-void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const double* block_scale) {
+void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const double* block_scale,
+                    const double* c_scale = nullptr) {
   h->G = G;
   h->M = M;
   h->ldm = round_up(M, 32);
+  if (!h->mv) {
+    h->msig = h->ldm;
+    h->m_ref = h->M_global * G;
+    h->rows_b.assign(G, h->M_global);
+  }
   h->nb.resize(G);
   h->p0.resize(G);
   h->r0.resize(G);
   h->wts.resize(G);
+  h->wtc.resize(G);
   int64_t p = 0, r = 0;
   int nmax = 0;
   for (int b = 0; b < G; ++b) {
@@ -591,6 +610,7 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
     nmax = std::max<int>(nmax, (int)n_i[b]);
     // w = 1/sqrt(scale) (structured.cpp:430)
     h->wts[b] = 1.0 / std::sqrt(block_scale ? block_scale[b] : 1.0);
+    h->wtc[b] = c_scale ? 1.0 / std::sqrt(c_scale[b]) : h->wts[b];
   }
   h->n = p;
   h->nmax = nmax;
@@ -601,10 +621,12 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
   h->d_p0 = dalloc<int64_t>(G);
   h->d_r0 = dalloc<int64_t>(G);
   h->d_wts = dalloc<double>(G);
+  h->d_wtc = dalloc<double>(G);
   CK(cudaMemcpy(h->d_nb, h->nb.data(), sizeof(int) * G, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_p0, h->p0.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_r0, h->r0.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_wts, h->wts.data(), sizeof(double) * G, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_wtc, h->wtc.data(), sizeof(double) * G, cudaMemcpyHostToDevice));
   std::vector<int> narrow, wide;
   for (int b = 0; b < G; ++b) (h->nb[b] <= 32 ? narrow : wide).push_back(b);
   h->n_narrow = (int)narrow.size();
@@ -617,7 +639,7 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
   // pass cost model of finalize() (structured.cpp:296-305)
   h->pi_cost = h->xstar_t_cost = h->xstar_cost = 0;
   for (int b = 0; b < G; ++b) {
-    const uint64_t rr = (uint64_t)h->M_global, nn = (uint64_t)h->nb[b];
+    const uint64_t rr = (uint64_t)h->rows_b[b], nn = (uint64_t)h->nb[b];
     h->pi_cost += 2 * rr * nn + 2 * rr;
     h->xstar_t_cost += rr * nn + nn * (nn + 1) / 2 + rr;
     h->xstar_cost += rr * nn + nn * (nn + 1) / 2 + rr;
@@ -707,19 +729,19 @@ void build_qr_plan(glsgpu_sur* h) {
           // tile-contiguous Q: leaf c = rows [256 c, 256 c + 256) (zero-padded) = Q tile c of block b
           it.r0 = c * narrow_leaf_rows();
           it.rows = std::min<int64_t>(narrow_leaf_rows(), rows - it.r0);
-          it.src = h->X + h->p0[b] * h->ldx;
-          it.lds = h->ldx;
+          it.src = h->Xqr ? h->Xqr + h->p0[b] * h->ldm : h->X + h->p0[b] * h->ldx;
+          it.lds = h->Xqr ? h->ldm : h->ldx;
           it.valid = h->M;
-          it.scale = h->wts[b];
+          it.scale = h->Xqr ? 1.0 : h->wts[b];
           it.refl = h->Q + h->qoff[b] + c * narrow_leaf_rows() * (int64_t)n;  // tile c (and 2c + 1: reg leaves)
           it.ldr = QRR_NT;
           it.rr0 = 0;
           it.rhalf = (int64_t)QRR_NT * n;
         } else if (lvl == 0) {
-          it.src = h->X + h->p0[b] * h->ldx;
-          it.lds = h->ldx;
+          it.src = h->Xqr ? h->Xqr + h->p0[b] * h->ldm : h->X + h->p0[b] * h->ldx;
+          it.lds = h->Xqr ? h->ldm : h->ldx;
           it.valid = h->M;
-          it.scale = h->wts[b];
+          it.scale = h->Xqr ? 1.0 : h->wts[b];
           it.refl = h->Q + h->p0[b] * h->ldm;
           it.ldr = h->ldm;
         } else {
@@ -907,10 +929,17 @@ void run_qr(glsgpu_sur* h) {
   CK(cudaMemcpyAsync(flags.data(), h->d_rank_flags, sizeof(int) * h->G, cudaMemcpyDeviceToHost, h->s));
   CK(cudaStreamSynchronize(h->s));
   for (int b = 0; b < h->G; ++b)
-    if (flags[b]) fail(GLSGPU_ERR_RANK_DEFICIENT, "sur_preconditioner: block " + std::to_string(b) + " is rank deficient", b);
+    if (flags[b]) {
+      if (h->rank_msg == 1) fail(GLSGPU_ERR_RANK_DEFICIENT, "qr: matrix is numerically rank deficient", b);
+      fail(GLSGPU_ERR_RANK_DEFICIENT,
+           std::string(h->mv ? "mvrglm_preconditioner: stacked block " : "sur_preconditioner: block ") +
+               std::to_string(b) + " is rank deficient",
+           b);
+    }
 }
 
-void validate(int G, int64_t M, const int64_t* n_i, const double* block_scale, const double* omega) {
+void validate(int G, int64_t M, const int64_t* n_i, const double* block_scale, const double* omega,
+              bool need_m_gt_n = true) {
   if (G < 1) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_sur: need at least one block");
   if (!n_i || !omega) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create: null argument");
   if (M < 1) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_sur: block row mismatch");
@@ -923,7 +952,7 @@ void validate(int G, int64_t M, const int64_t* n_i, const double* block_scale, c
   }
   int64_t n = 0;
   for (int b = 0; b < G; ++b) n += n_i[b];
-  if (M * G <= n) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_glm: need m > n >= 1");
+  if (need_m_gt_n && M * G <= n) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_glm: need m > n >= 1");
 }
 
 void upload_omega(glsgpu_sur* h, const double* omega) {
@@ -977,7 +1006,7 @@ void destroy_impl(glsgpu_sur* h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->graph) cudaGraphExecDestroy(h->graph);
   for (auto e : h->tev) cudaEventDestroy(e);
-  void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
+  void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->d_wtc, h->Xqr, h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
                   h->qr_store, h->qr_tau, h->qr_scratch, h->d_rank_flags, h->d_blk_narrow, h->d_blk_wide,
                   h->mvec, h->t,
                   h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,
@@ -991,11 +1020,18 @@ void destroy_impl(glsgpu_sur* h) {
   delete h;
 }
 
+// MVRGLM embedding of glsgpu_mvrglm_create (set on the handle before the geometry is built)
+struct MvDesc {
+  int64_t M0 = 0, ktot = 0;
+  std::vector<int64_t> kb, kofs;
+  const double* c_scale = nullptr;
+};
+
 glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* omega, const double* block_scale,
                           int device, int64_t M_global = -1, int rank = 0, int nranks = 1,
-                          const void* nccl_id = nullptr) {
+                          const void* nccl_id = nullptr, const MvDesc* mvd = nullptr, bool qr_only = false) {
   if (M_global < 0) M_global = M;
-  validate(G, M_global, n_i, block_scale, omega);
+  validate(G, M_global, n_i, block_scale, omega, /*need_m_gt_n=*/!qr_only);
   if (nranks < 1 || rank < 0 || rank >= nranks) fail(GLSGPU_ERR_INVALID, "glsgpu: bad rank / nranks");
   if (nranks > 1) {
     if (!nccl_id) fail(GLSGPU_ERR_INVALID, "glsgpu: sharded handle needs an NCCL unique id");
@@ -1023,7 +1059,17 @@ glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* om
       std::memcpy(&id, nccl_id, sizeof(id));
       nccl_check(nccl().CommInitRank(&h->comm, nranks, id, rank), "ncclCommInitRank");
     }
-    build_geometry(h, G, M, n_i, block_scale);
+    if (mvd) {
+      h->mv = true;
+      h->M0 = mvd->M0;
+      h->kb = mvd->kb;
+      h->kofs = mvd->kofs;
+      h->msig = mvd->M0;
+      h->m_ref = (int64_t)G * mvd->M0 + mvd->ktot;
+      h->rows_b.resize(G);
+      for (int b = 0; b < G; ++b) h->rows_b[b] = mvd->M0 + mvd->kb[b];
+    }
+    build_geometry(h, G, M, n_i, block_scale, mvd ? mvd->c_scale : nullptr);
     upload_omega(h, omega);
   } catch (...) {
     destroy_impl(h);
@@ -1115,13 +1161,34 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
 }
 
 // m-vector host (ld M per equation) <-> device (ld ldm)
+// MVRGLM handles map the reference's embedded order (G M0 observation rows, then the k constraint rows,
+// equation 0's first; structured.cpp:85-90) onto the padded per-block layout [obs; constraints; 0].
 void h2d_mvec(glsgpu_sur* h, double* dst, const double* src) {
-  CK(cudaMemcpy2DAsync(dst, h->ldm * sizeof(double), src, h->M * sizeof(double), h->M * sizeof(double), h->G,
+  if (!h->mv) {
+    CK(cudaMemcpy2DAsync(dst, h->ldm * sizeof(double), src, h->M * sizeof(double), h->M * sizeof(double), h->G,
+                         cudaMemcpyHostToDevice, h->s));
+    return;
+  }
+  CK(cudaMemsetAsync(dst, 0, sizeof(double) * h->ldm * h->G, h->s));
+  CK(cudaMemcpy2DAsync(dst, h->ldm * sizeof(double), src, h->M0 * sizeof(double), h->M0 * sizeof(double), h->G,
                        cudaMemcpyHostToDevice, h->s));
+  for (int b = 0; b < h->G; ++b)
+    if (h->kb[b])
+      CK(cudaMemcpyAsync(dst + (int64_t)b * h->ldm + h->M0, src + (int64_t)h->G * h->M0 + h->kofs[b],
+                         sizeof(double) * h->kb[b], cudaMemcpyHostToDevice, h->s));
 }
 void d2h_mvec(glsgpu_sur* h, double* dst, const double* src) {
-  CK(cudaMemcpy2DAsync(dst, h->M * sizeof(double), src, h->ldm * sizeof(double), h->M * sizeof(double), h->G,
+  if (!h->mv) {
+    CK(cudaMemcpy2DAsync(dst, h->M * sizeof(double), src, h->ldm * sizeof(double), h->M * sizeof(double), h->G,
+                         cudaMemcpyDeviceToHost, h->s));
+    return;
+  }
+  CK(cudaMemcpy2DAsync(dst, h->M0 * sizeof(double), src, h->ldm * sizeof(double), h->M0 * sizeof(double), h->G,
                        cudaMemcpyDeviceToHost, h->s));
+  for (int b = 0; b < h->G; ++b)
+    if (h->kb[b])
+      CK(cudaMemcpyAsync(dst + (int64_t)h->G * h->M0 + h->kofs[b], src + (int64_t)b * h->ldm + h->M0,
+                         sizeof(double) * h->kb[b], cudaMemcpyDeviceToHost, h->s));
 }
 
 // t_out = (Q' (w_b x))_b partials reduced: a Q'-apply of an m-vector already on the device.
@@ -1136,9 +1203,11 @@ double norm_probe(glsgpu_sur* h, int64_t iters) {
   // so the power iteration is exactly an iteration on the G-vector x with |v| = sqrt(M |x|^2).  Each
   // entry of Sigma v is the reference's own p-ascending sum; only the norm's summation order differs.
   // O(iters G^2) on the host instead of iters full Kronecker passes over M x G.
+  // MVRGLM: Sigma = diag(Omega0 (x) I_M0, 0_k): the start vector has m = G M0 + k entries, the k constraint
+  // entries vanish after the first apply and the rest stay row-constant per block over the M0 rows under Sigma
   const int G = h->G;
-  const double Mg = static_cast<double>(h->M_global);
-  const double m = Mg * G;
+  const double Mg = static_cast<double>(h->mv ? h->M0 : h->M_global);
+  const double m = static_cast<double>(h->m_ref);
   std::vector<double> x((size_t)G, 1.0 / std::sqrt(m)), y((size_t)G);
   double nrm = 0.0;
   for (int64_t it = 0; it < iters; ++it) {
@@ -1190,6 +1259,23 @@ __global__ void k_init_scalars(const double* partials, int count, SolveState* st
 }
 
 __global__ void k_set_t0(SolveState* st) { st->t0 = globaltimer(); }
+
+// MVRGLM embed: X[pos[i]] = 1 (the selector rows C_b(q, restr_b[q]) = 1, structured.cpp:83-84)
+__global__ void k_set_ones(double* X, const int64_t* pos, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    X[pos[i]] = 1.0;
+}
+// dst = D^-1/2 src per block of `per` columns: rows < msig times wz_b, the rest times wc_b (the stacked
+// [Z0 w_z; C_i w_c] of MvRglmPreconditioner, structured.cpp:380-384)
+__global__ void k_scale_rows(double* dst, const double* src, int64_t ld, int64_t ncols, int64_t per, int64_t msig,
+                             const double* wz, const double* wc) {
+  const int64_t total = ld * ncols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = i / ld, k = i - col * ld;
+    const int b = (int)(col / per);
+    dst[i] = src[i] * (k < msig ? wz[b] : wc[b]);
+  }
+}
 
 void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int iter_idx) {
   Geo g = geo_of(h);
@@ -1496,7 +1582,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   glsgpu_pcg_config cfg;
   if (cfg_in) cfg = *cfg_in;
   else glsgpu_default_config(&cfg);
-  const int64_t m = h->M_global * h->G;
+  const int64_t m = h->m_ref;  // rows of the reference's GLM (M G for SUR; G M0 + k for MVRGLM)
   const int64_t max_iter = cfg.max_iter ? cfg.max_iter : (m - h->n + 1);
   const int64_t cap_d = std::max<int64_t>(1, std::min<int64_t>(max_iter + 1, rows ? std::max<int64_t>(rows_cap, 1) : 1));
   ensure_solver(h, cap_d);
@@ -1884,6 +1970,141 @@ int glsgpu_sur_shard(const glsgpu_sur* h, int* rank, int* nranks, int64_t* M_glo
   if (rank) *rank = h->rank;
   if (nranks) *nranks = h->nranks;
   if (M_global) *M_global = h->M_global;
+  return GLSGPU_OK;
+}
+
+// ------------------------------------------------------------------------------------------ MVRGLM
+// make_mvrglm + mvrglm_preconditioner (structured.cpp:63-74,365-414,468-477) on the device.  The embedded
+// model (embed_mvrglm, structured.cpp:77-95) is laid out as G padded blocks of M = M0 + max k_b rows:
+// block b = [Z0; C_b; 0] with C_b(q, restr_b[q]) = 1, its Y rows [Y_b; 0], and the Kronecker apply
+// confined to the M0 observation rows (msig).  Host m-vectors keep the reference's order.
+int glsgpu_mvrglm_create(int G, int64_t M0, int64_t N0, const double* Z0, const double* Y, const double* omega,
+                         const int64_t* roff, const int64_t* ridx, const double* z_scale, const double* c_scale,
+                         int device, glsgpu_sur** out, int* bad_block) {
+  API_BEGIN
+  if (!out || !Z0 || !Y || !omega || !roff) fail(GLSGPU_ERR_INVALID, "glsgpu_mvrglm_create: null argument");
+  *out = nullptr;
+  if (G < 1) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_mvrglm: Omega0 must be G x G");
+  if (N0 < 1 || M0 < N0) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_mvrglm: Z0 must be tall");
+  if (roff[0] != 0) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "restrictions: need one list per equation");
+  MvDesc d;
+  d.M0 = M0;
+  d.kb.resize(G);
+  d.kofs.resize(G);
+  int64_t kmax = 0;
+  for (int i = 0; i < G; ++i) {  // check_restrictions (structured.cpp:13-24)
+    if (roff[i + 1] < roff[i]) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "restrictions: need one list per equation");
+    for (int64_t q = roff[i]; q < roff[i + 1]; ++q) {
+      if (!ridx || ridx[q] < 0 || ridx[q] >= N0) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "restrictions: index out of range");
+      if (q > roff[i] && ridx[q] <= ridx[q - 1])
+        fail(GLSGPU_ERR_DIMENSION_MISMATCH, "restrictions: indices must be strictly increasing");
+    }
+    d.kb[i] = roff[i + 1] - roff[i];
+    d.kofs[i] = roff[i];
+    kmax = std::max(kmax, d.kb[i]);
+  }
+  d.ktot = roff[G];
+  for (int i = 0; i < G; ++i)  // structured.cpp:372-374
+    if ((z_scale && !(z_scale[i] > 0.0)) || (c_scale && !(c_scale[i] > 0.0)))
+      fail(GLSGPU_ERR_SINGULAR_D, "mvrglm_preconditioner: scales must be positive", i);
+  d.c_scale = c_scale;
+  const int64_t Mp = M0 + kmax;
+  std::vector<int64_t> n_i((size_t)G, N0);
+  glsgpu_sur* h = create_common(G, Mp, n_i.data(), omega, z_scale, device, -1, 0, 1, nullptr, &d);
+  try {
+    const int64_t ld = h->ldm, n = h->n;
+    h->X_own = dalloc<double>((size_t)(ld * n));
+    h->Y_own = dalloc<double>((size_t)(ld * G));
+    CK(cudaMemsetAsync(h->X_own, 0, sizeof(double) * ld * n, h->s));
+    CK(cudaMemsetAsync(h->Y_own, 0, sizeof(double) * ld * G, h->s));
+    // Z0 once, then device copies into every block's observation rows
+    CK(cudaMemcpy2DAsync(h->X_own, ld * sizeof(double), Z0, M0 * sizeof(double), M0 * sizeof(double), N0,
+                         cudaMemcpyHostToDevice, h->s));
+    for (int b = 1; b < G; ++b)
+      CK(cudaMemcpy2DAsync(h->X_own + (int64_t)b * N0 * ld, ld * sizeof(double), h->X_own, ld * sizeof(double),
+                           M0 * sizeof(double), N0, cudaMemcpyDeviceToDevice, h->s));
+    if (d.ktot > 0) {
+      std::vector<int64_t> pos((size_t)d.ktot);
+      for (int b = 0; b < G; ++b)
+        for (int64_t q = 0; q < d.kb[b]; ++q)
+          pos[(size_t)(roff[b] + q)] = ((int64_t)b * N0 + ridx[roff[b] + q]) * ld + M0 + q;
+      int64_t* dpos = dalloc<int64_t>(pos.size());
+      CK(cudaMemcpyAsync(dpos, pos.data(), sizeof(int64_t) * pos.size(), cudaMemcpyHostToDevice, h->s));
+      k_set_ones<<<(unsigned)std::min<int64_t>((d.ktot + NT - 1) / NT, GRID_CAP), NT, 0, h->s>>>(h->X_own, dpos, d.ktot);
+      h->launches++;
+      CKL("k_set_ones");
+      CK(cudaStreamSynchronize(h->s));
+      CK(cudaFree(dpos));
+    }
+    CK(cudaMemcpy2DAsync(h->Y_own, ld * sizeof(double), Y, M0 * sizeof(double), M0 * sizeof(double), G,
+                         cudaMemcpyHostToDevice, h->s));
+    h->X = h->X_own;
+    h->ldx = ld;
+    h->Y = h->Y_own;
+    h->ldy = ld;
+    bool two = false;
+    for (int b = 0; b < G; ++b) two = two || h->wts[b] != h->wtc[b];
+    if (two) {
+      h->Xqr = dalloc<double>((size_t)(ld * n));
+      k_scale_rows<<<GRID_CAP, NT, 0, h->s>>>(h->Xqr, h->X_own, ld, n, N0, h->msig, h->d_wts, h->d_wtc);
+      h->launches++;
+      CKL("k_scale_rows");
+    }
+    alloc_common(h);
+    run_qr(h);
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  *out = h;
+  API_END(bad_block)
+}
+
+// mv_reduce (structured.cpp:121-130): thin QR Z0 = Q0 R0 on the device (the TSQR tree), then Q0' Y.
+int glsgpu_mv_reduce(int G, int64_t M0, int64_t N0, const double* Z0, const double* Y, double* R0, double* QtY,
+                     int device) {
+  API_BEGIN
+  if (!Z0 || !Y || !R0 || !QtY) fail(GLSGPU_ERR_INVALID, "glsgpu_mv_reduce: null argument");
+  if (G < 1 || N0 < 1 || M0 < N0) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "qr: need rows >= cols >= 1");
+  const int64_t nb = N0;
+  const double one = 1.0;
+  glsgpu_sur* h = create_common(1, M0, &nb, &one, nullptr, device, -1, 0, 1, nullptr, nullptr, /*qr_only=*/true);
+  h->rank_msg = 1;
+  try {
+    const int64_t ld = h->ldm;
+    h->X_own = dalloc<double>((size_t)(ld * N0));
+    h->Y_own = dalloc<double>((size_t)ld);
+    CK(cudaMemsetAsync(h->X_own, 0, sizeof(double) * ld * N0, h->s));
+    CK(cudaMemsetAsync(h->Y_own, 0, sizeof(double) * ld, h->s));
+    CK(cudaMemcpy2DAsync(h->X_own, ld * sizeof(double), Z0, M0 * sizeof(double), M0 * sizeof(double), N0,
+                         cudaMemcpyHostToDevice, h->s));
+    h->X = h->X_own;
+    h->ldx = ld;
+    h->Y = h->Y_own;
+    h->ldy = ld;
+    alloc_common(h);
+    run_qr(h);
+    ensure_solver(h, 1);
+    for (int j = 0; j < G; ++j) {  // Q0' Y, one column per Q'-pass
+      h2d_mvec(h, h->r, Y + (int64_t)j * M0);
+      qt_apply(h, MODE_QT_R, nullptr, h->t, nullptr, 0);
+      CK(cudaMemcpyAsync(QtY + (int64_t)j * N0, h->t, sizeof(double) * N0, cudaMemcpyDeviceToHost, h->s));
+    }
+    CK(cudaMemcpyAsync(R0, h->R, sizeof(double) * N0 * N0, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  destroy_impl(h);
+  API_END((int*)nullptr)
+}
+
+// Rows m (the reference's embedded GLM: M G for SUR, G M0 + k for MVRGLM) and parameters n of a handle.
+int glsgpu_model_dims(const glsgpu_sur* h, int64_t* m, int64_t* n) {
+  if (!h) return GLSGPU_ERR_INVALID;
+  if (m) *m = h->m_ref;
+  if (n) *n = h->n;
   return GLSGPU_OK;
 }
 

@@ -32,8 +32,14 @@ struct Geo {
   const int* nb;    // [G] widths
   const int64_t* p0;  // [G] first parameter of block b
   const int64_t* r0;  // [G] offset of R_b
-  const double* wts;  // [G] w_b = 1/sqrt(block_scale_b)
+  const double* wts;  // [G] w_b = 1/sqrt(block_scale_b): rows k < msig of block b
+  const double* wtc;  // [G] weight of rows k >= msig (MVRGLM constraint rows, 1/sqrt(c_scale_b)); = wts for SUR
+  int64_t msig;       // rows of every block under Sigma (SUR: ldm; MVRGLM: M0 -- the constraint rows below it
+                      // have zero variance, Sigma = diag(Omega0 (x) I_M0, 0), operators.cpp:51-57)
 };
+
+// per-row weight of block b (Block::inv_sqrt_d, structured.cpp:287-292)
+__device__ __forceinline__ double row_wgt(const Geo& g, double wz, double wc, int64_t k) { return k < g.msig ? wz : wc; }
 
 // Solver state kept on the device; the scalar control of run_aug (proj/src/pcg.cpp:134-211)
 // executes in k_scalar_a / k_scalar_c so no host round trip happens inside an iteration.
@@ -132,7 +138,7 @@ template <int CPL, int RW>
 __global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles, const double* __restrict__ omegaT,
                                              const double* src, const double* pr, const double* div, double* u_io,
                                              double* out, double* partials, int in_mode, const SolveState* st,
-                                             WBuf wbuf) {
+                                             WBuf wbuf, int64_t msig) {
   if (st && !st->active) return;
   extern __shared__ double xs[];  // [G][TR]
   constexpr int TR = 8 * RW;
@@ -236,11 +242,13 @@ __global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles,
       if (c < G) {
 #pragma unroll
         for (int i = 0; i < RW; ++i) {
-          out[(int64_t)c * ldm + k0 + rbase + i] = acc[i][q];
+          // rows >= msig carry zero variance (MVRGLM constraint rows): Sigma x is 0 there
+          const double o = (k0 + rbase + i < msig) ? acc[i][q] : 0.0;
+          out[(int64_t)c * ldm + k0 + rbase + i] = o;
           const double x = xs[c * TR + rbase + i];
-          p_xo += x * acc[i][q];
+          p_xo += x * o;
           p_xx += x * x;
-          p_oo += acc[i][q] * acc[i][q];
+          p_oo += o * o;
         }
       }
     }
@@ -371,7 +379,7 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
   const int ch = item % g.nch;
   const int nb = g.nb[b];
   const int64_t p0 = g.p0[b];
-  const double wgt = g.wts[b];
+  const double wz = g.wts[b], wc = g.wtc[b];
   const int64_t k0 = (int64_t)ch * g.CH;
   const int64_t k1 = (k0 + g.CH < g.ldm) ? k0 + g.CH : g.ldm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -401,6 +409,7 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
   // Row phase: compute x_k (and the side effects of the mode).
   for (int64_t k = k0 + threadIdx.x; k < k1; k += NT) {
     const int64_t off = vo + k;
+    const double wgt = row_wgt(g, wz, wc, k);
     double x;
     double qv[NB];
     if (FUSED) {
@@ -589,7 +598,8 @@ template <bool FMA>
 __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CUtensorMap vmap, int G, int64_t ldm,
                                                      int64_t ntiles, const double* __restrict__ omegaT,
                                                      double* __restrict__ u_io, double* __restrict__ out,
-                                                     double* partials, const SolveState* st, WBuf wbuf) {
+                                                     double* partials, const SolveState* st, WBuf wbuf,
+                                                     int64_t msig) {
   if (!st->active) return;
   extern __shared__ __align__(128) double ksm[];
   __shared__ __align__(8) uint64_t om_full[KW_OS], om_empty[KW_OS], el_full[KW_ES], el_empty[KW_ES], xs_full[2],
@@ -769,10 +779,12 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
           const double* xc = xs + c * KW_XS + 8 * rg;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            stg_cs2(dst + 2 * h, acc[2 * h][q], acc[2 * h + 1][q]);
+            const int64_t row = k0 + 8 * rg + 2 * h;  // rows >= msig: zero variance (MVRGLM constraint rows)
+            const double o0 = row < msig ? acc[2 * h][q] : 0.0, o1 = row + 1 < msig ? acc[2 * h + 1][q] : 0.0;
+            stg_cs2(dst + 2 * h, o0, o1);
             const double2 x2 = *reinterpret_cast<const double2*>(xc + 2 * h);
-            p_a += x2.x * acc[2 * h][q];
-            p_a += x2.y * acc[2 * h + 1][q];
+            p_a += x2.x * o0;
+            p_a += x2.y * o1;
           }
         }
       }
@@ -967,8 +979,8 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     const int ch = (int)(item % g.nch);
     const int nb = g.nb[b];
     const int64_t p0 = g.p0[b];
-    const double wgt = g.wts[b];
-    const double iwgt = 1.0 / wgt;  // Q-side X v = Q (R v) / w (exact when w = 1)
+    const double wz = g.wts[b], wc = g.wtc[b];
+    const double iwz = 1.0 / wz, iwc = 1.0 / wc;  // Q-side X v = Q (R v) / w (exact when w = 1)
     const int64_t vbase = (int64_t)b * g.ldm;
     // tv holds >= 32 entries (zero past n_b): the fused row dots read all 32
     for (int j = tid; j < (nb > 32 ? nb : 32); j += NT)
@@ -1002,6 +1014,8 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
         for (int t = tid; t < rows; t += NT) {
           const int64_t k = kb + t;
           const int64_t vo = vbase + k;
+          const bool zrow = k < g.msig;
+          const double wgt = zrow ? wz : wc, iwgt = zrow ? iwz : iwc;
           double arow[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) arow[j] = M0[(int64_t)j * T + t];
@@ -1080,6 +1094,8 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
       for (int t = tid; t < rows; t += NT) {
         const int64_t k = kb + t;
         const int64_t vo = vbase + k;
+        const bool zrow = k < g.msig;
+        const double wgt = zrow ? wz : wc, iwgt = zrow ? iwz : iwc;
         if (MODE == SMODE_B) {
           // (w / sw updates are deferred to the next pass A)
           const double suv = V[t], rv = V[T + t];
@@ -1277,7 +1293,7 @@ __global__ void __launch_bounds__(NT) k_rowpass(Geo g, const double* Q, const do
     const int ch = (int)(item % g.nch);
     const int nb = g.nb[b];
     const int64_t p0 = g.p0[b];
-    const double wgt = g.wts[b];
+    const double wz = g.wts[b], wc = g.wtc[b];
     __syncthreads();
     for (int j = threadIdx.x; j < nb; j += NT) ts[j] = t[p0 + j];
     __syncthreads();
@@ -1299,6 +1315,7 @@ __global__ void __launch_bounds__(NT) k_rowpass(Geo g, const double* Q, const do
         proj = proj + q3 * ts[j + 3];
       }
       for (; j < nb; ++j) proj = proj + Qb[(int64_t)j * g.ldm + k] * ts[j];
+      const double wgt = row_wgt(g, wz, wc, k);
       if (xstar_mode) {
         out[vo + k] = proj * wgt;
       } else {

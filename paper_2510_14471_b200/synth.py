@@ -19,7 +19,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["SurProblem", "CONFIGS", "make_problem", "omega_half", "config_meta"]
+__all__ = ["SurProblem", "MvProblem", "CONFIGS", "make_problem", "make_mv_problem", "omega_half", "config_meta"]
 
 
 @dataclasses.dataclass
@@ -43,6 +43,62 @@ class SurProblem:
     @property
     def m(self) -> int:
         return self.M * self.G
+
+
+@dataclasses.dataclass
+class MvProblem:
+    """Multivariate model Y = Z0 B + U with exclusion restrictions (gls::MvRglm,
+    proj/include/gls/structured.hpp:37-52): restrictions[i] lists the zero-forced rows of B[:, i]."""
+    name: str
+    G: int
+    M0: int
+    N0: int
+    Z0: np.ndarray            # (M0, N0) float64, Fortran order
+    Y: np.ndarray             # (M0, G) float64, Fortran order
+    omega: np.ndarray         # (G, G) float64, symmetric
+    restrictions: list        # G int64 arrays, strictly increasing, < N0
+    beta: np.ndarray          # (G * N0,) true coefficients, zeros at the restricted entries
+    tol_rel: float
+    max_iter: int = 0
+    z_scale: Optional[np.ndarray] = None  # per-equation auxiliary variances (observation rows)
+    c_scale: Optional[np.ndarray] = None  # per-equation auxiliary variances (constraint rows)
+
+    @property
+    def k(self) -> int:
+        return int(sum(len(r) for r in self.restrictions))
+
+    @property
+    def m(self) -> int:             # rows of embed_mvrglm: G M0 observation rows + k constraint rows
+        return self.G * self.M0 + self.k
+
+    @property
+    def n(self) -> int:
+        return self.G * self.N0
+
+    def csr(self):
+        """restrictions as CSR (roff[G + 1], ridx), the C-ABI / oracle form."""
+        roff = np.zeros(self.G + 1, dtype=np.int64)
+        roff[1:] = np.cumsum([len(r) for r in self.restrictions])
+        ridx = (np.concatenate([np.asarray(r, dtype=np.int64) for r in self.restrictions])
+                if roff[-1] else np.zeros(1, dtype=np.int64))
+        return roff, np.ascontiguousarray(ridx, dtype=np.int64)
+
+    def kept(self):
+        """kept_columns (proj/src/experiments.cpp:453-465): the unrestricted rows of each B column."""
+        return [np.setdiff1d(np.arange(self.N0), r) for r in self.restrictions]
+
+    def to_sur(self) -> "SurProblem":
+        """sur_from_exclusions (proj/src/experiments.cpp:467-480): X_i = Z0[:, kept_i]."""
+        kept = self.kept()
+        nb = np.array([len(k) for k in kept], dtype=np.int64)
+        X = np.asfortranarray(np.concatenate([self.Z0[:, k] for k in kept], axis=1))
+        beta = np.concatenate([self.beta[i * self.N0 + k] for i, k in enumerate(kept)])
+        return SurProblem(self.name + "-sur", self.G, self.M0, nb, X, self.Y, self.omega, beta, self.tol_rel,
+                          self.max_iter)
+
+    def gather_sur(self, b_full: np.ndarray) -> np.ndarray:
+        """gather_sur_params (proj/src/experiments.cpp:482-489): the kept entries of a G N0 estimate."""
+        return np.concatenate([b_full[i * self.N0 + k] for i, k in enumerate(self.kept())])
 
 
 # c -> (G, M, widths rule, Omega rule, tol, max_iter); BASELINE.json:configs[c]
@@ -153,3 +209,46 @@ def random_sur(G: int, M: int, nb, seed: int, cond_omega: Optional[float] = None
         p += nb[i]
     Y = np.asfortranarray(mean + r.standard_normal((M, G)) @ omega_half(omega))
     return SurProblem(f"rand{seed}", G, M, nb, X, Y, omega, beta, 1e-12, 0)
+
+
+def make_mv_problem(c: int = 3, M: Optional[int] = None, G: Optional[int] = None, N: Optional[int] = None,
+                    seed: Optional[int] = None) -> MvProblem:
+    """Config 3 as the multivariate model it is (BASELINE.json:configs[3]): the same draws as
+    make_problem(3, ...), with the Bernoulli(1/2) zero pattern of B as exclusion restrictions."""
+    cfg = CONFIGS[c]
+    assert cfg["widths"].startswith("pattern:")
+    G = int(G if G is not None else cfg["G"])
+    M = int(M if M is not None else cfg["M"])
+    seed = int(seed if seed is not None else 1000 + c)
+    N0 = int(N if N is not None else int(cfg["widths"].split(":")[1]))
+    omega = make_omega(G, cfg["omega"], seed)
+    rp = _rng(seed, 4)
+    zero = rp.random((N0, G)) < 0.5
+    for i in range(G):
+        if zero[:, i].all():
+            zero[rp.integers(N0), i] = False
+    B = _rng(seed, 1).standard_normal((N0, G))
+    B[zero] = 0.0
+    X0 = np.asfortranarray(_rng(seed, 0).standard_normal((M, N0)))
+    Z = _rng(seed, 3).standard_normal((G, M)).T
+    Y = np.asfortranarray(X0 @ B + Z @ omega_half(omega))
+    restr = [np.flatnonzero(zero[:, i]).astype(np.int64) for i in range(G)]
+    return MvProblem(f"c{c}-mv", G, M, N0, X0, Y, omega, restr, np.asarray(B.T.reshape(-1), dtype=np.float64),
+                     cfg["tol"], cfg["max_iter"])
+
+
+def random_mv(G: int, M0: int, N0: int, seed: int, frac: float = 0.5) -> MvProblem:
+    """Small generic multivariate model with random exclusions (edge-case tests)."""
+    r = _rng(seed, 0)
+    Z0 = np.asfortranarray(r.standard_normal((M0, N0)))
+    zero = r.random((N0, G)) < frac
+    for i in range(G):
+        if zero[:, i].all():
+            zero[0, i] = False
+    B = r.standard_normal((N0, G))
+    B[zero] = 0.0
+    L = np.tril(r.standard_normal((G, G)))
+    omega = np.asfortranarray(0.5 * ((L @ L.T + 0.1 * np.eye(G)) + (L @ L.T + 0.1 * np.eye(G)).T))
+    Y = np.asfortranarray(Z0 @ B + r.standard_normal((M0, G)) @ omega_half(omega))
+    restr = [np.flatnonzero(zero[:, i]).astype(np.int64) for i in range(G)]
+    return MvProblem(f"mv{seed}", G, M0, N0, Z0, Y, omega, restr, np.asarray(B.T.reshape(-1)), 1e-12, 0)
