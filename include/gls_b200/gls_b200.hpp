@@ -167,24 +167,55 @@ inline SurModel make_sur(const std::vector<Vector>& blocks, const std::vector<st
   return s;
 }
 
-// The SUR indefinite preconditioner resident on a B200 (SurPreconditioner, structured.cpp:416-453).
-class SurOperator {
- public:
-  SurOperator(const SurModel& sur, const Vector* block_scale, int device = 0) {
-    if (block_scale && block_scale->size() != sur.equations())
-      throw DimensionMismatch("sur_preconditioner: need one scale per block");
-    int bad = -1;
-    check(glsgpu_sur_create((int)sur.equations(), (std::int64_t)sur.M, sur.widths.data(), sur.X.data(),
-                            sur.y.data(), sur.sigma0.data(), block_scale ? block_scale->data() : nullptr, device, &h_,
-                            &bad));
-    m_ = sur.M * sur.equations();
-    n_ = sur.total_params();
+// MvRglm (structured.hpp:33-43): Y = Z0 B + U, restrictions[i] = zero-forced rows of B[:, i].
+struct MvRglm {
+  std::size_t M0 = 0, N0 = 0;
+  Vector z0;      // M0 x N0 column-major
+  Vector y;       // M0 x G
+  Vector omega0;  // G x G
+  std::vector<std::vector<std::int64_t>> restrictions;
+  std::size_t obs() const { return M0; }
+  std::size_t params_per_eq() const { return N0; }
+  std::size_t equations() const { return restrictions.size(); }
+  std::size_t total_restrictions() const {
+    std::size_t k = 0;
+    for (const auto& r : restrictions) k += r.size();
+    return k;
   }
-  ~SurOperator() {
+};
+
+// make_mvrglm (structured.cpp:63-74): same checks, same messages.
+inline MvRglm make_mvrglm(Vector z0, std::size_t M0, std::size_t N0, Vector y, Vector omega0,
+                          std::vector<std::vector<std::int64_t>> restrictions) {
+  const std::size_t g = restrictions.size();
+  if (z0.size() != M0 * N0 || M0 < N0) throw DimensionMismatch("make_mvrglm: Z0 must be tall");
+  if (y.size() != M0 * g) throw DimensionMismatch("make_mvrglm: Y/Z0 row mismatch");
+  if (omega0.size() != g * g) throw DimensionMismatch("make_mvrglm: Omega0 must be G x G");
+  for (const auto& list : restrictions)
+    for (std::size_t q = 0; q < list.size(); ++q) {
+      if (list[q] < 0 || (std::size_t)list[q] >= N0) throw DimensionMismatch("restrictions: index out of range");
+      if (q > 0 && list[q] <= list[q - 1]) throw DimensionMismatch("restrictions: indices must be strictly increasing");
+    }
+  MvRglm mv;
+  mv.M0 = M0;
+  mv.N0 = N0;
+  mv.z0 = std::move(z0);
+  mv.y = std::move(y);
+  mv.omega0 = std::move(omega0);
+  mv.restrictions = std::move(restrictions);
+  return mv;
+}
+
+// A block-QR indefinite preconditioner resident on a B200 (BlockQrPreconditioner, structured.cpp:282-363)
+// together with its GLM's X and Sigma: the SUR operator (sur_preconditioner) or the MVRGLM one
+// (mvrglm_preconditioner).  Host m-vectors use the reference's embedded row order.
+class BlockQrOperator {
+ public:
+  ~BlockQrOperator() {
     if (h_) glsgpu_sur_destroy(h_);
   }
-  SurOperator(const SurOperator&) = delete;
-  SurOperator& operator=(const SurOperator&) = delete;
+  BlockQrOperator(const BlockQrOperator&) = delete;
+  BlockQrOperator& operator=(const BlockQrOperator&) = delete;
 
   std::size_t rows() const { return m_; }
   std::size_t params() const { return n_; }
@@ -216,9 +247,55 @@ class SurOperator {
   void reset_apply_counters() const { check(glsgpu_reset_apply_counters(h_)); }
   glsgpu_sur* handle() const { return h_; }
 
- private:
+ protected:
+  BlockQrOperator() = default;
+  void adopt(glsgpu_sur* h) {
+    h_ = h;
+    std::int64_t m = 0, n = 0;
+    check(glsgpu_model_dims(h_, &m, &n));
+    m_ = (std::size_t)m;
+    n_ = (std::size_t)n;
+  }
   glsgpu_sur* h_ = nullptr;
   std::size_t m_ = 0, n_ = 0;
+};
+
+// The SUR indefinite preconditioner (SurPreconditioner, structured.cpp:416-453).
+class SurOperator : public BlockQrOperator {
+ public:
+  SurOperator(const SurModel& sur, const Vector* block_scale, int device = 0) {
+    if (block_scale && block_scale->size() != sur.equations())
+      throw DimensionMismatch("sur_preconditioner: need one scale per block");
+    int bad = -1;
+    glsgpu_sur* h = nullptr;
+    check(glsgpu_sur_create((int)sur.equations(), (std::int64_t)sur.M, sur.widths.data(), sur.X.data(),
+                            sur.y.data(), sur.sigma0.data(), block_scale ? block_scale->data() : nullptr, device, &h,
+                            &bad));
+    adopt(h);
+  }
+};
+
+// The MVRGLM indefinite preconditioner (MvRglmPreconditioner, structured.cpp:365-414) with the operator
+// of embed_mvrglm (structured.cpp:77-95).
+class MvRglmOperator : public BlockQrOperator {
+ public:
+  MvRglmOperator(const MvRglm& mv, const Vector* z_scale, const Vector* c_scale, int device = 0) {
+    const std::size_t g = mv.equations();
+    if ((z_scale && z_scale->size() != g) || (c_scale && c_scale->size() != g))
+      throw DimensionMismatch("mvrglm_preconditioner: need one scale per equation");
+    std::vector<std::int64_t> roff(g + 1, 0), ridx;
+    for (std::size_t i = 0; i < g; ++i) {
+      ridx.insert(ridx.end(), mv.restrictions[i].begin(), mv.restrictions[i].end());
+      roff[i + 1] = (std::int64_t)ridx.size();
+    }
+    if (ridx.empty()) ridx.push_back(0);
+    int bad = -1;
+    glsgpu_sur* h = nullptr;
+    check(glsgpu_mvrglm_create((int)g, (std::int64_t)mv.M0, (std::int64_t)mv.N0, mv.z0.data(), mv.y.data(),
+                               mv.omega0.data(), roff.data(), ridx.data(), z_scale ? z_scale->data() : nullptr,
+                               c_scale ? c_scale->data() : nullptr, device, &h, &bad));
+    adopt(h);
+  }
 };
 
 inline std::unique_ptr<SurOperator> sur_preconditioner(const SurModel& sur, const Vector& block_scale,
@@ -228,19 +305,38 @@ inline std::unique_ptr<SurOperator> sur_preconditioner(const SurModel& sur, cons
 inline std::unique_ptr<SurOperator> sur_preconditioner(const SurModel& sur, int device = 0) {
   return std::make_unique<SurOperator>(sur, nullptr, device);
 }
+inline std::unique_ptr<MvRglmOperator> mvrglm_preconditioner(const MvRglm& mv, const Vector& z_scale,
+                                                             const Vector& c_scale, int device = 0) {
+  return std::make_unique<MvRglmOperator>(mv, &z_scale, &c_scale, device);
+}
+inline std::unique_ptr<MvRglmOperator> mvrglm_preconditioner(const MvRglm& mv, int device = 0) {
+  return std::make_unique<MvRglmOperator>(mv, nullptr, nullptr, device);
+}
 
-inline double operator_norm_probe(const SurOperator& op, std::size_t iters = 12) {
+// mv_reduce (structured.cpp:121-130) on the device: Z0 -> R0 (N0 x N0), Y -> Q0'Y.  R0 is the reference's up
+// to row signs (TSQR), which the GLS estimate does not see.
+inline MvRglm mv_reduce(const MvRglm& mv, int device = 0) {
+  MvRglm red;
+  red.M0 = red.N0 = mv.N0;
+  red.z0.resize(mv.N0 * mv.N0);
+  red.y.resize(mv.N0 * mv.equations());
+  red.omega0 = mv.omega0;
+  red.restrictions = mv.restrictions;
+  check(glsgpu_mv_reduce((int)mv.equations(), (std::int64_t)mv.M0, (std::int64_t)mv.N0, mv.z0.data(), mv.y.data(),
+                         red.z0.data(), red.y.data(), device));
+  return red;
+}
+
+inline double operator_norm_probe(const BlockQrOperator& op, std::size_t iters = 12) {
   double nrm = 0.0;
   check(glsgpu_operator_norm_probe(op.handle(), (std::int64_t)iters, &nrm));
   return nrm;
 }
 
-// pcg_aug (pcg.cpp:346-350 -> run_aug, Recovery variant) on the device.
-inline AugSolveResult pcg_aug(const SurModel& sur, const SurOperator& op, const Vector& w1, const Vector& z1,
-                              const PcgConfig& config, const Vector* true_beta = nullptr) {
+// pcg_aug (pcg.cpp:346-350 -> run_aug, Recovery variant) on the device, on the operator's GLM.
+inline AugSolveResult pcg_aug(const BlockQrOperator& op, const Vector& w1, const Vector& z1, const PcgConfig& config,
+                              const Vector* true_beta = nullptr) {
   const std::size_t m = op.rows(), n = op.params();
-  if (m != sur.M * sur.equations() || n != sur.total_params())
-    throw DimensionMismatch("pcg_aug: preconditioner dims do not match the GLM");
   if (w1.size() != m || z1.size() != n) throw DimensionMismatch("pcg_aug: bad initial iterate size");
   glsgpu_pcg_config c;
   glsgpu_default_config(&c);
@@ -280,6 +376,22 @@ inline AugSolveResult pcg_aug(const SurModel& sur, const SurOperator& op, const 
     out.trace.rows[i] = PcgTraceRow{(std::size_t)rows[i].iter, rows[i].c, rows[i].aug_residual_norm,
                                     rows[i].dual_feas_norm, rows[i].rmse, (long long)rows[i].elapsed_ns};
   return out;
+}
+
+// pcg_aug(embed_sur(sur), op, ...): the SurModel form of the reference's call.
+inline AugSolveResult pcg_aug(const SurModel& sur, const BlockQrOperator& op, const Vector& w1, const Vector& z1,
+                              const PcgConfig& config, const Vector* true_beta = nullptr) {
+  if (op.rows() != sur.M * sur.equations() || op.params() != sur.total_params())
+    throw DimensionMismatch("pcg_aug: preconditioner dims do not match the GLM");
+  return pcg_aug(op, w1, z1, config, true_beta);
+}
+
+// pcg_aug(embed_mvrglm(mv), op, ...)
+inline AugSolveResult pcg_aug(const MvRglm& mv, const BlockQrOperator& op, const Vector& w1, const Vector& z1,
+                              const PcgConfig& config, const Vector* true_beta = nullptr) {
+  if (op.rows() != mv.M0 * mv.equations() + mv.total_restrictions() || op.params() != mv.N0 * mv.equations())
+    throw DimensionMismatch("pcg_aug: preconditioner dims do not match the GLM");
+  return pcg_aug(op, w1, z1, config, true_beta);
 }
 
 }  // namespace gls_b200

@@ -75,9 +75,71 @@ int main(int argc, char** argv) {
     const double rel = std::sqrt(num / den);
     const bool ok = (std::int64_t)g.solution.iterations == orr.iterations &&
                     (int)g.solution.termination == orr.termination && rel <= 1e-10;
-    std::printf("{\"device\": true, \"iterations\": %zu, \"oracle_iterations\": %lld, \"rel_b\": %.3e, \"ok\": %s}\n",
-                g.solution.iterations, (long long)orr.iterations, rel, ok ? "true" : "false");
-    return ok ? 0 : 1;
+
+    // MVRGLM route (mv_reduce, then mvrglm_preconditioner with the K2 auxiliary) vs the SUR route of the same
+    // model (X_i = the kept columns of Z0): the same GLS estimator
+    const std::size_t G2 = 4, M0 = 600, N0 = 10;
+    gls_b200::Vector z0(M0 * N0), y2(M0 * G2), om2(G2 * G2, 0.0);
+    for (auto& v : z0) v = nd(gen);
+    std::vector<std::vector<std::int64_t>> restr(G2);
+    for (std::size_t i = 0; i < G2; ++i)
+      for (std::size_t j = 0; j < N0; ++j)
+        if ((i + 2 * j) % 3 == 0) restr[i].push_back((std::int64_t)j);
+    for (auto& v : y2) v = nd(gen);
+    for (std::size_t i = 0; i < G2; ++i)
+      for (std::size_t j = 0; j < G2; ++j) om2[i + j * G2] = (i == j ? 1.5 : 0.0) + 0.2 / (1.0 + std::abs((int)i - (int)j));
+    gls_b200::MvRglm mv = gls_b200::make_mvrglm(z0, M0, N0, y2, om2, restr);
+    gls_b200::MvRglm red = gls_b200::mv_reduce(mv);
+    double zf = 0.0;
+    for (double v : red.z0) zf += v * v;
+    gls_b200::Vector zs(G2), cs(G2);
+    for (std::size_t i = 0; i < G2; ++i) {
+      zs[i] = om2[i + i * G2];
+      cs[i] = zs[i] / (zf / (double)N0);  // experiments.cpp:835-847 (K2)
+    }
+    auto mop = gls_b200::mvrglm_preconditioner(red, zs, cs);
+    gls_b200::PcgConfig mcfg;
+    mcfg.tol_rel = 1e-12;
+    mcfg.max_iter = 3 * (red.total_restrictions() + 1) + 10;
+    gls_b200::AugSolveResult gm = gls_b200::pcg_aug(red, *mop, gls_b200::Vector(mop->rows(), 0.0),
+                                                    gls_b200::Vector(mop->params(), 0.0), mcfg);
+    std::vector<gls_b200::Vector> kblocks;
+    std::vector<std::int64_t> kw;
+    for (std::size_t i = 0; i < G2; ++i) {
+      gls_b200::Vector blk;
+      std::size_t q = 0;
+      for (std::size_t j = 0; j < N0; ++j) {
+        if (q < restr[i].size() && (std::size_t)restr[i][q] == j) { ++q; continue; }
+        blk.insert(blk.end(), z0.begin() + j * M0, z0.begin() + (j + 1) * M0);
+      }
+      kw.push_back((std::int64_t)(blk.size() / M0));
+      kblocks.push_back(blk);
+    }
+    gls_b200::SurModel ks = gls_b200::make_sur(kblocks, kw, M0, y2, om2);
+    auto sop = gls_b200::sur_preconditioner(ks);
+    gls_b200::PcgConfig scfg;
+    scfg.tol_rel = 1e-13;
+    gls_b200::AugSolveResult gs = gls_b200::pcg_aug(ks, *sop, gls_b200::Vector(sop->rows(), 0.0),
+                                                    gls_b200::Vector(sop->params(), 0.0), scfg);
+    double mn = 0.0, md = 0.0;
+    std::size_t p = 0;
+    for (std::size_t i = 0; i < G2; ++i) {
+      std::size_t q = 0;
+      for (std::size_t j = 0; j < N0; ++j) {
+        if (q < restr[i].size() && (std::size_t)restr[i][q] == j) { ++q; continue; }
+        const double d = gm.solution.b[i * N0 + j] - gs.solution.b[p];
+        mn += d * d;
+        md += gs.solution.b[p] * gs.solution.b[p];
+        ++p;
+      }
+    }
+    const double rel_mv = std::sqrt(mn / md);
+    const bool ok_mv = rel_mv <= 1e-5 && mop->counters().factorizations == G2;
+    std::printf("{\"device\": true, \"iterations\": %zu, \"oracle_iterations\": %lld, \"rel_b\": %.3e, "
+                "\"mvrglm_iterations\": %zu, \"mvrglm_vs_sur\": %.3e, \"ok\": %s}\n",
+                g.solution.iterations, (long long)orr.iterations, rel, gm.solution.iterations, rel_mv,
+                ok && ok_mv ? "true" : "false");
+    return ok && ok_mv ? 0 : 1;
   } catch (const gls_b200::DeviceError& e) {
     std::printf("{\"device\": false, \"error\": \"%s\"}\n", e.what());
     return expect_device ? 2 : 0;  // no device: loud failure, never a CPU fallback

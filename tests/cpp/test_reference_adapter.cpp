@@ -6,6 +6,11 @@
 //      B200 operator behind the reference's IndefinitePreconditioner interface)
 //   C. gls::gpu::pcg_aug_sur(sur, cfg, ...)                                                  (whole loop on the B200)
 // agree: same termination and iteration count, b within 1e-10; B's counters equal A's.
+// And the multivariate route of the harness (experiments.cpp:537-557, K2 auxiliary of experiments.cpp:835-847):
+//   D. reference mv_reduce + pcg_aug(embed_mvrglm(red), *mvrglm_preconditioner(red, z, c), ...)
+//   E. the same reference loop on gls::gpu::mvrglm_preconditioner, F. gls::gpu::pcg_aug_mvrglm,
+//   G. gls::gpu::mv_reduce against the reference's (R0 up to row signs).
+// MVRGLM stops are last-bit sensitive, so D/E/F agree to 1e-5 with stops within 10.
 // Prints one JSON line per case; exit code = number of failed checks.
 #include <cmath>
 #include <cstdio>
@@ -72,6 +77,58 @@ int main() {
         "\"ok\": %s}\n",
         cs.g, cs.m0, a.solution.iterations, to_string(a.solution.termination), b.solution.iterations, rb,
         c.solution.iterations, rc, ok_cnt ? "true" : "false", (ok_b && ok_c && ok_cnt) ? "true" : "false");
+  }
+  {
+    const std::size_t g = 6, m0 = 900, n0 = 12;
+    Rng master(21);
+    DenseMatrix z0 = master.split(0).gaussian_matrix(m0, n0);
+    DenseMatrix y = master.split(1).gaussian_matrix(m0, g);
+    DenseMatrix om = gen_spd_with_cond(g, 6.0, master.split(2).seed());
+    std::vector<std::vector<std::size_t>> restr(g);
+    for (std::size_t i = 0; i < g; ++i)
+      for (std::size_t j = 0; j < n0; ++j)
+        if ((i + j) % 3 == 0) restr[i].push_back(j);
+    MvRglm mv = make_mvrglm(z0, y, om, restr);
+    auto [red, rec] = mv_reduce(mv);
+    auto [red_g, rec_g] = gpu::mv_reduce(mv);
+    double dr = 0.0, nr = 0.0;
+    for (std::size_t j = 0; j < n0; ++j) {
+      const double sg = (red.z0(j, j) > 0) == (red_g.z0(j, j) > 0) ? 1.0 : -1.0;
+      for (std::size_t k = 0; k < n0; ++k) {
+        dr += std::pow(red_g.z0(j, k) - sg * red.z0(j, k), 2);
+        nr += red.z0(j, k) * red.z0(j, k);
+      }
+    }
+    const double rel_r = std::sqrt(dr / nr);
+    const double zf = red.z0.frobenius_norm();
+    Vector zs(g), cs(g);
+    for (std::size_t i = 0; i < g; ++i) {
+      zs[i] = om(i, i);
+      cs[i] = zs[i] / (zf * zf / (double)n0);
+    }
+    Glm glm = embed_mvrglm(red);
+    PcgConfig cfg;
+    cfg.tol_rel = 1e-12;
+    cfg.max_iter = 3 * (red.total_restrictions() + 1) + 10;
+    const Vector w1(glm.x.rows(), 0.0), z1(glm.x.cols(), 0.0);
+    auto op_ref = mvrglm_preconditioner(red, zs, cs);
+    AugSolveResult d = pcg_aug(glm, *op_ref, w1, z1, cfg);
+    auto op_gpu = gpu::mvrglm_preconditioner(red, zs, cs);
+    AugSolveResult e = pcg_aug(glm, *op_gpu, w1, z1, cfg);
+    AugSolveResult f = gpu::pcg_aug_mvrglm(red, cfg, w1, z1, nullptr, &zs, &cs);
+    const double re = rel(e.solution.b, d.solution.b), rf = rel(f.solution.b, d.solution.b);
+    auto near = [&](const AugSolveResult& x) {
+      const long di = (long)x.solution.iterations - (long)d.solution.iterations;
+      return di <= 10 && di >= -10;
+    };
+    const bool ok = rel_r <= 1e-12 && re <= 1e-5 && rf <= 1e-5 && near(e) && near(f) &&
+                    op_gpu->counters().factorizations == g;
+    fails += !ok;
+    std::printf("{\"mvrglm\": true, \"ref_iters\": %zu, \"ref_term\": \"%s\", \"gpu_op_iters\": %zu, "
+                "\"gpu_op_rel_b\": %.3e, \"gpu_solve_iters\": %zu, \"gpu_solve_rel_b\": %.3e, "
+                "\"mv_reduce_rel_R\": %.3e, \"ok\": %s}\n",
+                d.solution.iterations, to_string(d.solution.termination), e.solution.iterations, re,
+                f.solution.iterations, rf, rel_r, ok ? "true" : "false");
   }
   // error mapping: a rank-deficient block raises gls::RankDeficient through the adapter
   {

@@ -60,9 +60,13 @@ def test_header_api_matches_oracle():
 @pytest.mark.gpu
 def test_reference_pcg_aug_runs_on_the_gpu_operator():
     """The reference's own pcg_aug(embed_sur(sur), *op) with op = the B200 preconditioner, and the whole
-    loop on the B200, both match the reference's CPU run (same iterations, b within 1e-10, counters)."""
+    loop on the B200, both match the reference's CPU run (same iterations, b within 1e-10, counters); the
+    same for the MVRGLM route (mvrglm_preconditioner / pcg_aug_mvrglm / mv_reduce) within its envelope."""
     rc, lines, err = _run(_ensure("test_reference_adapter"))
     assert rc == 0, (lines, err)
-    cases = [x for x in lines if "ok" in x]
+    cases = [x for x in lines if "ok" in x and "mvrglm" not in x]
     assert len(cases) == 3 and all(c["ok"] for c in cases)
+    # the harness's multivariate route: reference mv_reduce + MVRGLM vs the B200 operator / loop / mv_reduce
+    mv = [x for x in lines if x.get("mvrglm")]
+    assert len(mv) == 1 and mv[0]["ok"], mv
     assert any(x.get("rank_deficient_maps_to_gls_RankDeficient") for x in lines)
