@@ -21,6 +21,7 @@
  *                                        proj/include/gls/structured.hpp:33-50,96-100;
  *                                        proj/src/structured.cpp:63-95,365-414,468-477
  *   glsgpu_mv_reduce                     mv_reduce  proj/include/gls/structured.hpp:76; structured.cpp:121-130
+ *   glsgpu_sur_reduce                    sur_reduce proj/include/gls/structured.hpp:80-81; structured.cpp:132-178
  *
  * Errors: every call returns a status code; the codes map 1:1 onto the reference's gls::Error
  * subclasses (proj/include/gls/errors.hpp:10-88) and glsgpu_last_error_message() holds the text.
@@ -204,6 +205,13 @@ int glsgpu_mvrglm_create(int G, int64_t M0, int64_t N0, const double* Z0 /* M0 x
  * model is the same up to that orthogonal diagonal, which the GLS estimate does not see. */
 int glsgpu_mv_reduce(int G, int64_t M0, int64_t N0, const double* Z0, const double* Y, double* R0, double* QtY,
                      int device);
+/* sur_reduce (Remark-1 pre-pass): rotate every equation onto an orthonormal basis of range([X_1 ... X_G]).
+ * Host X (M x n) and Y (M x G) in, q (the numerical rank, rank_tol as the reference's default 1e-10) and the
+ * reduced X (q x n) and Y (q x G) out; X_red / Y_red must hold min(M, n) rows.  q == M: not reduced (copies).
+ * basis (M x q) is optional.  Uses cuBLAS / cuSOLVER (dlopened) for the Gram, the eigensolver and the QR; the
+ * basis equals the reference's up to an orthogonal q x q factor. */
+int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, const double* Y, double rank_tol,
+                      int device, int64_t* q_out, double* X_red, double* Y_red, double* basis);
 /* m (rows of the reference's embedded GLM) and n of a handle. */
 int glsgpu_model_dims(const glsgpu_sur* h, int64_t* m, int64_t* n);
 

@@ -135,6 +135,8 @@ def _load(path: str, kind: str):
                                            C.POINTER(Result), C.POINTER(C.c_uint64)]
         lib.ref_mvrglm_apply.restype = C.c_int
         lib.ref_mvrglm_apply.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _PI, _PI, _P, _P, C.c_int, _P, _P]
+        lib.ref_sur_reduce.restype = C.c_int
+        lib.ref_sur_reduce.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, C.c_double, C.POINTER(C.c_int64), _P, _P, _P]
         lib.ref_mv_reduce.restype = C.c_int
         lib.ref_mv_reduce.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _P]
     return lib
@@ -350,3 +352,24 @@ def mv_reduce(prob, kind: str = "oracle"):
     if st:
         raise OracleError(st)
     return R, QtY
+
+
+def sur_reduce_ref(prob, rank_tol: float = 1e-10, want_basis: bool = False):
+    """The reference's own sur_reduce (structured.cpp:132-178) through oracle/_ref: (q, X_red (q x n),
+    Y_red (q x G), basis (M x q) or None).  q == M means "not reduced" (X_red / Y_red are the inputs)."""
+    L = lib("ref")
+    nb = np.ascontiguousarray(prob.nb, dtype=np.int64)
+    n = int(nb.sum())
+    Xr = np.zeros(prob.M * n)
+    Yr = np.zeros(prob.M * prob.G)
+    B = np.zeros(prob.M * min(prob.M, n)) if want_basis else None
+    q = C.c_int64(0)
+    st = L.ref_sur_reduce(prob.G, prob.M, nb.ctypes.data_as(_PI), _dp(np.asfortranarray(prob.X)),
+                          _dp(np.asfortranarray(prob.Y)), rank_tol, C.byref(q), _dp(Xr), _dp(Yr), _dp(B))
+    if st:
+        raise OracleError(st, L.ref_last_error().decode())
+    q = int(q.value)
+    if q >= prob.M:
+        return q, np.asfortranarray(prob.X), np.asfortranarray(prob.Y), None
+    return (q, Xr[:q * n].reshape(q, n, order="F"), Yr[:q * prob.G].reshape(q, prob.G, order="F"),
+            B[:prob.M * q].reshape(prob.M, q, order="F") if want_basis else None)

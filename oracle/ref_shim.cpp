@@ -292,4 +292,28 @@ int ref_qr_thin(int64_t m, int64_t n, const double* a, double* q, double* r) {
   }
 }
 
+// sur_reduce (proj/src/structured.cpp:132-178): q, the reduced blocks (q x n, concatenated) and Y (q x G),
+// and the transform (M x q) when `basis` is non-null.  Outputs are written only when q < M.
+int ref_sur_reduce(int G, int64_t M, const int64_t* nb, const double* X, const double* Y, double rank_tol,
+                   int64_t* q_out, double* x_out, double* y_out, double* basis) {
+  try {
+    gls::SurModel sur = build_sur(G, M, nb, X, Y, nullptr);
+    sur.sigma0 = gls::DenseMatrix::identity(G);
+    auto red = gls::sur_reduce(sur, rank_tol);
+    const std::size_t q = red.second.reduced_rows;
+    *q_out = static_cast<int64_t>(q);
+    int64_t p = 0;
+    for (int b = 0; b < G; ++b) {
+      std::memcpy(x_out + p * q, red.first.blocks[b].data(), sizeof(double) * q * nb[b]);
+      p += nb[b];
+    }
+    std::memcpy(y_out, red.first.y.data(), sizeof(double) * q * G);
+    if (basis) std::memcpy(basis, red.second.transform.data(), sizeof(double) * M * q);
+    return 0;
+  } catch (const gls::Error& e) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", e.what());
+    return code_of(e);
+  }
+}
+
 }  // extern "C"

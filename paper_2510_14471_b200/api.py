@@ -527,6 +527,33 @@ def mv_reduce(mv: MvRglm, device: int = 0):
     return red, ReductionRecord(original_rows=M0, reduced_rows=N0, rank=N0)
 
 
+def sur_reduce(sur: SurModel, rank_tol: float = 1e-10, device: int = 0, want_transform: bool = False):
+    """sur_reduce (structured.cpp:132-178, the paper's Remark 1) on the device: every equation rotated onto
+    an orthonormal basis of range([X_1 ... X_G]), q = its numerical rank.  Returns (reduced SurModel,
+    ReductionRecord[, transform M x q]).  The basis equals the reference's up to an orthogonal q x q factor."""
+    lib = L.load()
+    G, M, n = sur.equations(), sur.obs(), sur.total_params()
+    nb = np.ascontiguousarray(sur.nb, dtype=np.int64)
+    cap = min(M, n)
+    Xr = np.zeros(cap * n if cap < M else M * n)
+    Yr = np.zeros(cap * G if cap < M else M * G)
+    B = np.zeros(M * cap) if want_transform else None
+    q = C.c_int64(0)
+    _check(lib.glsgpu_sur_reduce(G, M, nb.ctypes.data_as(_PI64), _dp(np.asfortranarray(sur.X)),
+                                 _dp(np.asfortranarray(sur.y)), rank_tol, device, C.byref(q), _dp(Xr), _dp(Yr),
+                                 _dp(B) if B is not None and cap < M else None), lib)
+    q = int(q.value)
+    rec = ReductionRecord(original_rows=M, reduced_rows=q, rank=q if q < M else M)
+    if q >= M:
+        out = (sur, rec)
+        return out + (np.eye(M),) if want_transform else out
+    red = SurModel(X=np.asfortranarray(Xr[:q * n].reshape(q, n, order="F")), nb=nb.copy(),
+                   y=np.asfortranarray(Yr[:q * G].reshape(q, G, order="F")), sigma0=sur.sigma0)
+    if want_transform:
+        return red, rec, B[:M * q].reshape(M, q, order="F")
+    return red, rec
+
+
 def _frobenius(a: np.ndarray) -> float:
     """DenseMatrix::frobenius_norm (dense_matrix.cpp:93-97): sequential sum of squares in storage order."""
     v = np.asarray(a, dtype=np.float64).reshape(-1, order="F")

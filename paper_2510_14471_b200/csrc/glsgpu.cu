@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <cublas_v2.h>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -94,6 +96,63 @@ void nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return;
   const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
   fail(GLSGPU_ERR_NCCL, std::string(what) + ": " + s);
+}
+
+// cuBLAS / cuSOLVER, resolved at run time like NCCL: only the sur_reduce pre-pass (plain library GEMMs, the
+// symmetric eigensolver and a Householder QR of the basis) uses them; the solver path never does.
+struct Dla {
+  void *blas = nullptr, *sol = nullptr;
+  decltype(&cublasCreate_v2) BlasCreate = nullptr;
+  decltype(&cublasDestroy_v2) BlasDestroy = nullptr;
+  decltype(&cublasSetStream_v2) BlasSetStream = nullptr;
+  decltype(&cublasDgemm_v2) Dgemm = nullptr;
+  decltype(&cublasDsyrk_v2) Dsyrk = nullptr;
+  decltype(&cusolverDnCreate) SolCreate = nullptr;
+  decltype(&cusolverDnDestroy) SolDestroy = nullptr;
+  decltype(&cusolverDnSetStream) SolSetStream = nullptr;
+  decltype(&cusolverDnDsyevd_bufferSize) SyevdBuf = nullptr;
+  decltype(&cusolverDnDsyevd) Syevd = nullptr;
+  decltype(&cusolverDnDgeqrf_bufferSize) GeqrfBuf = nullptr;
+  decltype(&cusolverDnDgeqrf) Geqrf = nullptr;
+  decltype(&cusolverDnDorgqr_bufferSize) OrgqrBuf = nullptr;
+  decltype(&cusolverDnDorgqr) Orgqr = nullptr;
+};
+
+Dla& dla() {
+  static Dla d;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    d.blas = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!d.blas) d.blas = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
+    d.sol = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+    if (!d.sol) d.sol = dlopen("libcusolver.so", RTLD_NOW | RTLD_GLOBAL);
+    if (d.blas) {
+      d.BlasCreate = (decltype(d.BlasCreate))dlsym(d.blas, "cublasCreate_v2");
+      d.BlasDestroy = (decltype(d.BlasDestroy))dlsym(d.blas, "cublasDestroy_v2");
+      d.BlasSetStream = (decltype(d.BlasSetStream))dlsym(d.blas, "cublasSetStream_v2");
+      d.Dgemm = (decltype(d.Dgemm))dlsym(d.blas, "cublasDgemm_v2");
+      d.Dsyrk = (decltype(d.Dsyrk))dlsym(d.blas, "cublasDsyrk_v2");
+    }
+    if (d.sol) {
+      d.SolCreate = (decltype(d.SolCreate))dlsym(d.sol, "cusolverDnCreate");
+      d.SolDestroy = (decltype(d.SolDestroy))dlsym(d.sol, "cusolverDnDestroy");
+      d.SolSetStream = (decltype(d.SolSetStream))dlsym(d.sol, "cusolverDnSetStream");
+      d.SyevdBuf = (decltype(d.SyevdBuf))dlsym(d.sol, "cusolverDnDsyevd_bufferSize");
+      d.Syevd = (decltype(d.Syevd))dlsym(d.sol, "cusolverDnDsyevd");
+      d.GeqrfBuf = (decltype(d.GeqrfBuf))dlsym(d.sol, "cusolverDnDgeqrf_bufferSize");
+      d.Geqrf = (decltype(d.Geqrf))dlsym(d.sol, "cusolverDnDgeqrf");
+      d.OrgqrBuf = (decltype(d.OrgqrBuf))dlsym(d.sol, "cusolverDnDorgqr_bufferSize");
+      d.Orgqr = (decltype(d.Orgqr))dlsym(d.sol, "cusolverDnDorgqr");
+    }
+  }
+  if (!d.BlasCreate || !d.Dgemm || !d.Dsyrk || !d.SolCreate || !d.Syevd || !d.Geqrf || !d.Orgqr)
+    fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: libcublas / libcusolver not loadable (needed by glsgpu_sur_reduce)");
+  return d;
+}
+
+void blas_check(int st, const char* what) {
+  if (st != 0) fail(GLSGPU_ERR_CUDA, std::string(what) + ": status " + std::to_string(st));
 }
 
 }  // namespace
@@ -2106,6 +2165,137 @@ int glsgpu_model_dims(const glsgpu_sur* h, int64_t* m, int64_t* n) {
   if (m) *m = h->m_ref;
   if (n) *n = h->n;
   return GLSGPU_OK;
+}
+
+// sur_reduce (structured.cpp:132-178, Remark 1 of the paper) on the device.  W = [X_1 ... X_G]; the numerical
+// rank q counts the eigenvalues of W'W above max((rank_tol s_max)^2, 64 eps lambda_max); the basis of
+// range(W) is W V_q Lambda_q^-1/2 re-orthonormalised by a Householder QR; every block and Y are rotated onto
+// it.  The basis equals the reference's up to an orthogonal q x q factor (eigenvector signs / rotations inside
+// clusters, QR signs), which the reduced model's GLS estimate and every Gram X_i'X_j, X_i'Y do not see.
+int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, const double* Y, double rank_tol,
+                      int device, int64_t* q_out, double* X_red, double* Y_red, double* basis) {
+  API_BEGIN
+  if (!n_i || !X || !Y || !q_out || !X_red || !Y_red) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_reduce: null argument");
+  if (G < 1 || M < 1) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "make_sur: need at least one block");
+  int64_t n = 0;
+  for (int b = 0; b < G; ++b) {
+    if (n_i[b] < 1) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "sur_reduce: empty block", b);
+    n += n_i[b];
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    fail(GLSGPU_ERR_NO_DEVICE, "glsgpu: no CUDA device available (there is no CPU fallback)");
+  }
+  CK(cudaSetDevice(device));
+  Dla& L = dla();
+  cudaStream_t s = nullptr;
+  cublasHandle_t hb = nullptr;
+  cusolverDnHandle_t hs = nullptr;
+  std::vector<void*> bufs;
+  auto alloc = [&](size_t count) {
+    double* p = dalloc<double>(count);
+    bufs.push_back(p);
+    return p;
+  };
+  auto cleanup = [&]() {
+    if (s) cudaStreamSynchronize(s);
+    for (void* p : bufs) cudaFree(p);
+    if (hb) L.BlasDestroy(hb);
+    if (hs) L.SolDestroy(hs);
+    if (s) cudaStreamDestroy(s);
+  };
+  try {
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    blas_check(L.BlasCreate(&hb), "cublasCreate");
+    blas_check(L.BlasSetStream(hb, s), "cublasSetStream");
+    blas_check(L.SolCreate(&hs), "cusolverDnCreate");
+    blas_check(L.SolSetStream(hs, s), "cusolverDnSetStream");
+    double* dX = alloc((size_t)(M * n));
+    double* dY = alloc((size_t)(M * G));
+    double* gram = alloc((size_t)(n * n));
+    double* lam = alloc((size_t)n);
+    int* info = reinterpret_cast<int*>(alloc(1));
+    CK(cudaMemcpyAsync(dX, X, sizeof(double) * M * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dY, Y, sizeof(double) * M * G, cudaMemcpyHostToDevice, s));
+    const double one = 1.0, zero = 0.0;
+    // W'W (lower triangle) and its eigen-decomposition (sym_eig, linalg.cpp:376-400: ascending eigenvalues)
+    blas_check(L.Dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)n, (int)M, &one, dX, (int)M, &zero, gram, (int)n),
+               "cublasDsyrk");
+    int lwork = 0;
+    blas_check(L.SyevdBuf(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, gram, (int)n, lam, &lwork),
+               "cusolverDnDsyevd_bufferSize");
+    double* work = alloc((size_t)std::max(lwork, 1));
+    blas_check(L.Syevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, gram, (int)n, lam, work, lwork, info),
+               "cusolverDnDsyevd");
+    std::vector<double> ev((size_t)n);
+    int hinfo = 0;
+    CK(cudaMemcpyAsync(ev.data(), lam, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hinfo != 0) fail(GLSGPU_ERR_CUDA, "sur_reduce: eigensolver did not converge (info " + std::to_string(hinfo) + ")");
+    // numerical rank (structured.cpp:142-152)
+    const double lam_max = std::max(ev[(size_t)n - 1], 0.0);
+    const double smax = std::sqrt(lam_max);
+    const double lam_floor = 64.0 * 2.220446049250313e-16 * lam_max;
+    const double lam_cut = std::max(rank_tol * smax * (rank_tol * smax), lam_floor);
+    int64_t q = 0;
+    for (double l : ev)
+      if (l > lam_cut) ++q;
+    if (q >= M) {  // nothing to reduce: transform = I (structured.cpp:154-159)
+      *q_out = M;
+      std::memcpy(X_red, X, sizeof(double) * M * n);
+      std::memcpy(Y_red, Y, sizeof(double) * M * G);
+      if (basis) {
+        std::memset(basis, 0, sizeof(double) * M * M);
+        for (int64_t i = 0; i < M; ++i) basis[i + i * M] = 1.0;
+      }
+      cleanup();
+      return GLSGPU_OK;
+    }
+    // V_q Lambda_q^-1/2, largest eigenvalue first (structured.cpp:161-169)
+    std::vector<double> vh((size_t)(n * q));
+    {
+      std::vector<double> vfull((size_t)(n * n));
+      CK(cudaMemcpyAsync(vfull.data(), gram, sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t j = 0; j < q; ++j) {
+        const int64_t idx = n - 1 - j;
+        const double inv = 1.0 / std::sqrt(ev[(size_t)idx]);
+        for (int64_t r = 0; r < n; ++r) vh[(size_t)(r + j * n)] = vfull[(size_t)(r + idx * n)] * inv;
+      }
+    }
+    double* vq = alloc((size_t)(n * q));
+    CK(cudaMemcpyAsync(vq, vh.data(), sizeof(double) * n * q, cudaMemcpyHostToDevice, s));
+    double* B = alloc((size_t)(M * q));
+    blas_check(L.Dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)M, (int)q, (int)n, &one, dX, (int)M, vq, (int)n, &zero, B, (int)M),
+               "cublasDgemm W V");
+    // re-orthonormalise: basis = qr_thin(basis).q (structured.cpp:170)
+    double* tau = alloc((size_t)q);
+    int lw2 = 0, lw3 = 0;
+    blas_check(L.GeqrfBuf(hs, (int)M, (int)q, B, (int)M, &lw2), "cusolverDnDgeqrf_bufferSize");
+    blas_check(L.OrgqrBuf(hs, (int)M, (int)q, (int)q, B, (int)M, tau, &lw3), "cusolverDnDorgqr_bufferSize");
+    double* w2 = alloc((size_t)std::max(std::max(lw2, lw3), 1));
+    blas_check(L.Geqrf(hs, (int)M, (int)q, B, (int)M, tau, w2, std::max(lw2, lw3), info), "cusolverDnDgeqrf");
+    blas_check(L.Orgqr(hs, (int)M, (int)q, (int)q, B, (int)M, tau, w2, std::max(lw2, lw3), info), "cusolverDnDorgqr");
+    // reduced blocks and responses: basis' X_i, basis' Y (structured.cpp:172-176)
+    double* xr = alloc((size_t)(q * n));
+    double* yr = alloc((size_t)(q * G));
+    blas_check(L.Dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)q, (int)n, (int)M, &one, B, (int)M, dX, (int)M, &zero, xr, (int)q),
+               "cublasDgemm basis' X");
+    blas_check(L.Dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)q, G, (int)M, &one, B, (int)M, dY, (int)M, &zero, yr, (int)q),
+               "cublasDgemm basis' Y");
+    CK(cudaMemcpyAsync(X_red, xr, sizeof(double) * q * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(Y_red, yr, sizeof(double) * q * G, cudaMemcpyDeviceToHost, s));
+    if (basis) CK(cudaMemcpyAsync(basis, B, sizeof(double) * M * q, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *q_out = q;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  API_END((int*)nullptr)
 }
 
 }  // extern "C"

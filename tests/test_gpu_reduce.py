@@ -1,0 +1,98 @@
+"""GPU tests of the sur_reduce row (glsgpu_sur_reduce, structured.cpp:132-178) against the reference's own
+reduction (tests/golden/red_*.npz, tests/test_oracle_reduce.py).
+
+The device basis equals the reference's up to an orthogonal q x q factor (eigenvector signs / rotations,
+QR signs), so the bar is on what the reduction must preserve: the numerical rank q, every Gram of the model
+(X_i'X_j, X_i'Y, |P_W Y|), and the reduced model's GLS estimate.  The reduced solves stop on roundoff-level
+tests, so the solve is judged against the reference's own envelope under exactly such rotations: the
+restatement (bitwise the reference) on three randomly rotated copies of the reference's reduced model.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_14471_b200 import api, synth
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+RED = sorted(glob.glob(os.path.join(GOLDEN, "red_*.npz")))
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def require_device():
+    assert api.device_count() > 0, "no CUDA device: the GPU tests must run on the B200 box (no CPU fallback exists)"
+
+
+def golden(z):
+    p = synth.SurProblem("g", int(z["G"]), int(z["M"]), z["nb"], np.asfortranarray(z["X"]), np.asfortranarray(z["Y"]),
+                         np.asfortranarray(z["omega"]), z["beta"], float(z["tol_rel"]), int(z["max_iter"]))
+    return p
+
+
+@pytest.mark.parametrize("path", RED, ids=os.path.basename)
+def test_sur_reduce_matches_reference_reduction(path):
+    z = np.load(path)
+    p = golden(z)
+    sur = api.sur_from_problem(p)
+    red, rec, B = api.sur_reduce(sur, want_transform=True)
+    q = int(z["q"])
+    assert rec.reduced_rows == q == red.obs() and rec.original_rows == p.M
+    assert np.max(np.abs(B.T @ B - np.eye(q))) < 1e-12
+    Xr, Yr = red.X, red.y
+    for a, b in ((Xr.T @ Xr, z["X_red"].T @ z["X_red"]), (Xr.T @ Yr, z["X_red"].T @ z["Y_red"]),
+                 (Yr.T @ Yr, z["Y_red"].T @ z["Y_red"])):
+        assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+    # the device basis is the reference's up to an orthogonal factor: T = B_ref' B_gpu is orthogonal
+    _, _, _, Bref = oracle.sur_reduce_ref(p, want_basis=True) if oracle.have("ref") else (None, None, None, None)
+    if Bref is not None:
+        T = Bref.T @ B
+        assert np.max(np.abs(T.T @ T - np.eye(q))) < 1e-10
+
+
+@pytest.mark.parametrize("path", RED, ids=os.path.basename)
+def test_reduced_solve_within_the_reference_envelope(path):
+    z = np.load(path)
+    p = golden(z)
+    red, _ = api.sur_reduce(api.sur_from_problem(p))
+    cfg = api.PcgConfig(tol_rel=p.tol_rel, max_iter=p.max_iter, diag_every=0)
+    g = api.pcg_aug(red, config=cfg)
+    q = int(z["q"])
+    variants = []
+    for seed in range(3):
+        T, _ = np.linalg.qr(np.random.default_rng(seed).standard_normal((q, q)))
+        rp = synth.SurProblem("r", p.G, q, p.nb, np.asfortranarray(T @ z["X_red"]), np.asfortranarray(T @ z["Y_red"]),
+                              p.omega, p.beta, p.tol_rel, p.max_iter)
+        variants.append(oracle.solve(rp, cfg=oracle.make_config(tol_rel=p.tol_rel, max_iter=p.max_iter)))
+    spread = max(rel(v.b, z["b"]) for v in variants)
+    its = [int(z["iterations"])] + [v.iterations for v in variants]
+    terms = {str(z["termination"])} | {v.termination for v in variants}
+    s = g.solution
+    assert s.termination.name in terms | {"Converged", "MaxIter", "Breakdown"}
+    assert min(its) - 5 <= s.iterations <= max(its) + 5, (s.iterations, its)
+    assert rel(s.b, z["b"]) <= 5.0 * spread + 1e-10, (rel(s.b, z["b"]), spread)
+    # Remark 1: the reduced estimator is the unreduced one
+    assert rel(s.b, z["b_full"]) <= 1e-7
+
+
+def test_sur_reduce_full_rank_tall_and_nothing_to_reduce():
+    # q == M (n >= M with full row rank): the model comes back unchanged, transform = I
+    p = synth.random_sur(2, 6, [4, 4], seed=5)
+    red, rec = api.sur_reduce(api.sur_from_problem(p))
+    assert rec.reduced_rows == p.M and np.array_equal(red.X, p.X)
+
+
+def test_sur_reduce_c3_scale_row_count():
+    """Config 3's SUR (X_i = column subsets of one X0): rank(W) = N0, so M = 20000 rows reduce to N0."""
+    p = synth.make_problem(3, M=20000, G=16, N=24)
+    red, rec = api.sur_reduce(api.sur_from_problem(p))
+    assert rec.reduced_rows == 24
+    o = oracle.solve(p, cfg=oracle.make_config(tol_rel=1e-12))
+    g = api.pcg_aug(red, config=api.PcgConfig(tol_rel=1e-12, diag_every=0))
+    assert rel(g.solution.b, o.b) <= 1e-8, rel(g.solution.b, o.b)
