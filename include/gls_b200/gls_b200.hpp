@@ -327,6 +327,25 @@ inline MvRglm mv_reduce(const MvRglm& mv, int device = 0) {
   return red;
 }
 
+// sur_reduce (structured.cpp:132-178, Remark 1) on the device: q = numerical rank of W = [X_1 ... X_G]; every
+// block and Y rotated onto an orthonormal basis of range(W) (the reference's up to an orthogonal q x q factor).
+inline SurModel sur_reduce(const SurModel& sur, double rank_tol = 1e-10, std::size_t* rank = nullptr,
+                           int device = 0) {
+  const std::size_t g = sur.equations(), n = sur.total_params(), cap = std::min(sur.M, n);
+  Vector xr((cap < sur.M ? cap : sur.M) * n), yr((cap < sur.M ? cap : sur.M) * g);
+  std::int64_t q = 0;
+  check(glsgpu_sur_reduce((int)g, (std::int64_t)sur.M, sur.widths.data(), sur.X.data(), sur.y.data(), rank_tol,
+                          device, &q, xr.data(), yr.data(), nullptr));
+  if (rank) *rank = (std::size_t)q;
+  SurModel red;
+  red.M = (std::size_t)q;
+  red.widths = sur.widths;
+  red.X.assign(xr.begin(), xr.begin() + (std::size_t)q * n);
+  red.y.assign(yr.begin(), yr.begin() + (std::size_t)q * g);
+  red.sigma0 = sur.sigma0;
+  return red;
+}
+
 inline double operator_norm_probe(const BlockQrOperator& op, std::size_t iters = 12) {
   double nrm = 0.0;
   check(glsgpu_operator_norm_probe(op.handle(), (std::int64_t)iters, &nrm));

@@ -205,6 +205,39 @@ inline std::pair<MvRglm, ReductionRecord> mv_reduce(const MvRglm& mv, int device
   return {std::move(red), std::move(rec)};
 }
 
+// sur_reduce on the device (structured.cpp:132-178); the record's transform is not materialised (empty).
+inline std::pair<SurModel, ReductionRecord> sur_reduce(const SurModel& sur, double rank_tol = 1e-10, int device = 0) {
+  const std::size_t g = sur.equations(), m0 = sur.obs();
+  std::vector<std::int64_t> widths(g);
+  Vector x;
+  for (std::size_t i = 0; i < g; ++i) {
+    widths[i] = (std::int64_t)sur.blocks[i].cols();
+    x.insert(x.end(), sur.blocks[i].data(), sur.blocks[i].data() + m0 * sur.blocks[i].cols());
+  }
+  const std::size_t n = x.size() / m0, rows = std::min(m0, n) < m0 ? std::min(m0, n) : m0;
+  Vector xr(rows * n), yr(rows * g);
+  std::int64_t q = 0;
+  check(glsgpu_sur_reduce((int)g, (std::int64_t)m0, widths.data(), x.data(), sur.y.data(), rank_tol, device, &q,
+                          xr.data(), yr.data(), nullptr));
+  ReductionRecord rec;
+  rec.original_rows = m0;
+  rec.reduced_rows = (std::size_t)q;
+  rec.rank = (std::size_t)q;
+  if ((std::size_t)q >= m0) return {sur, std::move(rec)};
+  SurModel red;
+  red.sigma0 = sur.sigma0;
+  red.y = DenseMatrix(q, g);
+  std::copy(yr.begin(), yr.begin() + q * g, red.y.data());
+  std::size_t p = 0;
+  for (std::size_t i = 0; i < g; ++i) {
+    DenseMatrix b(q, (std::size_t)widths[i]);
+    std::copy(xr.begin() + p * q, xr.begin() + (p + widths[i]) * q, b.data());
+    red.blocks.push_back(std::move(b));
+    p += widths[i];
+  }
+  return {std::move(red), std::move(rec)};
+}
+
 inline std::unique_ptr<IndefinitePreconditioner> sur_preconditioner(const SurModel& sur, const Vector& block_scale,
                                                                     int device = 0) {
   return std::make_unique<GpuSurPreconditioner>(sur, block_scale, device);

@@ -130,6 +130,32 @@ int main() {
                 d.solution.iterations, to_string(d.solution.termination), e.solution.iterations, re,
                 f.solution.iterations, rf, rel_r, ok ? "true" : "false");
   }
+  {
+    // sur_reduce: the reference's vs the device's on a model whose W has rank 5 < n (shared columns)
+    Rng master(31);
+    DenseMatrix base = master.split(0).gaussian_matrix(300, 5);
+    std::vector<DenseMatrix> blocks;
+    for (std::size_t i = 0; i < 4; ++i) {
+      DenseMatrix b(300, 3);
+      for (std::size_t j = 0; j < 3; ++j)
+        for (std::size_t r = 0; r < 300; ++r) b(r, j) = base(r, (i + j) % 5);
+      blocks.push_back(b);
+    }
+    SurModel sur = make_sur(blocks, master.split(1).gaussian_matrix(300, 4), gen_spd_with_cond(4, 5.0, 3));
+    auto [rr, rrec] = sur_reduce(sur);
+    auto [rg, grec] = gpu::sur_reduce(sur);
+    double dg = 0.0, ng = 0.0;
+    for (std::size_t i = 0; i < 4; ++i)
+      for (std::size_t j = 0; j < 4; ++j) {
+        const DenseMatrix a = rr.blocks[i].transpose() * rr.blocks[j], b = rg.blocks[i].transpose() * rg.blocks[j];
+        dg += (a - b).frobenius_norm() * (a - b).frobenius_norm();
+        ng += a.frobenius_norm() * a.frobenius_norm();
+      }
+    const bool ok = rrec.rank == 5 && grec.rank == 5 && rg.obs() == 5 && std::sqrt(dg / ng) <= 1e-12;
+    fails += !ok;
+    std::printf("{\"sur_reduce\": true, \"ref_q\": %zu, \"gpu_q\": %zu, \"gram_rel\": %.3e, \"ok\": %s}\n", rrec.rank,
+                grec.rank, std::sqrt(dg / ng), ok ? "true" : "false");
+  }
   // error mapping: a rank-deficient block raises gls::RankDeficient through the adapter
   {
     SurModel sur = make_case(3, 50, 4, 11);

@@ -64,9 +64,11 @@ def test_reference_pcg_aug_runs_on_the_gpu_operator():
     same for the MVRGLM route (mvrglm_preconditioner / pcg_aug_mvrglm / mv_reduce) within its envelope."""
     rc, lines, err = _run(_ensure("test_reference_adapter"))
     assert rc == 0, (lines, err)
-    cases = [x for x in lines if "ok" in x and "mvrglm" not in x]
+    cases = [x for x in lines if "ok" in x and "mvrglm" not in x and "sur_reduce" not in x]
     assert len(cases) == 3 and all(c["ok"] for c in cases)
     # the harness's multivariate route: reference mv_reduce + MVRGLM vs the B200 operator / loop / mv_reduce
     mv = [x for x in lines if x.get("mvrglm")]
     assert len(mv) == 1 and mv[0]["ok"], mv
+    red = [x for x in lines if x.get("sur_reduce")]
+    assert len(red) == 1 and red[0]["ok"], red
     assert any(x.get("rank_deficient_maps_to_gls_RankDeficient") for x in lines)

