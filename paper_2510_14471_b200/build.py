@@ -52,7 +52,8 @@ REF_INCLUDE = "/root/reference/proj/include"
 
 CPP_DEPS = [os.path.join(ROOT, "include", "glsgpu.h"), os.path.join(ROOT, "include", "gls_b200", "gls_b200.hpp"),
             os.path.join(ROOT, "integration", "gls_gpu_adapter.hpp"), os.path.join(CPP_TESTS, "test_header_api.cpp"),
-            os.path.join(CPP_TESTS, "test_reference_adapter.cpp")]
+            os.path.join(CPP_TESTS, "test_reference_adapter.cpp"), os.path.join(ROOT, "include", "gls_b200", "io.hpp"),
+            os.path.join(CPP_TESTS, "test_io.cpp"), os.path.join(CPP_TESTS, "ref_io.cpp")]
 
 
 def cpp_deps_digest() -> str:
@@ -76,7 +77,15 @@ def build_cpp_tests(verbose: bool = False) -> list:
         "-L", PKG, "-lglsgpu", "-L", os.path.join(ROOT, "oracle"), "-loracle", rpath,
         "-o", os.path.join(out, "test_header_api"),
     ]]
+    cmds.append([
+        "g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(CPP_TESTS, "test_io.cpp"),
+        "-L", PKG, "-lglsgpu", rpath, "-o", os.path.join(out, "test_io"),
+    ])
     if os.path.isdir(REF_INCLUDE) and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libglsref.so")):
+        cmds.append([
+            "g++", "-std=c++20", "-O2", "-I", REF_INCLUDE, os.path.join(CPP_TESTS, "ref_io.cpp"),
+            "-L", os.path.join(ROOT, "oracle", "_ref"), "-lglsref", rpath, "-o", os.path.join(out, "ref_io"),
+        ])
         cmds.append([
             "g++", "-std=c++20", "-O2", "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"), "-I",
             os.path.join(ROOT, "integration"), os.path.join(CPP_TESTS, "test_reference_adapter.cpp"),
