@@ -53,6 +53,10 @@ class SingularTriangular : public Error {
   using Error::Error;
 };
 // Not in the reference: the device side (CUDA failure, no device, unsupported shape, NCCL).
+class SingularCovariance : public Error {
+ public:
+  using Error::Error;
+};
 class DeviceError : public Error {
  public:
   using Error::Error;
@@ -65,6 +69,7 @@ inline void check(int code) {
     case GLSGPU_ERR_DIMENSION_MISMATCH: throw DimensionMismatch(msg);
     case GLSGPU_ERR_RANK_DEFICIENT: throw RankDeficient(msg);
     case GLSGPU_ERR_SINGULAR_D: throw SingularD(msg);
+    case GLSGPU_ERR_SINGULAR_COVARIANCE: throw SingularCovariance(msg);
     case GLSGPU_ERR_SINGULAR_TRIANGULAR: throw SingularTriangular(msg);
     default: throw DeviceError(msg);
   }
@@ -387,6 +392,42 @@ inline AugSolveResult pcg_aug(const BlockQrOperator& op, const Vector& w1, const
   out.solution.residual_seminorm = r.residual_seminorm;
   out.trace.termination = (Termination)r.termination;
   out.trace.w1_projected = r.w1_projected != 0;
+  out.trace.has_breakdown_iteration = r.breakdown_iteration >= 0;
+  out.trace.breakdown_iteration = r.breakdown_iteration >= 0 ? (std::size_t)r.breakdown_iteration : 0;
+  const std::size_t k = std::min<std::size_t>((std::size_t)r.n_rows, rows.size());
+  out.trace.rows.resize(k);
+  for (std::size_t i = 0; i < k; ++i)
+    out.trace.rows[i] = PcgTraceRow{(std::size_t)rows[i].iter, rows[i].c, rows[i].aug_residual_norm,
+                                    rows[i].dual_feas_norm, rows[i].rmse, (long long)rows[i].elapsed_ns};
+  return out;
+}
+
+// pcg_normal_equations(embed_sur(sur), nullptr, config, true_beta) (pcg.cpp:364-511) on the device: the PCG-NE
+// comparison solver (identity preconditioner) on the operator's SUR model.
+inline AugSolveResult pcg_normal_equations(const SurOperator& op, const PcgConfig& config,
+                                           const Vector* true_beta = nullptr) {
+  const std::size_t m = op.rows(), n = op.params();
+  glsgpu_pcg_config c;
+  glsgpu_default_config(&c);
+  c.tol_rel = config.tol_rel;
+  c.max_iter = (std::int64_t)config.max_iter;
+  c.breakdown_tol = config.breakdown_tol;
+  c.stagnation_window = (std::int64_t)config.stagnation_window;
+  c.growth_tol = config.growth_tol;
+  c.growth_window = (std::int64_t)config.growth_window;
+  c.record_z_every = (std::int64_t)config.record_z_every;
+  const std::size_t max_iter = config.max_iter ? config.max_iter : 2 * n;
+  std::vector<glsgpu_trace_row> rows(max_iter + 1);
+  AugSolveResult out;
+  out.solution.b.resize(n);
+  out.solution.w.resize(m);
+  glsgpu_result r;
+  check(glsgpu_pcg_ne(op.handle(), &c, true_beta ? true_beta->data() : nullptr, out.solution.b.data(),
+                      out.solution.w.data(), rows.data(), (std::int64_t)rows.size(), &r));
+  out.solution.iterations = (std::size_t)r.iterations;
+  out.solution.termination = (Termination)r.termination;
+  out.solution.residual_seminorm = r.residual_seminorm;
+  out.trace.termination = (Termination)r.termination;
   out.trace.has_breakdown_iteration = r.breakdown_iteration >= 0;
   out.trace.breakdown_iteration = r.breakdown_iteration >= 0 ? (std::size_t)r.breakdown_iteration : 0;
   const std::size_t k = std::min<std::size_t>((std::size_t)r.n_rows, rows.size());

@@ -22,6 +22,8 @@
  *                                        proj/src/structured.cpp:63-95,365-414,468-477
  *   glsgpu_mv_reduce                     mv_reduce  proj/include/gls/structured.hpp:76; structured.cpp:121-130
  *   glsgpu_sur_reduce                    sur_reduce proj/include/gls/structured.hpp:80-81; structured.cpp:132-178
+ *   glsgpu_pcg_ne                        pcg_normal_equations(embed_sur(sur), nullptr, cfg, true_beta)
+ *                                        proj/include/gls/pcg.hpp; proj/src/pcg.cpp:364-511
  *
  * Errors: every call returns a status code; the codes map 1:1 onto the reference's gls::Error
  * subclasses (proj/include/gls/errors.hpp:10-88) and glsgpu_last_error_message() holds the text.
@@ -48,6 +50,7 @@ enum {
   GLSGPU_ERR_RANK_DEFICIENT = 2,      /* gls::RankDeficient ("block i is rank deficient") */
   GLSGPU_ERR_SINGULAR_D = 3,          /* gls::SingularD (non-positive block scale) */
   GLSGPU_ERR_SINGULAR_TRIANGULAR = 4, /* gls::SingularTriangular */
+  GLSGPU_ERR_SINGULAR_COVARIANCE = 5, /* gls::SingularCovariance (PCG-NE: Sigma not positive definite) */
   GLSGPU_ERR_CUDA = 10,               /* CUDA runtime failure */
   GLSGPU_ERR_NO_DEVICE = 11,          /* no CUDA device: there is no CPU fallback */
   GLSGPU_ERR_OUT_OF_MEMORY = 12,
@@ -212,6 +215,11 @@ int glsgpu_mv_reduce(int G, int64_t M0, int64_t N0, const double* Z0, const doub
  * basis equals the reference's up to an orthogonal q x q factor. */
 int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, const double* Y, double rank_tol,
                       int device, int64_t* q_out, double* X_red, double* Y_red, double* basis);
+/* pcg_normal_equations(embed_sur(sur), nullptr, cfg, true_beta): the PCG-NE comparison solver on the handle's
+ * SUR model (identity preconditioner).  b_out (n) required; w_out (m, the implied Sigma^-1 (y - X b)) and rows
+ * optional; res->sigma_scale holds the G-norm probe.  SingularCovariance when Omega is not positive definite. */
+int glsgpu_pcg_ne(glsgpu_sur* h, const glsgpu_pcg_config* cfg, const double* beta_true, double* b_out,
+                  double* w_out, glsgpu_trace_row* rows, int64_t rows_cap, glsgpu_result* res);
 /* m (rows of the reference's embedded GLM) and n of a handle. */
 int glsgpu_model_dims(const glsgpu_sur* h, int64_t* m, int64_t* n);
 

@@ -44,6 +44,7 @@ inline void check(int code) {
     case GLSGPU_ERR_RANK_DEFICIENT: throw RankDeficient(msg);
     case GLSGPU_ERR_SINGULAR_D: throw SingularD(msg);
     case GLSGPU_ERR_SINGULAR_TRIANGULAR: throw SingularTriangular(msg);
+    case GLSGPU_ERR_SINGULAR_COVARIANCE: throw SingularCovariance(msg);
     default: throw Error("glsgpu: " + msg);
   }
 }

@@ -23,6 +23,7 @@ REF_SO = os.path.join(HERE, "_ref", "libglsref.so")
 
 TERMINATION = {0: "Converged", 1: "Breakdown", 2: "Stagnation", 3: "MaxIter", 4: "Direct"}
 STATUS = {0: "ok", 1: "DimensionMismatch", 2: "RankDeficient", 3: "SingularD", 4: "SingularTriangular",
+          5: "SingularCovariance",
           12: "NoMemory", 98: "std::exception", 99: "gls::Error"}
 
 
@@ -113,6 +114,9 @@ def _load(path: str, kind: str):
         lib.orc_mvrglm_apply.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _PI, _PI, _P, _P, C.c_int, _P, _P]
         lib.orc_mvrglm_norm_probe.restype = C.c_double
         lib.orc_mvrglm_norm_probe.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _PI, _PI]
+        lib.orc_pcg_ne_sur.restype = C.c_int
+        lib.orc_pcg_ne_sur.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, _P, C.POINTER(Config), _P, _P, _P,
+                                       C.POINTER(TraceRow), C.c_int64, C.POINTER(Result)]
         lib.orc_mv_reduce.restype = C.c_int
         lib.orc_mv_reduce.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _P]
     else:
@@ -135,6 +139,9 @@ def _load(path: str, kind: str):
                                            C.POINTER(Result), C.POINTER(C.c_uint64)]
         lib.ref_mvrglm_apply.restype = C.c_int
         lib.ref_mvrglm_apply.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _PI, _PI, _P, _P, C.c_int, _P, _P]
+        lib.ref_pcg_ne_sur.restype = C.c_int
+        lib.ref_pcg_ne_sur.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, _P, C.POINTER(Config), _P, _P, _P,
+                                       C.POINTER(TraceRow), C.c_int64, C.POINTER(Result)]
         lib.ref_sur_reduce.restype = C.c_int
         lib.ref_sur_reduce.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, C.c_double, C.POINTER(C.c_int64), _P, _P, _P]
         lib.ref_mv_reduce.restype = C.c_int
@@ -373,3 +380,30 @@ def sur_reduce_ref(prob, rank_tol: float = 1e-10, want_basis: bool = False):
         return q, np.asfortranarray(prob.X), np.asfortranarray(prob.Y), None
     return (q, Xr[:q * n].reshape(q, n, order="F"), Yr[:q * prob.G].reshape(q, prob.G, order="F"),
             B[:prob.M * q].reshape(prob.M, q, order="F") if want_basis else None)
+
+
+def solve_ne(prob, kind: str = "oracle", cfg: Optional[Config] = None, trace: bool = True,
+             beta_true: Optional[np.ndarray] = None) -> SolveOut:
+    """pcg_normal_equations(embed_sur(sur), nullptr, cfg, true_beta) (pcg.cpp:364-511): the PCG-NE comparison
+    solver.  kind="oracle": the SUR-structured restatement; kind="ref": the literal reference (dense m x m
+    Cholesky of Sigma; small sizes only).  sigma_scale holds the oracle's g_scale (0 for the reference)."""
+    L = lib(kind)
+    if cfg is None:
+        cfg = make_config(tol_rel=prob.tol_rel, max_iter=prob.max_iter)
+    nb = np.ascontiguousarray(prob.nb, dtype=np.int64)
+    m, n = prob.M * prob.G, int(nb.sum())
+    max_iter = cfg.max_iter if cfg.max_iter else 2 * n
+    cap = max_iter + 1 if trace else 0
+    rows = (TraceRow * max(cap, 1))()
+    b, w, res = np.zeros(n), np.zeros(m), Result()
+    bt = None if beta_true is None else np.ascontiguousarray(beta_true, dtype=np.float64)
+    args = [prob.G, prob.M, nb.ctypes.data_as(_PI), _dp(prob.X), _dp(prob.Y), _dp(prob.omega), C.byref(cfg), _dp(bt),
+            _dp(b), _dp(w), rows if trace else None, cap, C.byref(res)]
+    st = (L.orc_pcg_ne_sur if kind == "oracle" else L.ref_pcg_ne_sur)(*args)
+    if st:
+        raise OracleError(st, L.ref_last_error().decode() if kind != "oracle" else "")
+    tr = np.frombuffer(rows, dtype=TRACE_DTYPE, count=min(res.n_rows, cap)).copy() if trace else np.zeros(0, TRACE_DTYPE)
+    return SolveOut(b=b, w=w, iterations=int(res.iterations), termination=TERMINATION[res.termination],
+                    breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
+                    residual_seminorm=float(res.residual_seminorm), w1_projected=False, trace=tr,
+                    sigma_scale=float(res.sigma_scale))

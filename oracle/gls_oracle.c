@@ -982,3 +982,197 @@ int orc_mv_reduce(int G, int64_t M0, int64_t N0, const double* Z0, const double*
   free(q);
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------ PCG-NE on the SUR model
+ * pcg_normal_equations(embed_sur(sur), nullptr, cfg, true_beta) (proj/src/pcg.cpp:364-511): CG on
+ * X' Sigma^-1 X b = X' Sigma^-1 y with the identity preconditioner.  The reference factors the dense m x m
+ * Sigma = Omega (x) I_M (cholesky, linalg.cpp:174-193); that factor is L (x) I_M with L = cholesky(Omega) by
+ * the same loop (the off-pattern terms subtract exact zeros), and its chol_solve (linalg.cpp:195-210) is,
+ * row by row of reshape(v, M, G), the G-dimensional forward / backward substitution with L, summed in the
+ * same ascending order.  So the restatement never forms the m x m matrix. */
+#define ORC_SINGULAR_COVARIANCE 5
+
+static int chol_g(int G, const double* omega, double* L) {
+  double max_diag = 0.0;
+  for (int i = 0; i < G; ++i) max_diag = fmax(max_diag, fabs(omega[i + i * G]));
+  const double floor_ = 64.0 * DBL_EPSILON * max_diag;
+  for (int64_t k = 0; k < (int64_t)G * G; ++k) L[k] = 0.0;
+  for (int j = 0; j < G; ++j) {
+    double d = omega[j + j * G];
+    for (int k = 0; k < j; ++k) d -= L[j + k * G] * L[j + k * G];
+    if (d <= floor_) return ORC_SINGULAR_COVARIANCE;
+    L[j + j * G] = sqrt(d);
+    for (int i = j + 1; i < G; ++i) {
+      double v = omega[i + j * G];
+      for (int k = 0; k < j; ++k) v -= L[i + k * G] * L[j + k * G];
+      L[i + j * G] = v / L[j + j * G];
+    }
+  }
+  return ORC_OK;
+}
+
+/* x = (L L')^-1 x for Sigma = (L L') (x) I_M, in place; x is M x G column-major */
+static void chol_solve_kron(int G, int64_t M, const double* L, double* x) {
+  for (int64_t r = 0; r < M; ++r) {
+    for (int i = 0; i < G; ++i) {
+      double s = x[r + (int64_t)i * M];
+      for (int j = 0; j < i; ++j) s -= L[i + j * G] * x[r + (int64_t)j * M];
+      x[r + (int64_t)i * M] = s / L[i + i * G];
+    }
+    for (int i = G; i-- > 0;) {
+      double s = x[r + (int64_t)i * M];
+      for (int j = i + 1; j < G; ++j) s -= L[j + i * G] * x[r + (int64_t)j * M];
+      x[r + (int64_t)i * M] = s / L[i + i * G];
+    }
+  }
+}
+
+int orc_pcg_ne_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y, const double* omega,
+                   const orc_config* cfg, const double* beta_true, double* b_out, double* w_out,
+                   orc_trace_row* rows, int64_t rows_cap, orc_result* res) {
+  const int64_t m = M * G, n = total_params(G, nb);
+  double* L = (double*)malloc(sizeof(double) * (size_t)G * G);
+  if (!L) return ORC_NO_MEMORY;
+  int st = chol_g(G, omega, L);
+  if (st) { free(L); return st; }
+  const int64_t start = now_ns();
+  const int64_t max_iter = cfg->max_iter ? cfg->max_iter : 2 * n;
+  const int64_t stride = cfg->record_z_every ? cfg->record_z_every : 1;
+  size_t mb = sizeof(double) * (size_t)m, nbytes = sizeof(double) * (size_t)n;
+  double *tm = malloc(mb), *v = malloc(nbytes), *x = malloc(nbytes), *f = malloc(nbytes), *kf = malloc(nbytes),
+         *p = malloc(nbytes), *gp = malloc(nbytes), *x_best = malloc(nbytes), *h = malloc(nbytes);
+  if (!tm || !v || !x || !f || !kf || !p || !gp || !x_best || !h) { st = ORC_NO_MEMORY; goto done; }
+  res->w1_projected = 0;
+  res->breakdown_iteration = -1;
+#define APPLY_G(in, out)                       \
+  do {                                         \
+    x_apply(G, M, nb, X, (in), tm);            \
+    chol_solve_kron(G, M, L, tm);              \
+    x_apply_t(G, M, nb, X, tm, (out));         \
+  } while (0)
+  /* crude norm probe for the breakdown scale (pcg.cpp:381-392) */
+  double g_scale = 0.0;
+  for (int64_t k = 0; k < n; ++k) v[k] = 1.0 / sqrt((double)n);
+  for (int it = 0; it < 12; ++it) {
+    APPLY_G(v, gp);
+    memcpy(v, gp, nbytes);
+    g_scale = vnorm2(n, v);
+    if (g_scale == 0.0) break;
+    for (int64_t k = 0; k < n; ++k) v[k] /= g_scale;
+  }
+  res->sigma_scale = g_scale;
+  /* h = X' Sigma^-1 y; x = 0; f = -h; kf = f (no preconditioner) */
+  memcpy(tm, Y, mb);
+  chol_solve_kron(G, M, L, tm);
+  x_apply_t(G, M, nb, X, tm, h);
+  for (int64_t k = 0; k < n; ++k) { x[k] = 0.0; f[k] = -1.0 * h[k]; }
+  memcpy(kf, f, nbytes);
+  double c = vdot(n, f, kf);
+  if (c < 0.0) c = 0.0;
+  const double c1 = c, threshold = cfg->tol_rel * cfg->tol_rel * c1;
+  memcpy(p, kf, nbytes);
+  double k_gain = 0.0;
+#define NE_FLOOR(fn2, kfn)                                                         \
+  ((fn2) > 0.0 ? (k_gain = fmax(k_gain, (kfn) / sqrt(fn2))) : 0.0,                \
+   16.0 * DBL_EPSILON * fmax(k_gain, 1e-3) * (fn2))
+  (void)NE_FLOOR(vdot(n, f, f), vnorm2(n, kf));
+  int64_t nrows = 0;
+#define NE_ROW(iter_, cval_, sampled_)                                                          \
+  do {                                                                                          \
+    if (rows && nrows < rows_cap) {                                                             \
+      orc_trace_row* row_ = &rows[nrows];                                                       \
+      row_->iter = (iter_);                                                                     \
+      row_->c = (cval_);                                                                        \
+      row_->aug_residual_norm = vnorm2(n, f);                                                   \
+      row_->dual_feas_norm = vnorm2(n, f);                                                      \
+      if ((sampled_) && beta_true) {                                                            \
+        double acc_ = 0.0;                                                                      \
+        for (int64_t k_ = 0; k_ < n; ++k_) { const double d_ = x[k_] - beta_true[k_]; acc_ += d_ * d_; } \
+        row_->rmse = sqrt(acc_ / (double)n);                                                    \
+      } else {                                                                                  \
+        row_->rmse = NAN;                                                                       \
+      }                                                                                         \
+      row_->elapsed_ns = now_ns() - start;                                                      \
+    }                                                                                           \
+    ++nrows;                                                                                    \
+  } while (0)
+  NE_ROW(0, c, 1);
+  memcpy(x_best, x, nbytes);
+  double c_best = c;
+  int64_t best_iter = 0, stagnant = 0, done_it = 0;
+  int term = T_MAXITER;
+  if (c1 == 0.0) {
+    term = T_CONVERGED;
+  } else {
+    for (int64_t i = 1; i <= max_iter; ++i) {
+      APPLY_G(p, gp);
+      const double d = vdot(n, p, gp);
+      if (fabs(d) <= cfg->breakdown_tol * vdot(n, p, p) * fmax(g_scale, 1e-300)) {
+        term = T_BREAKDOWN;
+        res->breakdown_iteration = i;
+        break;
+      }
+      const double lambda = c / d;
+      for (int64_t k = 0; k < n; ++k) x[k] += -lambda * p[k];
+      for (int64_t k = 0; k < n; ++k) f[k] += -lambda * gp[k];
+      memcpy(kf, f, nbytes);
+      double c_next = vdot(n, f, kf);
+      done_it = i;
+      const int sampled = (i % stride == 0) || c_next <= threshold || i == max_iter;
+      NE_ROW(i, c_next, sampled);
+      const double floor_c = NE_FLOOR(vdot(n, f, f), vnorm2(n, kf));
+      const int exhausted = fabs(c_next) <= floor_c / 64.0 || (fabs(c_next) <= floor_c && c_next <= 1e-6 * c);
+      if (c_next < 0.0 && fabs(c_next) > floor_c) {
+        term = T_BREAKDOWN;
+        res->breakdown_iteration = i;
+        break;
+      }
+      if (c_next < 0.0) c_next = 0.0;
+      if (c_next < c_best) {
+        c_best = c_next;
+        memcpy(x_best, x, nbytes);
+        best_iter = i;
+      }
+      if (c_next <= threshold || exhausted) {
+        term = T_CONVERGED;
+        break;
+      }
+      if (fabs(c_next - c) <= 1e-15 * c) {
+        if (++stagnant >= cfg->stagnation_window) {
+          term = T_STAGNATION;
+          break;
+        }
+      } else {
+        stagnant = 0;
+      }
+      if (c_next > cfg->growth_tol * c_best && i - best_iter >= cfg->growth_window) {
+        term = T_BREAKDOWN;
+        res->breakdown_iteration = i;
+        break;
+      }
+      const double mu = c_next / c;
+      c = c_next;
+      for (int64_t k = 0; k < n; ++k) p[k] = kf[k] + mu * p[k];
+    }
+  }
+  {
+    const int keep_last = term == T_CONVERGED;
+    const double* b = keep_last ? x : x_best;
+    memcpy(b_out, b, nbytes);
+    if (w_out) { /* implied_w(b) = Sigma^-1 (y - X b) */
+      x_apply(G, M, nb, X, b, tm);
+      for (int64_t k = 0; k < m; ++k) w_out[k] = Y[k] - tm[k];
+      chol_solve_kron(G, M, L, w_out);
+    }
+    res->iterations = done_it;
+    res->termination = term;
+    res->residual_seminorm = keep_last ? c : c_best;
+    res->n_rows = nrows;
+  }
+#undef APPLY_G
+#undef NE_FLOOR
+#undef NE_ROW
+done:
+  free(L); free(tm); free(v); free(x); free(f); free(kf); free(p); free(gp); free(x_best); free(h);
+  return st;
+}

@@ -316,4 +316,41 @@ int ref_sur_reduce(int G, int64_t M, const int64_t* nb, const double* X, const d
   }
 }
 
+// pcg_normal_equations(embed_sur(sur), nullptr, cfg, true_beta) (proj/src/pcg.cpp:364-511)
+int ref_pcg_ne_sur(int G, int64_t M, const int64_t* nb, const double* X, const double* Y, const double* omega,
+                   const Config* cfg, const double* beta_true, double* b_out, double* w_out, TraceRow* rows,
+                   int64_t rows_cap, Result* res) {
+  try {
+    gls::SurModel sur = build_sur(G, M, nb, X, Y, omega);
+    gls::Glm glm = gls::embed_sur(sur);
+    const std::size_t m = glm.x.rows(), n = glm.x.cols();
+    gls::Vector beta;
+    if (beta_true) beta.assign(beta_true, beta_true + n);
+    gls::AugSolveResult out = gls::pcg_normal_equations(glm, nullptr, pcg_config_of(cfg), beta_true ? &beta : nullptr);
+    std::memcpy(b_out, out.solution.b.data(), sizeof(double) * n);
+    if (w_out) std::memcpy(w_out, out.solution.w.data(), sizeof(double) * m);
+    res->iterations = static_cast<int64_t>(out.solution.iterations);
+    res->termination = static_cast<int32_t>(out.solution.termination);
+    res->w1_projected = 0;
+    res->breakdown_iteration =
+        out.trace.breakdown_iteration ? static_cast<int64_t>(*out.trace.breakdown_iteration) : -1;
+    res->residual_seminorm = out.solution.residual_seminorm;
+    res->n_rows = static_cast<int64_t>(out.trace.rows.size());
+    res->sigma_scale = 0.0;
+    if (rows) {
+      const int64_t k = std::min<int64_t>(rows_cap, res->n_rows);
+      for (int64_t i = 0; i < k; ++i) {
+        const auto& r = out.trace.rows[i];
+        rows[i] = TraceRow{static_cast<int64_t>(r.iter), r.c, r.aug_residual_norm, r.dual_feas_norm, r.rmse,
+                           r.elapsed_ns};
+      }
+    }
+    return 0;
+  } catch (const gls::Error& e) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s", e.what());
+    if (dynamic_cast<const gls::SingularCovariance*>(&e)) return 5;
+    return code_of(e);
+  }
+}
+
 }  // extern "C"

@@ -52,7 +52,7 @@ EXPORTS = [
     "glsgpu_operator_norm_probe", "glsgpu_counters", "glsgpu_reset_apply_counters", "glsgpu_sur_solve",
     "glsgpu_default_config", "glsgpu_kernel_stats", "glsgpu_launch_count", "glsgpu_get_factors", "glsgpu_synth_normal",
     "glsgpu_synth_response", "glsgpu_nccl_unique_id", "glsgpu_sur_create_sharded", "glsgpu_sur_shard",
-    "glsgpu_mvrglm_create", "glsgpu_mv_reduce", "glsgpu_model_dims", "glsgpu_sur_reduce",
+    "glsgpu_mvrglm_create", "glsgpu_mv_reduce", "glsgpu_model_dims", "glsgpu_sur_reduce", "glsgpu_pcg_ne",
 ]
 
 _lib = None
@@ -104,6 +104,8 @@ def load() -> C.CDLL:
                                        C.POINTER(H), C.POINTER(C.c_int)]
     L.glsgpu_mv_reduce.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _P, C.c_int]
     L.glsgpu_model_dims.argtypes = [H, _PI64, _PI64]
+    L.glsgpu_pcg_ne.argtypes = [H, C.POINTER(PcgConfigC), _P, _P, _P, C.POINTER(TraceRowC), C.c_int64,
+                                C.POINTER(ResultC)]
     L.glsgpu_sur_reduce.argtypes = [C.c_int, C.c_int64, _PI64, _P, _P, C.c_double, C.c_int, _PI64, _P, _P, _P]
     _lib = L
     return L

@@ -56,7 +56,11 @@ class DeviceError(GlsError):
     """CUDA failure / no device / unsupported shape (not in the reference: the device side)."""
 
 
-_ERRORS = {1: DimensionMismatch, 2: RankDeficient, 3: SingularD, 4: SingularTriangular}
+class SingularCovariance(GlsError):
+    pass
+
+
+_ERRORS = {1: DimensionMismatch, 2: RankDeficient, 3: SingularD, 4: SingularTriangular, 5: SingularCovariance}
 
 
 def _check(code: int, lib=None):
@@ -580,6 +584,34 @@ def auxiliary_scales(omega0: np.ndarray, rule: str, z0: Optional[np.ndarray] = N
     f = _frobenius(z0)
     z_scale2 = f * f / float(z0.shape[1])
     return z, z / z_scale2
+
+
+def pcg_normal_equations(sur_or_op, config: Optional[PcgConfig] = None, true_beta=None, want_w: bool = True,
+                         want_trace: bool = True) -> AugSolveResult:
+    """pcg_normal_equations(embed_sur(sur), nullptr, config, true_beta) (pcg.cpp:364-511) on the device: the
+    PCG-NE comparison solver (identity preconditioner).  Raises SingularCovariance for a singular Omega."""
+    op = sur_or_op if isinstance(sur_or_op, GpuSurPreconditioner) else sur_preconditioner(sur_or_op)
+    cfg = config or PcgConfig()
+    m, n = op.m, op.n
+    max_iter = cfg.max_iter if cfg.max_iter else 2 * n
+    cap = (max_iter + 1) if want_trace else 0
+    rows = (L.TraceRowC * max(cap, 1))()
+    b = np.empty(n)
+    w = np.empty(m) if want_w else None
+    bt = None if true_beta is None else np.ascontiguousarray(true_beta, dtype=np.float64)
+    res = L.ResultC()
+    cc = cfg.to_c()
+    _check(op._lib.glsgpu_pcg_ne(op.handle, C.byref(cc), _dp(bt), _dp(b), _dp(w), rows if want_trace else None, cap,
+                                 C.byref(res)), op._lib)
+    k = min(res.n_rows, cap)
+    tr = np.frombuffer(rows, dtype=TRACE_DTYPE, count=k).copy() if want_trace else np.zeros(0, TRACE_DTYPE)
+    term = Termination(res.termination)
+    sol = GlsSolution(b=b, w=w, iterations=int(res.iterations), termination=term,
+                      residual_seminorm=float(res.residual_seminorm))
+    trace = PcgTrace(rows=tr, termination=term,
+                     breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
+                     w1_projected=False)
+    return AugSolveResult(solution=sol, trace=trace, sigma_scale=float(res.sigma_scale), solve_ms=float(res.solve_ms))
 
 
 def nccl_unique_id() -> bytes:

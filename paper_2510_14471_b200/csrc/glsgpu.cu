@@ -15,6 +15,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -179,6 +180,8 @@ struct glsgpu_sur {
   std::vector<int64_t> rows_b;      // rows of block b in the reference's operator (cost model)
   double* Xqr = nullptr;            // pre-scaled QR source D^-1/2 X (two weights per block); null: X * w_b
   int rank_msg = 0;                 // 1: plain qr_thin (mv_reduce) wording of RankDeficient
+  double* omegaInvT = nullptr;      // PCG-NE: Omega^-1 (row-major, as omegaT), built on first use
+  double* d_ones = nullptr;         // PCG-NE: unit row weights for the X' pass
   const double* X = nullptr;
   int64_t ldx = 0;
   double* X_own = nullptr;
@@ -1065,7 +1068,7 @@ void destroy_impl(glsgpu_sur* h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->graph) cudaGraphExecDestroy(h->graph);
   for (auto e : h->tev) cudaEventDestroy(e);
-  void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->d_wtc, h->Xqr, h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
+  void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->d_wtc, h->Xqr, h->omegaInvT, h->d_ones, h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
                   h->qr_store, h->qr_tau, h->qr_scratch, h->d_rank_flags, h->d_blk_narrow, h->d_blk_wide,
                   h->mvec, h->t,
                   h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,
@@ -1318,6 +1321,28 @@ __global__ void k_init_scalars(const double* partials, int count, SolveState* st
 }
 
 __global__ void k_set_t0(SolveState* st) { st->t0 = globaltimer(); }
+
+// PCG-NE: out_b = X_b v_b (rows < M; padding rows 0), grid.y = block
+__global__ void k_xapply(Geo g, const double* __restrict__ X, int64_t ldx, const double* __restrict__ v,
+                         double* __restrict__ out) {
+  const int b = blockIdx.y;
+  const int nb = g.nb[b];
+  const int64_t p0 = g.p0[b];
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.ldm; k += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (k < g.M)
+      for (int j = 0; j < nb; ++j) s = s + X[(p0 + j) * ldx + k] * v[p0 + j];
+    out[(int64_t)b * g.ldm + k] = s;
+  }
+}
+// r = y - r over the M x G rows (padding rows stay 0)
+__global__ void k_ysub(Geo g, const double* __restrict__ y, int64_t ldy, double* __restrict__ r) {
+  const int b = blockIdx.y;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.ldm; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)b * g.ldm + k;
+    r[o] = k < g.M ? y[(int64_t)b * ldy + k] - r[o] : 0.0;
+  }
+}
 
 // MVRGLM embed: X[pos[i]] = 1 (the selector rows C_b(q, restr_b[q]) = 1, structured.cpp:83-84)
 __global__ void k_set_ones(double* X, const int64_t* pos, int64_t count) {
@@ -2295,6 +2320,262 @@ int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, con
     throw;
   }
   cleanup();
+  API_END((int*)nullptr)
+}
+
+// pcg_normal_equations(embed_sur(sur), nullptr, cfg, true_beta) (pcg.cpp:364-511): CG on X' Sigma^-1 X b =
+// X' Sigma^-1 y, the PCG-NE comparison solver of the harness (experiments.cpp:604-613,906-909).  The reference
+// factors the dense m x m Sigma; Sigma^-1 = Omega^-1 (x) I_M is applied here as a Kronecker pass with Omega^-1
+// (from cholesky(Omega), the reference's own pivot floor, so a singular Omega raises SingularCovariance as the
+// dense factorisation does).  Per iteration: X p (k_xapply), Sigma^-1 (k_kron), X' (the column pass over X)
+// on the device; the n-vector recurrences on the host.
+int glsgpu_pcg_ne(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const double* beta_true, double* b_out,
+                  double* w_out, glsgpu_trace_row* rows, int64_t rows_cap, glsgpu_result* res) {
+  API_BEGIN
+  if (!h || !b_out || !res) fail(GLSGPU_ERR_INVALID, "glsgpu_pcg_ne: null argument");
+  if (h->coll) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu_pcg_ne: row-sharded handles are not supported");
+  if (h->mv && h->m_ref != (int64_t)h->G * h->M0)
+    fail(GLSGPU_ERR_SINGULAR_COVARIANCE, "pcg_normal_equations: covariance is singular");
+  CK(cudaSetDevice(h->dev));
+  glsgpu_pcg_config cfg;
+  if (cfg_in) cfg = *cfg_in;
+  else glsgpu_default_config(&cfg);
+  const int G = h->G;
+  const int64_t n = h->n;
+  // cholesky(Omega) (linalg.cpp:174-193) -> Omega^-1
+  if (!h->omegaInvT) {
+    std::vector<double> L((size_t)G * G, 0.0);
+    double max_diag = 0.0;
+    for (int i = 0; i < G; ++i) max_diag = std::max(max_diag, std::fabs(h->omega_h[(size_t)i * G + i]));
+    const double floor_ = 64.0 * 2.220446049250313e-16 * max_diag;
+    for (int j = 0; j < G; ++j) {
+      double d = h->omega_h[(size_t)j * G + j];
+      for (int k = 0; k < j; ++k) d -= L[j + (size_t)k * G] * L[j + (size_t)k * G];
+      if (d <= floor_) fail(GLSGPU_ERR_SINGULAR_COVARIANCE, "pcg_normal_equations: covariance is singular");
+      L[j + (size_t)j * G] = std::sqrt(d);
+      for (int i = j + 1; i < G; ++i) {
+        double v = h->omega_h[i + (size_t)j * G];
+        for (int k = 0; k < j; ++k) v -= L[i + (size_t)k * G] * L[j + (size_t)k * G];
+        L[i + (size_t)j * G] = v / L[j + (size_t)j * G];
+      }
+    }
+    std::vector<double> inv((size_t)G * G);
+    for (int c = 0; c < G; ++c) {  // column c of (L L')^-1
+      std::vector<double> x((size_t)G, 0.0);
+      x[(size_t)c] = 1.0;
+      for (int i = 0; i < G; ++i) {
+        double s = x[(size_t)i];
+        for (int j = 0; j < i; ++j) s -= L[i + (size_t)j * G] * x[(size_t)j];
+        x[(size_t)i] = s / L[i + (size_t)i * G];
+      }
+      for (int i = G; i-- > 0;) {
+        double s = x[(size_t)i];
+        for (int j = i + 1; j < G; ++j) s -= L[j + (size_t)i * G] * x[(size_t)j];
+        x[(size_t)i] = s / L[i + (size_t)i * G];
+      }
+      for (int i = 0; i < G; ++i) inv[(size_t)i + (size_t)c * G] = x[(size_t)i];
+    }
+    std::vector<double> t((size_t)G * G);
+    for (int p = 0; p < G; ++p)
+      for (int c = 0; c < G; ++c)
+        t[(size_t)p * G + c] = 0.5 * (inv[(size_t)p + (size_t)c * G] + inv[(size_t)c + (size_t)p * G]);
+    h->omegaInvT = dalloc<double>((size_t)G * G);
+    CK(cudaMemcpy(h->omegaInvT, t.data(), sizeof(double) * G * G, cudaMemcpyHostToDevice));
+    std::vector<double> ones((size_t)G, 1.0);
+    h->d_ones = dalloc<double>((size_t)G);
+    CK(cudaMemcpy(h->d_ones, ones.data(), sizeof(double) * G, cudaMemcpyHostToDevice));
+  }
+  ensure_solver(h, 1);
+  cudaStream_t s = h->s;
+  Geo g = geo_of(h);
+  const dim3 rgrid((unsigned)std::min<int64_t>((h->ldm + NT - 1) / NT, 64), (unsigned)G);
+  // Sigma^-1 x: the Kronecker pass with Omega^-1 in place of Omega
+  auto sigma_inv = [&](const double* src, double* out) {
+    double* keep = h->omegaT;
+    h->omegaT = h->omegaInvT;
+    launch_kron(h, src, nullptr, nullptr, nullptr, out, h->partA, 0, nullptr, nullptr);
+    h->omegaT = keep;
+  };
+  // X' x over the user X (unit row weights)
+  auto xt = [&](const double* in, double* out) {
+    Geo gx = g;
+    gx.wts = gx.wtc = h->d_ones;
+    ColArgs a = base_args(h);
+    a.A = h->X;
+    a.lda = h->ldx;
+    a.avalid = h->M;
+    a.vin = in;
+    if (h->n_narrow) {
+      a.blocks = h->d_blk_narrow;
+      k_colpass<MODE_QT_V, true><<<h->n_narrow * h->nch, NT, 0, s>>>(gx, a, nullptr);
+      h->launches++;
+    }
+    if (h->n_wide) {
+      a.blocks = h->d_blk_wide;
+      k_colpass<MODE_QT_V, false><<<h->n_wide * h->nch, NT, (size_t)h->CH * sizeof(double), s>>>(gx, a, nullptr);
+      h->launches++;
+    }
+    CKL("k_colpass X'");
+    launch_reduce_t(h, out, nullptr, 0);
+  };
+  std::vector<double> hv((size_t)n), gp((size_t)n);
+  auto apply_g = [&](const std::vector<double>& v, std::vector<double>& out) {
+    CK(cudaMemcpyAsync(h->t, v.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    k_xapply<<<rgrid, NT, 0, s>>>(g, h->X, h->ldx, h->t, h->r);
+    h->launches++;
+    CKL("k_xapply");
+    sigma_inv(h->r, h->su);
+    xt(h->su, h->t2);
+    CK(cudaMemcpyAsync(out.data(), h->t2, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  };
+  auto dot = [](const std::vector<double>& a, const std::vector<double>& b) {
+    double acc = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) acc += a[i] * b[i];
+    return acc;
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  const int64_t max_iter = cfg.max_iter ? cfg.max_iter : 2 * n;
+  const int64_t stride = cfg.record_z_every ? cfg.record_z_every : 1;
+  // crude norm probe for the breakdown scale (pcg.cpp:381-392)
+  double g_scale = 0.0;
+  {
+    std::vector<double> v((size_t)n, 1.0 / std::sqrt((double)n));
+    for (int it = 0; it < 12; ++it) {
+      apply_g(v, gp);
+      v = gp;
+      g_scale = std::sqrt(dot(v, v));
+      if (g_scale == 0.0) break;
+      for (double& t : v) t /= g_scale;
+    }
+  }
+  // h = X' Sigma^-1 y
+  CK(cudaMemsetAsync(h->r, 0, sizeof(double) * h->ldm * G, s));
+  k_ysub<<<rgrid, NT, 0, s>>>(g, h->Y, h->ldy, h->r);
+  h->launches++;
+  sigma_inv(h->r, h->su);
+  xt(h->su, h->t2);
+  CK(cudaMemcpyAsync(hv.data(), h->t2, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<double> x((size_t)n, 0.0), f((size_t)n), kf, p, x_best;
+  for (int64_t k = 0; k < n; ++k) f[(size_t)k] = -1.0 * hv[(size_t)k];
+  kf = f;
+  double c = std::max(dot(f, kf), 0.0);
+  const double c1 = c, threshold = cfg.tol_rel * cfg.tol_rel * c1;
+  p = kf;
+  double k_gain = 0.0;
+  auto c_floor = [&](double fn2, double kfn) {
+    if (fn2 > 0.0) k_gain = std::max(k_gain, kfn / std::sqrt(fn2));
+    return 16.0 * 2.220446049250313e-16 * std::max(k_gain, 1e-3) * fn2;
+  };
+  (void)c_floor(dot(f, f), std::sqrt(dot(kf, kf)));
+  int64_t nrows = 0;
+  auto push_row = [&](int64_t iter, double cval, bool sampled) {
+    if (rows && nrows < rows_cap) {
+      glsgpu_trace_row& r = rows[nrows];
+      r.iter = iter;
+      r.c = cval;
+      r.aug_residual_norm = r.dual_feas_norm = std::sqrt(dot(f, f));
+      if (sampled && beta_true) {
+        double acc = 0.0;
+        for (int64_t k = 0; k < n; ++k) acc += (x[(size_t)k] - beta_true[k]) * (x[(size_t)k] - beta_true[k]);
+        r.rmse = std::sqrt(acc / (double)n);
+      } else {
+        r.rmse = std::nan("");
+      }
+      r.elapsed_ns = (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                         std::chrono::steady_clock::now() - t0).count();
+    }
+    ++nrows;
+  };
+  push_row(0, c, true);
+  x_best = x;
+  double c_best = c;
+  int64_t best_iter = 0, stagnant = 0, done = 0, bd_iter = -1;
+  int term = T_MAXITER;
+  if (c1 == 0.0) {
+    term = T_CONVERGED;
+  } else {
+    for (int64_t i = 1; i <= max_iter; ++i) {
+      apply_g(p, gp);
+      const double d = dot(p, gp);
+      if (std::fabs(d) <= cfg.breakdown_tol * dot(p, p) * std::max(g_scale, 1e-300)) {
+        term = T_BREAKDOWN;
+        bd_iter = i;
+        break;
+      }
+      const double lambda = c / d;
+      for (int64_t k = 0; k < n; ++k) x[(size_t)k] += -lambda * p[(size_t)k];
+      for (int64_t k = 0; k < n; ++k) f[(size_t)k] += -lambda * gp[(size_t)k];
+      kf = f;
+      double c_next = dot(f, kf);
+      done = i;
+      const bool sampled = (i % stride == 0) || c_next <= threshold || i == max_iter;
+      push_row(i, c_next, sampled);
+      const double floor_c = c_floor(dot(f, f), std::sqrt(dot(kf, kf)));
+      const bool exhausted = std::fabs(c_next) <= floor_c / 64.0 || (std::fabs(c_next) <= floor_c && c_next <= 1e-6 * c);
+      if (c_next < 0.0 && std::fabs(c_next) > floor_c) {
+        term = T_BREAKDOWN;
+        bd_iter = i;
+        break;
+      }
+      if (c_next < 0.0) c_next = 0.0;
+      if (c_next < c_best) {
+        c_best = c_next;
+        x_best = x;
+        best_iter = i;
+      }
+      if (c_next <= threshold || exhausted) {
+        term = T_CONVERGED;
+        break;
+      }
+      if (std::fabs(c_next - c) <= 1e-15 * c) {
+        if (++stagnant >= cfg.stagnation_window) {
+          term = T_STAGNATION;
+          break;
+        }
+      } else {
+        stagnant = 0;
+      }
+      if (c_next > cfg.growth_tol * c_best && i - best_iter >= cfg.growth_window) {
+        term = T_BREAKDOWN;
+        bd_iter = i;
+        break;
+      }
+      const double mu = c_next / c;
+      c = c_next;
+      for (int64_t k = 0; k < n; ++k) p[(size_t)k] = kf[(size_t)k] + mu * p[(size_t)k];
+    }
+  }
+  const bool keep_last = term == T_CONVERGED;
+  const std::vector<double>& b = keep_last ? x : x_best;
+  std::memcpy(b_out, b.data(), sizeof(double) * n);
+  if (w_out) {  // implied_w(b) = Sigma^-1 (y - X b)
+    CK(cudaMemcpyAsync(h->t, b.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    k_xapply<<<rgrid, NT, 0, s>>>(g, h->X, h->ldx, h->t, h->r);
+    k_ysub<<<rgrid, NT, 0, s>>>(g, h->Y, h->ldy, h->r);
+    h->launches += 2;
+    sigma_inv(h->r, h->su);
+    d2h_mvec(h, w_out, h->su);
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  res->iterations = done;
+  res->termination = term;
+  res->w1_projected = 0;
+  res->breakdown_iteration = bd_iter;
+  res->residual_seminorm = keep_last ? c : c_best;
+  res->n_rows = nrows;
+  res->sigma_scale = g_scale;
+  res->solve_ms = ms;
   API_END((int*)nullptr)
 }
 
