@@ -216,6 +216,8 @@ struct glsgpu_sur {
   double* mvec = nullptr;
   CUtensorMap vmap;
   bool vmap_ok = false;
+  CUtensorMap vmap64;               // 64-row boxes of the same slab (k_kron_mma)
+  bool vmap64_ok = false;
   double *wb[3] = {nullptr, nullptr, nullptr}, *swb[3] = {nullptr, nullptr, nullptr};
   double *r = nullptr, *u = nullptr, *su = nullptr, *pr = nullptr;
   double *t = nullptr, *vs = nullptr, *est = nullptr, *t2 = nullptr, *xtw = nullptr, *zvec = nullptr,
@@ -322,7 +324,14 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
 // the warp-specialised FP64 kernel serves the compute-bound shapes; the generic k_kron the rest
 bool kron_gemm_ok(const glsgpu_sur* h) { return h->G > 128 && h->G <= 256 && h->G % 8 == 0 && h->vmap_ok; }
 
+// the DMMA kernel serves the fused-multiply-add mode (bitwise the same FMA chain as k_kron_ws<true>)
+bool kron_mma_ok(const glsgpu_sur* h) {
+  static const bool off = std::getenv("GLSGPU_NO_DMMA") != nullptr;
+  return !off && kron_gemm_ok(h) && h->kron_fma && h->vmap64_ok;
+}
+
 int kron_grid(const glsgpu_sur* h) {
+  if (kron_mma_ok(h)) return (int)std::min<int64_t>((h->ldm + KM_BM - 1) / KM_BM, 148);
   if (kron_gemm_ok(h)) return (int)std::min<int64_t>(h->ldm / KG_BM, 148);
   const int cpl = kron_cpl(h->G);
   const int tr = 8 * (cpl >= 16 ? 2 : 4);
@@ -336,6 +345,13 @@ void launch_pass_a(glsgpu_sur* h) {
     return;
   }
   const int grid = kron_grid(h);
+  if (kron_mma_ok(h)) {
+    k_kron_mma<<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, h->su,
+                                                      h->partA, h->st, wbuf_of(h), h->msig);
+    if (!h->capturing) h->launches++;
+    CKL("k_kron_mma");
+    return;
+  }
   if (h->kron_fma)
     k_kron_ws<true><<<grid, KW_NT, kw_smem_bytes(), h->s>>>(h->vmap, h->G, h->ldm, h->ldm / KG_BM, h->omegaT, h->u,
                                                             h->su, h->partA, h->st, wbuf_of(h), h->msig);
@@ -497,6 +513,7 @@ void stream_attrs(glsgpu_sur* h) {
   };
   set((const void*)k_kron_ws<false>, 0, 0);
   set((const void*)k_kron_ws<true>, 0, 0);
+  set((const void*)k_kron_mma, 0, 0);
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);
   set((const void*)k_stream<SMODE_C, false>, 0, 0);
@@ -1143,7 +1160,7 @@ glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* om
 // 2-D tensor map over the vector slab: rows = ldm (inner), columns = MV_COUNT * G; boxes of 32 rows x
 // 8 columns (one pass-A element chunk of one vector).  cuTensorMapEncodeTiled comes from the driver
 // through the runtime's entry-point query (no libcuda link).
-bool make_vmap(glsgpu_sur* h) {
+bool make_vmap(glsgpu_sur* h, CUtensorMap* map, int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -1155,9 +1172,9 @@ bool make_vmap(glsgpu_sur* h) {
   }
   const cuuint64_t dims[2] = {(cuuint64_t)h->ldm, (cuuint64_t)MV_COUNT * h->G};
   const cuuint64_t strides[1] = {(cuuint64_t)h->ldm * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)KG_BM, (cuuint32_t)KG_BK};
+  const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)KG_BK};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult rc = encode(&h->vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->mvec, dims, strides, box, estr,
+  const CUresult rc = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->mvec, dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return rc == CUDA_SUCCESS;
@@ -1175,7 +1192,8 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     h->u = h->mvec + MV_U * mv;
     h->su = h->mvec + MV_SU * mv;
     h->pr = h->mvec + MV_PR * mv;
-    h->vmap_ok = make_vmap(h);
+    h->vmap_ok = make_vmap(h, &h->vmap, KG_BM);
+    h->vmap64_ok = make_vmap(h, &h->vmap64, KM_BM);
     h->t = dalloc<double>(h->n);
     h->vs = dalloc<double>(h->n);
     h->est = dalloc<double>(h->n);

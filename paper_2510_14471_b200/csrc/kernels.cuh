@@ -815,6 +815,256 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Pass A on the FP64 tensor cores (128 < G <= 256, G % 8 == 0; kron_fma): the same work as k_kron_ws with
+// the Kronecker product Sigma u = U Omega issued as DMMA (mma.sync m16n8k4 .f64).  A DMMA chains its four
+// products k = 0..3 as fused multiply-adds in ascending k (checked bitwise on this GPU against a sequential
+// fma chain, scripts/micro/dmma_layout.cu), so each output is the p-ascending FMA chain from 0.0 that
+// k_kron_ws<true> computes, with one instruction per 256 FMAs instead of 32.
+//   * 64-row tiles: every vector segment the element warps move is 512 contiguous bytes (32-row tiles, 256-byte
+//     segments, measured 8.1 ms against 7.5 ms at c4).
+//   * U is handed over in 8-column chunks through a ring (KM_UR slots), not as a double-buffered tile: the
+//     math of Omega slab s needs exactly U columns [8 s, 8 s + 8).
+//   * 8 math warps, warp w owns output columns [32 w, 32 w + 32) of the tile: 4 m16 x 4 n8 DMMA blocks,
+//     64 accumulators per lane.  A (U) and B (Omega) fragments come from shared memory with strides of 68 / 260
+//     doubles, which make both fragment loads bank-conflict free.  u . Sigma u reads the tile's u back from
+//     global memory (L2) in the epilogue.
+//   * 1 loader warp streams Omega' in 8-row slabs (one 2 KB bulk copy per row into the padded slab).
+//   * KM_EW element warps: per chunk, 64 x 8 boxes of u, pr, w, sw, su (2-D TMA, KM_ES-stage ring), then per
+//     element the deferred w / sw update (pcg.cpp:151-152), u = pr + mu u (pcg.cpp:210), u.u.
+constexpr int KM_BM = 64;                           // rows per tile
+constexpr int KM_EW = 2;                            // element warps (3 spill the math warps' registers)
+constexpr int KM_NT = (KW_MATH + 1 + KM_EW) * 32;
+constexpr int KM_OK = 8;                            // Omega rows per slab = U columns per chunk
+constexpr int KM_OS = 4;                            // Omega slab stages
+constexpr int KM_OLD = KG_LD + 4;                   // Omega slab row stride (doubles)
+constexpr int KM_XS = KM_BM + 4;                    // U chunk stride per column (doubles)
+constexpr int KM_UC = KM_OK * KM_XS;                // U chunk doubles
+constexpr int KM_UR = 16;                           // U chunk slots
+constexpr int KM_ES = 4;                            // element chunk stages
+constexpr int KM_EC = 5 * KM_OK * KM_BM;            // element chunk doubles: 5 vectors x 8 columns x 64 rows
+constexpr size_t km_smem_bytes() {
+  return (size_t)(KM_UR * KM_UC + KM_OS * KM_OK * KM_OLD + KM_ES * KM_EC) * sizeof(double);
+}
+
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ CUtensorMap vmap64, int G, int64_t ldm,
+                                                       int64_t ntiles, const double* __restrict__ omegaT,
+                                                       double* __restrict__ u_io, double* __restrict__ out,
+                                                       double* partials, const SolveState* st, WBuf wbuf, int64_t msig) {
+  if (!st->active) return;
+  extern __shared__ __align__(128) double ksm[];
+  __shared__ __align__(8) uint64_t om_full[KM_OS], om_empty[KM_OS], el_full[KM_ES], el_empty[KM_ES], uc_full[KM_UR],
+      uc_empty[KM_UR];
+  __shared__ double red[KM_NT / 32][2];
+  double* const ucb = ksm;                                // [KM_UR][KM_OK][KM_XS]
+  double* const omb = ksm + KM_UR * KM_UC;                // [KM_OS][KM_OK][KM_OLD]
+  double* const elb = omb + KM_OS * KM_OK * KM_OLD;       // [KM_ES][5][KM_OK][KM_BM]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nchunk = G / KM_OK;   // chunks (= Omega slabs) per tile
+  const int64_t ntl = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA
+  if (tid == 0) {
+    for (int i = 0; i < KM_OS; ++i) {
+      mbar_init(&om_full[i], 1);
+      mbar_init(&om_empty[i], KW_MATH);
+    }
+    for (int i = 0; i < KM_ES; ++i) {
+      mbar_init(&el_full[i], 1);
+      mbar_init(&el_empty[i], KM_EW);
+    }
+    for (int i = 0; i < KM_UR; ++i) {
+      mbar_init(&uc_full[i], KM_EW);
+      mbar_init(&uc_empty[i], KW_MATH);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  double p_a = 0.0, p_b = 0.0;  // math warps: u . Sigma u; element warps: u . u
+  if (warp == KW_MATH) {
+    // ---------------- Omega loader: slab s = rows [8 s, 8 s + 8) of Omega', one bulk copy per row
+    if (lane == 0) {
+      const uint32_t row_bytes = (uint32_t)(G * sizeof(double));
+      RingPos w;
+      int s = 0;
+      for (int64_t q = 0; q < ntl * nchunk; ++q) {
+        if (q >= KM_OS) mbar_wait(&om_empty[w.slot], w.phase ^ 1u);
+        mbar_expect_tx(&om_full[w.slot], row_bytes * KM_OK);
+        double* dst = omb + w.slot * KM_OK * KM_OLD;
+        const double* src = omegaT + (int64_t)s * KM_OK * G;
+#pragma unroll
+        for (int r = 0; r < KM_OK; ++r) tma_load_1d(dst + r * KM_OLD, src + (int64_t)r * G, row_bytes, &om_full[w.slot]);
+        w.next(KM_OS);
+        if (++s == nchunk) s = 0;
+      }
+    }
+  } else if (warp > KW_MATH) {
+    // ---------------- element warps: element i = (column i / 64, row i % 64) of a chunk, i = etid + 32 KM_EW e
+    const int ew = warp - KW_MATH - 1;
+    const int etid = ew * 32 + lane;
+    const bool upd = st->mu_pending != 0, wupd = st->upd_pending != 0;
+    const double mu = st->mu, lp = st->lam_prev;
+    const int cur = st->cur;
+    const int bu = MV_U * G, bp = MV_PR * G, bw = (MV_W + cur) * G, bsw = (MV_SW + cur) * G, bsu = MV_SU * G;
+    double* __restrict__ wn = wbuf.w[st->nxt];
+    double* __restrict__ swn = wbuf.sw[st->nxt];
+    const uint32_t chunk_bytes = (uint32_t)((1 + (upd ? 1 : 0) + (wupd ? 3 : 0)) * KM_OK * KM_BM * sizeof(double));
+    const int64_t total = ntl * nchunk;
+    const bool issuer = (ew == 0 && lane == 0);
+    RingPos ip;
+    int64_t e_issue = 0, it_tile = blockIdx.x;
+    int it_c0 = 0;
+    auto issue = [&]() {
+      if (e_issue >= KM_ES) mbar_wait(&el_empty[ip.slot], ip.phase ^ 1u);
+      double* E = elb + ip.slot * KM_EC;
+      uint64_t* bar = &el_full[ip.slot];
+      mbar_expect_tx(bar, chunk_bytes);
+      const int row = (int)(it_tile * KM_BM);
+      tma_load_2d(E, &vmap64, row, bu + it_c0, bar);
+      if (upd) tma_load_2d(E + 1 * KM_OK * KM_BM, &vmap64, row, bp + it_c0, bar);
+      if (wupd) {
+        tma_load_2d(E + 2 * KM_OK * KM_BM, &vmap64, row, bw + it_c0, bar);
+        tma_load_2d(E + 3 * KM_OK * KM_BM, &vmap64, row, bsw + it_c0, bar);
+        tma_load_2d(E + 4 * KM_OK * KM_BM, &vmap64, row, bsu + it_c0, bar);
+      }
+      ip.next(KM_ES);
+      ++e_issue;
+      it_c0 += KM_OK;
+      if (it_c0 == G) {
+        it_c0 = 0;
+        it_tile += gridDim.x;
+      }
+    };
+    if (issuer)
+      while (e_issue < KM_ES - 1 && e_issue < total) issue();
+    RingPos cp, up;
+    for (int64_t jl = 0; jl < ntl; ++jl) {
+      const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
+      for (int k = 0; k < nchunk; ++k) {
+        if (issuer && e_issue < total) issue();
+        mbar_wait(&el_full[cp.slot], cp.phase);
+        if (jl * nchunk + k >= KM_UR) mbar_wait(&uc_empty[up.slot], up.phase ^ 1u);
+        const double* E = elb + cp.slot * KM_EC;
+        double* U = ucb + up.slot * KM_UC;
+#pragma unroll
+        for (int e = 0; e < KM_OK * KM_BM / (32 * KM_EW); ++e) {
+          const int i = etid + 32 * KM_EW * e;
+          const int cc = i / KM_BM, rr = i % KM_BM;
+          const int c = k * KM_OK + cc;
+          const int64_t grow = k0 + rr;
+          const int64_t off = (int64_t)c * ldm + grow;
+          const bool in = grow < ldm;
+          const double uo = E[(0 * KM_OK + cc) * KM_BM + rr];
+          if (wupd && in) {
+            stg_cs(wn + off, E[(2 * KM_OK + cc) * KM_BM + rr] + (-lp) * uo);
+            stg_cs(swn + off, E[(3 * KM_OK + cc) * KM_BM + rr] + (-lp) * E[(4 * KM_OK + cc) * KM_BM + rr]);
+          }
+          double v = uo;
+          if (upd) {
+            v = E[(1 * KM_OK + cc) * KM_BM + rr] + mu * uo;
+            if (in) u_io[off] = v;  // read back by the math warps' epilogue (L2)
+          }
+          U[cc * KM_XS + rr] = v;
+          p_b += v * v;
+        }
+        // this warp's reads of the element slot are done; its U chunk writes are published to the math warps
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&el_empty[cp.slot]);
+          mbar_arrive(&uc_full[up.slot]);
+        }
+        cp.next(KM_ES);
+        up.next(KM_UR);
+      }
+    }
+  } else {
+    // ---------------- math warps: DMMA m16n8k4, warp owns columns [32 warp, 32 warp + 32) of every tile
+    const int g = lane >> 2, t = lane & 3;
+    const int n0 = 32 * warp;
+    RingPos rp, up;
+    for (int64_t jl = 0; jl < ntl; ++jl) {
+      const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
+      double acc[4][4][4];  // [m16 tile][n8 tile][fragment]
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
+      for (int s = 0; s < nchunk; ++s) {
+        mbar_wait(&uc_full[up.slot], up.phase);
+        mbar_wait(&om_full[rp.slot], rp.phase);
+        const double* om = omb + rp.slot * KM_OK * KM_OLD + n0 + g;
+        const double* U = ucb + up.slot * KM_UC + t * KM_XS + g;
+#pragma unroll
+        for (int kk = 0; kk < KM_OK / 4; ++kk) {
+          const double* ob = om + (kk * 4 + t) * KM_OLD;
+          const double b0 = ob[0], b1 = ob[8], b2 = ob[16], b3 = ob[24];
+          const double* ua = U + kk * 4 * KM_XS;
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            const double a0 = ua[16 * mi], a1 = ua[16 * mi + 8];
+            dmma_16x8x4(acc[mi][0], a0, a1, b0);
+            dmma_16x8x4(acc[mi][1], a0, a1, b1);
+            dmma_16x8x4(acc[mi][2], a0, a1, b2);
+            dmma_16x8x4(acc[mi][3], a0, a1, b3);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&om_empty[rp.slot]);
+          mbar_arrive(&uc_empty[up.slot]);
+        }
+        rp.next(KM_OS);
+        up.next(KM_UR);
+      }
+      // epilogue: acc[mi][ni] = rows 16 mi + (g, g + 8) x columns n0 + 8 ni + 2 t (+1); rows >= msig carry
+      // zero variance; u . Sigma u with the tile's u from global memory (L2)
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = n0 + 8 * ni + 2 * t + (q & 1);
+            const int64_t grow = k0 + 16 * mi + g + 8 * (q >> 1);
+            if (c < G && grow < ldm) {
+              const double o = grow < msig ? acc[mi][ni][q] : 0.0;
+              const int64_t off = (int64_t)c * ldm + grow;
+              stg_cs(out + off, o);
+              p_a += u_io[off] * o;
+            }
+          }
+    }
+  }
+  // (d, u.u) partials of this CTA, fixed order (pcg.cpp:144-145)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    p_a += __shfl_xor_sync(FULL, p_a, o);
+    p_b += __shfl_xor_sync(FULL, p_b, o);
+  }
+  if (lane == 0) {
+    red[warp][0] = p_a;
+    red[warp][1] = p_b;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, bb = 0.0;
+    for (int w = 0; w < KM_NT / 32; ++w) {
+      a += red[w][0];
+      bb += red[w][1];
+    }
+    partials[blockIdx.x * 3 + 0] = a;
+    partials[blockIdx.x * 3 + 1] = bb;
+    partials[blockIdx.x * 3 + 2] = 0.0;
+  }
+}
+
 enum { SMODE_B = 0, SMODE_C = 1, SMODE_QT_R = 2, SMODE_QT_D = 3, SMODE_QT_V = 4, SMODE_DIAG = 5, SMODE_XS = 6 };
 
 struct StreamArgs {
