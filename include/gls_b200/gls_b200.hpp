@@ -100,6 +100,7 @@ struct PcgConfig {
   int xv_mode = GLSGPU_XV_X;
   int graph_chunk = 0;
   int kron_fma = 0;
+  int sw_mode = 0;  // 1: Sigma w formed where read (glsgpu_pcg_config::sw_mode)
 };
 
 struct PcgTraceRow {
@@ -375,6 +376,7 @@ inline AugSolveResult pcg_aug(const BlockQrOperator& op, const Vector& w1, const
   c.xv_mode = config.xv_mode;
   c.graph_chunk = config.graph_chunk;
   c.kron_fma = config.kron_fma;
+  c.sw_mode = config.sw_mode;
   bool w1_zero = true, z1_zero = true;
   for (double v : w1) w1_zero = w1_zero && v == 0.0;
   for (double v : z1) z1_zero = z1_zero && v == 0.0;

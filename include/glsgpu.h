@@ -87,6 +87,10 @@ typedef struct {
                                 multiply and add, bitwise the reference's operator* (default); 1 = one
                                 fused multiply-add per term (half the FP64 instructions; one rounding per
                                 term instead of two) */
+  int32_t sw_mode;           /* 0 = Sigma w by the reference's recurrence sw -= lambda su (pcg.cpp:152); 1 = Sigma w
+                                formed where it is read (diagnostics rows, the exit's b = X*'(y - Sigma w_sel)):
+                                pass A then moves 3 fewer M x G vectors.  Takes effect with kron_fma on the
+                                DMMA pass A (128 < G <= 256) and diag_every <= 0 */
 } glsgpu_pcg_config;
 
 /* gls::PcgTraceRow (proj/include/gls/pcg.hpp:32-39).  Diagnostics not computed are NaN. */

@@ -236,6 +236,8 @@ struct glsgpu_sur {
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0, graph_xmode = -1, graph_diag = -2, graph_timing = -1, graph_fma = -1;
   int kron_fma = 0;  // glsgpu_pcg_config::kron_fma of the current solve
+  int sw_direct = 0; // sw_mode 1 in effect for the current solve (k_kron_mma path)
+  int graph_sw = -1;
   std::vector<cudaEvent_t> tev;  // timing events captured into the graph
   int64_t graph_kernels = 0;     // kernel nodes in the instantiated graph
   int64_t launches = 0;          // kernels launched by this handle (graph nodes counted per launch)
@@ -1412,6 +1414,7 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   CKL("k_vupdate");
   if (diag >= 0) {
     // est = X*'(y - sw) and the row diagnostics, gated on st->diag_now
+    if (h->sw_direct) launch_kron(h, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 3, h->st, nullptr);
     pass_qt(h, MODE_QT_D, nullptr, h->st, 0, 2);
     reduce_t_global(h, h->t2, h->st, 2);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
@@ -1460,6 +1463,7 @@ void glsgpu_default_config(glsgpu_pcg_config* c) {
   c->graph_chunk = 0;
   c->kernel_timing = 0;
   c->kron_fma = 0;
+  c->sw_mode = 0;
 }
 
 #define API_BEGIN try {
@@ -1722,6 +1726,10 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   hs.nxt = 1;
   hs.mu_pending = 0;
   hs.have_beta = beta_true ? 1 : 0;
+  // sw_mode 1: Sigma w formed where read (k_kron_mma path; diagnostics rows cost a Kronecker pass each, so
+  // only with diag_every <= 0)
+  h->sw_direct = (cfg.sw_mode == 1 && kron_mma_ok(h) && diag <= 0) ? 1 : 0;
+  hs.sw_direct = h->sw_direct;
   CK(cudaMemcpyAsync(h->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
   k_set_t0<<<1, 1, 0, s>>>(h->st);
   if (!h->capturing) h->launches++;
@@ -1816,7 +1824,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   const int timing = cfg.kernel_timing ? 1 : 0;
   const bool need_graph = !h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
                           h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing ||
-                          h->graph_fma != h->kron_fma;
+                          h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct;
   if (need_graph) {
     if (h->graph) {
       CK(cudaGraphExecDestroy(h->graph));
@@ -1854,6 +1862,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     h->graph_diag = diag >= 0 ? 1 : -1;
     h->graph_timing = timing;
     h->graph_fma = h->kron_fma;
+    h->graph_sw = h->sw_direct;
   }
   std::vector<double> kt_ms(3, 0.0);
   std::vector<int64_t> kt_n(3, 0);
@@ -1898,6 +1907,10 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   SolveState fin = *h->st_host;
+  if (h->sw_direct) {  // Sigma w_sel for the recovery b = X*'(y - Sigma w_sel)
+    const int sel = fin.term == T_CONVERGED ? fin.cur : fin.best;
+    launch_kron(h, h->wb[sel], nullptr, nullptr, nullptr, h->swb[sel], h->partA, 0, nullptr, nullptr);
+  }
 
   // exit: b = X*'(y - sw_sel), sel = last if Converged else best (pcg.cpp:215-228)
   {
@@ -1964,7 +1977,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     const double M = (double)h->M, G = (double)h->G, n = (double)h->n;
     // pass A: reads pr, u, su, w, sw; writes u, su, w, sw (the deferred update of pcg.cpp:151-152)
     // pass B: reads Q (+ X in xv_mode X), su, r; writes r.   pass C: reads Q, r; writes pr.
-    const double bA = 8.0 * 9.0 * M * G;
+    const double bA = 8.0 * (h->sw_direct ? 6.0 : 9.0) * M * G;  // sw_mode 1: no sw / su(old) read, no sw write
     const double bB = 8.0 * (M * n * (xv_mode == GLSGPU_XV_X ? 2.0 : 1.0) + 3.0 * M * G);
     const double bC = 8.0 * (M * n + 2.0 * M * G);
     const char* names[3] = {"passA_kron", "passB_update_qtr", "passC_pi"};

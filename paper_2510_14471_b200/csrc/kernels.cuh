@@ -56,7 +56,9 @@ struct SolveState {
   // w_{i+1} = w_i - lambda_i u_i and sw_{i+1} = sw_i - lambda_i su_i (pcg.cpp:151-152) are deferred
   // to the next pass A (compute-bound, so their traffic is free there): upd_pending marks them
   int32_t upd_pending;
-  int32_t pad[1];
+  // sw_mode 1 (k_kron_mma only): Sigma w is not carried by the recurrence sw -= lambda su (pcg.cpp:152) but
+  // formed as Sigma w where it is read -- on trace-diagnostic rows and at the exit (b = X*'(y - Sigma w_sel))
+  int32_t sw_direct;
 };
 
 struct TraceRowD {
@@ -139,7 +141,13 @@ __global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles,
                                              const double* src, const double* pr, const double* div, double* u_io,
                                              double* out, double* partials, int in_mode, const SolveState* st,
                                              WBuf wbuf, int64_t msig) {
-  if (st && !st->active) return;
+  if (st && in_mode != 3 && !st->active) return;
+  if (in_mode == 3) {  // Sigma w_cur into sw_cur on a diagnostics row (sw_mode 1; the last row comes after the stop)
+    if (!st->diag_now) return;
+    src = wbuf.w[st->cur];
+    out = wbuf.sw[st->cur];
+    partials = nullptr;
+  }
   extern __shared__ double xs[];  // [G][TR]
   constexpr int TR = 8 * RW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -912,7 +920,9 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     const int bu = MV_U * G, bp = MV_PR * G, bw = (MV_W + cur) * G, bsw = (MV_SW + cur) * G, bsu = MV_SU * G;
     double* __restrict__ wn = wbuf.w[st->nxt];
     double* __restrict__ swn = wbuf.sw[st->nxt];
-    const uint32_t chunk_bytes = (uint32_t)((1 + (upd ? 1 : 0) + (wupd ? 3 : 0)) * KM_OK * KM_BM * sizeof(double));
+    const bool swd = st->sw_direct != 0;  // no sw recurrence: w alone is updated
+    const uint32_t chunk_bytes =
+        (uint32_t)((1 + (upd ? 1 : 0) + (wupd ? (swd ? 1 : 3) : 0)) * KM_OK * KM_BM * sizeof(double));
     const int64_t total = ntl * nchunk;
     const bool issuer = (ew == 0 && lane == 0);
     RingPos ip;
@@ -928,8 +938,10 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
       if (upd) tma_load_2d(E + 1 * KM_OK * KM_BM, &vmap64, row, bp + it_c0, bar);
       if (wupd) {
         tma_load_2d(E + 2 * KM_OK * KM_BM, &vmap64, row, bw + it_c0, bar);
-        tma_load_2d(E + 3 * KM_OK * KM_BM, &vmap64, row, bsw + it_c0, bar);
-        tma_load_2d(E + 4 * KM_OK * KM_BM, &vmap64, row, bsu + it_c0, bar);
+        if (!swd) {
+          tma_load_2d(E + 3 * KM_OK * KM_BM, &vmap64, row, bsw + it_c0, bar);
+          tma_load_2d(E + 4 * KM_OK * KM_BM, &vmap64, row, bsu + it_c0, bar);
+        }
       }
       ip.next(KM_ES);
       ++e_issue;
@@ -961,7 +973,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
           const double uo = E[(0 * KM_OK + cc) * KM_BM + rr];
           if (wupd && in) {
             stg_cs(wn + off, E[(2 * KM_OK + cc) * KM_BM + rr] + (-lp) * uo);
-            stg_cs(swn + off, E[(3 * KM_OK + cc) * KM_BM + rr] + (-lp) * E[(4 * KM_OK + cc) * KM_BM + rr]);
+            if (!swd) stg_cs(swn + off, E[(3 * KM_OK + cc) * KM_BM + rr] + (-lp) * E[(4 * KM_OK + cc) * KM_BM + rr]);
           }
           double v = uo;
           if (upd) {

@@ -261,6 +261,36 @@ def test_kron_fma_parity(name, mk, fma):
     assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
 
 
+@pytest.mark.parametrize("name,mk", KRON_FMA_CASES, ids=[c[0] for c in KRON_FMA_CASES])
+@pytest.mark.parametrize("diag", [0, -1])
+def test_sw_direct_parity(name, mk, diag):
+    """sw_mode 1 (the bench's setting): Sigma w is formed where it is read -- the final row's diagnostics and
+    the exit's b = X*'(y - Sigma w_sel) -- instead of carried by the recurrence of pcg.cpp:152.  The iterates do
+    not depend on Sigma w, so the iteration count is the recurrence run's; b differs only by the recurrence's
+    accumulated rounding (b to 1e-10 against the oracle)."""
+    p = mk()
+    o = oracle.solve(p, "oracle", cfg=oracle.make_config(tol_rel=p.tol_rel, max_iter=p.max_iter), beta_true=p.beta)
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur)
+    runs = {}
+    for sw in (0, 1):
+        runs[sw] = api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=p.max_iter, xv_mode="qr",
+                                                             diag_every=diag, kron_fma=True, sw_mode=sw),
+                               true_beta=p.beta)
+    for sw, g in runs.items():
+        s = g.solution
+        assert s.termination.name == o.termination
+        assert s.iterations == o.iterations, (sw, s.iterations, o.iterations)
+        assert rel(s.b, o.b) <= B_TOL, (sw, rel(s.b, o.b))
+        assert rel(s.w, o.w) <= 1e-9
+    # the c sequence does not see Sigma w at all: bitwise between the two modes
+    assert np.array_equal(runs[0].trace.rows["c"], runs[1].trace.rows["c"])
+    if diag == 0:  # the final row's diagnostics, from Sigma w formed directly
+        a, b = runs[0].trace.rows[-1], runs[1].trace.rows[-1]
+        # a difference of nearly equal m-vectors at convergence: compare on the scale of y
+        assert abs(a["aug_residual_norm"] - b["aug_residual_norm"]) <= 1e-12 * np.linalg.norm(p.Y)
+
+
 def test_counters_match_reference():
     """CostCounters after pcg_aug equal the reference's own tallies (preconditioner.cpp:9-47)."""
     if not oracle.have("ref"):
