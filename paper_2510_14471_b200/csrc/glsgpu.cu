@@ -197,6 +197,7 @@ struct glsgpu_sur {
     int64_t max_rows;
     bool any_global;
     int64_t ffirst = 0, fcount = 0;  // register-resident item range (n <= 32, rows <= 256)
+    std::vector<int64_t> fblock;     // [G + 1]: fast items of block b are [ffirst + fblock[b], ffirst + fblock[b + 1])
   };
   std::vector<Level> qr_levels;
   QrItem* d_items = nullptr;
@@ -789,7 +790,9 @@ void build_qr_plan(glsgpu_sur* h) {
     glsgpu_sur::Level L{0, 0, 0, 0, false};
     std::vector<QrItem> fast;
     const int64_t first = (int64_t)items.size();
+    L.fblock.assign((size_t)h->G + 1, 0);
     for (int b = 0; b < h->G; ++b) {
+      L.fblock[(size_t)b] = (int64_t)fast.size();
       const BT& t = trees[b];
       if ((int)t.rows.size() <= lvl) continue;
       const int n = h->nb[b];
@@ -867,6 +870,7 @@ void build_qr_plan(glsgpu_sur* h) {
         items.push_back(it);
       }
     }
+    L.fblock[(size_t)h->G] = (int64_t)fast.size();
     L.first = first;
     L.count = (int64_t)items.size() - first;
     L.ffirst = (int64_t)items.size();
@@ -927,6 +931,86 @@ void launch_formq(glsgpu_sur* h, int64_t max_rows, int grid, int smem, const QrI
   }
   if (!h->capturing) h->launches++;
   CKL("k_qr_formq");
+}
+
+// The TSQR of blocks [b0, b1) only, every level, when every item is a lane-per-column leaf (narrow blocks):
+// lets glsgpu_sur_create factor one group of blocks while the next group's columns are still in flight.
+bool qr_groupable(const glsgpu_sur* h) {
+  if (h->coll || !qr_lc()) return false;
+  for (const auto& L : h->qr_levels)
+    if (L.count) return false;
+  return true;
+}
+
+void run_qr_blocks(glsgpu_sur* h, int b0, int b1, int lc_grid_f, int lc_grid_q) {
+  const int nl = (int)h->qr_levels.size();
+  for (int l = 0; l < nl; ++l) {
+    const auto& L = h->qr_levels[l];
+    const int64_t f0 = L.fblock[(size_t)b0], cnt = L.fblock[(size_t)b1] - f0;
+    if (cnt <= 0) continue;
+    k_qr_factor_lc<<<(int)std::min<int64_t>(cnt, lc_grid_f), QRC_NT, qrc_smem_bytes(), h->s>>>(
+        h->d_items + L.ffirst + f0, (int)cnt);
+    if (!h->capturing) h->launches++;
+    CKL("k_qr_factor_lc group");
+  }
+  for (int l = nl - 1; l >= 0; --l) {
+    const auto& L = h->qr_levels[l];
+    const int64_t f0 = L.fblock[(size_t)b0], cnt = L.fblock[(size_t)b1] - f0;
+    if (cnt <= 0) continue;
+    k_qr_formq_lc<<<(int)std::min<int64_t>(cnt, lc_grid_q), QRC_NT, qrc_smem_bytes(), h->s>>>(
+        h->d_items + L.ffirst + f0, (int)cnt);
+    if (!h->capturing) h->launches++;
+    CKL("k_qr_formq_lc group");
+  }
+}
+
+void rank_check(glsgpu_sur* h);
+
+// group-pipelined setup from host X: group g's columns go up on a copy stream while the solver stream
+// factors group g - 1 (the whole TSQR tree of its blocks), so the QR hides under the host-to-device copy
+void upload_and_qr_pipelined(glsgpu_sur* h, const double* X_host, int groups) {
+  CK(cudaFuncSetAttribute(k_qr_factor_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
+  CK(cudaFuncSetAttribute(k_qr_formq_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
+  int occ_f = 1, occ_q = 1, nsm = 148;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_qr_factor_lc, QRC_NT, qrc_smem_bytes()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, k_qr_formq_lc, QRC_NT, qrc_smem_bytes()));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));
+  cudaStream_t cs = nullptr;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev((size_t)groups, nullptr);
+  try {
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t ready;  // the padding-row memsets on h->s precede every column copy
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, h->s));
+    CK(cudaStreamWaitEvent(cs, ready, 0));
+    const int G = h->G;
+    for (int g = 0; g < groups; ++g) {
+      const int b0 = (int)((int64_t)g * G / groups), b1 = (int)((int64_t)(g + 1) * G / groups);
+      const int64_t c0 = h->p0[(size_t)b0], c1 = b1 < G ? h->p0[(size_t)b1] : h->n;
+      if (c1 > c0)
+        CK(cudaMemcpy2DAsync(h->X_own + c0 * h->ldm, h->ldm * sizeof(double), X_host + c0 * h->M, h->M * sizeof(double),
+                             h->M * sizeof(double), (size_t)(c1 - c0), cudaMemcpyHostToDevice, cs));
+      CK(cudaEventRecord(ev[(size_t)g], cs));
+    }
+    for (int g = 0; g < groups; ++g) {
+      const int b0 = (int)((int64_t)g * G / groups), b1 = (int)((int64_t)(g + 1) * G / groups);
+      CK(cudaStreamWaitEvent(h->s, ev[(size_t)g], 0));
+      run_qr_blocks(h, b0, b1, std::max(1, occ_f) * nsm, std::max(1, occ_q) * nsm);
+    }
+    CK(cudaStreamSynchronize(h->s));
+    cudaEventDestroy(ready);
+  } catch (...) {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    cudaStreamSynchronize(cs);
+    cudaStreamDestroy(cs);
+    throw;
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  cudaStreamDestroy(cs);
+  rank_check(h);
 }
 
 void run_qr(glsgpu_sur* h) {
@@ -1002,6 +1086,10 @@ void run_qr(glsgpu_sur* h) {
       CKL("k_qr_formq_reg");
     }
   }
+  rank_check(h);
+}
+
+void rank_check(glsgpu_sur* h) {
   Geo g = geo_of(h);
   k_rank_check<<<(h->G + 127) / 128, 128, 0, h->s>>>(g, h->R, h->d_rank_flags);
   if (!h->capturing) h->launches++;
@@ -1489,10 +1577,9 @@ int glsgpu_sur_create(int G, int64_t M, const int64_t* n_i, const double* X, con
   try {
     h->X_own = dalloc<double>((size_t)(h->ldm * h->n));
     h->Y_own = dalloc<double>((size_t)(h->ldm * G));
-    CK(cudaMemsetAsync(h->X_own, 0, sizeof(double) * h->ldm * h->n, h->s));
+    if (h->ldm > M)  // padding rows only: the copies write rows [0, M)
+      CK(cudaMemset2DAsync(h->X_own + M, h->ldm * sizeof(double), 0, (h->ldm - M) * sizeof(double), h->n, h->s));
     CK(cudaMemsetAsync(h->Y_own, 0, sizeof(double) * h->ldm * G, h->s));
-    CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
-                         cudaMemcpyHostToDevice, h->s));
     CK(cudaMemcpy2DAsync(h->Y_own, h->ldm * sizeof(double), Y, M * sizeof(double), M * sizeof(double), G,
                          cudaMemcpyHostToDevice, h->s));
     h->X = h->X_own;
@@ -1500,7 +1587,14 @@ int glsgpu_sur_create(int G, int64_t M, const int64_t* n_i, const double* X, con
     h->Y = h->Y_own;
     h->ldy = h->ldm;
     alloc_common(h);
-    run_qr(h);
+    static const bool no_overlap = std::getenv("GLSGPU_NO_OVERLAP") != nullptr;
+    if (!no_overlap && qr_groupable(h) && G >= 2) {
+      upload_and_qr_pipelined(h, X, std::min(G, 8));
+    } else {
+      CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
+                           cudaMemcpyHostToDevice, h->s));
+      run_qr(h);
+    }
   } catch (...) {
     destroy_impl(h);
     throw;
