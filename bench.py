@@ -354,10 +354,14 @@ def run_ours(args):
                 op2.close()
                 del Xd, Yd
             else:
-                sur = api.SurModel(X=Xh.numpy().T, nb=nb, y=Yh.numpy().T, sigma0=omega)
-                op2 = api.GpuSurPreconditioner(sur, device=dev)
+                # create once (step 0, untimed warm-up), then per step: new host data through the C-ABI
+                # (glsgpu_sur_update: H2D of X and Y pipelined with the TSQR), the solve, b back to the host
+                if s == 0:
+                    sur = api.SurModel(X=Xh.numpy().T, nb=nb, y=Yh.numpy().T, sigma0=omega)
+                    op2 = api.GpuSurPreconditioner(sur, device=dev)
+                else:
+                    op2.update(Xh.numpy().T, Yh.numpy().T)
                 r2 = api.pcg_aug(sur, op2, config=ecfg, want_w=False)
-                op2.close()
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if world > 1:
@@ -367,9 +371,12 @@ def run_ours(args):
             if s > 0:  # first e2e step is a warm-up (allocator / context)
                 e_iters += r2.solution.iterations
                 e_time += dt
+        if world == 1:
+            op2.close()
         e2e = {"value": e_iters / e_time, "unit": UNIT, "h2d_bytes_per_step": int(8 * (M * n + M * G)),
                "d2h_bytes_per_step": int(8 * n + 48 * (r2.trace.rows.size)), "steps": ksteps,
-               "timer": "host wall clock (max over ranks) around create(H2D + QR) + solve + b D2H + destroy"}
+               "timer": ("host wall clock (max over ranks) around: H2D of the step's X and Y from pinned memory "
+                         "pipelined with the TSQR (glsgpu_sur_update; 1 GPU) or create (N > 1) + solve + b D2H")}
         del Xh, Yh
 
     cpu = None

@@ -151,6 +151,10 @@ int glsgpu_sur_create_device(int G, int64_t M, const int64_t* n_i, const double*
                              const double* Y_dev, int64_t ldy, const double* omega, const double* block_scale,
                              int device, glsgpu_sur** out, int* bad_block);
 
+/* New X (M x n) and Y (M x G) from HOST buffers for a handle made by glsgpu_sur_create (same shapes): upload and
+ * refactor, reusing the handle's device memory and TSQR plan (create once, solve many). */
+int glsgpu_sur_update(glsgpu_sur* h, const double* X, const double* Y, int* bad_block);
+
 /* Re-run the setup QR from the resident X (the per-solve setup cost; bench steps time it). */
 int glsgpu_sur_refactor(glsgpu_sur* h, int* bad_block);
 

@@ -52,7 +52,7 @@ EXPORTS = [
     "glsgpu_operator_norm_probe", "glsgpu_counters", "glsgpu_reset_apply_counters", "glsgpu_sur_solve",
     "glsgpu_default_config", "glsgpu_kernel_stats", "glsgpu_launch_count", "glsgpu_get_factors", "glsgpu_synth_normal",
     "glsgpu_synth_response", "glsgpu_nccl_unique_id", "glsgpu_sur_create_sharded", "glsgpu_sur_shard",
-    "glsgpu_mvrglm_create", "glsgpu_mv_reduce", "glsgpu_model_dims", "glsgpu_sur_reduce", "glsgpu_pcg_ne",
+    "glsgpu_mvrglm_create", "glsgpu_mv_reduce", "glsgpu_model_dims", "glsgpu_sur_reduce", "glsgpu_pcg_ne", "glsgpu_sur_update",
 ]
 
 _lib = None
@@ -75,6 +75,7 @@ def load() -> C.CDLL:
     L.glsgpu_sur_create_device.argtypes = [C.c_int, C.c_int64, _PI64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                            _P, _P, C.c_int, C.POINTER(H), C.POINTER(C.c_int)]
     L.glsgpu_sur_refactor.argtypes = [H, C.POINTER(C.c_int)]
+    L.glsgpu_sur_update.argtypes = [H, _P, _P, C.POINTER(C.c_int)]
     L.glsgpu_sur_destroy.argtypes = [H]
     L.glsgpu_sur_dims.argtypes = [H, C.POINTER(C.c_int), _PI64, _PI64]
     L.glsgpu_sur_stream.argtypes = [H]

@@ -337,6 +337,16 @@ class GpuSurPreconditioner:
         _check(self._lib.glsgpu_get_factors(self._h, _dp(Q), _dp(R)), self._lib)
         return Q, R
 
+    def update(self, X: np.ndarray, y: np.ndarray):
+        """New data of the same shapes (glsgpu_sur_update): upload X (M x n) and Y (M x G), refactor; the device
+        memory and the TSQR plan of this operator are reused."""
+        Xf = np.asfortranarray(X, dtype=np.float64)
+        Yf = np.asfortranarray(y, dtype=np.float64)
+        if Xf.shape != (self.m // len(self._nb), self.n) or Yf.shape != (self.m // len(self._nb), len(self._nb)):
+            raise DimensionMismatch("update: shapes differ from the operator's")
+        bad = C.c_int(-1)
+        _check(self._lib.glsgpu_sur_update(self._h, _dp(Xf), _dp(Yf), C.byref(bad)), self._lib)
+
     def refactor(self):
         bad = C.c_int(-1)
         _check(self._lib.glsgpu_sur_refactor(self._h, C.byref(bad)), self._lib)

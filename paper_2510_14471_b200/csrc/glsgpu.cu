@@ -1573,6 +1573,12 @@ int glsgpu_sur_create(int G, int64_t M, const int64_t* n_i, const double* X, con
   API_BEGIN
   if (!out || !X || !Y) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create: null argument");
   *out = nullptr;
+  static const bool trace = std::getenv("GLSGPU_TRACE_CREATE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  const auto t0 = now();
   glsgpu_sur* h = create_common(G, M, n_i, omega, block_scale, device);
   try {
     h->X_own = dalloc<double>((size_t)(h->ldm * h->n));
@@ -1587,19 +1593,47 @@ int glsgpu_sur_create(int G, int64_t M, const int64_t* n_i, const double* X, con
     h->Y = h->Y_own;
     h->ldy = h->ldm;
     alloc_common(h);
+    CK(cudaStreamSynchronize(h->s));
+    const auto t1 = now();
     static const bool no_overlap = std::getenv("GLSGPU_NO_OVERLAP") != nullptr;
-    if (!no_overlap && qr_groupable(h) && G >= 2) {
+    const bool piped = !no_overlap && qr_groupable(h) && G >= 2;
+    if (piped) {
       upload_and_qr_pipelined(h, X, std::min(G, 8));
     } else {
       CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
                            cudaMemcpyHostToDevice, h->s));
       run_qr(h);
     }
+    if (trace)
+      std::fprintf(stderr, "glsgpu_sur_create: allocate + plan %.1f ms, upload + QR %.1f ms (%s)\n", ms(t0, t1),
+                   ms(t1, now()), piped ? "pipelined" : "serial");
   } catch (...) {
     destroy_impl(h);
     throw;
   }
   *out = h;
+  API_END(bad_block)
+}
+
+// New data for an existing host-created SUR handle (same G, M, widths): upload X and Y and refactor, reusing
+// every allocation and the TSQR plan -- the per-solve cost of a "create once, solve many" caller.
+int glsgpu_sur_update(glsgpu_sur* h, const double* X, const double* Y, int* bad_block) {
+  API_BEGIN
+  if (!h || !X || !Y) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_update: null argument");
+  if (!h->X_own || h->mv || h->coll) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu_sur_update: needs a glsgpu_sur_create handle");
+  CK(cudaSetDevice(h->dev));
+  const int64_t M = h->M;
+  CK(cudaMemcpy2DAsync(h->Y_own, h->ldm * sizeof(double), Y, M * sizeof(double), M * sizeof(double), h->G,
+                       cudaMemcpyHostToDevice, h->s));
+  static const bool no_overlap = std::getenv("GLSGPU_NO_OVERLAP") != nullptr;
+  if (!no_overlap && qr_groupable(h) && h->G >= 2) {
+    upload_and_qr_pipelined(h, X, std::min(h->G, 8));
+  } else {
+    CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
+                         cudaMemcpyHostToDevice, h->s));
+    run_qr(h);
+  }
+  h->frob_x = -1.0;  // |X|_F of the new X (w1 projection) is recomputed on demand
   API_END(bad_block)
 }
 

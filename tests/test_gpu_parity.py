@@ -381,3 +381,19 @@ def test_device_synth_is_shard_invariant():
     assert torch.equal(torch.cat(parts, dim=1), full)
     v = full.cpu().numpy().ravel()
     assert abs(v.mean()) < 0.1 and abs(v.std() - 1.0) < 0.05
+
+
+def test_update_matches_fresh_create():
+    """glsgpu_sur_update (new data, same shapes; pipelined upload + TSQR) solves exactly as a fresh handle."""
+    p1 = synth.make_problem(4, M=700, G=24)
+    p2 = synth.make_problem(4, M=700, G=24, seed=77)
+    cfg = api.PcgConfig(tol_rel=1e-10, max_iter=200, xv_mode="qr", diag_every=0)
+    op = api.sur_preconditioner(api.sur_from_problem(p1))
+    api.pcg_aug(None, op, config=cfg)
+    op.update(p2.X, p2.Y)
+    g_upd = api.pcg_aug(None, op, config=cfg)
+    g_new = api.pcg_aug(api.sur_from_problem(p2), config=cfg)
+    assert g_upd.solution.iterations == g_new.solution.iterations
+    assert np.array_equal(g_upd.solution.b, g_new.solution.b)
+    with pytest.raises(api.DimensionMismatch):
+        op.update(p2.X[:, :-1], p2.Y)
