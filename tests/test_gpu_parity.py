@@ -387,6 +387,7 @@ def test_update_matches_fresh_create():
     """glsgpu_sur_update (new data, same shapes; pipelined upload + TSQR) solves exactly as a fresh handle."""
     p1 = synth.make_problem(4, M=700, G=24)
     p2 = synth.make_problem(4, M=700, G=24, seed=77)
+    p2.omega = p1.omega  # update replaces X and Y; Omega stays the handle's
     cfg = api.PcgConfig(tol_rel=1e-10, max_iter=200, xv_mode="qr", diag_every=0)
     op = api.sur_preconditioner(api.sur_from_problem(p1))
     api.pcg_aug(None, op, config=cfg)
