@@ -350,7 +350,7 @@ void launch_pass_a(glsgpu_sur* h) {
   const int grid = kron_grid(h);
   if (kron_mma_ok(h)) {
     k_kron_mma<<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, h->su,
-                                                      h->partA, h->st, wbuf_of(h), h->msig);
+                                                      h->partA, h->st, wbuf_of(h), h->msig, -1);
     if (!h->capturing) h->launches++;
     CKL("k_kron_mma");
     return;
@@ -363,6 +363,19 @@ void launch_pass_a(glsgpu_sur* h) {
                                                              h->su, h->partA, h->st, wbuf_of(h), h->msig);
   if (!h->capturing) h->launches++;
   CKL("k_kron_ws");
+}
+
+// Sigma x on the tensor-core kernel for a vector of the slab (column block `blk`, e.g. MV_W + k for w[k]), or
+// (blk == -2) Sigma w_cur into sw_cur gated on the diagnostics row; false when that kernel does not serve
+bool kron_mma_apply(glsgpu_sur* h, int blk, double* out) {
+  // fused multiply-adds: only where the solve runs kron_fma (exact mode keeps the reference's mul / add sums)
+  if (!(kron_gemm_ok(h) && h->vmap64_ok && h->kron_fma) || std::getenv("GLSGPU_NO_DMMA")) return false;
+  const int grid = (int)std::min<int64_t>((h->ldm + KM_BM - 1) / KM_BM, 148);
+  k_kron_mma<<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT,
+                                                    h->u, out, nullptr, h->st, wbuf_of(h), h->msig, blk);
+  if (!h->capturing) h->launches++;
+  CKL("k_kron_mma apply");
+  return true;
 }
 
 int rowpass_grid(const glsgpu_sur* h) { return (int)std::min<int64_t>((int64_t)h->G * h->nch, GRID_CAP); }
@@ -1502,7 +1515,8 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   CKL("k_vupdate");
   if (diag >= 0) {
     // est = X*'(y - sw) and the row diagnostics, gated on st->diag_now
-    if (h->sw_direct) launch_kron(h, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 3, h->st, nullptr);
+    if (h->sw_direct && !kron_mma_apply(h, -2, nullptr))
+      launch_kron(h, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 3, h->st, nullptr);
     pass_qt(h, MODE_QT_D, nullptr, h->st, 0, 2);
     reduce_t_global(h, h->t2, h->st, 2);
     k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
@@ -1909,8 +1923,9 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   else CK(cudaMemsetAsync(h->zvec, 0, sizeof(double) * h->n, s));
   if (beta_true) CK(cudaMemcpyAsync(h->beta_d, beta_true, sizeof(double) * h->n, cudaMemcpyHostToDevice, s));
 
-  // sw = Sigma w; r = (sw + X z) - y; pr = Pi r; c
-  launch_kron(h, h->wb[0], nullptr, nullptr, nullptr, h->swb[0], h->partA, 0, nullptr, nullptr);
+  // sw = Sigma w (zero for w1 = 0: swb[0] was cleared above); r = (sw + X z) - y; pr = Pi r; c
+  if (w1 && !kron_mma_apply(h, MV_W + 0, h->swb[0]))
+    launch_kron(h, h->wb[0], nullptr, nullptr, nullptr, h->swb[0], h->partA, 0, nullptr, nullptr);
   {
     dim3 grid((unsigned)std::min<int64_t>((h->ldm + NT - 1) / NT, 64), (unsigned)h->G);
     k_init_residual<<<grid, NT, 0, s>>>(g, h->X, h->ldx, h->zvec, h->swb[0], h->Y, h->ldy, h->r);
@@ -2037,7 +2052,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   SolveState fin = *h->st_host;
   if (h->sw_direct) {  // Sigma w_sel for the recovery b = X*'(y - Sigma w_sel)
     const int sel = fin.term == T_CONVERGED ? fin.cur : fin.best;
-    launch_kron(h, h->wb[sel], nullptr, nullptr, nullptr, h->swb[sel], h->partA, 0, nullptr, nullptr);
+    if (!kron_mma_apply(h, MV_W + sel, h->swb[sel]))
+      launch_kron(h, h->wb[sel], nullptr, nullptr, nullptr, h->swb[sel], h->partA, 0, nullptr, nullptr);
   }
 
   // exit: b = X*'(y - sw_sel), sel = last if Converged else best (pcg.cpp:215-228)
