@@ -349,8 +349,9 @@ void launch_pass_a(glsgpu_sur* h) {
   }
   const int grid = kron_grid(h);
   if (kron_mma_ok(h)) {
-    k_kron_mma<<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, h->su,
-                                                      h->partA, h->st, wbuf_of(h), h->msig, -1);
+    k_kron_mma<false><<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM,
+                                                             h->omegaT, h->u, h->su, h->partA, h->st, wbuf_of(h),
+                                                             h->msig, -1);
     if (!h->capturing) h->launches++;
     CKL("k_kron_mma");
     return;
@@ -371,8 +372,8 @@ bool kron_mma_apply(glsgpu_sur* h, int blk, double* out) {
   // fused multiply-adds: only where the solve runs kron_fma (exact mode keeps the reference's mul / add sums)
   if (!(kron_gemm_ok(h) && h->vmap64_ok && h->kron_fma) || std::getenv("GLSGPU_NO_DMMA")) return false;
   const int grid = (int)std::min<int64_t>((h->ldm + KM_BM - 1) / KM_BM, 148);
-  k_kron_mma<<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT,
-                                                    h->u, out, nullptr, h->st, wbuf_of(h), h->msig, blk);
+  k_kron_mma<true><<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM,
+                                                          h->omegaT, h->u, out, nullptr, h->st, wbuf_of(h), h->msig, blk);
   if (!h->capturing) h->launches++;
   CKL("k_kron_mma apply");
   return true;
@@ -529,7 +530,8 @@ void stream_attrs(glsgpu_sur* h) {
   };
   set((const void*)k_kron_ws<false>, 0, 0);
   set((const void*)k_kron_ws<true>, 0, 0);
-  set((const void*)k_kron_mma, 0, 0);
+  set((const void*)k_kron_mma<false>, 0, 0);
+  set((const void*)k_kron_mma<true>, 0, 0);
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);
   set((const void*)k_stream<SMODE_C, false>, 0, 0);

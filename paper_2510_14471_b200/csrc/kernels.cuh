@@ -861,15 +861,16 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
                : "d"(a0), "d"(a1), "d"(b0));
 }
 
+template <bool APPLY>
 __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ CUtensorMap vmap64, int G, int64_t ldm,
                                                        int64_t ntiles, const double* __restrict__ omegaT,
                                                        double* __restrict__ u_io, double* __restrict__ out,
                                                        double* partials, const SolveState* st, WBuf wbuf, int64_t msig,
                                                        int plain) {
-  // plain == -1: pass A.  plain >= 0: out = Sigma x for x = column block `plain` of the vector slab (no updates,
-  // no partials).  plain == -2: the same for x = w_cur into sw_cur on a diagnostics row (sw_mode 1).
-  if (plain == -1 && !st->active) return;
-  if (plain == -2) {
+  // APPLY = false: pass A (plain ignored).  APPLY: out = Sigma x, no updates, no partials, for x = column block
+  // `plain` of the vector slab, or (plain == -2) x = w_cur into sw_cur on a diagnostics row (sw_mode 1).
+  if (!APPLY && !st->active) return;
+  if (APPLY && plain == -2) {
     if (!st->diag_now) return;
     out = wbuf.sw[st->cur];
   }
@@ -921,10 +922,10 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     // ---------------- element warps: element i = (column i / 64, row i % 64) of a chunk, i = etid + 32 KM_EW e
     const int ew = warp - KW_MATH - 1;
     const int etid = ew * 32 + lane;
-    const bool upd = plain == -1 && st->mu_pending != 0, wupd = plain == -1 && st->upd_pending != 0;
+    const bool upd = !APPLY && st->mu_pending != 0, wupd = !APPLY && st->upd_pending != 0;
     const double mu = st->mu, lp = st->lam_prev;
     const int cur = st->cur;
-    const int bu = plain == -1 ? MV_U * G : (plain == -2 ? (MV_W + cur) * G : plain * G);
+    const int bu = !APPLY ? MV_U * G : (plain == -2 ? (MV_W + cur) * G : plain * G);
     const int bp = MV_PR * G, bw = (MV_W + cur) * G, bsw = (MV_SW + cur) * G, bsu = MV_SU * G;
     double* __restrict__ wn = wbuf.w[st->nxt];
     double* __restrict__ swn = wbuf.sw[st->nxt];
@@ -1057,7 +1058,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
               const double o = grow < msig ? acc[mi][ni][q] : 0.0;
               const int64_t off = (int64_t)c * ldm + grow;
               stg_cs(out + off, o);
-              if (plain == -1) p_a += u_io[off] * o;
+              if (!APPLY) p_a += u_io[off] * o;
             }
           }
     }
@@ -1073,7 +1074,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     red[warp][1] = p_b;
   }
   __syncthreads();
-  if (tid == 0 && plain == -1) {
+  if (tid == 0 && !APPLY) {
     double a = 0.0, bb = 0.0;
     for (int w = 0; w < KM_NT / 32; ++w) {
       a += red[w][0];
