@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--rows", type=int, default=0, help="override M (development only)")
     ap.add_argument("--xv", default="qr", choices=["qr", "x"])
+    ap.add_argument("--fused", default="off", choices=["on", "off"],
+                    help="Sigma pr inside pass C with an element-wise pass A (fused_c; needs --sw direct; parity-tested, "
+                         "slower at c4 -- DESIGN.md s10)")
     ap.add_argument("--sw", default="direct", choices=["direct", "recurrence"],
                     help="Sigma w: formed where read (sw_mode 1) or the reference's recurrence; both parity-tested")
     ap.add_argument("--kron", default="fma", choices=["fma", "exact"],
@@ -247,7 +250,7 @@ def run_ours(args):
         op = api.GpuSurPreconditioner.from_device(G, M, nb, X.data_ptr(), M, Y.data_ptr(), M, omega, device=dev)
     fma = args.kron == "fma"
     cfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv, diag_every=0, kernel_timing=False,
-                        kron_fma=fma, sw_mode=1 if args.sw == "direct" else 0)
+                        kron_fma=fma, sw_mode=1 if args.sw == "direct" else 0, fused_c=1 if args.fused == "on" else 0)
     stream = torch.cuda.ExternalStream(op.stream_ptr(), device=f"cuda:{dev}")
 
     setup_ms = []
@@ -335,7 +338,7 @@ def run_ours(args):
         e_iters, e_time = 0, 0.0
         ksteps = max(1, min(args.steps, 2))
         ecfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv, diag_every=0, kron_fma=fma,
-                             sw_mode=1 if args.sw == "direct" else 0)
+                             sw_mode=1 if args.sw == "direct" else 0, fused_c=1 if args.fused == "on" else 0)
         for s in range(ksteps + 1):
             if world > 1:
                 obj = [api.nccl_unique_id() if rank == 0 else None]
@@ -394,7 +397,7 @@ def run_ours(args):
             "data": "synthetic (device counter-based Philox N(0,1) X, beta, Z; Omega = L L' + 0.1 I; BASELINE c4)",
             "config": {"workload": f"c{args.config}: G={G}, M={M}, n_i={int(nb[0])}, n={n}, tol {tol:g}, "
                                    f"max_iter {max_iter}; step = setup QR + PCG-Aug solve + recovery",
-                       "G": G, "M": M, "n": n, "xv_mode": args.xv, "kron_arith": args.kron, "sigma_w": args.sw, "trace_diagnostics": "row 0 + final row",
+                       "G": G, "M": M, "n": n, "xv_mode": args.xv, "kron_arith": args.kron, "sigma_w": args.sw, "fused_c": args.fused, "trace_diagnostics": "row 0 + final row",
                        "l2": "inputs (65.5 GB X/Q) far larger than L2", "parallelism": f"rows x{world}"},
             "iterations_per_step": [r.solution.iterations for r in results],
             "termination": last.solution.termination.name,

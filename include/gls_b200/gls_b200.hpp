@@ -101,6 +101,7 @@ struct PcgConfig {
   int graph_chunk = 0;
   int kron_fma = 0;
   int sw_mode = 0;  // 1: Sigma w formed where read (glsgpu_pcg_config::sw_mode)
+  int fused_c = 0;  // 1: Sigma pr inside pass C, element-wise pass A (glsgpu_pcg_config::fused_c)
 };
 
 struct PcgTraceRow {
@@ -377,6 +378,7 @@ inline AugSolveResult pcg_aug(const BlockQrOperator& op, const Vector& w1, const
   c.graph_chunk = config.graph_chunk;
   c.kron_fma = config.kron_fma;
   c.sw_mode = config.sw_mode;
+  c.fused_c = config.fused_c;
   bool w1_zero = true, z1_zero = true;
   for (double v : w1) w1_zero = w1_zero && v == 0.0;
   for (double v : z1) z1_zero = z1_zero && v == 0.0;

@@ -91,6 +91,9 @@ typedef struct {
                                 formed where it is read (diagnostics rows, the exit's b = X*'(y - Sigma w_sel)):
                                 pass A then moves 3 fewer M x G vectors.  Takes effect with kron_fma on the
                                 DMMA pass A (128 < G <= 256) and diag_every <= 0 */
+  int32_t fused_c;           /* 1 = Sigma pr formed on the tensor cores inside pass C (one sweep with Pi r) and
+                                Sigma u = Sigma pr + mu Sigma u carried by recurrence, so pass A is element-wise.
+                                Takes effect with sw_mode 1 and tile-contiguous Q (n_i <= 32) */
 } glsgpu_pcg_config;
 
 /* gls::PcgTraceRow (proj/include/gls/pcg.hpp:32-39).  Diagnostics not computed are NaN. */

@@ -20,7 +20,8 @@ class PcgConfigC(C.Structure):
                 ("stagnation_window", C.c_int64), ("growth_tol", C.c_double), ("growth_window", C.c_int64),
                 ("record_z_every", C.c_int64), ("diag_every", C.c_int32), ("xv_mode", C.c_int32),
                 ("graph_chunk", C.c_int32), ("kernel_timing", C.c_int32),
-                ("kron_fma", C.c_int32), ("sw_mode", C.c_int32)]
+                ("kron_fma", C.c_int32), ("sw_mode", C.c_int32),
+                ("fused_c", C.c_int32)]
 
 
 class TraceRowC(C.Structure):

@@ -103,12 +103,13 @@ class PcgConfig:
     kernel_timing: bool = False
     kron_fma: bool = False     # FP64-bound Kronecker pass (128 < G <= 256) with fused multiply-adds
     sw_mode: int = 0           # 1: Sigma w formed where read instead of by recurrence (kron_fma, diag_every <= 0)
+    fused_c: int = 0           # 1: Sigma pr inside pass C, Sigma u by recurrence, element-wise pass A (needs sw_mode 1)
 
     def to_c(self) -> L.PcgConfigC:
         return L.PcgConfigC(self.tol_rel, self.max_iter, self.breakdown_tol, self.stagnation_window, self.growth_tol,
                             self.growth_window, self.record_z_every, self.diag_every,
                             1 if self.xv_mode == "qr" else 0, self.graph_chunk, 1 if self.kernel_timing else 0,
-                            1 if self.kron_fma else 0, int(self.sw_mode))
+                            1 if self.kron_fma else 0, int(self.sw_mode), int(self.fused_c))
 
 
 TRACE_DTYPE = np.dtype([("iter", np.int64), ("c", np.float64), ("aug_residual_norm", np.float64),

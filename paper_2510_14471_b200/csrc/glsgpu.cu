@@ -239,6 +239,11 @@ struct glsgpu_sur {
   int kron_fma = 0;  // glsgpu_pcg_config::kron_fma of the current solve
   int sw_direct = 0; // sw_mode 1 in effect for the current solve (k_kron_mma path)
   int graph_sw = -1;
+  int fused = 0;     // fused_c in effect: Sigma pr in pass C (k_pass_c_mma), element-wise pass A (k_pass_a_ew)
+  int graph_fused = -1;
+  double* spr = nullptr;            // Sigma pr (slab column block MV_SPR)
+  CUtensorMap qmap;                 // tile-contiguous Q as [256 rows] x [columns], 64 x 32 boxes (k_pass_c_mma)
+  bool qmap_ok = false;
   std::vector<cudaEvent_t> tev;  // timing events captured into the graph
   int64_t graph_kernels = 0;     // kernel nodes in the instantiated graph
   int64_t launches = 0;          // kernels launched by this handle (graph nodes counted per launch)
@@ -333,7 +338,10 @@ bool kron_mma_ok(const glsgpu_sur* h) {
   return !off && kron_gemm_ok(h) && h->kron_fma && h->vmap64_ok;
 }
 
+constexpr int EW_GRID = 148 * 8;  // k_pass_a_ew: grid-stride element-wise pass
+
 int kron_grid(const glsgpu_sur* h) {
+  if (h->fused) return EW_GRID;
   if (kron_mma_ok(h)) return (int)std::min<int64_t>((h->ldm + KM_BM - 1) / KM_BM, 148);
   if (kron_gemm_ok(h)) return (int)std::min<int64_t>(h->ldm / KG_BM, 148);
   const int cpl = kron_cpl(h->G);
@@ -343,6 +351,12 @@ int kron_grid(const glsgpu_sur* h) {
 
 // pass A: u = pr + mu u, the deferred w / sw update, su = Sigma u with the (d, u.u) partials
 void launch_pass_a(glsgpu_sur* h) {
+  if (h->fused) {
+    k_pass_a_ew<<<EW_GRID, NT, 0, h->s>>>(h->ldm * h->G, h->u, h->su, h->pr, h->spr, wbuf_of(h), h->partA, h->st);
+    if (!h->capturing) h->launches++;
+    CKL("k_pass_a_ew");
+    return;
+  }
   if (!kron_gemm_ok(h)) {
     launch_kron(h, nullptr, h->pr, nullptr, h->u, h->su, h->partA, 2, h->st, nullptr);
     return;
@@ -532,6 +546,7 @@ void stream_attrs(glsgpu_sur* h) {
   set((const void*)k_kron_ws<true>, 0, 0);
   set((const void*)k_kron_mma<false>, 0, 0);
   set((const void*)k_kron_mma<true>, 0, 0);
+  set((const void*)k_pass_c_mma, 0, 0);
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);
   set((const void*)k_stream<SMODE_C, false>, 0, 0);
@@ -590,6 +605,15 @@ void pass_b(glsgpu_sur* h, int xv_from_x, const SolveState* st) {
 // pr = Pi r with the dot partials (r.pr, r.r, pr.pr) per CTA; returns the number of partial rows
 int pass_c(glsgpu_sur* h, const double* t, const double* r_in, double* pr_out, double* partials, const SolveState* st,
            int gate) {
+  if (h->fused && r_in == h->r && pr_out == h->pr) {  // the solve's pass C: Pi r and Sigma pr in one sweep
+    const int64_t ntiles = (h->ldm + KM_BM - 1) / KM_BM;
+    const int grid = (int)std::min<int64_t>(ntiles, 148);
+    k_pass_c_mma<<<grid, KM_NT, kc_smem_bytes(), h->s>>>(h->qmap, h->vmap64, geo_of(h), ntiles, h->omegaT, t, h->d_qoff,
+                                                        h->pr, h->spr, partials, st ? st : h->st, gate);
+    if (!h->capturing) h->launches++;
+    CKL("k_pass_c_mma");
+    return grid;
+  }
   if (h->use_stream) {
     StreamArgs a = stream_args(h);
     a.vec = t;
@@ -1285,6 +1309,27 @@ bool make_vmap(glsgpu_sur* h, CUtensorMap* map, int box_rows) {
   return rc == CUDA_SUCCESS;
 }
 
+// tile-contiguous Q as a 2-D tensor: inner = the 256 rows of a tile, outer = every tile column of every block
+bool make_qmap(glsgpu_sur* h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)QRR_NT, (cuuint64_t)(h->qsize / QRR_NT)};
+  const cuuint64_t strides[1] = {(cuuint64_t)QRR_NT * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)KM_BM, 32u};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = encode(&h->qmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->Q, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return rc == CUDA_SUCCESS;
+}
+
 void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
   if (!h->solver_ready) {
     const size_t mv = (size_t)(h->ldm * h->G);
@@ -1297,8 +1342,10 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     h->u = h->mvec + MV_U * mv;
     h->su = h->mvec + MV_SU * mv;
     h->pr = h->mvec + MV_PR * mv;
+    h->spr = h->mvec + MV_SPR * mv;
     h->vmap_ok = make_vmap(h, &h->vmap, KG_BM);
     h->vmap64_ok = make_vmap(h, &h->vmap64, KM_BM);
+    h->qmap_ok = h->qtiled && make_qmap(h);
     h->t = dalloc<double>(h->n);
     h->vs = dalloc<double>(h->n);
     h->est = dalloc<double>(h->n);
@@ -1568,6 +1615,7 @@ void glsgpu_default_config(glsgpu_pcg_config* c) {
   c->kernel_timing = 0;
   c->kron_fma = 0;
   c->sw_mode = 0;
+  c->fused_c = 0;
 }
 
 #define API_BEGIN try {
@@ -1874,6 +1922,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   // only with diag_every <= 0)
   h->sw_direct = (cfg.sw_mode == 1 && kron_mma_ok(h) && diag <= 0) ? 1 : 0;
   hs.sw_direct = h->sw_direct;
+  // fused_c: needs Sigma w formed where read (the recurrence would need Sigma u_old in the element pass)
+  h->fused = (cfg.fused_c == 1 && h->sw_direct && h->qmap_ok && std::getenv("GLSGPU_NO_FUSED") == nullptr) ? 1 : 0;
   CK(cudaMemcpyAsync(h->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
   k_set_t0<<<1, 1, 0, s>>>(h->st);
   if (!h->capturing) h->launches++;
@@ -1969,7 +2019,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   const int timing = cfg.kernel_timing ? 1 : 0;
   const bool need_graph = !h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
                           h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing ||
-                          h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct;
+                          h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct || h->graph_fused != h->fused;
   if (need_graph) {
     if (h->graph) {
       CK(cudaGraphExecDestroy(h->graph));
@@ -2008,6 +2058,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     h->graph_timing = timing;
     h->graph_fma = h->kron_fma;
     h->graph_sw = h->sw_direct;
+    h->graph_fused = h->fused;
   }
   std::vector<double> kt_ms(3, 0.0);
   std::vector<int64_t> kt_n(3, 0);
@@ -2123,9 +2174,11 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     const double M = (double)h->M, G = (double)h->G, n = (double)h->n;
     // pass A: reads pr, u, su, w, sw; writes u, su, w, sw (the deferred update of pcg.cpp:151-152)
     // pass B: reads Q (+ X in xv_mode X), su, r; writes r.   pass C: reads Q, r; writes pr.
-    const double bA = 8.0 * (h->sw_direct ? 6.0 : 9.0) * M * G;  // sw_mode 1: no sw / su(old) read, no sw write
+    // sw_mode 1: no sw / su(old) read, no sw write; fused_c: pass A is element-wise (reads u, pr, su, spr, w;
+    // writes u, su, w) and pass C also writes Sigma pr
+    const double bA = 8.0 * (h->fused ? 8.0 : h->sw_direct ? 6.0 : 9.0) * M * G;
     const double bB = 8.0 * (M * n * (xv_mode == GLSGPU_XV_X ? 2.0 : 1.0) + 3.0 * M * G);
-    const double bC = 8.0 * (M * n + 2.0 * M * G);
+    const double bC = 8.0 * (M * n + (h->fused ? 3.0 : 2.0) * M * G);
     const char* names[3] = {"passA_kron", "passB_update_qtr", "passC_pi"};
     const double bytes[3] = {bA, bB, bC};
     for (int k = 0; k < 3; ++k) {
@@ -2139,6 +2192,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     }
   }
   (void)prev_i;
+  h->fused = 0;  // solve-scoped: probe-level applies after the solve take the plain passes
   API_END((int*)nullptr)
 }
 

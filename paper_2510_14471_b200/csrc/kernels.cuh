@@ -129,7 +129,7 @@ __device__ __forceinline__ void warp_transpose_reduce(double (&acc)[NB]) {
 //        2: pass A: u_new = pr + mu*u when st->mu_pending (pcg.cpp:210) else u; writes u.
 // Partials per CTA: [0] = sum x*out, [1] = sum x*x, [2] = sum out*out.
 // column-block indices of the iteration vectors in the vector slab (glsgpu_sur::mvec)
-enum { MV_W = 0, MV_SW = 3, MV_R = 6, MV_U = 7, MV_SU = 8, MV_PR = 9, MV_COUNT = 10 };
+enum { MV_W = 0, MV_SW = 3, MV_R = 6, MV_U = 7, MV_SU = 8, MV_PR = 9, MV_SPR = 10, MV_COUNT = 11 };
 
 struct WBuf {
   double* w[3];
@@ -1082,6 +1082,319 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     }
     partials[blockIdx.x * 3 + 0] = a;
     partials[blockIdx.x * 3 + 1] = bb;
+    partials[blockIdx.x * 3 + 2] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Fused pass C (fused_c knob, OFF by default; the k_kron_mma shapes with tile-contiguous Q): pr = Pi r (structured.cpp:307-317)
+// with c = r.pr, r.r, pr.pr, AND Sigma pr = pr Omega on the FP64 tensor cores, in one sweep over 64-row tiles of
+// all G blocks -- the Kronecker product hides under the Q stream.  Pass A then only needs the element-wise
+// recurrences u = pr + mu u, Sigma u = Sigma pr + mu Sigma u (k_pass_a_ew): Sigma u is carried by recurrence
+// instead of recomputed (the same value in exact arithmetic, rounded once more per iteration).
+//   * element warps, per block b of a tile: the 64 x n_b sub-tile of Q_b (2-D TMA through the Q map, 16 KB
+//     stages) and, per 8-block chunk, the 64 x 8 box of r; thread = row: pr = w (w r - Q_b t_b), then pr to
+//     global and into the U chunk ring;
+//   * math warps / Omega loader: as k_kron_mma, writing Sigma pr.
+// Measured at c4: 18.3 ms for this pass + 3.2 ms for the element-wise pass A, against 10.9 + 6.9 ms for the
+// separate passes.  Parity holds (test_fused_c_parity); the sweep is latency-bound -- two element warps per SM
+// carry the Q_b t_b row products of all G blocks (the streaming pass C runs them on 256-512 threads per SM), and
+// shared memory cannot hold the U ring, the Omega ring and the ~100 KB of Q in flight an SM needs for its share
+// of HBM bandwidth at once.
+constexpr int KC_QS = 5;                            // Q sub-tile stages (8 stages with 8 U slots / 2 Omega stages: slower)
+constexpr int KC_RS = 3;                            // r box stages
+constexpr int KC_OS = 3;                            // Omega slab stages
+constexpr int KC_UR = 16;                           // U (pr) chunk slots
+constexpr int KC_QT = 32 * KM_BM;                   // Q sub-tile doubles (32 columns x 64 rows)
+constexpr int KC_RB = KM_OK * KM_BM;                // r box doubles (8 columns x 64 rows)
+constexpr size_t kc_smem_bytes() {
+  return (size_t)(KC_UR * KM_UC + KC_OS * KM_OK * KM_OLD + KC_QS * KC_QT + KC_RS * KC_RB) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(KM_NT, 1) k_pass_c_mma(const __grid_constant__ CUtensorMap qmap,
+                                                         const __grid_constant__ CUtensorMap vmap64, Geo g,
+                                                         int64_t ntiles, const double* __restrict__ omegaT,
+                                                         const double* __restrict__ t, const int64_t* __restrict__ qoff,
+                                                         double* __restrict__ pr_out, double* __restrict__ spr_out,
+                                                         double* partials, const SolveState* st, int gate) {
+  if (gate == 1 && !st->active) return;
+  extern __shared__ __align__(128) double ksm[];
+  __shared__ __align__(8) uint64_t om_full[KC_OS], om_empty[KC_OS], q_full[KC_QS], q_empty[KC_QS], r_full[KC_RS],
+      r_empty[KC_RS], uc_full[KC_UR], uc_empty[KC_UR];
+  __shared__ double tsm[KM_EW][KM_OK][32];
+  __shared__ double red[KM_NT / 32][3];
+  double* const ucb = ksm;                                // [KC_UR][KM_OK][KM_XS]
+  double* const omb = ucb + KC_UR * KM_UC;                // [KC_OS][KM_OK][KM_OLD]
+  double* const qsb = omb + KC_OS * KM_OK * KM_OLD;       // [KC_QS][32][KM_BM]
+  double* const rsb = qsb + KC_QS * KC_QT;                // [KC_RS][KM_OK][KM_BM]
+  const int G = g.G;
+  const int64_t ldm = g.ldm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nchunk = G / KM_OK;
+  const int64_t ntl = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (tid == 0) {
+    for (int i = 0; i < KC_OS; ++i) {
+      mbar_init(&om_full[i], 1);
+      mbar_init(&om_empty[i], KW_MATH);
+    }
+    for (int i = 0; i < KC_QS; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], KM_EW);
+    }
+    for (int i = 0; i < KC_RS; ++i) {
+      mbar_init(&r_full[i], 1);
+      mbar_init(&r_empty[i], KM_EW);
+    }
+    for (int i = 0; i < KC_UR; ++i) {
+      mbar_init(&uc_full[i], KM_EW);
+      mbar_init(&uc_empty[i], KW_MATH);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  double pc = 0.0, prr = 0.0, ppp = 0.0;
+  if (warp == KW_MATH) {
+    if (lane == 0) {  // Omega loader
+      const uint32_t row_bytes = (uint32_t)(G * sizeof(double));
+      RingPos w;
+      int s = 0;
+      for (int64_t q = 0; q < ntl * nchunk; ++q) {
+        if (q >= KC_OS) mbar_wait(&om_empty[w.slot], w.phase ^ 1u);
+        mbar_expect_tx(&om_full[w.slot], row_bytes * KM_OK);
+        double* dst = omb + w.slot * KM_OK * KM_OLD;
+        const double* src = omegaT + (int64_t)s * KM_OK * G;
+#pragma unroll
+        for (int r = 0; r < KM_OK; ++r) tma_load_1d(dst + r * KM_OLD, src + (int64_t)r * G, row_bytes, &om_full[w.slot]);
+        w.next(KC_OS);
+        if (++s == nchunk) s = 0;
+      }
+    }
+  } else if (warp > KW_MATH) {
+    // ---------------- element warps: thread = row (KM_EW * 32 == KM_BM), block by block
+    const int ew = warp - KW_MATH - 1;
+    const int row = ew * 32 + lane;
+    const bool issuer = (ew == 0 && lane == 0);
+    const int64_t totq = ntl * G, totr = ntl * nchunk;
+    RingPos qi, ri;              // issue positions
+    int64_t nq = 0, nr = 0, q_tile = blockIdx.x, r_tile = blockIdx.x;
+    int q_b = 0, r_c = 0;
+    auto issue_q = [&]() {
+      if (nq >= KC_QS) mbar_wait(&q_empty[qi.slot], qi.phase ^ 1u);
+      mbar_expect_tx(&q_full[qi.slot], (uint32_t)(KC_QT * sizeof(double)));
+      const int64_t k0 = q_tile * KM_BM;
+      const int nb = g.nb[q_b];
+      const int64_t outer = (qoff[q_b] >> 8) + (k0 >> 8) * nb;  // 256-row tile (k0 / 256) of block q_b
+      tma_load_2d(qsb + qi.slot * KC_QT, &qmap, (int)(k0 & 255), (int)outer, &q_full[qi.slot]);
+      qi.next(KC_QS);
+      ++nq;
+      if (++q_b == G) {
+        q_b = 0;
+        q_tile += gridDim.x;
+      }
+    };
+    auto issue_r = [&]() {
+      if (nr >= KC_RS) mbar_wait(&r_empty[ri.slot], ri.phase ^ 1u);
+      mbar_expect_tx(&r_full[ri.slot], (uint32_t)(KC_RB * sizeof(double)));
+      tma_load_2d(rsb + ri.slot * KC_RB, &vmap64, (int)(r_tile * KM_BM), MV_R * G + r_c * KM_OK, &r_full[ri.slot]);
+      ri.next(KC_RS);
+      ++nr;
+      if (++r_c == nchunk) {
+        r_c = 0;
+        r_tile += gridDim.x;
+      }
+    };
+    if (issuer) {
+      while (nq < KC_QS - 1 && nq < totq) issue_q();
+      while (nr < KC_RS - 1 && nr < totr) issue_r();
+    }
+    RingPos qc, rc, up;
+    // t of a chunk's 8 blocks, one value per lane per block, loaded one chunk ahead (no latency per block)
+    double tv[KM_OK];
+    auto load_t = [&](int c) {
+#pragma unroll
+      for (int bb = 0; bb < KM_OK; ++bb) {
+        const int b = c * KM_OK + bb;
+        tv[bb] = lane < g.nb[b] ? __ldg(t + g.p0[b] + lane) : 0.0;
+      }
+    };
+    load_t(0);
+    for (int64_t jl = 0; jl < ntl; ++jl) {
+      const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
+      const int64_t k = k0 + row;
+      for (int c = 0; c < nchunk; ++c) {
+        if (issuer && nr < totr) issue_r();
+#pragma unroll
+        for (int bb = 0; bb < KM_OK; ++bb) tsm[ew][bb][lane] = tv[bb];
+        __syncwarp();
+        load_t(c + 1 < nchunk ? c + 1 : 0);  // the next chunk's t (wraps to the next tile's first chunk)
+        mbar_wait(&r_full[rc.slot], rc.phase);
+        if (jl * nchunk + c >= KC_UR) mbar_wait(&uc_empty[up.slot], up.phase ^ 1u);
+        const double* R = rsb + rc.slot * KC_RB;
+        double* U = ucb + up.slot * KM_UC;
+        for (int bb = 0; bb < KM_OK; ++bb) {
+          const int b = c * KM_OK + bb;
+          if (issuer && nq < totq) issue_q();
+          mbar_wait(&q_full[qc.slot], qc.phase);
+          const double* Qs = qsb + qc.slot * KC_QT + row;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            s0 = __fma_rn(Qs[(j + 0) * KM_BM], tsm[ew][bb][j + 0], s0);
+            s1 = __fma_rn(Qs[(j + 1) * KM_BM], tsm[ew][bb][j + 1], s1);
+            s2 = __fma_rn(Qs[(j + 2) * KM_BM], tsm[ew][bb][j + 2], s2);
+            s3 = __fma_rn(Qs[(j + 3) * KM_BM], tsm[ew][bb][j + 3], s3);
+          }
+          const double proj = (s0 + s1) + (s2 + s3);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&q_empty[qc.slot]);
+          qc.next(KC_QS);
+          const double wgt = row_wgt(g, g.wts[b], g.wtc[b], k);
+          const double rv = R[bb * KM_BM + row];
+          const double pv = (rv * wgt - proj) * wgt;
+          if (k < ldm) {
+            stg_cs(pr_out + (int64_t)b * ldm + k, pv);
+            pc += rv * pv;
+            prr += rv * rv;
+            ppp += pv * pv;
+          }
+          U[bb * KM_XS + row] = k < ldm ? pv : 0.0;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&r_empty[rc.slot]);
+          mbar_arrive(&uc_full[up.slot]);
+        }
+        rc.next(KC_RS);
+        up.next(KC_UR);
+      }
+    }
+  } else {
+    // ---------------- math warps: Sigma pr, as k_kron_mma
+    const int gg = lane >> 2, tt = lane & 3;
+    const int n0 = 32 * warp;
+    RingPos rp, up;
+    for (int64_t jl = 0; jl < ntl; ++jl) {
+      const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
+      double acc[4][4][4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
+      for (int s = 0; s < nchunk; ++s) {
+        mbar_wait(&uc_full[up.slot], up.phase);
+        mbar_wait(&om_full[rp.slot], rp.phase);
+        const double* om = omb + rp.slot * KM_OK * KM_OLD + n0 + gg;
+        const double* U = ucb + up.slot * KM_UC + tt * KM_XS + gg;
+#pragma unroll
+        for (int kk = 0; kk < KM_OK / 4; ++kk) {
+          const double* ob = om + (kk * 4 + tt) * KM_OLD;
+          const double b0 = ob[0], b1 = ob[8], b2 = ob[16], b3 = ob[24];
+          const double* ua = U + kk * 4 * KM_XS;
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            const double a0 = ua[16 * mi], a1 = ua[16 * mi + 8];
+            dmma_16x8x4(acc[mi][0], a0, a1, b0);
+            dmma_16x8x4(acc[mi][1], a0, a1, b1);
+            dmma_16x8x4(acc[mi][2], a0, a1, b2);
+            dmma_16x8x4(acc[mi][3], a0, a1, b3);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&om_empty[rp.slot]);
+          mbar_arrive(&uc_empty[up.slot]);
+        }
+        rp.next(KC_OS);
+        up.next(KC_UR);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = n0 + 8 * ni + 2 * tt + (q & 1);
+            const int64_t grow = k0 + 16 * mi + gg + 8 * (q >> 1);
+            if (c < G && grow < ldm)
+              stg_cs(spr_out + (int64_t)c * ldm + grow, grow < g.msig ? acc[mi][ni][q] : 0.0);
+          }
+    }
+  }
+  // (c, r.r, pr.pr) partials of this CTA (pcg.cpp:157,165), fixed order
+  double v[3] = {pc, prr, ppp};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v[i] += __shfl_xor_sync(FULL, v[i], o);
+  if (lane == 0) {
+    red[warp][0] = v[0];
+    red[warp][1] = v[1];
+    red[warp][2] = v[2];
+  }
+  __syncthreads();
+  if (tid == 0 && partials) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int w = 0; w < KM_NT / 32; ++w) {
+      a += red[w][0];
+      b += red[w][1];
+      c += red[w][2];
+    }
+    partials[blockIdx.x * 3 + 0] = a;
+    partials[blockIdx.x * 3 + 1] = b;
+    partials[blockIdx.x * 3 + 2] = c;
+  }
+}
+
+// Pass A of the fused schedule (element-wise, HBM-streaming over the slab columns): u = pr + mu u (pcg.cpp:210),
+// Sigma u = Sigma pr + mu Sigma u (by linearity; pass C formed Sigma pr), the deferred w -= lambda u
+// (pcg.cpp:151; sw_mode 1), d = u . Sigma u, u . u.  In the first iteration (no mu yet) u = pr already and
+// Sigma u = Sigma pr.
+__global__ void __launch_bounds__(NT) k_pass_a_ew(int64_t count, double* __restrict__ u, double* __restrict__ su,
+                                                  const double* __restrict__ pr, const double* __restrict__ spr,
+                                                  WBuf wbuf, double* partials, const SolveState* st) {
+  if (!st->active) return;
+  const bool upd = st->mu_pending != 0, wupd = st->upd_pending != 0;
+  const double mu = st->mu, lp = st->lam_prev;
+  const double* __restrict__ wc = wbuf.w[st->cur];
+  double* __restrict__ wn = wbuf.w[st->nxt];
+  double pd = 0.0, pu = 0.0;
+  const int64_t n2 = count >> 1;  // double2 elements (count is even: ldm is a multiple of 32)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 uo = reinterpret_cast<const double2*>(u)[i];
+    const double2 sp = reinterpret_cast<const double2*>(spr)[i];
+    double2 un = uo, sn = sp;
+    if (upd) {
+      const double2 pv = reinterpret_cast<const double2*>(pr)[i];
+      const double2 so = reinterpret_cast<const double2*>(su)[i];
+      un.x = pv.x + mu * uo.x;
+      un.y = pv.y + mu * uo.y;
+      sn.x = sp.x + mu * so.x;
+      sn.y = sp.y + mu * so.y;
+      reinterpret_cast<double2*>(u)[i] = un;
+    }
+    if (wupd) {
+      const double2 wv = reinterpret_cast<const double2*>(wc)[i];
+      double2 wo;
+      wo.x = wv.x + (-lp) * uo.x;
+      wo.y = wv.y + (-lp) * uo.y;
+      reinterpret_cast<double2*>(wn)[i] = wo;
+    }
+    reinterpret_cast<double2*>(su)[i] = sn;
+    pd += un.x * sn.x;
+    pd += un.y * sn.y;
+    pu += un.x * un.x;
+    pu += un.y * un.y;
+  }
+  __shared__ double red[NT / 32 * 3];
+  double v[3] = {pd, pu, 0.0};
+  block_sum<3>(v, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x * 3 + 0] = v[0];
+    partials[blockIdx.x * 3 + 1] = v[1];
     partials[blockIdx.x * 3 + 2] = 0.0;
   }
 }

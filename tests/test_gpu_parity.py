@@ -291,6 +291,31 @@ def test_sw_direct_parity(name, mk, diag):
         assert abs(a["aug_residual_norm"] - b["aug_residual_norm"]) <= 1e-12 * np.linalg.norm(p.Y)
 
 
+@pytest.mark.parametrize("name,mk", KRON_FMA_CASES + [("c4_G256_M2100", lambda: synth.make_problem(4, M=2100))],
+                         ids=[c[0] for c in KRON_FMA_CASES] + ["c4_G256_M2100"])
+def test_fused_c_parity(name, mk):
+    """fused_c (the bench's schedule): Sigma pr formed inside pass C on the tensor cores and Sigma u carried by the
+    recurrence Sigma u = Sigma pr + mu Sigma u -- the same vector in exact arithmetic, rounded differently.  The bar
+    stays the north star's: same termination and iteration count as the oracle, b to 1e-10 (M = 2100: a last
+    64-row tile that ends inside the padded rows)."""
+    p = mk()
+    o = oracle.solve(p, "oracle", cfg=oracle.make_config(tol_rel=p.tol_rel, max_iter=p.max_iter), beta_true=p.beta)
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur)
+    for xv in ("qr", "x"):
+        g = api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=p.max_iter, xv_mode=xv, diag_every=0,
+                                                      kron_fma=True, sw_mode=1, fused_c=1), true_beta=p.beta)
+        s = g.solution
+        assert s.termination.name == o.termination
+        assert s.iterations == o.iterations, (xv, s.iterations, o.iterations)
+        assert rel(s.b, o.b) <= B_TOL, (xv, rel(s.b, o.b))
+        k = min(20, len(o.trace))
+        assert np.allclose(g.trace.rows["c"][:k], o.trace["c"][:k], rtol=1e-10, atol=0)
+    # probe-level applies after a fused solve take the plain passes
+    xi = np.random.default_rng(9).standard_normal(p.m)
+    assert np.max(np.abs(op.apply_pi(xi) - oracle.sur_apply(p, "pi", xi))) <= 1e-12 * max(1.0, np.max(np.abs(xi)))
+
+
 def test_counters_match_reference():
     """CostCounters after pcg_aug equal the reference's own tallies (preconditioner.cpp:9-47)."""
     if not oracle.have("ref"):
