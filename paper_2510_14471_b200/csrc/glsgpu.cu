@@ -253,6 +253,11 @@ struct glsgpu_sur {
   bool coll = false;  // collective path (NCCL all-gathers, cross-rank TSQR level); also nranks == 1 + id
   bool use_stream = false;  // TMA-staged passes (n_i <= 128, 16-byte aligned X columns, ldx >= ldm)
   bool qtiled = false;      // Q tile-contiguous: block b, rows [256 k, 256 k + 256) contiguous (n_i <= 32)
+  // wide blocks (some n_i > 32, all <= 128): the QR writes column-major Q; the streaming passes read a tiled copy
+  // with 64-row tiles (one contiguous bulk copy per tile instead of n_i strided 512-byte segments)
+  double* qt = nullptr;
+  int64_t* d_qtoff = nullptr;
+  int qt_rows = 0;          // rows per tile of the copy: the tile rows the streaming passes pick (<= 256)
   std::vector<int64_t> qoff;  // offset of Q_b
   int64_t* d_qoff = nullptr;
   int64_t qsize = 0;
@@ -466,6 +471,7 @@ StreamCfg stream_cfg(const glsgpu_sur* h, int nmat, int nv) {
   // narrow blocks (nmax <= 32, k_stream<MODE, true>) read 32 column slots per stage
   const int64_t slots = nmax <= 32 ? std::max<int64_t>(nmat * nmax + nv, 32) : nmat * nmax + nv;
   for (int T : {256, 128, 64, 32}) {
+    if (h->qt_rows && T > h->qt_rows) continue;  // never more rows than a tile of the wide blocks' Q copy
     const int64_t stage = slots * T * 8;
     const int64_t extra = (int64_t)(T + nmax + std::max(nmax, 32)) * 8;
     if (2 * stage + extra <= budget) {
@@ -501,7 +507,14 @@ StreamArgs stream_args(glsgpu_sur* h) {
   a.tpart = h->tpart;
   a.nmax = h->nmax;
   a.qtiled = h->qtiled ? 1 : 0;
+  a.qtile = 256;
   a.qoff = h->d_qoff;
+  if (h->qt) {
+    a.Q = h->qt;
+    a.qtiled = 1;
+    a.qtile = h->qt_rows;
+    a.qoff = h->d_qtoff;
+  }
   return a;
 }
 
@@ -1129,6 +1142,12 @@ void run_qr(glsgpu_sur* h) {
 }
 
 void rank_check(glsgpu_sur* h) {
+  if (h->qt) {  // the streaming passes' tiled copy of the new Q
+    const dim3 grid(64, (unsigned)h->G);
+    k_q_relayout<<<grid, NT, 0, h->s>>>(h->Q, h->ldm, h->d_p0, h->d_nb, h->d_qtoff, h->qt_rows, h->G, h->qt);
+    if (!h->capturing) h->launches++;
+    CKL("k_q_relayout");
+  }
   Geo g = geo_of(h);
   k_rank_check<<<(h->G + 127) / 128, 128, 0, h->s>>>(g, h->R, h->d_rank_flags);
   if (!h->capturing) h->launches++;
@@ -1187,6 +1206,20 @@ void alloc_common(glsgpu_sur* h) {
   }
   h->qsize = qsize;
   h->Q = dalloc<double>((size_t)qsize);
+  if (h->use_stream && !h->qtiled && std::getenv("GLSGPU_NO_QTILE") == nullptr) {
+    // tile rows = what pass C and pass B (QR mode) pick for these widths, so their tiles move as one bulk copy
+    h->qt_rows = 0;
+    h->qt_rows = (int)std::min(stream_cfg(h, 1, stream_nvec<SMODE_C>()).T, stream_cfg(h, 1, stream_nvec<SMODE_B>()).T);
+    std::vector<int64_t> qto(h->G, 0);
+    int64_t tot = 0;
+    for (int b = 0; b < h->G; ++b) {
+      qto[b] = tot;
+      tot += round_up(h->ldm, h->qt_rows) * h->nb[b];
+    }
+    h->qt = dalloc<double>((size_t)tot);
+    h->d_qtoff = dalloc<int64_t>(h->G);
+    CK(cudaMemcpy(h->d_qtoff, qto.data(), sizeof(int64_t) * h->G, cudaMemcpyHostToDevice));
+  }
   h->d_qoff = dalloc<int64_t>(h->G);
   CK(cudaMemcpy(h->d_qoff, h->qoff.data(), sizeof(int64_t) * h->G, cudaMemcpyHostToDevice));
   int64_t rtot = 0;
@@ -1214,7 +1247,8 @@ void destroy_impl(glsgpu_sur* h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->graph) cudaGraphExecDestroy(h->graph);
   for (auto e : h->tev) cudaEventDestroy(e);
-  void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->d_wtc, h->Xqr, h->omegaInvT, h->d_ones, h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
+  void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->d_wtc, h->Xqr, h->omegaInvT, h->d_ones, h->qt, h->d_qtoff,
+                  h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
                   h->qr_store, h->qr_tau, h->qr_scratch, h->d_rank_flags, h->d_blk_narrow, h->d_blk_wide,
                   h->mvec, h->t,
                   h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,

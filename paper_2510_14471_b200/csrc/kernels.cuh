@@ -1420,7 +1420,8 @@ struct StreamArgs {
   double* partials;     // per-CTA dot partials (C: 3, DIAG: 1)
   int xv_from_x, sel_best, gate;
   int T, S, nmax;
-  int qtiled;           // Q stored tile-contiguous (256-row tiles per block, column-major inside)
+  int qtiled;           // Q stored tile-contiguous (qtile-row tiles per block, column-major inside)
+  int qtile;            // rows per Q tile (256 for narrow blocks, 64 for the wide blocks' tiled copy)
   const int64_t* qoff;  // [G] offset of Q_b (tiled layout)
   int64_t stage_doubles;
 };
@@ -1499,7 +1500,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     const uint32_t seg = (uint32_t)rows * 8u;
     // tile-contiguous Q with T == 256: the whole tile (padded to 256 rows) is ONE contiguous region,
     // moved as 4 bulk copies; otherwise one copy per column segment
-    const bool qbig = (MODE != SMODE_DIAG) && a.qtiled && T == 256;
+    const bool qbig = (MODE != SMODE_DIAG) && a.qtiled && T == a.qtile;
     const int nq = qbig ? 4 : nb;
     const int nseg = nq + (nmat - 1) * nb + NV;
     const uint32_t qpiece = (uint32_t)(T * nb * 8 / 4);
@@ -1516,11 +1517,11 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           src = a.X + (p0 + q) * a.ldx + kb;
           dst = base + (int64_t)q * T;
         } else if (qbig) {
-          src = a.Q + a.qoff[b] + (kb >> 8) * (int64_t)(256 * nb) + (int64_t)q * (qpiece / 8);
+          src = a.Q + a.qoff[b] + (kb / a.qtile) * (int64_t)(a.qtile * nb) + (int64_t)q * (qpiece / 8);
           dst = base + (int64_t)q * (qpiece / 8);
           bytes = qpiece;
         } else if (a.qtiled) {
-          src = a.Q + a.qoff[b] + (kb >> 8) * (int64_t)(256 * nb) + (int64_t)q * 256 + (kb & 255);
+          src = a.Q + a.qoff[b] + (kb / a.qtile) * (int64_t)(a.qtile * nb) + (int64_t)q * a.qtile + (kb % a.qtile);
           dst = base + (int64_t)q * T;
         } else {
           src = a.Q + (p0 + q) * g.ldm + kb;
@@ -1773,6 +1774,26 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
         a.partials[blockIdx.x] = v[0];
       }
     }
+  }
+}
+
+// Tiled copy of a column-major Q (ld ldm) for the wide blocks' streaming passes: block b, rows [TQ k, TQ k + TQ)
+// become one contiguous TQ x n_b column-major tile at qtoff[b] + k TQ n_b (rows past ldm are zero).
+__global__ void k_q_relayout(const double* __restrict__ Q, int64_t ldm, const int64_t* __restrict__ p0,
+                             const int* __restrict__ nb, const int64_t* __restrict__ qtoff, int TQ, int G,
+                             double* __restrict__ Qt) {
+  const int b = blockIdx.y;
+  if (b >= G) return;
+  const int n = nb[b];
+  const int64_t ntile = (ldm + TQ - 1) / TQ;
+  const int64_t total = ntile * TQ * n;
+  const double* src = Q + p0[b] * ldm;
+  double* dst = Qt + qtoff[b];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / ((int64_t)TQ * n), rem = i - k * TQ * n;
+    const int j = (int)(rem / TQ), r = (int)(rem - (int64_t)j * TQ);
+    const int64_t row = k * TQ + r;
+    dst[i] = row < ldm ? src[(int64_t)j * ldm + row] : 0.0;
   }
 }
 
