@@ -869,7 +869,8 @@ void build_qr_plan(glsgpu_sur* h) {
           it.lds = h->Xqr ? h->ldm : h->ldx;
           it.valid = h->M;
           it.scale = h->Xqr ? 1.0 : h->wts[b];
-          it.refl = h->Q + h->qoff[b] + c * narrow_leaf_rows() * (int64_t)n;  // tile c (and 2c + 1: reg leaves)
+          // leaf rows [r0, r0 + L) inside the 256-row Q tiles (L = 128: half a tile; 512: two tiles)
+          it.refl = h->Q + h->qoff[b] + (it.r0 / QRR_NT) * QRR_NT * (int64_t)n + it.r0 % QRR_NT;
           it.ldr = QRR_NT;
           it.rr0 = 0;
           it.rhalf = (int64_t)QRR_NT * n;

@@ -839,7 +839,10 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
 //     global memory (L2) in the epilogue.
 //   * 1 loader warp streams Omega' in 8-row slabs (one 2 KB bulk copy per row into the padded slab).
 //   * KM_EW element warps: per chunk, 64 x 8 boxes of u, pr, w, sw, su (2-D TMA, KM_ES-stage ring), then per
-//     element the deferred w / sw update (pcg.cpp:151-152), u = pr + mu u (pcg.cpp:210), u.u.
+//     element the deferred w / sw update (pcg.cpp:151-152), u = pr + mu u (pcg.cpp:210), u.u -- each as one fused
+//     multiply-add (kron_fma), like d = u . Sigma u in the epilogue.  An FP64 instruction issued by these warps
+//     stalls the SM's DMMA pipe (measured: one extra FP64 instruction per element costs about 1 ms of the pass at
+//     c4), so the element work is kept to three per element.
 constexpr int KM_BM = 64;                           // rows per tile
 constexpr int KM_EW = 2;                            // element warps (3 spill the math warps' registers)
 constexpr int KM_NT = (KW_MATH + 1 + KM_EW) * 32;
@@ -963,6 +966,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     if (issuer)
       while (e_issue < KM_ES - 1 && e_issue < total) issue();
     RingPos cp, up;
+    constexpr int NE = KM_OK * KM_BM / (32 * KM_EW);  // elements per thread per chunk
     for (int64_t jl = 0; jl < ntl; ++jl) {
       const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
       for (int k = 0; k < nchunk; ++k) {
@@ -972,7 +976,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
         const double* E = elb + cp.slot * KM_EC;
         double* U = ucb + up.slot * KM_UC;
 #pragma unroll
-        for (int e = 0; e < KM_OK * KM_BM / (32 * KM_EW); ++e) {
+        for (int e = 0; e < NE; ++e) {
           const int i = etid + 32 * KM_EW * e;
           const int cc = i / KM_BM, rr = i % KM_BM;
           const int c = k * KM_OK + cc;
@@ -981,16 +985,16 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
           const bool in = grow < ldm;
           const double uo = E[(0 * KM_OK + cc) * KM_BM + rr];
           if (wupd && in) {
-            stg_cs(wn + off, E[(2 * KM_OK + cc) * KM_BM + rr] + (-lp) * uo);
-            if (!swd) stg_cs(swn + off, E[(3 * KM_OK + cc) * KM_BM + rr] + (-lp) * E[(4 * KM_OK + cc) * KM_BM + rr]);
+            stg_cs(wn + off, __fma_rn(-lp, uo, E[(2 * KM_OK + cc) * KM_BM + rr]));
+            if (!swd) stg_cs(swn + off, __fma_rn(-lp, E[(4 * KM_OK + cc) * KM_BM + rr], E[(3 * KM_OK + cc) * KM_BM + rr]));
           }
           double v = uo;
           if (upd) {
-            v = E[(1 * KM_OK + cc) * KM_BM + rr] + mu * uo;
+            v = __fma_rn(mu, uo, E[(1 * KM_OK + cc) * KM_BM + rr]);
             if (in) u_io[off] = v;  // read back by the math warps' epilogue (L2)
           }
           U[cc * KM_XS + rr] = v;
-          p_b += v * v;
+          p_b = __fma_rn(v, v, p_b);
         }
         // this warp's reads of the element slot are done; its U chunk writes are published to the math warps
         fence_proxy_async_smem();
@@ -1058,7 +1062,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
               const double o = grow < msig ? acc[mi][ni][q] : 0.0;
               const int64_t off = (int64_t)c * ldm + grow;
               stg_cs(out + off, o);
-              if (!APPLY) p_a += u_io[off] * o;
+              if (!APPLY) p_a = __fma_rn(u_io[off], o, p_a);
             }
           }
     }
