@@ -621,7 +621,7 @@ int pass_c(glsgpu_sur* h, const double* t, const double* r_in, double* pr_out, d
   if (h->fused && r_in == h->r && pr_out == h->pr) {  // the solve's pass C: Pi r and Sigma pr in one sweep
     const int64_t ntiles = (h->ldm + KM_BM - 1) / KM_BM;
     const int grid = (int)std::min<int64_t>(ntiles, 148);
-    k_pass_c_mma<<<grid, KM_NT, kc_smem_bytes(), h->s>>>(h->qmap, h->vmap64, geo_of(h), ntiles, h->omegaT, t, h->d_qoff,
+    k_pass_c_mma<<<grid, KC_NT, kc_smem_bytes(), h->s>>>(h->qmap, h->vmap64, geo_of(h), ntiles, h->omegaT, t, h->d_qoff,
                                                         h->pr, h->spr, partials, st ? st : h->st, gate);
     if (!h->capturing) h->launches++;
     CKL("k_pass_c_mma");

@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
 //     stalls the SM's DMMA pipe (measured: one extra FP64 instruction per element costs about 1 ms of the pass at
 //     c4), so the element work is kept to three per element.
 constexpr int KM_BM = 64;                           // rows per tile
-constexpr int KM_EW = 2;                            // element warps (3 spill the math warps' registers)
+constexpr int KM_EW = 3;                            // element warps
 constexpr int KM_NT = (KW_MATH + 1 + KM_EW) * 32;
 constexpr int KM_OK = 8;                            // Omega rows per slab = U columns per chunk
 constexpr int KM_OS = 4;                            // Omega slab stages
@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     if (issuer)
       while (e_issue < KM_ES - 1 && e_issue < total) issue();
     RingPos cp, up;
-    constexpr int NE = KM_OK * KM_BM / (32 * KM_EW);  // elements per thread per chunk
+    constexpr int NE = (KM_OK * KM_BM + 32 * KM_EW - 1) / (32 * KM_EW);  // elements per thread per chunk
     for (int64_t jl = 0; jl < ntl; ++jl) {
       const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
       for (int k = 0; k < nchunk; ++k) {
@@ -978,6 +978,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
           const int i = etid + 32 * KM_EW * e;
+          if ((KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
           const int cc = i / KM_BM, rr = i % KM_BM;
           const int c = k * KM_OK + cc;
           const int64_t grow = k0 + rr;
@@ -1105,6 +1106,8 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
 // carry the Q_b t_b row products of all G blocks (the streaming pass C runs them on 256-512 threads per SM), and
 // shared memory cannot hold the U ring, the Omega ring and the ~100 KB of Q in flight an SM needs for its share
 // of HBM bandwidth at once.
+constexpr int KC_EW = 2;                            // element warps of the fused pass C
+constexpr int KC_NT = (KW_MATH + 1 + KC_EW) * 32;
 constexpr int KC_QS = 5;                            // Q sub-tile stages (8 stages with 8 U slots / 2 Omega stages: slower)
 constexpr int KC_RS = 3;                            // r box stages
 constexpr int KC_OS = 3;                            // Omega slab stages
@@ -1115,7 +1118,7 @@ constexpr size_t kc_smem_bytes() {
   return (size_t)(KC_UR * KM_UC + KC_OS * KM_OK * KM_OLD + KC_QS * KC_QT + KC_RS * KC_RB) * sizeof(double);
 }
 
-__global__ void __launch_bounds__(KM_NT, 1) k_pass_c_mma(const __grid_constant__ CUtensorMap qmap,
+__global__ void __launch_bounds__(KC_NT, 1) k_pass_c_mma(const __grid_constant__ CUtensorMap qmap,
                                                          const __grid_constant__ CUtensorMap vmap64, Geo g,
                                                          int64_t ntiles, const double* __restrict__ omegaT,
                                                          const double* __restrict__ t, const int64_t* __restrict__ qoff,
@@ -1125,8 +1128,8 @@ __global__ void __launch_bounds__(KM_NT, 1) k_pass_c_mma(const __grid_constant__
   extern __shared__ __align__(128) double ksm[];
   __shared__ __align__(8) uint64_t om_full[KC_OS], om_empty[KC_OS], q_full[KC_QS], q_empty[KC_QS], r_full[KC_RS],
       r_empty[KC_RS], uc_full[KC_UR], uc_empty[KC_UR];
-  __shared__ double tsm[KM_EW][KM_OK][32];
-  __shared__ double red[KM_NT / 32][3];
+  __shared__ double tsm[KC_EW][KM_OK][32];
+  __shared__ double red[KC_NT / 32][3];
   double* const ucb = ksm;                                // [KC_UR][KM_OK][KM_XS]
   double* const omb = ucb + KC_UR * KM_UC;                // [KC_OS][KM_OK][KM_OLD]
   double* const qsb = omb + KC_OS * KM_OK * KM_OLD;       // [KC_QS][32][KM_BM]
@@ -1143,14 +1146,14 @@ __global__ void __launch_bounds__(KM_NT, 1) k_pass_c_mma(const __grid_constant__
     }
     for (int i = 0; i < KC_QS; ++i) {
       mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], KM_EW);
+      mbar_init(&q_empty[i], KC_EW);
     }
     for (int i = 0; i < KC_RS; ++i) {
       mbar_init(&r_full[i], 1);
-      mbar_init(&r_empty[i], KM_EW);
+      mbar_init(&r_empty[i], KC_EW);
     }
     for (int i = 0; i < KC_UR; ++i) {
-      mbar_init(&uc_full[i], KM_EW);
+      mbar_init(&uc_full[i], KC_EW);
       mbar_init(&uc_empty[i], KW_MATH);
     }
     mbar_fence_init();
@@ -1174,7 +1177,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_pass_c_mma(const __grid_constant__
       }
     }
   } else if (warp > KW_MATH) {
-    // ---------------- element warps: thread = row (KM_EW * 32 == KM_BM), block by block
+    // ---------------- element warps: thread = row (KC_EW * 32 == KM_BM), block by block
     const int ew = warp - KW_MATH - 1;
     const int row = ew * 32 + lane;
     const bool issuer = (ew == 0 && lane == 0);
@@ -1342,7 +1345,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_pass_c_mma(const __grid_constant__
   __syncthreads();
   if (tid == 0 && partials) {
     double a = 0.0, b = 0.0, c = 0.0;
-    for (int w = 0; w < KM_NT / 32; ++w) {
+    for (int w = 0; w < KC_NT / 32; ++w) {
       a += red[w][0];
       b += red[w][1];
       c += red[w][2];
