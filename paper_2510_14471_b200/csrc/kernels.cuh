@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
   } else if (warp > KW_MATH) {
     // ---------------- element warps: element i = (column i / 64, row i % 64) of a chunk, i = etid + 32 KM_EW e
     const int ew = warp - KW_MATH - 1;
-    const int etid = ew * 32 + lane;
+    const int etid = ((ew + 1) % KM_EW) * 32 + lane;  // the uneven last element slot goes to a non-issuing warp
     const bool upd = !APPLY && st->mu_pending != 0, wupd = !APPLY && st->upd_pending != 0;
     const double mu = st->mu, lp = st->lam_prev;
     const int cur = st->cur;
