@@ -837,7 +837,8 @@ __global__ void __launch_bounds__(KW_NT, 1) k_kron_ws(const __grid_constant__ CU
 //     64 accumulators per lane.  A (U) and B (Omega) fragments come from shared memory with strides of 68 / 260
 //     doubles, which make both fragment loads bank-conflict free.  u . Sigma u reads the tile's u back from
 //     global memory (L2) in the epilogue.
-//   * 1 loader warp streams Omega' in 8-row slabs (one 2 KB bulk copy per row into the padded slab).
+//   * 1 loader warp: lane 0 streams Omega' in 8-row slabs (one 2 KB bulk copy per row into the padded slab),
+//     lane 1 issues the element stages (KM_ES in flight).
 //   * KM_EW element warps: per chunk, 64 x 8 boxes of u, pr, w, sw, su (2-D TMA, KM_ES-stage ring), then per
 //     element the deferred w / sw update (pcg.cpp:151-152), u = pr + mu u (pcg.cpp:210), u.u -- each as one fused
 //     multiply-add (kron_fma), like d = u . Sigma u in the epilogue.  An FP64 instruction issued by these warps
@@ -920,57 +921,55 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
         w.next(KM_OS);
         if (++s == nchunk) s = 0;
       }
+    } else if (lane == 1) {
+      // ---------------- element stages: chunk q = 64 x 8 boxes of u (and pr, w, sw, su as needed), KM_ES in flight
+      const bool upd = !APPLY && st->mu_pending != 0, wupd = !APPLY && st->upd_pending != 0;
+      const int cur = st->cur;
+      const int bu = !APPLY ? MV_U * G : (plain == -2 ? (MV_W + cur) * G : plain * G);
+      const int bp = MV_PR * G, bw = (MV_W + cur) * G, bsw = (MV_SW + cur) * G, bsu = MV_SU * G;
+      const bool swd = st->sw_direct != 0;
+      const uint32_t chunk_bytes =
+          (uint32_t)((1 + (upd ? 1 : 0) + (wupd ? (swd ? 1 : 3) : 0)) * KM_OK * KM_BM * sizeof(double));
+      RingPos ip;
+      int64_t it_tile = blockIdx.x;
+      int it_c0 = 0;
+      for (int64_t q = 0; q < ntl * nchunk; ++q) {
+        if (q >= KM_ES) mbar_wait(&el_empty[ip.slot], ip.phase ^ 1u);
+        double* E = elb + ip.slot * KM_EC;
+        uint64_t* bar = &el_full[ip.slot];
+        mbar_expect_tx(bar, chunk_bytes);
+        const int row = (int)(it_tile * KM_BM);
+        tma_load_2d(E, &vmap64, row, bu + it_c0, bar);
+        if (upd) tma_load_2d(E + 1 * KM_OK * KM_BM, &vmap64, row, bp + it_c0, bar);
+        if (wupd) {
+          tma_load_2d(E + 2 * KM_OK * KM_BM, &vmap64, row, bw + it_c0, bar);
+          if (!swd) {
+            tma_load_2d(E + 3 * KM_OK * KM_BM, &vmap64, row, bsw + it_c0, bar);
+            tma_load_2d(E + 4 * KM_OK * KM_BM, &vmap64, row, bsu + it_c0, bar);
+          }
+        }
+        ip.next(KM_ES);
+        it_c0 += KM_OK;
+        if (it_c0 == G) {
+          it_c0 = 0;
+          it_tile += gridDim.x;
+        }
+      }
     }
   } else if (warp > KW_MATH) {
     // ---------------- element warps: element i = (column i / 64, row i % 64) of a chunk, i = etid + 32 KM_EW e
     const int ew = warp - KW_MATH - 1;
-    const int etid = ((ew + 1) % KM_EW) * 32 + lane;  // the uneven last element slot goes to a non-issuing warp
+    const int etid = ew * 32 + lane;
     const bool upd = !APPLY && st->mu_pending != 0, wupd = !APPLY && st->upd_pending != 0;
     const double mu = st->mu, lp = st->lam_prev;
-    const int cur = st->cur;
-    const int bu = !APPLY ? MV_U * G : (plain == -2 ? (MV_W + cur) * G : plain * G);
-    const int bp = MV_PR * G, bw = (MV_W + cur) * G, bsw = (MV_SW + cur) * G, bsu = MV_SU * G;
     double* __restrict__ wn = wbuf.w[st->nxt];
     double* __restrict__ swn = wbuf.sw[st->nxt];
     const bool swd = st->sw_direct != 0;  // no sw recurrence: w alone is updated
-    const uint32_t chunk_bytes =
-        (uint32_t)((1 + (upd ? 1 : 0) + (wupd ? (swd ? 1 : 3) : 0)) * KM_OK * KM_BM * sizeof(double));
-    const int64_t total = ntl * nchunk;
-    const bool issuer = (ew == 0 && lane == 0);
-    RingPos ip;
-    int64_t e_issue = 0, it_tile = blockIdx.x;
-    int it_c0 = 0;
-    auto issue = [&]() {
-      if (e_issue >= KM_ES) mbar_wait(&el_empty[ip.slot], ip.phase ^ 1u);
-      double* E = elb + ip.slot * KM_EC;
-      uint64_t* bar = &el_full[ip.slot];
-      mbar_expect_tx(bar, chunk_bytes);
-      const int row = (int)(it_tile * KM_BM);
-      tma_load_2d(E, &vmap64, row, bu + it_c0, bar);
-      if (upd) tma_load_2d(E + 1 * KM_OK * KM_BM, &vmap64, row, bp + it_c0, bar);
-      if (wupd) {
-        tma_load_2d(E + 2 * KM_OK * KM_BM, &vmap64, row, bw + it_c0, bar);
-        if (!swd) {
-          tma_load_2d(E + 3 * KM_OK * KM_BM, &vmap64, row, bsw + it_c0, bar);
-          tma_load_2d(E + 4 * KM_OK * KM_BM, &vmap64, row, bsu + it_c0, bar);
-        }
-      }
-      ip.next(KM_ES);
-      ++e_issue;
-      it_c0 += KM_OK;
-      if (it_c0 == G) {
-        it_c0 = 0;
-        it_tile += gridDim.x;
-      }
-    };
-    if (issuer)
-      while (e_issue < KM_ES - 1 && e_issue < total) issue();
     RingPos cp, up;
     constexpr int NE = (KM_OK * KM_BM + 32 * KM_EW - 1) / (32 * KM_EW);  // elements per thread per chunk
     for (int64_t jl = 0; jl < ntl; ++jl) {
       const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
       for (int k = 0; k < nchunk; ++k) {
-        if (issuer && e_issue < total) issue();
         mbar_wait(&el_full[cp.slot], cp.phase);
         if (jl * nchunk + k >= KM_UR) mbar_wait(&uc_empty[up.slot], up.phase ^ 1u);
         const double* E = elb + cp.slot * KM_EC;
