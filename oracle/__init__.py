@@ -119,6 +119,10 @@ def _load(path: str, kind: str):
                                        C.POINTER(TraceRow), C.c_int64, C.POINTER(Result)]
         lib.orc_mv_reduce.restype = C.c_int
         lib.orc_mv_reduce.argtypes = [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _P]
+        lib.orc_set_threads.restype = None
+        lib.orc_set_threads.argtypes = [C.c_int]
+        lib.orc_get_threads.restype = C.c_int
+        lib.orc_get_threads.argtypes = []
     else:
         lib.ref_pcg_aug_sur.restype = C.c_int
         lib.ref_pcg_aug_sur.argtypes = [C.c_int, C.c_int64, _PI, _P, _P, _P, _P, _P, _P, C.POINTER(Config), _P,
@@ -156,6 +160,18 @@ def lib(kind: str = "oracle"):
     if kind not in _libs:
         _libs[kind] = _load(ORACLE_SO if kind == "oracle" else REF_SO, kind)
     return _libs[kind]
+
+
+def set_threads(n: int) -> int:
+    """Threads of the restatement's independent per-block / per-tile loops (OpenMP; results are bitwise the
+    single-threaded ones).  Returns the count now in effect."""
+    L = lib("oracle")
+    L.orc_set_threads(int(n))
+    return int(L.orc_get_threads())
+
+
+def threads() -> int:
+    return int(lib("oracle").orc_get_threads())
 
 
 def have(kind: str) -> bool:

@@ -30,6 +30,39 @@
 #include <string.h>
 #include <float.h>
 #include <time.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Threads: the per-block loops (QR of each block, the Q / Q' / X / X' applies of each block), the
+ * per-column Kronecker apply and the element-wise vector updates run in parallel over INDEPENDENT
+ * outputs; every output keeps the reference's own sequential order, so the results are bitwise the
+ * single-threaded ones.  The long dot products (vdot) stay sequential.  orc_set_threads(1) gives the
+ * reference's single thread. */
+static int orc_nthreads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+static int orc_tid(void) {
+#ifdef _OPENMP
+  return omp_get_thread_num();
+#else
+  return 0;
+#endif
+}
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+int orc_get_threads(void) { return orc_nthreads(); }
+#define ORC_PAR _Pragma("omp parallel for schedule(static)")
+#define ORC_PAR_DYN _Pragma("omp parallel for schedule(dynamic, 1)")
 
 #define ORC_OK 0
 #define ORC_DIMENSION_MISMATCH 1
@@ -260,8 +293,10 @@ typedef struct {
   double* Q;    /* M x n */
   double* R;    /* concatenated */
   double* wts;  /* 1/sqrt(block_scale) */
-  double* local;
-  double* tvec;
+  double* local; /* per-thread scratch: nthr x M */
+  double* tvec;  /* per-thread scratch: nthr x nmax */
+  int nthr;
+  int64_t nmax;
 } orc_sur;
 
 static void orc_sur_free(orc_sur* s) {
@@ -292,8 +327,10 @@ static int orc_sur_build(int G, int64_t M, const int64_t* nb, const double* X, c
   s->Q = (double*)malloc(sizeof(double) * (size_t)(M * s->n));
   s->R = (double*)malloc(sizeof(double) * (size_t)(rtot > 0 ? rtot : 1));
   s->wts = (double*)malloc(sizeof(double) * G);
-  s->local = (double*)malloc(sizeof(double) * (size_t)M);
-  s->tvec = (double*)malloc(sizeof(double) * (size_t)(nmax > 0 ? nmax : 1));
+  s->nthr = orc_nthreads();
+  s->nmax = nmax > 0 ? nmax : 1;
+  s->local = (double*)malloc(sizeof(double) * (size_t)M * (size_t)s->nthr);
+  s->tvec = (double*)malloc(sizeof(double) * (size_t)s->nmax * (size_t)s->nthr);
   if (!s->p0 || !s->r0 || !s->Q || !s->R || !s->wts || !s->local || !s->tvec) { orc_sur_free(s); return ORC_NO_MEMORY; }
   int64_t p = 0, r = 0;
   for (int b = 0; b < G; ++b) {
@@ -301,10 +338,24 @@ static int orc_sur_build(int G, int64_t M, const int64_t* nb, const double* X, c
     const double w = scale ? 1.0 / sqrt(scale[b]) : 1.0 / sqrt(1.0);
     s->wts[b] = w;
     s->p0[b] = p; s->r0[b] = r;
-    int st = orc_qr_thin(M, nb[b], X + p * M, M, w, s->Q + p * M, M, s->R + r);
-    if (st != ORC_OK) { if (bad_block) *bad_block = b; orc_sur_free(s); return st; }
     p += nb[b]; r += nb[b] * nb[b];
   }
+  /* the blocks' QRs are independent; the first failing block (in block order) is reported, as the
+   * reference's sequential loop would */
+  int* bst = (int*)malloc(sizeof(int) * (size_t)G);
+  if (!bst) { orc_sur_free(s); return ORC_NO_MEMORY; }
+  ORC_PAR_DYN
+  for (int b = 0; b < G; ++b)
+    bst[b] = orc_qr_thin(M, nb[b], X + s->p0[b] * M, M, s->wts[b], s->Q + s->p0[b] * M, M, s->R + s->r0[b]);
+  for (int b = 0; b < G; ++b)
+    if (bst[b] != ORC_OK) {
+      const int st = bst[b];
+      if (bad_block) *bad_block = b;
+      free(bst);
+      orc_sur_free(s);
+      return st;
+    }
+  free(bst);
   *out = s;
   return ORC_OK;
 }
@@ -312,17 +363,19 @@ static int orc_sur_build(int G, int64_t M, const int64_t* nb, const double* X, c
 /* pi_impl: proj/src/structured.cpp:307-317 */
 static void sur_pi(const orc_sur* s, const double* xi, double* out) {
   const int64_t M = s->M;
+  ORC_PAR_DYN
   for (int b = 0; b < s->G; ++b) {
     const double w = s->wts[b];
     const int64_t nbb = s->nb[b];
     const double* Qb = s->Q + s->p0[b] * M;
-    double* local = s->local;
+    double* local = s->local + (size_t)orc_tid() * (size_t)M;
+    double* tvec = s->tvec + (size_t)orc_tid() * (size_t)s->nmax;
     for (int64_t i = 0; i < M; ++i) local[i] = xi[b * M + i] * w;             /* gather */
-    gemv_t(M, nbb, Qb, M, local, s->tvec);                                      /* Q' local */
+    gemv_t(M, nbb, Qb, M, local, tvec);                                         /* Q' local */
     for (int64_t i = 0; i < M; ++i) out[b * M + i] = 0.0;
     /* proj = Q t, then local -= proj: do it in the reference's order (apply then subtract) */
     double* proj = out + b * M; /* reuse output slot as proj scratch */
-    gemv(M, nbb, Qb, M, s->tvec, proj);
+    gemv(M, nbb, Qb, M, tvec, proj);
     for (int64_t i = 0; i < M; ++i) local[i] -= proj[i];
     for (int64_t i = 0; i < M; ++i) out[b * M + i] = local[i] * w;              /* scatter */
   }
@@ -331,50 +384,64 @@ static void sur_pi(const orc_sur* s, const double* xi, double* out) {
 /* xstar_t_impl: proj/src/structured.cpp:319-328 */
 static int sur_xstar_t(const orc_sur* s, const double* xi, double* out) {
   const int64_t M = s->M;
+  int st_all = ORC_OK;
+  ORC_PAR_DYN
   for (int b = 0; b < s->G; ++b) {
     const double w = s->wts[b];
     const int64_t nbb = s->nb[b];
-    double* local = s->local;
+    double* local = s->local + (size_t)orc_tid() * (size_t)M;
     for (int64_t i = 0; i < M; ++i) local[i] = xi[b * M + i] * w;
     gemv_t(M, nbb, s->Q + s->p0[b] * M, M, local, out + s->p0[b]);
     int st = tri_solve(nbb, s->R + s->r0[b], out + s->p0[b], 0);
-    if (st) return st;
+    if (st) {
+#pragma omp atomic write
+      st_all = st;
+    }
   }
-  return ORC_OK;
+  return st_all;
 }
 
 /* xstar_impl: proj/src/structured.cpp:330-340 */
 static int sur_xstar(const orc_sur* s, const double* v, double* out) {
   const int64_t M = s->M;
+  int st_all = ORC_OK;
+  ORC_PAR_DYN
   for (int b = 0; b < s->G; ++b) {
     const double w = s->wts[b];
     const int64_t nbb = s->nb[b];
-    double* vi = s->tvec;
+    double* vi = s->tvec + (size_t)orc_tid() * (size_t)s->nmax;
+    double* local = s->local + (size_t)orc_tid() * (size_t)M;
     memcpy(vi, v + s->p0[b], sizeof(double) * (size_t)nbb);
     int st = tri_solve(nbb, s->R + s->r0[b], vi, 1);
-    if (st) return st;
-    gemv(M, nbb, s->Q + s->p0[b] * M, M, vi, s->local);
-    for (int64_t i = 0; i < M; ++i) out[b * M + i] = s->local[i] * w;
+    if (st) {
+#pragma omp atomic write
+      st_all = st;
+      continue;
+    }
+    gemv(M, nbb, s->Q + s->p0[b] * M, M, vi, local);
+    for (int64_t i = 0; i < M; ++i) out[b * M + i] = local[i] * w;
   }
-  return ORC_OK;
+  return st_all;
 }
 
 /* ------------------------------------------------------------------ structured X applies
  * The reference applies the dense embed_sur X (structured.cpp:107-119) with
  * DenseMatrix::apply / apply_transpose (dense_matrix.cpp:69-91).  Per block, same order. */
 static void x_apply(int G, int64_t M, const int64_t* nb, const double* X, const double* v, double* y) {
+  int64_t* p0 = (int64_t*)malloc(sizeof(int64_t) * (size_t)G);
   int64_t p = 0;
-  for (int b = 0; b < G; ++b) {
-    gemv(M, nb[b], X + p * M, M, v + p, y + b * M);
-    p += nb[b];
-  }
+  for (int b = 0; b < G; ++b) { p0[b] = p; p += nb[b]; }
+  ORC_PAR_DYN
+  for (int b = 0; b < G; ++b) gemv(M, nb[b], X + p0[b] * M, M, v + p0[b], y + b * M);
+  free(p0);
 }
 static void x_apply_t(int G, int64_t M, const int64_t* nb, const double* X, const double* w, double* out) {
+  int64_t* p0 = (int64_t*)malloc(sizeof(int64_t) * (size_t)G);
   int64_t p = 0;
-  for (int b = 0; b < G; ++b) {
-    gemv_t(M, nb[b], X + p * M, M, w + b * M, out + p);
-    p += nb[b];
-  }
+  for (int b = 0; b < G; ++b) { p0[b] = p; p += nb[b]; }
+  ORC_PAR_DYN
+  for (int b = 0; b < G; ++b) gemv_t(M, nb[b], X + p0[b] * M, M, w + b * M, out + p0[b]);
+  free(p0);
 }
 static double x_frobenius(int G, int64_t M, const int64_t* nb, const double* X) {
   /* DenseMatrix::frobenius_norm (dense_matrix.cpp:93-97): storage order, off-block zeros add +0 */
@@ -389,14 +456,22 @@ static double x_frobenius(int G, int64_t M, const int64_t* nb, const double* X) 
  * SymmetricOperator::apply Kron branch (proj/src/operators.cpp:45-50): vec(reshape(x,M,G) * core)
  * with operator* (dense_matrix.cpp:125-139): j -> p -> i, skipping core(p,j) == 0. */
 void orc_kron_apply(int G, int64_t M, const double* omega, const double* x, double* out) {
-  for (int64_t k = 0; k < M * G; ++k) out[k] = 0.0;
-  for (int j = 0; j < G; ++j) {
-    double* cj = out + (int64_t)j * M;
-    for (int p = 0; p < G; ++p) {
-      const double bpj = omega[p + (int64_t)j * G];
-      if (bpj == 0.0) continue;
-      const double* ap = x + (int64_t)p * M;
-      for (int64_t i = 0; i < M; ++i) cj[i] += ap[i] * bpj;
+  /* row tiles are independent; inside a tile the j -> p -> i order of operator* is kept, so every
+   * output is the same p-ascending sum as the reference's */
+  const int64_t TR = 512;
+  const int64_t ntile = (M + TR - 1) / TR;
+  ORC_PAR_DYN
+  for (int64_t t = 0; t < ntile; ++t) {
+    const int64_t i0 = t * TR, i1 = (i0 + TR < M) ? i0 + TR : M;
+    for (int j = 0; j < G; ++j) {
+      double* cj = out + (int64_t)j * M;
+      for (int64_t i = i0; i < i1; ++i) cj[i] = 0.0;
+      for (int p = 0; p < G; ++p) {
+        const double bpj = omega[p + (int64_t)j * G];
+        if (bpj == 0.0) continue;
+        const double* ap = x + (int64_t)p * M;
+        for (int64_t i = i0; i < i1; ++i) cj[i] += ap[i] * bpj;
+      }
     }
   }
 }
@@ -527,6 +602,7 @@ static int run_aug(const orc_model* mo, const double* Y, const double* w1, const
     if (feas > 1e-14 * sc && feas > 0.0) {
       st = mo->xstar(s, xtw, tmp);
       if (st) goto done;
+      ORC_PAR
       for (int64_t i = 0; i < m; ++i) w[i] -= tmp[i];
       res->w1_projected = 1;
     }
@@ -534,6 +610,7 @@ static int run_aug(const orc_model* mo, const double* Y, const double* w1, const
   if (z1) memcpy(z, z1, nbytes); else memset(z, 0, nbytes);
   mo->sigma(s, w, sw);                                                  /* sw = Sigma w */
   mo->x_apply(s, z, xv);
+  ORC_PAR
   for (int64_t i = 0; i < m; ++i) r[i] = (sw[i] + xv[i]) - Y[i];         /* sub(add(sw, Xz), y) */
   mo->pi(s, r, pr);
   double c = vdot(m, r, pr);
@@ -556,6 +633,7 @@ static int run_aug(const orc_model* mo, const double* Y, const double* w1, const
   /* recover(sw) = X*'(y - sw) and push_row (pcg.cpp:96-116) */
 #define RECOVER(swsel, outv)                                           \
   do {                                                                 \
+    ORC_PAR \
     for (int64_t i_ = 0; i_ < m; ++i_) tmp[i_] = Y[i_] - (swsel)[i_];  \
     st = mo->xstar_t(s, tmp, (outv));                                  \
     if (st) goto done;                                                 \
@@ -567,6 +645,7 @@ static int run_aug(const orc_model* mo, const double* Y, const double* w1, const
       row_->iter = (iter_);                                                                    \
       row_->c = (cval_);                                                                       \
       mo->x_apply(s, est, tmp);                                                                \
+      ORC_PAR \
       for (int64_t i_ = 0; i_ < m; ++i_) tmp[i_] = Y[i_] - (sw[i_] + tmp[i_]);                 \
       row_->aug_residual_norm = vnorm2(m, tmp);                                                \
       mo->x_apply_t(s, w, xtw);                                                                \
@@ -610,9 +689,12 @@ static int run_aug(const orc_model* mo, const double* Y, const double* w1, const
         break;
       }
       const double lambda = c / d;
+      ORC_PAR
       for (int64_t k = 0; k < m; ++k) w[k] += -lambda * u[k];          /* axpy(-lambda, u, w) */
+      ORC_PAR
       for (int64_t k = 0; k < m; ++k) sw[k] += -lambda * su[k];        /* axpy(-lambda, su, sw) */
       mo->x_apply(s, v, xv);
+      ORC_PAR
       for (int64_t k = 0; k < m; ++k) r[k] -= lambda * (su[k] + xv[k]);
       mo->pi(s, r, pr);
       double c_next = vdot(m, r, pr);
@@ -659,6 +741,7 @@ static int run_aug(const orc_model* mo, const double* Y, const double* w1, const
       st = mo->xstar_t(s, r, xr);
       if (st) goto done;
       for (int64_t k = 0; k < n; ++k) v[k] = xr[k] + mu * v[k];
+      ORC_PAR
       for (int64_t k = 0; k < m; ++k) u[k] = pr[k] + mu * u[k];
     }
   }

@@ -239,6 +239,8 @@ struct glsgpu_sur {
   int kron_fma = 0;  // glsgpu_pcg_config::kron_fma of the current solve
   int sw_direct = 0; // sw_mode 1 in effect for the current solve (k_kron_mma path)
   int graph_sw = -1;
+  TraceRowD* graph_rows = nullptr;  // the trace buffer the captured k_scalar_c / k_diag_finalize write
+  bool factors_ok = false;          // false after a rank-deficient update / refactor until a good one
   int fused = 0;     // fused_c in effect: Sigma pr in pass C (k_pass_c_mma), element-wise pass A (k_pass_a_ew)
   int graph_fused = -1;
   double* spr = nullptr;            // Sigma pr (slab column block MV_SPR)
@@ -1156,6 +1158,7 @@ void rank_check(glsgpu_sur* h) {
   std::vector<int> flags(h->G);
   CK(cudaMemcpyAsync(flags.data(), h->d_rank_flags, sizeof(int) * h->G, cudaMemcpyDeviceToHost, h->s));
   CK(cudaStreamSynchronize(h->s));
+  h->factors_ok = false;
   for (int b = 0; b < h->G; ++b)
     if (flags[b]) {
       if (h->rank_msg == 1) fail(GLSGPU_ERR_RANK_DEFICIENT, "qr: matrix is numerically rank deficient", b);
@@ -1164,6 +1167,15 @@ void rank_check(glsgpu_sur* h) {
                std::to_string(b) + " is rank deficient",
            b);
     }
+  h->factors_ok = true;
+}
+
+// every operator apply / solve needs the factors of the handle's current X (a failed update or refactor
+// leaves rank-deficient factors behind: the handle refuses work until a successful one)
+void require_factors(const glsgpu_sur* h) {
+  if (!h->factors_ok)
+    fail(GLSGPU_ERR_RANK_DEFICIENT, "glsgpu: the handle's last factorisation failed (rank deficient); update or "
+                                    "refactor it first");
 }
 
 void validate(int G, int64_t M, const int64_t* n_i, const double* block_scale, const double* omega,
@@ -1763,6 +1775,7 @@ int glsgpu_sur_refactor(glsgpu_sur* h, int* bad_block) {
   API_BEGIN
   if (!h) fail(GLSGPU_ERR_INVALID, "null handle");
   CK(cudaSetDevice(h->dev));
+  h->frob_x = -1.0;  // |X|_F of the (possibly changed in place) X is recomputed on demand
   run_qr(h);
   API_END(bad_block)
 }
@@ -1800,6 +1813,7 @@ int glsgpu_apply_pi(glsgpu_sur* h, const double* xi, double* out) {
   API_BEGIN
   if (!h || !xi || !out) fail(GLSGPU_ERR_INVALID, "apply_pi: null argument");
   CK(cudaSetDevice(h->dev));
+  require_factors(h);
   ensure_solver(h, 1);
   h->counters.pi_applies++;
   h->counters.apply_multiplies += h->pi_cost;
@@ -1815,6 +1829,7 @@ int glsgpu_apply_xstar_t(glsgpu_sur* h, const double* xi, double* out) {
   API_BEGIN
   if (!h || !xi || !out) fail(GLSGPU_ERR_INVALID, "apply_xstar_t: null argument");
   CK(cudaSetDevice(h->dev));
+  require_factors(h);
   ensure_solver(h, 1);
   h->counters.xstar_t_applies++;
   h->counters.apply_multiplies += h->xstar_t_cost;
@@ -1833,6 +1848,7 @@ int glsgpu_apply_xstar(glsgpu_sur* h, const double* v, double* out) {
   API_BEGIN
   if (!h || !v || !out) fail(GLSGPU_ERR_INVALID, "apply_xstar: null argument");
   CK(cudaSetDevice(h->dev));
+  require_factors(h);
   ensure_solver(h, 1);
   h->counters.xstar_applies++;
   h->counters.apply_multiplies += h->xstar_cost;
@@ -1918,6 +1934,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   const int64_t m = h->m_ref;  // rows of the reference's GLM (M G for SUR; G M0 + k for MVRGLM)
   const int64_t max_iter = cfg.max_iter ? cfg.max_iter : (m - h->n + 1);
   const int64_t cap_d = std::max<int64_t>(1, std::min<int64_t>(max_iter + 1, rows ? std::max<int64_t>(rows_cap, 1) : 1));
+  require_factors(h);
   ensure_solver(h, cap_d);
   const int xv_mode = cfg.xv_mode == GLSGPU_XV_QR ? GLSGPU_XV_QR : GLSGPU_XV_X;
   const int diag = cfg.diag_every;
@@ -2054,7 +2071,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   const int timing = cfg.kernel_timing ? 1 : 0;
   const bool need_graph = !h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
                           h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing ||
-                          h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct || h->graph_fused != h->fused;
+                          h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct || h->graph_fused != h->fused ||
+                          h->graph_rows != h->rows_d;
   if (need_graph) {
     if (h->graph) {
       CK(cudaGraphExecDestroy(h->graph));
@@ -2094,6 +2112,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     h->graph_fma = h->kron_fma;
     h->graph_sw = h->sw_direct;
     h->graph_fused = h->fused;
+    h->graph_rows = h->rows_d;
   }
   std::vector<double> kt_ms(3, 0.0);
   std::vector<int64_t> kt_n(3, 0);

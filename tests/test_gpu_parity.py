@@ -423,3 +423,38 @@ def test_update_matches_fresh_create():
     assert np.array_equal(g_upd.solution.b, g_new.solution.b)
     with pytest.raises(api.DimensionMismatch):
         op.update(p2.X[:, :-1], p2.Y)
+
+
+def test_handle_reuse_trace_buffer_grows():
+    """A handle reused with a larger trace cap (want_trace False -> True, or a larger max_iter) re-captures
+    its graph against the new trace buffer: the trace equals a fresh handle's (glsgpu.cu graph key)."""
+    p = synth.make_problem(0)
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur)
+    api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=5), want_trace=False)
+    api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=5))
+    g = api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=60), true_beta=p.beta)
+    f = api.pcg_aug(sur, config=api.PcgConfig(tol_rel=p.tol_rel, max_iter=60), true_beta=p.beta)
+    assert len(g.trace.rows) == len(f.trace.rows) == 61
+    for k in ("iter", "c", "aug_residual_norm", "dual_feas_norm", "rmse"):
+        assert np.array_equal(g.trace.rows[k], f.trace.rows[k], equal_nan=True), k
+
+
+def test_failed_refactor_invalidates_handle():
+    """A rank-deficient update leaves the handle refusing work until a good update."""
+    p = synth.make_problem(4, M=400, G=8)
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur)
+    cfg = api.PcgConfig(tol_rel=1e-10, max_iter=20, xv_mode="qr", diag_every=0)
+    ok = api.pcg_aug(sur, op, config=cfg)
+    bad = np.array(p.X, copy=True)
+    bad[:, 1] = bad[:, 0]  # block 0: two equal columns
+    with pytest.raises(api.RankDeficient):
+        op.update(bad, p.Y)
+    with pytest.raises(api.RankDeficient):
+        api.pcg_aug(sur, op, config=cfg)
+    with pytest.raises(api.RankDeficient):
+        op.apply_pi(np.ones(op.m))
+    op.update(p.X, p.Y)
+    again = api.pcg_aug(sur, op, config=cfg)
+    assert np.array_equal(again.solution.b, ok.solution.b)
