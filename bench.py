@@ -2,21 +2,31 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C] [--xv qr|x]
 
-A step is one complete GLS solve of the config on inputs resident in HBM: the setup QR of every
-block (sur_preconditioner) + PCG-Aug to tol 1e-10 with the config's 200-iteration cap + the b
-recovery.  `value` = PCG iterations completed / second over the K timed steps (CUDA events on the
-solver stream, barrier + synchronize on both sides, max over ranks).  `e2e` = the same metric through
-the C-ABI with HOST buffers (pinned X, Y copied in by glsgpu_sur_create every step, b copied out).
+A step is one complete GLS solve of the config on inputs resident in HBM: the setup QR of every block
+(sur_preconditioner) + PCG-Aug to tol 1e-10 with the config's 200-iteration cap + the b recovery.  `value` = PCG
+iterations completed / second over the K timed steps (CUDA events on the solver stream, barrier + synchronize on
+both sides, max over ranks).  With --gpus N > 1 (and no torchrun environment) the script re-launches itself under
+torch.distributed.run with N ranks, one per GPU; rank r owns a contiguous row shard of the SAME global model
+(row sharding; NCCL all-gathers of the per-iteration partial sums), so the total work is fixed
+("strong" scaling).
 
---impl reference times the reference's own CPU implementation (oracle/_ref, the unmodified gls_core
-compiled from the reference sources; single-threaded as written) on a bounded row sample of the same
-config, extrapolated linearly in M (every per-iteration and setup cost of the reference is linear in M).
+`e2e` = the same metric through the C-ABI with HOST inputs: every timed step uploads that step's X and Y from
+pinned host memory (glsgpu_sur_stage: on the handle's copy stream, overlapping the previous step's solve; the
+first upload is inside the timed region), refactors (glsgpu_sur_update_staged), solves, and reads b back.
+
+`parity_witness`: after the timed region, the bench's generator and knobs at a row sample against the oracle
+(same iterations / termination, b to 1e-10; tests/test_gpu_fullshape.py holds the full shapes).
+
+--impl reference times the reference's CPU algorithm on the box's host cores: the oracle port (bitwise-equal to the
+unmodified reference, tests/test_oracle.py), with every host thread, on a row sample of the same config; the
+literal reference (oracle/_ref) cannot hold this config (its dense embed_sur X is 16.8 TB).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -49,16 +59,14 @@ def parse():
                     help="Sigma w: formed where read (sw_mode 1) or the reference's recurrence; both parity-tested")
     ap.add_argument("--kron", default="fma", choices=["fma", "exact"],
                     help="Kronecker pass arithmetic (glsgpu_pcg_config::kron_fma); both are parity-tested")
+    ap.add_argument("--diag", type=int, default=0, help="diag_every (0: trace diagnostics on row 0 and the last row)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: max(5, min(steps, 10)))")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=0)
+    ap.add_argument("--cpu-rows", type=int, default=20000)
+    ap.add_argument("--no-witness", action="store_true")
+    ap.add_argument("--witness-rows", type=int, default=4000)
     return ap.parse_args()
-
-
-def workload(c: int, M: int):
-    meta = synth.config_meta(c)
-    prob = synth.make_problem(c, M=M, with_data=False)
-    return meta, prob
 
 
 def peaks():
@@ -132,41 +140,73 @@ def dist_env():
     return world, rank, local
 
 
-# ---------------------------------------------------------------------------------------- CPU baseline
-def cpu_sample(c: int, kind: str, rows: int, k1: int, k2: int):
-    """Time the CPU implementation on a row sample at two iteration caps; return per-iteration and
-    setup seconds at the sample size (slope / intercept)."""
-    import oracle
-    p = synth.make_problem(c, M=rows)
-    times = []
-    for k in (k1, k2):
-        cfg = oracle.make_config(tol_rel=p.tol_rel, max_iter=k)
-        t0 = time.perf_counter()
-        out = oracle.solve(p, kind, cfg=cfg, beta_true=p.beta)
-        times.append((time.perf_counter() - t0, out.iterations))
-    (t1, i1), (t2, i2) = times
-    per_it = (t2 - t1) / max(i2 - i1, 1)
-    setup = max(t1 - per_it * i1, 0.0)
-    return per_it, setup, p, sum(t for t, _ in times)
+def relaunch_distributed(n: int):
+    """--gpus N without a torchrun environment: re-run this command as N ranks (one per GPU) under
+    torch.distributed.run; rank 0 prints the JSON line."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execvp(cmd[0], cmd)
 
 
-def cpu_value(c: int, M: int, max_iter: int, kind: str, rows: int):
-    k1, k2 = (2, 6) if kind == "ref" else (3, 10)
-    per_it, setup, p, spent = cpu_sample(c, kind, rows, k1, k2)
-    scale = M / rows
-    iters = max_iter if max_iter else 200
-    step_s = setup * scale + iters * per_it * scale
-    return {
-        "value": iters / step_s,
-        "unit": UNIT,
-        "cores": 1,
-        "kind": "reference" if kind == "ref" else "port",
-        "sample": (f"config {c} with M={rows} rows (of {M}); solves capped at {k1} and {k2} iterations; "
-                   f"per-iteration {per_it * 1e3:.1f} ms and setup {setup:.2f} s at the sample, scaled x{scale:.0f} "
-                   f"(linear in M) to a {iters}-iteration solve: EXTRAPOLATED; {spent:.1f} s of CPU work; "
-                   + ("literal pcg_aug(embed_sur(sur), *sur_preconditioner(sur)) of the unmodified reference"
-                      if kind == "ref" else "structured restatement of run_aug (bitwise-equal to the reference)")),
-    }
+# ---------------------------------------------------------------------------------------- CPU side
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "?"
+
+
+class CpuSample:
+    """The oracle (bitwise-equal to the reference) on a row sample of config c, every host thread: one timed
+    solve capped at k1 iterations and one at k2, giving setup and per-iteration seconds at the sample."""
+
+    def __init__(self, c: int, rows: int, threads: int):
+        import oracle
+        self.oracle = oracle
+        self.threads = oracle.set_threads(threads)
+        self.c, self.rows = c, rows
+        self.p = synth.make_problem(c, M=rows)
+
+    def measure(self, k1: int = 1, k2: int = 3):
+        o = self.oracle
+        times = []
+        for k in (k1, k2):
+            cfg = o.make_config(tol_rel=self.p.tol_rel, max_iter=k)
+            t0 = time.perf_counter()
+            out = o.solve(self.p, "oracle", cfg=cfg, beta_true=self.p.beta)
+            times.append((time.perf_counter() - t0, out.iterations))
+        (t1, i1), (t2, i2) = times
+        per_it = (t2 - t1) / max(i2 - i1, 1)
+        setup = max(t1 - per_it * i1, 0.0)
+        return per_it, setup, t1 + t2
+
+    def value(self, M: int, iters: int, k1: int = 1, k2: int = 3):
+        per_it, setup, spent = self.measure(k1, k2)
+        scale = M / self.rows
+        step_s = setup * scale + iters * per_it * scale
+        return {
+            "value": iters / step_s, "unit": UNIT, "cores": self.threads, "kind": "port",
+            "sample": (f"config {self.c} with M={self.rows} rows (of {M}), the oracle (structured restatement of run_aug, "
+                       f"bitwise-equal to the unmodified reference) on {self.threads} threads ({cpu_model()}); solves "
+                       f"capped at {k1} and {k2} iterations: per-iteration {per_it * 1e3:.1f} ms and setup {setup:.2f} s "
+                       f"at the sample, scaled x{scale:.0f} (every cost is linear in M) to a {iters}-iteration solve: "
+                       f"EXTRAPOLATED in M; {spent:.1f} s of CPU work"),
+            "per_iteration_s_sample": per_it, "setup_s_sample": setup,
+        }
 
 
 def run_reference(args):
@@ -175,13 +215,11 @@ def run_reference(args):
         return
     meta = synth.config_meta(args.config)
     M = args.rows or meta["M"]
-    max_iter = meta["max_iter"] or 200
-    import oracle
-    kind = "ref" if oracle.have("ref") else "oracle"
-    rows = args.cpu_rows or (48 if kind == "ref" else 1000)
+    iters = meta["max_iter"] or 200
+    samp = CpuSample(args.config, min(args.cpu_rows, M), host_cores())
     vals = []
     for s in range(args.warmup + args.steps):
-        v = cpu_value(args.config, M, max_iter, kind, rows)
+        v = samp.value(M, iters)
         if s >= args.warmup:
             vals.append(v)
     value = statistics.mean(v["value"] for v in vals)
@@ -189,11 +227,14 @@ def run_reference(args):
     cb["value"] = value
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * max_iter / value,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * iters / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy Philox; BASELINE config shapes/distributions)",
-        "config": {"workload": f"c{args.config}", "G": meta["G"], "M": M, "parallelism": "none (1 CPU thread)"},
+        "config": {"workload": f"c{args.config}", "G": meta["G"], "M": M, "parallelism": f"{samp.threads} CPU threads"},
         "cpu_baseline": cb,
+        "reference_kind_note": ("the oracle port (bitwise-equal to the reference) stands in for oracle/_ref: the "
+                                "literal reference materialises the dense block-diagonal X of embed_sur "
+                                "(proj/src/structured.cpp:107-119), 16.8 TB at this config"),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -202,9 +243,7 @@ def run_reference(args):
 # ---------------------------------------------------------------------------------------- ours
 def run_ours(args):
     import torch
-    from paper_2510_14471_b200 import api
-    from paper_2510_14471_b200 import _lib as L
-    import ctypes as C
+    from paper_2510_14471_b200 import api, devsynth
 
     world, rank, local = dist_env()
     if world > 1:
@@ -212,45 +251,26 @@ def run_ours(args):
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = local
-    lib = L.load()
     meta = synth.config_meta(args.config)
     M = args.rows or meta["M"]
-    G = meta["G"]
-    seed = 1000 + args.config
-    prob = synth.make_problem(args.config, M=M, with_data=False)
-    nb = np.ascontiguousarray(prob.nb, dtype=np.int64)
-    n = int(nb.sum())
     max_iter = meta["max_iter"]
     tol = meta["tol"]
 
     # ---- synthetic inputs generated on the device (counter-based Philox normals; BASELINE distributions);
     # with N ranks each rank draws its own row shard of the SAME global matrices
-    if prob.name.startswith("c3"):
-        raise SystemExit("bench: config 3 uses host generation; run config 4 (the bench workload)")
-    row0, Ml = api.row_partition(M, world, rank) if world > 1 else (0, M)
-    X = torch.empty((n, Ml), dtype=torch.float64, device=f"cuda:{dev}")   # column-major Ml x n, ld = Ml
-    Y = torch.empty((G, Ml), dtype=torch.float64, device=f"cuda:{dev}")
-    rc = lib.glsgpu_synth_normal(C.c_void_p(X.data_ptr()), Ml, n, Ml, row0, M, seed, 0, dev)
-    assert rc == 0, lib.glsgpu_last_error_message()
-    beta = synth._rng(seed, 1).standard_normal(n)
-    omega = prob.omega
-    oh = synth.omega_half(omega)
-    rc = lib.glsgpu_synth_response(G, Ml, row0, M, nb.ctypes.data_as(C.POINTER(C.c_int64)), C.c_void_p(X.data_ptr()),
-                                   Ml, beta.ctypes.data_as(C.POINTER(C.c_double)),
-                                   oh.ctypes.data_as(C.POINTER(C.c_double)), seed, C.c_void_p(Y.data_ptr()), Ml, dev)
-    assert rc == 0, lib.glsgpu_last_error_message()
-    torch.cuda.synchronize()
-
+    dp = devsynth.device_problem(args.config, M=M, world=world, rank=rank, device=dev)
+    G, nb, n, Ml, omega, beta = dp.G, dp.nb, dp.n, dp.M_local, dp.omega, dp.beta
     if world > 1:
         obj = [api.nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(obj, src=0)
-        op = api.GpuSurPreconditioner.from_device_sharded(G, Ml, M, nb, X.data_ptr(), Ml, Y.data_ptr(), Ml, omega,
-                                                          obj[0], rank, world, device=dev)
+        op = api.GpuSurPreconditioner.from_device_sharded(G, Ml, M, nb, dp.X.data_ptr(), Ml, dp.Y.data_ptr(), Ml,
+                                                          omega, obj[0], rank, world, device=dev)
     else:
-        op = api.GpuSurPreconditioner.from_device(G, M, nb, X.data_ptr(), M, Y.data_ptr(), M, omega, device=dev)
+        op = api.GpuSurPreconditioner.from_device(G, M, nb, dp.X.data_ptr(), M, dp.Y.data_ptr(), M, omega, device=dev)
     fma = args.kron == "fma"
-    cfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv, diag_every=0, kernel_timing=False,
-                        kron_fma=fma, sw_mode=1 if args.sw == "direct" else 0, fused_c=1 if args.fused == "on" else 0)
+    knobs = dict(xv_mode=args.xv, diag_every=args.diag, kron_fma=fma, sw_mode=1 if args.sw == "direct" else 0,
+                 fused_c=1 if args.fused == "on" else 0)
+    cfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, kernel_timing=False, **knobs)
     stream = torch.cuda.ExternalStream(op.stream_ptr(), device=f"cuda:{dev}")
 
     setup_ms = []
@@ -316,7 +336,7 @@ def run_ours(args):
                 "traffic": traffic, "kernel": dom_name, "bytes_per_launch": d["bytes_per_launch"],
                 "avg_launch_ms": avg_ms, "peak_source": peak_src}
     iter_ms = 0.0
-    b_iter = 8.0 * (2.0 * M * n + 14.0 * M * G)
+    b_iter = 8.0 * (2.0 * Ml * n + 14.0 * Ml * G)
     passes = {}
     for k, d in kstats.items():
         if d["launches"]:
@@ -324,68 +344,73 @@ def run_ours(args):
             passes[k] = {"avg_ms": avg, "GB/s": d["bytes_per_launch"] / (avg / 1e3) / 1e9}
             iter_ms += avg
 
-    # ---- e2e through the C-ABI with host buffers (pinned X, Y -> device every step; b -> host)
+    # ---- e2e through the C-ABI with host buffers: per step, that step's X and Y go up from pinned host memory
+    # (staged: overlapping the previous step's solve), the refactor, the solve, b back to the host
     e2e = None
     if not args.no_e2e:
         Xh = torch.empty((n, Ml), dtype=torch.float64, pin_memory=True)
         Yh = torch.empty((G, Ml), dtype=torch.float64, pin_memory=True)
-        Xh.copy_(X)
-        Yh.copy_(Y)
+        Xh.copy_(dp.X)
+        Yh.copy_(dp.Y)
         torch.cuda.synchronize()
         op.close()
-        del X, Y, op
+        del op
+        dp.X = dp.Y = None
         torch.cuda.empty_cache()
-        e_iters, e_time = 0, 0.0
-        ksteps = max(1, min(args.steps, 2))
-        ecfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, xv_mode=args.xv, diag_every=0, kron_fma=fma,
-                             sw_mode=1 if args.sw == "direct" else 0, fused_c=1 if args.fused == "on" else 0)
-        for s in range(ksteps + 1):
-            if world > 1:
-                obj = [api.nccl_unique_id() if rank == 0 else None]
-                torch.distributed.broadcast_object_list(obj, src=0)
-                torch.distributed.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            if world > 1:
-                # the C-ABI's sharded entry takes device buffers: this rank's host shard goes in first
-                Xd = Xh.to(f"cuda:{dev}", non_blocking=True)
-                Yd = Yh.to(f"cuda:{dev}", non_blocking=True)
-                torch.cuda.synchronize()
-                op2 = api.GpuSurPreconditioner.from_device_sharded(G, Ml, M, nb, Xd.data_ptr(), Ml, Yd.data_ptr(), Ml,
-                                                                   omega, obj[0], rank, world, device=dev)
-                r2 = api.pcg_aug(None, op2, config=ecfg, want_w=False)
-                op2.close()
-                del Xd, Yd
-            else:
-                # create once (step 0, untimed warm-up), then per step: new host data through the C-ABI
-                # (glsgpu_sur_update: H2D of X and Y pipelined with the TSQR), the solve, b back to the host
-                if s == 0:
-                    sur = api.SurModel(X=Xh.numpy().T, nb=nb, y=Yh.numpy().T, sigma0=omega)
-                    op2 = api.GpuSurPreconditioner(sur, device=dev)
-                else:
-                    op2.update(Xh.numpy().T, Yh.numpy().T)
-                r2 = api.pcg_aug(sur, op2, config=ecfg, want_w=False)
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
-            if world > 1:
-                t = torch.tensor([dt], device=f"cuda:{dev}")
-                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-                dt = float(t.item())
-            if s > 0:  # first e2e step is a warm-up (allocator / context)
-                e_iters += r2.solution.iterations
-                e_time += dt
-        if world == 1:
-            op2.close()
-        e2e = {"value": e_iters / e_time, "unit": UNIT, "h2d_bytes_per_step": int(8 * (M * n + M * G)),
+        ksteps = args.e2e_steps or max(5, min(args.steps, 10))
+        ecfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, **knobs)
+        if world > 1:
+            obj = [api.nccl_unique_id() if rank == 0 else None]
+            torch.distributed.broadcast_object_list(obj, src=0)
+            op2 = api.GpuSurPreconditioner.from_host_sharded(G, Ml, M, nb, Xh, Yh, omega, obj[0], rank, world,
+                                                             device=dev)
+        else:
+            sur = api.SurModel(X=Xh.numpy().T, nb=nb, y=Yh.numpy().T, sigma0=omega)
+            op2 = api.GpuSurPreconditioner(sur, device=dev)
+        api.pcg_aug(None, op2, config=ecfg, want_w=False)  # untimed warm-up (allocations, graph capture)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e_iters = 0
+        t0 = time.perf_counter()
+        op2.stage(Xh, Yh)  # step 1's inputs: the pipeline fill, inside the timed region
+        for s in range(ksteps):
+            op2.update_staged()
+            if s + 1 < ksteps:
+                op2.stage(Xh, Yh)  # step s + 2's upload runs under this step's solve
+            r2 = api.pcg_aug(None, op2, config=ecfg, want_w=False)
+            e_iters += r2.solution.iterations
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=f"cuda:{dev}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dt = float(t.item())
+        op2.close()
+        e2e = {"value": e_iters / dt, "unit": UNIT, "h2d_bytes_per_step": int(8 * (Ml * n + Ml * G)),
                "d2h_bytes_per_step": int(8 * n + 48 * (r2.trace.rows.size)), "steps": ksteps,
-               "timer": ("host wall clock (max over ranks) around: H2D of the step's X and Y from pinned memory "
-                         "pipelined with the TSQR (glsgpu_sur_update; 1 GPU) or create (N > 1) + solve + b D2H")}
+               "timer": ("host wall clock (max over ranks) around K steps of: the step's X and Y uploaded from pinned "
+                         "host memory (glsgpu_sur_stage, on the copy stream under the previous step's solve; the first "
+                         "upload inside the timed region), glsgpu_sur_update_staged (refactor), the solve, b to the "
+                         "host")}
         del Xh, Yh
+
+    witness_line = None
+    if not args.no_witness and rank == 0:
+        try:
+            from oracle import witness  # the checker, after the timed region (never the thing measured)
+            wrows = min(args.witness_rows, M)
+            witness_line = witness.device_parity(args.config, M=wrows, max_iter=max_iter, knobs=knobs, device=dev,
+                                                 threads=host_cores())
+        except Exception as e:  # the witness reports; it never hides a failure
+            witness_line = {"error": f"{type(e).__name__}: {e}"}
+    if world > 1:
+        torch.distributed.barrier()
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         try:
-            cpu = cpu_value(args.config, M, max_iter, "oracle", args.cpu_rows or 1000)
+            cpu = CpuSample(args.config, min(args.cpu_rows, M), host_cores()).value(M, max_iter or 200)
         except Exception as e:  # the CPU baseline is a reported number, never the product
             cpu = {"error": str(e)}
 
@@ -397,7 +422,9 @@ def run_ours(args):
             "data": "synthetic (device counter-based Philox N(0,1) X, beta, Z; Omega = L L' + 0.1 I; BASELINE c4)",
             "config": {"workload": f"c{args.config}: G={G}, M={M}, n_i={int(nb[0])}, n={n}, tol {tol:g}, "
                                    f"max_iter {max_iter}; step = setup QR + PCG-Aug solve + recovery",
-                       "G": G, "M": M, "n": n, "xv_mode": args.xv, "kron_arith": args.kron, "sigma_w": args.sw, "fused_c": args.fused, "trace_diagnostics": "row 0 + final row",
+                       "G": G, "M": M, "n": n, "xv_mode": args.xv, "kron_arith": args.kron, "sigma_w": args.sw,
+                       "fused_c": args.fused, "diag_every": args.diag,
+                       "trace_diagnostics": "row 0 + final row" if args.diag == 0 else f"every {args.diag} rows",
                        "l2": "inputs (65.5 GB X/Q) far larger than L2", "parallelism": f"rows x{world}"},
             "iterations_per_step": [r.solution.iterations for r in results],
             "termination": last.solution.termination.name,
@@ -409,6 +436,7 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "parity_witness": witness_line,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -421,8 +449,13 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} ranks", file=sys.stderr)
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -154,9 +154,21 @@ int glsgpu_sur_create_device(int G, int64_t M, const int64_t* n_i, const double*
                              const double* Y_dev, int64_t ldy, const double* omega, const double* block_scale,
                              int device, glsgpu_sur** out, int* bad_block);
 
-/* New X (M x n) and Y (M x G) from HOST buffers for a handle made by glsgpu_sur_create (same shapes): upload and
- * refactor, reusing the handle's device memory and TSQR plan (create once, solve many). */
+/* New X (M x n) and Y (M x G) from HOST buffers for a handle made by glsgpu_sur_create or
+ * glsgpu_sur_create_sharded_host (same shapes; a sharded handle takes this rank's rows): upload and refactor,
+ * reusing the handle's device memory and TSQR plan (create once, solve many).  This is make_sur +
+ * sur_preconditioner for the next model (proj/src/structured.cpp:97-105,416-453) without reallocating. */
 int glsgpu_sur_update(glsgpu_sur* h, const double* X, const double* Y, int* bad_block);
+
+/* Pipelined form of glsgpu_sur_update for a stream of models: glsgpu_sur_stage queues the NEXT model's X and Y
+ * (pinned host memory, same shapes) for upload on the handle's copy stream as soon as the current factorisation
+ * has consumed the resident X -- so the upload overlaps the current solve -- and glsgpu_sur_update_staged makes it
+ * current (waits for the copy, refactors).  Between the two, the resident X belongs to the next model: solves
+ * must run in xv_mode QR without w1 / z1 (they never read X; the trace diagnostics use Q and R), and
+ * glsgpu_sur_refactor / glsgpu_pcg_ne refuse with GLSGPU_ERR_UNSUPPORTED.  X / Y stay untouched by the caller
+ * until glsgpu_sur_update_staged returns. */
+int glsgpu_sur_stage(glsgpu_sur* h, const double* X, const double* Y);
+int glsgpu_sur_update_staged(glsgpu_sur* h, int* bad_block);
 
 /* Re-run the setup QR from the resident X (the per-solve setup cost; bench steps time it). */
 int glsgpu_sur_refactor(glsgpu_sur* h, int* bad_block);
@@ -203,6 +215,25 @@ int glsgpu_sur_create_sharded(int G, int64_t M_local, int64_t M_global, const in
                               const double* block_scale, int device, const void* nccl_id, int rank, int nranks,
                               glsgpu_sur** out, int* bad_block);
 int glsgpu_sur_shard(const glsgpu_sur* h, int* rank, int* nranks, int64_t* M_global);
+
+/* Sharded handle from this rank's HOST rows (X: M_local x n, Y: M_local x G, ld M_local); the handle owns its
+ * device copies, so glsgpu_sur_update / _stage / _update_staged serve it (the per-step e2e path at N > 1). */
+int glsgpu_sur_create_sharded_host(int G, int64_t M_local, int64_t M_global, const int64_t* n_i, const double* X,
+                                   const double* Y, const double* omega, const double* block_scale, int device,
+                                   const void* nccl_id, int rank, int nranks, glsgpu_sur** out, int* bad_block);
+
+/* TEST-ONLY in-process rank group: nranks row-shard handles of ONE process on ONE device, each driven by its own
+ * host thread, exchange their all-gathers by device-to-device copies ordered with CUDA events and host barriers
+ * instead of NCCL (no kernel ever waits on another rank).  It runs the library's real sharded decomposition --
+ * cross-rank TSQR level, rank-order sums -- where only one GPU is available; solves run without CUDA graphs.
+ * Not a product backend: multi-GPU runs use glsgpu_sur_create_sharded[_host] over NCCL. */
+typedef struct glsgpu_local_group glsgpu_local_group;
+int glsgpu_local_group_create(int nranks, int device, glsgpu_local_group** out);
+int glsgpu_local_group_destroy(glsgpu_local_group* g);
+int glsgpu_sur_create_sharded_local(int G, int64_t M_local, int64_t M_global, const int64_t* n_i, const double* X_dev,
+                                    int64_t ldx, const double* Y_dev, int64_t ldy, const double* omega,
+                                    const double* block_scale, glsgpu_local_group* group, int rank, glsgpu_sur** out,
+                                    int* bad_block);
 
 /* Multivariate model with exclusion restrictions (gls::MvRglm) ------------------------------------
  * Y = Z0 B + U, restriction list i = the zero-forced rows of B[:, i] as CSR: equation i restricts parameters

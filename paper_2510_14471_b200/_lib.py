@@ -54,6 +54,8 @@ EXPORTS = [
     "glsgpu_default_config", "glsgpu_kernel_stats", "glsgpu_launch_count", "glsgpu_get_factors", "glsgpu_synth_normal",
     "glsgpu_synth_response", "glsgpu_nccl_unique_id", "glsgpu_sur_create_sharded", "glsgpu_sur_shard",
     "glsgpu_mvrglm_create", "glsgpu_mv_reduce", "glsgpu_model_dims", "glsgpu_sur_reduce", "glsgpu_pcg_ne", "glsgpu_sur_update",
+    "glsgpu_sur_stage", "glsgpu_sur_update_staged", "glsgpu_sur_create_sharded_host", "glsgpu_local_group_create",
+    "glsgpu_local_group_destroy", "glsgpu_sur_create_sharded_local",
 ]
 
 _lib = None
@@ -77,6 +79,16 @@ def load() -> C.CDLL:
                                            _P, _P, C.c_int, C.POINTER(H), C.POINTER(C.c_int)]
     L.glsgpu_sur_refactor.argtypes = [H, C.POINTER(C.c_int)]
     L.glsgpu_sur_update.argtypes = [H, _P, _P, C.POINTER(C.c_int)]
+    L.glsgpu_sur_stage.argtypes = [H, C.c_void_p, C.c_void_p]
+    L.glsgpu_sur_update_staged.argtypes = [H, C.POINTER(C.c_int)]
+    L.glsgpu_sur_create_sharded_host.argtypes = [C.c_int, C.c_int64, C.c_int64, _PI64, C.c_void_p, C.c_void_p, _P, _P,
+                                                 C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(H),
+                                                 C.POINTER(C.c_int)]
+    L.glsgpu_local_group_create.argtypes = [C.c_int, C.c_int, C.POINTER(H)]
+    L.glsgpu_local_group_destroy.argtypes = [H]
+    L.glsgpu_sur_create_sharded_local.argtypes = [C.c_int, C.c_int64, C.c_int64, _PI64, C.c_void_p, C.c_int64,
+                                                  C.c_void_p, C.c_int64, _P, _P, H, C.c_int, C.POINTER(H),
+                                                  C.POINTER(C.c_int)]
     L.glsgpu_sur_destroy.argtypes = [H]
     L.glsgpu_sur_dims.argtypes = [H, C.POINTER(C.c_int), _PI64, _PI64]
     L.glsgpu_sur_stream.argtypes = [H]

@@ -277,6 +277,54 @@ class GpuSurPreconditioner:
         self.n = int(self._nb.sum())
         return self
 
+    @classmethod
+    def from_host_sharded(cls, G: int, M_local: int, M_global: int, nb, X: np.ndarray, Y: np.ndarray, omega: np.ndarray,
+                          nccl_id: bytes, rank: int, nranks: int, block_scale=None,
+                          device: int = 0) -> "GpuSurPreconditioner":
+        """Row-sharded operator from this rank's HOST rows (X: M_local x n, Y: M_local x G); the handle owns its
+        device copies, so update / stage / update_staged serve it."""
+        self = cls.__new__(cls)
+        self._lib = L.load()
+        self.sur = None
+        self._h = C.c_void_p()
+        self._nb = np.ascontiguousarray(nb, dtype=np.int64)
+        bad = C.c_int(-1)
+        om = np.asfortranarray(omega, dtype=np.float64)
+        scale = None if block_scale is None else np.ascontiguousarray(block_scale, dtype=np.float64)
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        code = self._lib.glsgpu_sur_create_sharded_host(G, M_local, M_global, self._nb.ctypes.data_as(_PI64),
+                                                        C.c_void_p(_host_ptr(X, (M_local, int(self._nb.sum())))),
+                                                        C.c_void_p(_host_ptr(Y, (M_local, G))), _dp(om), _dp(scale),
+                                                        device, idbuf, rank, nranks, C.byref(self._h), C.byref(bad))
+        self.bad_block = bad.value
+        _check(code, self._lib)
+        self.m = M_local * G
+        self.n = int(self._nb.sum())
+        return self
+
+    @classmethod
+    def from_device_local_group(cls, group: "LocalGroup", rank: int, G: int, M_local: int, M_global: int, nb,
+                                X_ptr: int, ldx: int, Y_ptr: int, ldy: int, omega: np.ndarray,
+                                block_scale=None) -> "GpuSurPreconditioner":
+        """TEST-ONLY: rank `rank` of an in-process rank group on one device (glsgpu_sur_create_sharded_local).
+        Every rank must be created, and solved, from its own thread, concurrently."""
+        self = cls.__new__(cls)
+        self._lib = L.load()
+        self.sur = None
+        self._h = C.c_void_p()
+        self._nb = np.ascontiguousarray(nb, dtype=np.int64)
+        bad = C.c_int(-1)
+        om = np.asfortranarray(omega, dtype=np.float64)
+        scale = None if block_scale is None else np.ascontiguousarray(block_scale, dtype=np.float64)
+        code = self._lib.glsgpu_sur_create_sharded_local(G, M_local, M_global, self._nb.ctypes.data_as(_PI64),
+                                                         C.c_void_p(X_ptr), ldx, C.c_void_p(Y_ptr), ldy, _dp(om),
+                                                         _dp(scale), group.handle, rank, C.byref(self._h), C.byref(bad))
+        self.bad_block = bad.value
+        _check(code, self._lib)
+        self.m = M_local * G
+        self.n = int(self._nb.sum())
+        return self
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             self._lib.glsgpu_sur_destroy(self._h)
@@ -347,6 +395,22 @@ class GpuSurPreconditioner:
             raise DimensionMismatch("update: shapes differ from the operator's")
         bad = C.c_int(-1)
         _check(self._lib.glsgpu_sur_update(self._h, _dp(Xf), _dp(Yf), C.byref(bad)), self._lib)
+
+    def stage(self, X, Y):
+        """Queue the NEXT model's X (M x n) and Y (M x G) for upload (glsgpu_sur_stage): the copy overlaps the
+        current solve (xv_mode QR).  X / Y are numpy or CPU-torch arrays in that (column-major) layout -- pinned
+        memory for a truly asynchronous copy -- and must stay alive and unchanged until update_staged()."""
+        Mloc = self.m // len(self._nb)
+        xp = _host_ptr(X, (Mloc, self.n))
+        yp = _host_ptr(Y, (Mloc, len(self._nb)))
+        self._staged_refs = (X, Y)
+        _check(self._lib.glsgpu_sur_stage(self._h, C.c_void_p(xp), C.c_void_p(yp)), self._lib)
+
+    def update_staged(self):
+        """Make the staged model current: wait for its upload, refactor (glsgpu_sur_update_staged)."""
+        bad = C.c_int(-1)
+        _check(self._lib.glsgpu_sur_update_staged(self._h, C.byref(bad)), self._lib)
+        self._staged_refs = None
 
     def refactor(self):
         bad = C.c_int(-1)
@@ -624,6 +688,46 @@ def pcg_normal_equations(sur_or_op, config: Optional[PcgConfig] = None, true_bet
                      breakdown_iteration=None if res.breakdown_iteration < 0 else int(res.breakdown_iteration),
                      w1_projected=False)
     return AugSolveResult(solution=sol, trace=trace, sigma_scale=float(res.sigma_scale), solve_ms=float(res.solve_ms))
+
+
+def _host_ptr(a, shape) -> int:
+    """Address of a column-major (shape) float64 host array: a Fortran-ordered numpy array, or a C-contiguous
+    (cols, rows) numpy / CPU torch array (its transpose; pinned torch tensors give pinned pointers)."""
+    rows, cols = shape
+    if hasattr(a, "data_ptr"):  # torch tensor (cols, rows), row-major == rows x cols column-major
+        if tuple(a.shape) != (cols, rows) or not a.is_contiguous() or a.is_cuda or str(a.dtype) != "torch.float64":
+            raise DimensionMismatch(f"host tensor must be CPU float64 contiguous of shape {(cols, rows)}")
+        return int(a.data_ptr())
+    arr = np.asarray(a)
+    if arr.dtype != np.float64:
+        raise DimensionMismatch("host array must be float64")
+    if arr.shape == (rows, cols) and arr.flags.f_contiguous:
+        return int(arr.ctypes.data)
+    if arr.shape == (cols, rows) and arr.flags.c_contiguous:
+        return int(arr.ctypes.data)
+    raise DimensionMismatch(f"host array must be ({rows}, {cols}) Fortran-ordered")
+
+
+class LocalGroup:
+    """TEST-ONLY in-process rank group on one device (glsgpu_local_group_create): the library's real sharded
+    decomposition with device-to-device copies in place of NCCL, one host thread per rank."""
+
+    def __init__(self, nranks: int, device: int = 0):
+        self._lib = L.load()
+        self.handle = C.c_void_p()
+        _check(self._lib.glsgpu_local_group_create(nranks, device, C.byref(self.handle)), self._lib)
+        self.nranks = nranks
+
+    def close(self):
+        if self.handle and self.handle.value:
+            self._lib.glsgpu_local_group_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def nccl_unique_id() -> bytes:

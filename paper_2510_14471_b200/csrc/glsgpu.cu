@@ -16,6 +16,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -158,6 +160,24 @@ void blas_check(int st, const char* what) {
 
 }  // namespace
 
+// In-process rank group (TEST-ONLY exchange, include/glsgpu.h glsgpu_local_group_create): P row-shard handles in
+// ONE process on ONE device, each driven by its own host thread, exchange their all-gathers through device-to-device
+// copies ordered by CUDA events and host barriers.  No kernel ever waits on another rank (the stream dependencies
+// are resolved by the GPU front end), so the ranks cannot deadlock on one device; what runs is the library's real
+// sharded decomposition -- cross-rank TSQR level (k_stack_r), rank-order sums (k_sum_ranks, k_reduce3) -- with the
+// NCCL call replaced by these copies.  Graph capture is off for group handles (the copies cross streams).
+struct glsgpu_local_group {
+  int n = 0;
+  int dev = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool aborted = false;
+  std::vector<cudaEvent_t> ev_ready, ev_done;
+  std::vector<const double*> send;
+};
+
 struct glsgpu_sur {
   int dev = 0;
   cudaStream_t s = nullptr;
@@ -240,6 +260,14 @@ struct glsgpu_sur {
   int sw_direct = 0; // sw_mode 1 in effect for the current solve (k_kron_mma path)
   int graph_sw = -1;
   TraceRowD* graph_rows = nullptr;  // the trace buffer the captured k_scalar_c / k_diag_finalize write
+  // staged upload (glsgpu_sur_stage / glsgpu_sur_update_staged): the next model's X goes into X_own on the
+  // copy stream `cs` once the current factorisation has consumed it (ev_qr), Y into Y_next
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_qr = nullptr, ev_stage = nullptr;
+  bool staged = false;      // a staged upload awaits glsgpu_sur_update_staged
+  bool x_released = false;  // X_own holds (or is receiving) the NEXT model's X: nothing may read it now
+  double* Y_next = nullptr;
+  double* t3 = nullptr;     // Q-side diagnostics: s = R est, then Q' w
   bool factors_ok = false;          // false after a rank-deficient update / refactor until a good one
   int fused = 0;     // fused_c in effect: Sigma pr in pass C (k_pass_c_mma), element-wise pass A (k_pass_a_ew)
   int graph_fused = -1;
@@ -265,6 +293,7 @@ struct glsgpu_sur {
   int64_t qsize = 0;
   int64_t M_global = 0;
   ncclComm_t comm = nullptr;
+  glsgpu_local_group* grp = nullptr;  // test-only in-process exchange instead of NCCL
   double *loc3 = nullptr, *all3 = nullptr, *t_loc = nullptr, *t_all = nullptr;
   double *rloc = nullptr, *rall = nullptr, *rstack = nullptr, *gtau = nullptr;  // TSQR across ranks
   int64_t* d_stack_off = nullptr;
@@ -660,10 +689,12 @@ void pass_xs(glsgpu_sur* h, const double* t, double* out) {
 }
 
 // trace diagnostics pass over X: X'w partials (tpart) + residual partials; returns (pointer, rows)
-std::pair<double*, int> pass_diag(glsgpu_sur* h, const double* est, const SolveState* st, int gate) {
+std::pair<double*, int> pass_diag(glsgpu_sur* h, const double* est, const SolveState* st, int gate,
+                                  const double* s_q = nullptr) {
   if (h->use_stream) {
     StreamArgs a = stream_args(h);
-    a.vec = est;
+    a.vec = s_q ? s_q : est;  // Q source (xv_mode QR): X est = Q s / w with s = R est
+    a.qdiag = s_q ? 1 : 0;
     a.partials = h->rpart;
     a.gate = gate;
     const int grid = launch_stream<SMODE_DIAG>(h, a, st);
@@ -680,8 +711,59 @@ std::pair<double*, int> pass_diag(glsgpu_sur* h, const double* est, const SolveS
 }
 
 // ------------------------------------------------------------------------------------------ ranks
+void group_barrier(glsgpu_local_group* g) {
+  std::unique_lock<std::mutex> lk(g->mu);
+  if (g->aborted) fail(GLSGPU_ERR_INVALID, "glsgpu local group: another rank failed");
+  const uint64_t my = g->gen;
+  if (++g->arrived == g->n) {
+    g->arrived = 0;
+    ++g->gen;
+    g->cv.notify_all();
+    return;
+  }
+  if (!g->cv.wait_for(lk, std::chrono::seconds(300), [&] { return g->gen != my || g->aborted; })) {
+    g->aborted = true;
+    g->cv.notify_all();
+    fail(GLSGPU_ERR_INVALID, "glsgpu local group: barrier timeout (a rank stopped calling)");
+  }
+  if (g->aborted) fail(GLSGPU_ERR_INVALID, "glsgpu local group: another rank failed");
+}
+
+void group_abort(glsgpu_local_group* g) {
+  if (!g) return;
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->aborted = true;
+  g->cv.notify_all();
+}
+
+// a group rank that fails releases the others from their barriers
+struct GroupGuard {
+  glsgpu_local_group* g;
+  bool ok = false;
+  ~GroupGuard() {
+    if (!ok) group_abort(g);
+  }
+};
+
+// all-gather of `count` doubles per rank in rank order (recv: nranks x count)
 void allgather(glsgpu_sur* h, const double* send, double* recv, size_t count) {
-  nccl_check(nccl().AllGather(send, recv, count, ncclFloat64, h->comm, h->s), "ncclAllGather");
+  if (!h->grp) {
+    nccl_check(nccl().AllGather(send, recv, count, ncclFloat64, h->comm, h->s), "ncclAllGather");
+    return;
+  }
+  glsgpu_local_group* g = h->grp;
+  const int r = h->rank;
+  g->send[(size_t)r] = send;
+  CK(cudaEventRecord(g->ev_ready[(size_t)r], h->s));
+  group_barrier(g);  // every rank's send buffer and ready event are published
+  for (int q = 0; q < g->n; ++q) {
+    CK(cudaStreamWaitEvent(h->s, g->ev_ready[(size_t)q], 0));
+    CK(cudaMemcpyAsync(recv + (size_t)q * count, g->send[(size_t)q], count * sizeof(double), cudaMemcpyDeviceToDevice,
+                       h->s));
+  }
+  CK(cudaEventRecord(g->ev_done[(size_t)r], h->s));
+  group_barrier(g);  // every rank has enqueued its copies
+  for (int q = 0; q < g->n; ++q) CK(cudaStreamWaitEvent(h->s, g->ev_done[(size_t)q], 0));  // send buffers reusable
 }
 
 // CTA partials (count x 3) -> (pointer, rows) that a scalar kernel sums in fixed order: the partials
@@ -1269,6 +1351,14 @@ void destroy_impl(glsgpu_sur* h) {
                   h->rstack, h->gtau, h->d_stack_off, h->d_gitems, h->d_qoff};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (h->cs) {
+    cudaStreamSynchronize(h->cs);
+    cudaStreamDestroy(h->cs);
+  }
+  if (h->ev_qr) cudaEventDestroy(h->ev_qr);
+  if (h->ev_stage) cudaEventDestroy(h->ev_stage);
+  if (h->Y_next) cudaFree(h->Y_next);
+  if (h->t3) cudaFree(h->t3);
   if (h->st_host) cudaFreeHost(h->st_host);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->s) cudaStreamDestroy(h->s);
@@ -1284,12 +1374,15 @@ struct MvDesc {
 
 glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* omega, const double* block_scale,
                           int device, int64_t M_global = -1, int rank = 0, int nranks = 1,
-                          const void* nccl_id = nullptr, const MvDesc* mvd = nullptr, bool qr_only = false) {
+                          const void* nccl_id = nullptr, const MvDesc* mvd = nullptr, bool qr_only = false,
+                          glsgpu_local_group* grp = nullptr) {
   if (M_global < 0) M_global = M;
   validate(G, M_global, n_i, block_scale, omega, /*need_m_gt_n=*/!qr_only);
   if (nranks < 1 || rank < 0 || rank >= nranks) fail(GLSGPU_ERR_INVALID, "glsgpu: bad rank / nranks");
+  if (grp && (grp->n != nranks || grp->dev != device))
+    fail(GLSGPU_ERR_INVALID, "glsgpu: local group size / device differ from nranks / device");
   if (nranks > 1) {
-    if (!nccl_id) fail(GLSGPU_ERR_INVALID, "glsgpu: sharded handle needs an NCCL unique id");
+    if (!nccl_id && !grp) fail(GLSGPU_ERR_INVALID, "glsgpu: sharded handle needs an NCCL unique id");
     for (int b = 0; b < G; ++b)
       if (M < n_i[b]) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "glsgpu: every rank must own at least max n_i rows", b);
   }
@@ -1306,10 +1399,11 @@ glsgpu_sur* create_common(int G, int64_t M, const int64_t* n_i, const double* om
   h->rank = rank;
   h->nranks = nranks;
   h->M_global = M_global;
-  h->coll = nranks > 1 || nccl_id != nullptr;
+  h->coll = nranks > 1 || nccl_id != nullptr || grp != nullptr;
+  h->grp = grp;
   try {
     CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
-    if (h->coll) {
+    if (h->coll && !grp) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
       nccl_check(nccl().CommInitRank(&h->comm, nranks, id, rank), "ncclCommInitRank");
@@ -1394,6 +1488,7 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     h->vmap64_ok = make_vmap(h, &h->vmap64, KM_BM);
     h->qmap_ok = h->qtiled && make_qmap(h);
     h->t = dalloc<double>(h->n);
+    h->t3 = dalloc<double>(h->n);
     h->vs = dalloc<double>(h->n);
     h->est = dalloc<double>(h->n);
     h->t2 = dalloc<double>(h->n);
@@ -1578,6 +1673,47 @@ __global__ void k_scale_rows(double* dst, const double* src, int64_t ld, int64_t
   }
 }
 
+// X is the current factors' X (not overwritten by a staged upload of the next model)
+void require_x(const glsgpu_sur* h, const char* what) {
+  if (h->x_released)
+    fail(GLSGPU_ERR_UNSUPPORTED, std::string(what) + ": X was released to the staged upload of the next model "
+                                                     "(glsgpu_sur_stage); use xv_mode QR without w1 / z1, or "
+                                                     "glsgpu_sur_update_staged first");
+}
+
+// One trace row's diagnostics (pcg.cpp:96-116): est = X*'(y - sw) (recover), |y - sw - X est|, |X' w| and the
+// rmse.  gated: the per-iteration (captured) form, active on st->diag_now rows; otherwise trace row `row`.
+// xv_mode QR never reads X: X est = Q s / w with s = Q'(w (y - sw)) = R est itself, and X' w = R' Q' w / w.
+void diag_row(glsgpu_sur* h, int xv_mode, bool gated, int64_t row) {
+  const int gate = gated ? 2 : 0;
+  const SolveState* gst = gated ? h->st : nullptr;
+  Geo g = geo_of(h);
+  const bool q = xv_mode == GLSGPU_XV_QR && h->use_stream;
+  if (!q) require_x(h, "trace diagnostics (xv_mode X)");
+  pass_qt(h, MODE_QT_D, nullptr, h->st, 0, gate);
+  reduce_t_global(h, h->t2, gst, gate);
+  if (q) {
+    k_copy_gated<<<(unsigned)std::min<int64_t>((h->n + NT - 1) / NT, 148), NT, 0, h->s>>>(h->t3, h->t2, h->n, gst);
+    if (!h->capturing) h->launches++;
+    CKL("k_copy_gated");
+  }
+  k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, gst);
+  if (!h->capturing) h->launches++;
+  CKL("k_vupdate diag");
+  const auto rp = pass_diag(h, h->t2, h->st, gate, q ? h->t3 : nullptr);
+  reduce_t_global(h, q ? h->t3 : h->xtw, gst, gate);
+  if (q) {
+    k_rt_apply<<<dim3((unsigned)((h->nmax + 63) / 64), (unsigned)h->G), 64, 0, h->s>>>(g, h->R, h->t3, h->xtw, gst);
+    if (!h->capturing) h->launches++;
+    CKL("k_rt_apply");
+  }
+  const auto pr1 = combine1(h, rp.first, rp.second);
+  k_diag_finalize<<<1, NT, 0, h->s>>>(pr1.first, pr1.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d,
+                                      gated ? -1 : row);
+  if (!h->capturing) h->launches++;
+  CKL("k_diag_finalize");
+}
+
 void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int iter_idx) {
   Geo g = geo_of(h);
   const int gA = kron_grid(h);
@@ -1613,19 +1749,79 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
     // est = X*'(y - sw) and the row diagnostics, gated on st->diag_now
     if (h->sw_direct && !kron_mma_apply(h, -2, nullptr))
       launch_kron(h, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 3, h->st, nullptr);
-    pass_qt(h, MODE_QT_D, nullptr, h->st, 0, 2);
-    reduce_t_global(h, h->t2, h->st, 2);
-    k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
-    if (!h->capturing) h->launches++;
-    CKL("k_vupdate diag");
-    const auto rp = pass_diag(h, h->t2, h->st, 2);
-    reduce_t_global(h, h->xtw, h->st, 2);
-    const auto pr1 = combine1(h, rp.first, rp.second);
-    k_diag_finalize<<<1, NT, 0, h->s>>>(pr1.first, pr1.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d,
-                                        -1);
-    if (!h->capturing) h->launches++;
-    CKL("k_diag_finalize");
+    diag_row(h, xv_mode, true, -1);
   }
+}
+
+// the copy stream and events of the staged-upload path (created on first use)
+void ensure_stage_objects(glsgpu_sur* h) {
+  if (!h->cs) CK(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
+  if (!h->ev_qr) CK(cudaEventCreateWithFlags(&h->ev_qr, cudaEventDisableTiming));
+  if (!h->ev_stage) CK(cudaEventCreateWithFlags(&h->ev_stage, cudaEventDisableTiming));
+}
+
+// a staged upload still in flight is finished (or dropped) before X / Y are written another way
+void settle_staged(glsgpu_sur* h) {
+  if (h->cs) CK(cudaStreamSynchronize(h->cs));
+  h->staged = false;
+}
+
+// after a factorisation of X_own: the staged path may overwrite X_own once the QR has consumed it
+void mark_factored(glsgpu_sur* h) {
+  if (h->ev_qr) CK(cudaEventRecord(h->ev_qr, h->s));
+  h->x_released = false;
+  h->frob_x = -1.0;  // |X|_F of the new X (w1 projection) is recomputed on demand
+}
+
+// host X (M x n, ld M) and Y (M x G, ld M) -> X_own / Y_own, then the factorisation (pipelined by block groups
+// with the H2D where the TSQR allows it; the cross-rank TSQR level of a sharded handle runs after the copy)
+void upload_and_factor(glsgpu_sur* h, const double* X, const double* Y) {
+  const int64_t M = h->M;
+  CK(cudaMemcpy2DAsync(h->Y_own, h->ldm * sizeof(double), Y, M * sizeof(double), M * sizeof(double), h->G,
+                       cudaMemcpyHostToDevice, h->s));
+  static const bool no_overlap = std::getenv("GLSGPU_NO_OVERLAP") != nullptr;
+  if (!no_overlap && qr_groupable(h) && h->G >= 2) {
+    upload_and_qr_pipelined(h, X, std::min(h->G, 8));
+  } else {
+    CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
+                         cudaMemcpyHostToDevice, h->s));
+    run_qr(h);
+  }
+  mark_factored(h);
+}
+
+// handle that owns its X / Y (host inputs): glsgpu_sur_create (one rank) and glsgpu_sur_create_sharded_host
+glsgpu_sur* create_host_owned(int G, int64_t M, int64_t M_global, const int64_t* n_i, const double* X, const double* Y,
+                              const double* omega, const double* block_scale, int device, int rank, int nranks,
+                              const void* nccl_id) {
+  static const bool trace = std::getenv("GLSGPU_TRACE_CREATE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  const auto t0 = now();
+  glsgpu_sur* h = create_common(G, M, n_i, omega, block_scale, device, M_global, rank, nranks, nccl_id);
+  try {
+    h->X_own = dalloc<double>((size_t)(h->ldm * h->n));
+    h->Y_own = dalloc<double>((size_t)(h->ldm * G));
+    if (h->ldm > M)  // padding rows only: the copies write rows [0, M)
+      CK(cudaMemset2DAsync(h->X_own + M, h->ldm * sizeof(double), 0, (h->ldm - M) * sizeof(double), h->n, h->s));
+    CK(cudaMemsetAsync(h->Y_own, 0, sizeof(double) * h->ldm * G, h->s));
+    h->X = h->X_own;
+    h->ldx = h->ldm;
+    h->Y = h->Y_own;
+    h->ldy = h->ldm;
+    alloc_common(h);
+    CK(cudaStreamSynchronize(h->s));
+    const auto t1 = now();
+    upload_and_factor(h, X, Y);
+    if (trace)
+      std::fprintf(stderr, "glsgpu create: allocate + plan %.1f ms, upload + QR %.1f ms\n", ms(t0, t1), ms(t1, now()));
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  return h;
 }
 
 }  // namespace
@@ -1684,70 +1880,76 @@ int glsgpu_sur_create(int G, int64_t M, const int64_t* n_i, const double* X, con
   API_BEGIN
   if (!out || !X || !Y) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create: null argument");
   *out = nullptr;
-  static const bool trace = std::getenv("GLSGPU_TRACE_CREATE") != nullptr;
-  auto now = [] { return std::chrono::steady_clock::now(); };
-  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
-    return std::chrono::duration<double, std::milli>(b - a).count();
-  };
-  const auto t0 = now();
-  glsgpu_sur* h = create_common(G, M, n_i, omega, block_scale, device);
-  try {
-    h->X_own = dalloc<double>((size_t)(h->ldm * h->n));
-    h->Y_own = dalloc<double>((size_t)(h->ldm * G));
-    if (h->ldm > M)  // padding rows only: the copies write rows [0, M)
-      CK(cudaMemset2DAsync(h->X_own + M, h->ldm * sizeof(double), 0, (h->ldm - M) * sizeof(double), h->n, h->s));
-    CK(cudaMemsetAsync(h->Y_own, 0, sizeof(double) * h->ldm * G, h->s));
-    CK(cudaMemcpy2DAsync(h->Y_own, h->ldm * sizeof(double), Y, M * sizeof(double), M * sizeof(double), G,
-                         cudaMemcpyHostToDevice, h->s));
-    h->X = h->X_own;
-    h->ldx = h->ldm;
-    h->Y = h->Y_own;
-    h->ldy = h->ldm;
-    alloc_common(h);
-    CK(cudaStreamSynchronize(h->s));
-    const auto t1 = now();
-    static const bool no_overlap = std::getenv("GLSGPU_NO_OVERLAP") != nullptr;
-    const bool piped = !no_overlap && qr_groupable(h) && G >= 2;
-    if (piped) {
-      upload_and_qr_pipelined(h, X, std::min(G, 8));
-    } else {
-      CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
-                           cudaMemcpyHostToDevice, h->s));
-      run_qr(h);
-    }
-    if (trace)
-      std::fprintf(stderr, "glsgpu_sur_create: allocate + plan %.1f ms, upload + QR %.1f ms (%s)\n", ms(t0, t1),
-                   ms(t1, now()), piped ? "pipelined" : "serial");
-  } catch (...) {
-    destroy_impl(h);
-    throw;
-  }
-  *out = h;
+  *out = create_host_owned(G, M, M, n_i, X, Y, omega, block_scale, device, 0, 1, nullptr);
   API_END(bad_block)
 }
 
-// New data for an existing host-created SUR handle (same G, M, widths): upload X and Y and refactor, reusing
-// every allocation and the TSQR plan -- the per-solve cost of a "create once, solve many" caller.
+int glsgpu_sur_create_sharded_host(int G, int64_t M_local, int64_t M_global, const int64_t* n_i, const double* X,
+                                   const double* Y, const double* omega, const double* block_scale, int device,
+                                   const void* nccl_id, int rank, int nranks, glsgpu_sur** out, int* bad_block) {
+  API_BEGIN
+  if (!out || !X || !Y || !nccl_id) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create_sharded_host: null argument");
+  *out = nullptr;
+  *out = create_host_owned(G, M_local, M_global, n_i, X, Y, omega, block_scale, device, rank, nranks, nccl_id);
+  API_END(bad_block)
+}
+
+// New data for an existing host-created SUR handle (same G, M, widths; on a sharded handle this rank's rows):
+// upload X and Y and refactor, reusing every allocation and the TSQR plan -- the per-solve cost of a "create
+// once, solve many" caller.
 int glsgpu_sur_update(glsgpu_sur* h, const double* X, const double* Y, int* bad_block) {
   API_BEGIN
   if (!h || !X || !Y) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_update: null argument");
-  if (!h->X_own || h->mv || h->coll) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu_sur_update: needs a glsgpu_sur_create handle");
+  if (!h->X_own || h->mv) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu_sur_update: needs a host-created SUR handle");
   CK(cudaSetDevice(h->dev));
-  const int64_t M = h->M;
-  CK(cudaMemcpy2DAsync(h->Y_own, h->ldm * sizeof(double), Y, M * sizeof(double), M * sizeof(double), h->G,
-                       cudaMemcpyHostToDevice, h->s));
-  static const bool no_overlap = std::getenv("GLSGPU_NO_OVERLAP") != nullptr;
-  if (!no_overlap && qr_groupable(h) && h->G >= 2) {
-    upload_and_qr_pipelined(h, X, std::min(h->G, 8));
-  } else {
-    CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
-                         cudaMemcpyHostToDevice, h->s));
-    run_qr(h);
-  }
-  h->frob_x = -1.0;  // |X|_F of the new X (w1 projection) is recomputed on demand
+  settle_staged(h);
+  upload_and_factor(h, X, Y);
   API_END(bad_block)
 }
 
+// Stage the NEXT model's data (same shapes as glsgpu_sur_update): X and Y go up on the handle's copy stream as
+// soon as the current factorisation has consumed X_own, overlapping whatever the solver stream runs meanwhile
+// (a solve in xv_mode QR never reads X).  X and Y should be pinned host memory for the copy to be
+// asynchronous, and must stay untouched until glsgpu_sur_update_staged returns.
+int glsgpu_sur_stage(glsgpu_sur* h, const double* X, const double* Y) {
+  API_BEGIN
+  if (!h || !X || !Y) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_stage: null argument");
+  if (!h->X_own || h->mv) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu_sur_stage: needs a host-created SUR handle");
+  CK(cudaSetDevice(h->dev));
+  if (h->staged) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_stage: an upload is already staged");
+  ensure_stage_objects(h);
+  if (!h->Y_next) h->Y_next = dalloc<double>((size_t)(h->ldm * h->G));
+  const int64_t M = h->M;
+  // X_own / the spare Y are free once everything enqueued so far on the solver stream (the last factorisation
+  // among it) is done; the solve that follows runs concurrently with the copy
+  CK(cudaEventRecord(h->ev_qr, h->s));
+  CK(cudaStreamWaitEvent(h->cs, h->ev_qr, 0));
+  if (h->ldm > M) CK(cudaMemsetAsync(h->Y_next, 0, sizeof(double) * h->ldm * h->G, h->cs));
+  CK(cudaMemcpy2DAsync(h->Y_next, h->ldm * sizeof(double), Y, M * sizeof(double), M * sizeof(double), h->G,
+                       cudaMemcpyHostToDevice, h->cs));
+  CK(cudaMemcpy2DAsync(h->X_own, h->ldm * sizeof(double), X, M * sizeof(double), M * sizeof(double), h->n,
+                       cudaMemcpyHostToDevice, h->cs));
+  CK(cudaEventRecord(h->ev_stage, h->cs));
+  h->staged = true;
+  h->x_released = true;
+  API_END((int*)nullptr)
+}
+
+// Make the staged model current: the solver stream waits for the staged copy, then refactors (glsgpu_sur_update
+// without the copy).
+int glsgpu_sur_update_staged(glsgpu_sur* h, int* bad_block) {
+  API_BEGIN
+  if (!h) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_update_staged: null handle");
+  if (!h->staged) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_update_staged: nothing staged (glsgpu_sur_stage)");
+  CK(cudaSetDevice(h->dev));
+  CK(cudaStreamWaitEvent(h->s, h->ev_stage, 0));
+  std::swap(h->Y_own, h->Y_next);
+  h->Y = h->Y_own;
+  h->staged = false;
+  run_qr(h);
+  mark_factored(h);
+  API_END(bad_block)
+}
 int glsgpu_sur_create_device(int G, int64_t M, const int64_t* n_i, const double* X_dev, int64_t ldx,
                              const double* Y_dev, int64_t ldy, const double* omega, const double* block_scale,
                              int device, glsgpu_sur** out, int* bad_block) {
@@ -1775,8 +1977,9 @@ int glsgpu_sur_refactor(glsgpu_sur* h, int* bad_block) {
   API_BEGIN
   if (!h) fail(GLSGPU_ERR_INVALID, "null handle");
   CK(cudaSetDevice(h->dev));
-  h->frob_x = -1.0;  // |X|_F of the (possibly changed in place) X is recomputed on demand
+  require_x(h, "glsgpu_sur_refactor");
   run_qr(h);
+  mark_factored(h);  // also resets |X|_F: X may have been changed in place
   API_END(bad_block)
 }
 
@@ -1927,6 +2130,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
                      int64_t rows_cap, glsgpu_result* res) {
   API_BEGIN
   if (!h || !b_out || !res) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_solve: null argument");
+  GroupGuard group_guard{h->grp};
   CK(cudaSetDevice(h->dev));
   glsgpu_pcg_config cfg;
   if (cfg_in) cfg = *cfg_in;
@@ -1986,6 +2190,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   CK(cudaMemsetAsync(h->wb[0], 0, mvb, s));
   CK(cudaMemsetAsync(h->swb[0], 0, mvb, s));
   if (w1 && h->coll) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: w1 on a row-sharded handle");
+  if (w1) require_x(h, "w1");
+  if (xv_mode == GLSGPU_XV_X) require_x(h, "xv_mode X");
   if (w1) {
     h2d_mvec(h, h->wb[0], w1);
     // X'w via the diagnostics pass with est = 0 (only its column part is used here)
@@ -2032,7 +2238,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     launch_kron(h, h->wb[0], nullptr, nullptr, nullptr, h->swb[0], h->partA, 0, nullptr, nullptr);
   {
     dim3 grid((unsigned)std::min<int64_t>((h->ldm + NT - 1) / NT, 64), (unsigned)h->G);
-    k_init_residual<<<grid, NT, 0, s>>>(g, h->X, h->ldx, h->zvec, h->swb[0], h->Y, h->ldy, h->r);
+    if (z1) require_x(h, "z1");
+    k_init_residual<<<grid, NT, 0, s>>>(g, z1 ? h->X : nullptr, h->ldx, h->zvec, h->swb[0], h->Y, h->ldy, h->r);
     if (!h->capturing) h->launches++;
     CKL("k_init_residual");
   }
@@ -2048,18 +2255,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   CKL("k_vupdate init");
   CK(cudaMemcpyAsync(h->u, h->pr, mvb, cudaMemcpyDeviceToDevice, s));
   // row 0 diagnostics: est0 = recover(sw) (pcg.cpp:118-122)
-  if (diag >= 0) {
-    pass_qt(h, MODE_QT_D, nullptr, h->st, 0, 0);
-    reduce_t_global(h, h->t2, nullptr, 0);
-    k_vupdate<<<(h->G + 63) / 64, 64, 0, s>>>(g, h->R, h->t2, nullptr, 1, 2, nullptr);
-    if (!h->capturing) h->launches++;
-    const auto rp0 = pass_diag(h, h->t2, h->st, 0);
-    reduce_t_global(h, h->xtw, nullptr, 0);
-    const auto pr0 = combine1(h, rp0.first, rp0.second);
-    k_diag_finalize<<<1, NT, 0, s>>>(pr0.first, pr0.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d, 0);
-    if (!h->capturing) h->launches++;
-    CKL("row 0 diagnostics");
-  }
+  if (diag >= 0) diag_row(h, xv_mode, false, 0);
 
   // ---- the iteration loop: CUDA graphs of `chunk` iterations, device-side control
   int chunk = cfg.graph_chunk;
@@ -2068,11 +2264,13 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     const double t_iter_us = bytes_iter / 6.0e6 + 40.0;
     chunk = (int)std::clamp(2000.0 / t_iter_us, 2.0, 32.0);
   }
-  const int timing = cfg.kernel_timing ? 1 : 0;
-  const bool need_graph = !h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
+  const int timing = (cfg.kernel_timing && !h->grp) ? 1 : 0;
+  // a local-group (test-only) handle runs the iterations eagerly: its exchange crosses streams, which a
+  // captured graph cannot hold
+  const bool need_graph = !h->grp && (!h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
                           h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing ||
                           h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct || h->graph_fused != h->fused ||
-                          h->graph_rows != h->rows_d;
+                          h->graph_rows != h->rows_d);
   if (need_graph) {
     if (h->graph) {
       CK(cudaGraphExecDestroy(h->graph));
@@ -2122,6 +2320,10 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     CK(cudaStreamSynchronize(s));
     if (!h->st_host->active) break;
     prev_i = h->st_host->i;
+    if (h->grp) {
+      for (int k = 0; k < chunk; ++k) capture_iteration(h, xv_mode, diag >= 0 ? 1 : -1, 0, k);
+      continue;
+    }
     CK(cudaGraphLaunch(h->graph, s));
     h->launches += h->graph_kernels;
     if (timing) {
@@ -2247,6 +2449,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   }
   (void)prev_i;
   h->fused = 0;  // solve-scoped: probe-level applies after the solve take the plain passes
+  group_guard.ok = true;
   API_END((int*)nullptr)
 }
 
@@ -2331,6 +2534,72 @@ int glsgpu_sur_create_sharded(int G, int64_t M_local, int64_t M_global, const in
     throw;
   }
   *out = h;
+  API_END(bad_block)
+}
+
+int glsgpu_local_group_create(int nranks, int device, glsgpu_local_group** out) {
+  API_BEGIN
+  if (!out || nranks < 1) fail(GLSGPU_ERR_INVALID, "glsgpu_local_group_create: bad argument");
+  *out = nullptr;
+  CK(cudaSetDevice(device));
+  glsgpu_local_group* g = new glsgpu_local_group();
+  g->n = nranks;
+  g->dev = device;
+  g->ev_ready.assign((size_t)nranks, nullptr);
+  g->ev_done.assign((size_t)nranks, nullptr);
+  g->send.assign((size_t)nranks, nullptr);
+  try {
+    for (int r = 0; r < nranks; ++r) {
+      CK(cudaEventCreateWithFlags(&g->ev_ready[(size_t)r], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g->ev_done[(size_t)r], cudaEventDisableTiming));
+    }
+  } catch (...) {
+    for (auto e : g->ev_ready)
+      if (e) cudaEventDestroy(e);
+    for (auto e : g->ev_done)
+      if (e) cudaEventDestroy(e);
+    delete g;
+    throw;
+  }
+  *out = g;
+  API_END((int*)nullptr)
+}
+
+int glsgpu_local_group_destroy(glsgpu_local_group* g) {
+  if (!g) return GLSGPU_OK;
+  cudaSetDevice(g->dev);
+  for (auto e : g->ev_ready)
+    if (e) cudaEventDestroy(e);
+  for (auto e : g->ev_done)
+    if (e) cudaEventDestroy(e);
+  delete g;
+  return GLSGPU_OK;
+}
+
+int glsgpu_sur_create_sharded_local(int G, int64_t M_local, int64_t M_global, const int64_t* n_i, const double* X_dev,
+                                    int64_t ldx, const double* Y_dev, int64_t ldy, const double* omega,
+                                    const double* block_scale, glsgpu_local_group* group, int rank, glsgpu_sur** out,
+                                    int* bad_block) {
+  API_BEGIN
+  if (!out || !X_dev || !Y_dev || !group) fail(GLSGPU_ERR_INVALID, "glsgpu_sur_create_sharded_local: null argument");
+  GroupGuard group_guard{group};
+  if (ldx < M_local || ldy < M_local) fail(GLSGPU_ERR_DIMENSION_MISMATCH, "glsgpu: leading dimension < M_local");
+  *out = nullptr;
+  glsgpu_sur* h = create_common(G, M_local, n_i, omega, block_scale, group->dev, M_global, rank, group->n, nullptr,
+                                nullptr, false, group);
+  try {
+    h->X = X_dev;
+    h->ldx = ldx;
+    h->Y = Y_dev;
+    h->ldy = ldy;
+    alloc_common(h);
+    run_qr(h);
+  } catch (...) {
+    destroy_impl(h);
+    throw;
+  }
+  *out = h;
+  group_guard.ok = true;
   API_END(bad_block)
 }
 
@@ -2619,6 +2888,7 @@ int glsgpu_pcg_ne(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const double* 
   API_BEGIN
   if (!h || !b_out || !res) fail(GLSGPU_ERR_INVALID, "glsgpu_pcg_ne: null argument");
   if (h->coll) fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu_pcg_ne: row-sharded handles are not supported");
+  require_x(h, "glsgpu_pcg_ne");
   if (h->mv && h->m_ref != (int64_t)h->G * h->M0)
     fail(GLSGPU_ERR_SINGULAR_COVARIANCE, "pcg_normal_equations: covariance is singular");
   CK(cudaSetDevice(h->dev));

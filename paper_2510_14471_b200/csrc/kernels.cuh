@@ -1426,6 +1426,8 @@ struct StreamArgs {
   double* partials;     // per-CTA dot partials (C: 3, DIAG: 1)
   int xv_from_x, sel_best, gate;
   int T, S, nmax;
+  int qdiag;            // SMODE_DIAG from Q instead of X (xv_mode QR): X est = Q s / w with s = R est, and the
+                        // column partials are Q' w (X' w = R' Q' w / w, k_rt_apply)
   int qtiled;           // Q stored tile-contiguous (qtile-row tiles per block, column-major inside)
   int qtile;            // rows per Q tile (256 for narrow blocks, 64 for the wide blocks' tiled copy)
   const int64_t* qoff;  // [G] offset of Q_b (tiled layout)
@@ -1506,7 +1508,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     const uint32_t seg = (uint32_t)rows * 8u;
     // tile-contiguous Q with T == 256: the whole tile (padded to 256 rows) is ONE contiguous region,
     // moved as 4 bulk copies; otherwise one copy per column segment
-    const bool qbig = (MODE != SMODE_DIAG) && a.qtiled && T == a.qtile;
+    const bool qbig = (MODE != SMODE_DIAG || a.qdiag) && a.qtiled && T == a.qtile;
     const int nq = qbig ? 4 : nb;
     const int nseg = nq + (nmat - 1) * nb + NV;
     const uint32_t qpiece = (uint32_t)(T * nb * 8 / 4);
@@ -1519,7 +1521,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
       double* dst;
       uint32_t bytes = seg;
       if (q < nq) {  // first matrix: Q (X for DIAG)
-        if (MODE == SMODE_DIAG) {
+        if (MODE == SMODE_DIAG && !a.qdiag) {
           src = a.X + (p0 + q) * a.ldx + kb;
           dst = base + (int64_t)q * T;
         } else if (qbig) {
@@ -1652,7 +1654,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
             const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
             x = (yv - (V[t] + (-lp) * V[T + t])) * wgt;
           } else {  // SMODE_DIAG
-            const double xe = (k < g.M) ? rdot() : 0.0;
+            const double xe = (k < g.M) ? (a.qdiag ? rdot() * iwgt : rdot()) : 0.0;
             const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
             const double res = yv - ((V[T + t] + (-lp) * V[3 * T + t]) + xe);
             if (k < g.M) rsum += res * res;
@@ -1719,7 +1721,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           const double swv = V[t] + (-lp) * V[T + t];  // sw_{i+1} = sw_i - lambda_i su_i when pending
           xs[t] = (yv - swv) * wgt;
         } else {  // SMODE_DIAG
-          const double xe = (k < g.M) ? qdot(M0 + t) : 0.0;
+          const double xe = (k < g.M) ? (a.qdiag ? qdot(M0 + t) * iwgt : qdot(M0 + t)) : 0.0;
           const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
           const double swv = V[T + t] + (-lp) * V[3 * T + t];
           const double res = yv - (swv + xe);
@@ -1885,6 +1887,28 @@ __global__ void k_vupdate(Geo g, const double* R, double* t, double* vs, int xv_
     const double mu = st->mu;
     for (int j = 0; j < nb; ++j) vs[p0 + j] = tb[j] + mu * vs[p0 + j];
   }
+}
+
+// Q-side diagnostics (xv_mode QR, X not read): xtw_b = R_b' t_b / w_b, i.e. X_b' w from t_b = Q_b' w
+// (X_b = Q_b R_b / w_b); gated on the diagnostics row like k_vupdate mode 2.
+__global__ void k_rt_apply(Geo g, const double* R, const double* t, double* out, const SolveState* st) {
+  if (st && !st->diag_now) return;
+  const int b = blockIdx.y;
+  const int nb = g.nb[b];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nb) return;
+  const int64_t p0 = g.p0[b];
+  const double* Rb = R + g.r0[b];
+  double s = 0.0;
+  for (int i = 0; i <= j; ++i) s += Rb[i + (int64_t)j * nb] * t[p0 + i];
+  out[p0 + j] = s / g.wts[b];
+}
+
+// dst = src (n entries), gated on the diagnostics row when st is given
+__global__ void k_copy_gated(double* dst, const double* src, int64_t n, const SolveState* st) {
+  if (st && !st->diag_now) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2796,7 +2820,8 @@ __global__ void k_init_residual(Geo g, const double* X, int64_t ldx, const doubl
     double xz = 0.0;
     double yv = 0.0;
     if (k < g.M) {
-      for (int j = 0; j < nb; ++j) xz = xz + X[(p0 + j) * ldx + k] * z[p0 + j];
+      if (X)  // X == nullptr: z = 0 (X z = 0 exactly), X not read
+        for (int j = 0; j < nb; ++j) xz = xz + X[(p0 + j) * ldx + k] * z[p0 + j];
       yv = Y[(int64_t)b * ldy + k];
     }
     r[off] = (sw[off] + xz) - yv;
