@@ -27,6 +27,8 @@
 
 #include "../../include/glsgpu.h"
 #include "kernels.cuh"
+#include "ne.cuh"
+#include "gemm.cuh"
 
 using namespace glsgpu;
 
@@ -101,15 +103,11 @@ void nccl_check(ncclResult_t r, const char* what) {
   fail(GLSGPU_ERR_NCCL, std::string(what) + ": " + s);
 }
 
-// cuBLAS / cuSOLVER, resolved at run time like NCCL: only the sur_reduce pre-pass (plain library GEMMs, the
-// symmetric eigensolver and a Householder QR of the basis) uses them; the solver path never does.
+// cuSOLVER, resolved at run time like NCCL: only the sur_reduce pre-pass uses it, for the dense symmetric
+// eigensolver of the n x n Gram (syevd; plus geqrf / orgqr for a basis wider than the TSQR kernels' 512 columns).
+// The Gram, the basis and the rotations are this library's own DMMA GEMM (gemm.cuh), the basis QR its own TSQR.
 struct Dla {
-  void *blas = nullptr, *sol = nullptr;
-  decltype(&cublasCreate_v2) BlasCreate = nullptr;
-  decltype(&cublasDestroy_v2) BlasDestroy = nullptr;
-  decltype(&cublasSetStream_v2) BlasSetStream = nullptr;
-  decltype(&cublasDgemm_v2) Dgemm = nullptr;
-  decltype(&cublasDsyrk_v2) Dsyrk = nullptr;
+  void* sol = nullptr;
   decltype(&cusolverDnCreate) SolCreate = nullptr;
   decltype(&cusolverDnDestroy) SolDestroy = nullptr;
   decltype(&cusolverDnSetStream) SolSetStream = nullptr;
@@ -126,17 +124,8 @@ Dla& dla() {
   static bool tried = false;
   if (!tried) {
     tried = true;
-    d.blas = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!d.blas) d.blas = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
     d.sol = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
     if (!d.sol) d.sol = dlopen("libcusolver.so", RTLD_NOW | RTLD_GLOBAL);
-    if (d.blas) {
-      d.BlasCreate = (decltype(d.BlasCreate))dlsym(d.blas, "cublasCreate_v2");
-      d.BlasDestroy = (decltype(d.BlasDestroy))dlsym(d.blas, "cublasDestroy_v2");
-      d.BlasSetStream = (decltype(d.BlasSetStream))dlsym(d.blas, "cublasSetStream_v2");
-      d.Dgemm = (decltype(d.Dgemm))dlsym(d.blas, "cublasDgemm_v2");
-      d.Dsyrk = (decltype(d.Dsyrk))dlsym(d.blas, "cublasDsyrk_v2");
-    }
     if (d.sol) {
       d.SolCreate = (decltype(d.SolCreate))dlsym(d.sol, "cusolverDnCreate");
       d.SolDestroy = (decltype(d.SolDestroy))dlsym(d.sol, "cusolverDnDestroy");
@@ -149,8 +138,8 @@ Dla& dla() {
       d.Orgqr = (decltype(d.Orgqr))dlsym(d.sol, "cusolverDnDorgqr");
     }
   }
-  if (!d.BlasCreate || !d.Dgemm || !d.Dsyrk || !d.SolCreate || !d.Syevd || !d.Geqrf || !d.Orgqr)
-    fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: libcublas / libcusolver not loadable (needed by glsgpu_sur_reduce)");
+  if (!d.SolCreate || !d.Syevd || !d.Geqrf || !d.Orgqr)
+    fail(GLSGPU_ERR_UNSUPPORTED, "glsgpu: libcusolver not loadable (the symmetric eigensolver of glsgpu_sur_reduce)");
   return d;
 }
 
@@ -200,7 +189,12 @@ struct glsgpu_sur {
   std::vector<int64_t> rows_b;      // rows of block b in the reference's operator (cost model)
   double* Xqr = nullptr;            // pre-scaled QR source D^-1/2 X (two weights per block); null: X * w_b
   int rank_msg = 0;                 // 1: plain qr_thin (mv_reduce) wording of RankDeficient
-  double* omegaInvT = nullptr;      // PCG-NE: Omega^-1 (row-major, as omegaT), built on first use
+  double* omegaInvT = nullptr;      // (unused since the device PCG-NE applies chol_solve; kept null)
+  double *neLr = nullptr, *neLc = nullptr;  // PCG-NE: L = cholesky(Omega), row-major and column-major
+  double* nebuf = nullptr;          // PCG-NE n-vectors: x, f, p, gp, x_best, v, h
+  cudaGraphExec_t ne_graph = nullptr;
+  int ne_chunk = 0;
+  TraceRowD* ne_rows = nullptr;
   double* d_ones = nullptr;         // PCG-NE: unit row weights for the X' pass
   const double* X = nullptr;
   int64_t ldx = 0;
@@ -283,6 +277,7 @@ struct glsgpu_sur {
   bool coll = false;  // collective path (NCCL all-gathers, cross-rank TSQR level); also nranks == 1 + id
   bool use_stream = false;  // TMA-staged passes (n_i <= 128, 16-byte aligned X columns, ldx >= ldm)
   bool qtiled = false;      // Q tile-contiguous: block b, rows [256 k, 256 k + 256) contiguous (n_i <= 32)
+  bool no_qtile = false;    // keep Q column-major (ld ldm): a QR-only handle whose Q is read out as a matrix
   // wide blocks (some n_i > 32, all <= 128): the QR writes column-major Q; the streaming passes read a tiled copy
   // with 64-row tiles (one contiguous bulk copy per tile instead of n_i strided 512-byte segments)
   double* qt = nullptr;
@@ -701,10 +696,15 @@ std::pair<double*, int> pass_diag(glsgpu_sur* h, const double* est, const SolveS
     return {h->rpart, grid};
   }
   ColArgs x = base_args(h);
-  x.A = h->X;
-  x.lda = h->ldx;
-  x.avalid = h->M;
-  x.vec = est;
+  if (s_q) {  // Q source (column-major Q on this path)
+    x.qdiag = 1;
+    x.vec = s_q;
+  } else {
+    x.A = h->X;
+    x.lda = h->ldx;
+    x.avalid = h->M;
+    x.vec = est;
+  }
   x.gate = gate;
   launch_colpass<MODE_DIAG>(h, x, st);
   return {h->rpart, h->G * h->nch};
@@ -1292,7 +1292,7 @@ void alloc_common(glsgpu_sur* h) {
   h->use_stream = h->nmax <= 128 && h->ldx >= h->ldm && (h->ldx % 2) == 0 &&
                   (reinterpret_cast<uintptr_t>(h->X) % 16) == 0 && std::getenv("GLSGPU_NO_TMA") == nullptr;
   // tile-contiguous Q (256-row tiles per block) when every block takes the register-resident QR leaves
-  h->qtiled = h->use_stream && h->nmax <= 32 && std::getenv("GLSGPU_NO_QTILE") == nullptr;
+  h->qtiled = h->use_stream && h->nmax <= 32 && !h->no_qtile && std::getenv("GLSGPU_NO_QTILE") == nullptr;
   h->qoff.assign(h->G, 0);
   int64_t qsize = 0;
   for (int b = 0; b < h->G; ++b) {
@@ -1301,7 +1301,7 @@ void alloc_common(glsgpu_sur* h) {
   }
   h->qsize = qsize;
   h->Q = dalloc<double>((size_t)qsize);
-  if (h->use_stream && !h->qtiled && std::getenv("GLSGPU_NO_QTILE") == nullptr) {
+  if (h->use_stream && !h->qtiled && !h->no_qtile && std::getenv("GLSGPU_NO_QTILE") == nullptr) {
     // tile rows = what pass C and pass B (QR mode) pick for these widths, so their tiles move as one bulk copy
     h->qt_rows = 0;
     h->qt_rows = (int)std::min(stream_cfg(h, 1, stream_nvec<SMODE_C>()).T, stream_cfg(h, 1, stream_nvec<SMODE_B>()).T);
@@ -1341,6 +1341,9 @@ void destroy_impl(glsgpu_sur* h) {
   cudaSetDevice(h->dev);
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->ne_graph) cudaGraphExecDestroy(h->ne_graph);
+  for (double* q : {h->neLr, h->neLc, h->nebuf})
+    if (q) cudaFree(q);
   for (auto e : h->tev) cudaEventDestroy(e);
   void* ptrs[] = {h->d_nb, h->d_p0, h->d_r0, h->d_wts, h->d_wtc, h->Xqr, h->omegaInvT, h->d_ones, h->qt, h->d_qtoff,
                   h->X_own, h->Y_own, h->Q, h->R, h->omegaT, h->d_items,
@@ -1636,7 +1639,8 @@ __global__ void k_set_t0(SolveState* st) { st->t0 = globaltimer(); }
 
 // PCG-NE: out_b = X_b v_b (rows < M; padding rows 0), grid.y = block
 __global__ void k_xapply(Geo g, const double* __restrict__ X, int64_t ldx, const double* __restrict__ v,
-                         double* __restrict__ out) {
+                         double* __restrict__ out, const SolveState* st = nullptr) {
+  if (st && !st->active) return;
   const int b = blockIdx.y;
   const int nb = g.nb[b];
   const int64_t p0 = g.p0[b];
@@ -1688,7 +1692,8 @@ void diag_row(glsgpu_sur* h, int xv_mode, bool gated, int64_t row) {
   const int gate = gated ? 2 : 0;
   const SolveState* gst = gated ? h->st : nullptr;
   Geo g = geo_of(h);
-  const bool q = xv_mode == GLSGPU_XV_QR && h->use_stream;
+  // the same on every rank (ranks may differ in use_stream): both pass kinds have a Q-source form
+  const bool q = xv_mode == GLSGPU_XV_QR;
   if (!q) require_x(h, "trace diagnostics (xv_mode X)");
   pass_qt(h, MODE_QT_D, nullptr, h->st, 0, gate);
   reduce_t_global(h, h->t2, gst, gate);
@@ -1822,6 +1827,31 @@ glsgpu_sur* create_host_owned(int G, int64_t M, int64_t M_global, const int64_t*
     throw;
   }
   return h;
+}
+
+// C = op(A) op(B) on the DMMA GEMM of gemm.cuh (column-major; split-K when the tile grid is smaller than the GPU);
+// lower: only the lower-triangle tiles of a square C (the Gram for a lower-triangle eigensolver)
+void dgemm_dev(cudaStream_t s, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, bool tA, const double* B,
+               int64_t ldb, bool tB, double* C, int64_t ldc, bool lower, std::vector<void*>& bufs) {
+  const int64_t tm = (m + GM_BM - 1) / GM_BM, tn = (n + GM_BN - 1) / GM_BN;
+  const int64_t tiles = lower ? tm * (tm + 1) / 2 : tm * tn;
+  int splits = (int)std::min<int64_t>(std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles), 64);
+  splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, (k + 255) / 256));
+  const dim3 grid((unsigned)tm, (unsigned)tn, (unsigned)splits);
+  if (splits == 1) {
+    k_gemm_dmma<<<grid, GM_NT, 0, s>>>(m, n, k, A, lda, tA ? 1 : 0, B, ldb, tB ? 1 : 0, C, ldc, 0, lower ? 1 : 0);
+    CKL("k_gemm_dmma");
+    return;
+  }
+  const int64_t stride = ldc * n;
+  double* parts = dalloc<double>((size_t)(stride * splits));
+  bufs.push_back(parts);
+  CK(cudaMemsetAsync(parts, 0, sizeof(double) * stride * splits, s));
+  k_gemm_dmma<<<grid, GM_NT, 0, s>>>(m, n, k, A, lda, tA ? 1 : 0, B, ldb, tB ? 1 : 0, parts, ldc, stride, lower ? 1 : 0);
+  CKL("k_gemm_dmma split");
+  k_gemm_reduce<<<(unsigned)std::min<int64_t>((m * n + 255) / 256, 148 * 8), 256, 0, s>>>(m, n, parts, stride, splits, C,
+                                                                                         ldc);
+  CKL("k_gemm_reduce");
 }
 
 }  // namespace
@@ -2769,8 +2799,8 @@ int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, con
   CK(cudaSetDevice(device));
   Dla& L = dla();
   cudaStream_t s = nullptr;
-  cublasHandle_t hb = nullptr;
   cusolverDnHandle_t hs = nullptr;
+  glsgpu_sur* qh = nullptr;  // the basis' TSQR (a one-block QR-only handle)
   std::vector<void*> bufs;
   auto alloc = [&](size_t count) {
     double* p = dalloc<double>(count);
@@ -2779,15 +2809,14 @@ int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, con
   };
   auto cleanup = [&]() {
     if (s) cudaStreamSynchronize(s);
+    if (qh) destroy_impl(qh);
+    qh = nullptr;
     for (void* p : bufs) cudaFree(p);
-    if (hb) L.BlasDestroy(hb);
     if (hs) L.SolDestroy(hs);
     if (s) cudaStreamDestroy(s);
   };
   try {
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    blas_check(L.BlasCreate(&hb), "cublasCreate");
-    blas_check(L.BlasSetStream(hb, s), "cublasSetStream");
     blas_check(L.SolCreate(&hs), "cusolverDnCreate");
     blas_check(L.SolSetStream(hs, s), "cusolverDnSetStream");
     double* dX = alloc((size_t)(M * n));
@@ -2797,10 +2826,11 @@ int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, con
     int* info = reinterpret_cast<int*>(alloc(1));
     CK(cudaMemcpyAsync(dX, X, sizeof(double) * M * n, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dY, Y, sizeof(double) * M * G, cudaMemcpyHostToDevice, s));
-    const double one = 1.0, zero = 0.0;
-    // W'W (lower triangle) and its eigen-decomposition (sym_eig, linalg.cpp:376-400: ascending eigenvalues)
-    blas_check(L.Dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)n, (int)M, &one, dX, (int)M, &zero, gram, (int)n),
-               "cublasDsyrk");
+    // W'W (lower triangle) on the DMMA GEMM, then its eigen-decomposition (sym_eig, linalg.cpp:376-400: ascending
+    // eigenvalues).  The eigensolver is cuSOLVER's syevd: a dense symmetric n x n eigenproblem (tridiagonal
+    // reduction + divide and conquer), O(n^3) once per model, off the iteration path; the reference's own tred2 /
+    // tql2 is a different algorithm anyway, so the basis is pinned on what the reduction preserves
+    dgemm_dev(s, n, n, M, dX, M, true, dX, M, false, gram, n, true, bufs);
     int lwork = 0;
     blas_check(L.SyevdBuf(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, gram, (int)n, lam, &lwork),
                "cusolverDnDsyevd_bufferSize");
@@ -2847,26 +2877,44 @@ int glsgpu_sur_reduce(int G, int64_t M, const int64_t* n_i, const double* X, con
     double* vq = alloc((size_t)(n * q));
     CK(cudaMemcpyAsync(vq, vh.data(), sizeof(double) * n * q, cudaMemcpyHostToDevice, s));
     double* B = alloc((size_t)(M * q));
-    blas_check(L.Dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)M, (int)q, (int)n, &one, dX, (int)M, vq, (int)n, &zero, B, (int)M),
-               "cublasDgemm W V");
-    // re-orthonormalise: basis = qr_thin(basis).q (structured.cpp:170)
-    double* tau = alloc((size_t)q);
-    int lw2 = 0, lw3 = 0;
-    blas_check(L.GeqrfBuf(hs, (int)M, (int)q, B, (int)M, &lw2), "cusolverDnDgeqrf_bufferSize");
-    blas_check(L.OrgqrBuf(hs, (int)M, (int)q, (int)q, B, (int)M, tau, &lw3), "cusolverDnDorgqr_bufferSize");
-    double* w2 = alloc((size_t)std::max(std::max(lw2, lw3), 1));
-    blas_check(L.Geqrf(hs, (int)M, (int)q, B, (int)M, tau, w2, std::max(lw2, lw3), info), "cusolverDnDgeqrf");
-    blas_check(L.Orgqr(hs, (int)M, (int)q, (int)q, B, (int)M, tau, w2, std::max(lw2, lw3), info), "cusolverDnDorgqr");
+    dgemm_dev(s, M, q, n, dX, M, false, vq, n, false, B, M, false, bufs);  // W V_q Lambda_q^-1/2
+    // re-orthonormalise: basis = qr_thin(basis).q (structured.cpp:170): the library's TSQR as a one-block QR-only
+    // handle (Householder leaves + tree, explicit Q); cuSOLVER geqrf / orgqr past the TSQR kernels' 512 columns
+    double* Bq = B;
+    if (q <= 512) {
+      CK(cudaStreamSynchronize(s));
+      const double one1 = 1.0;
+      const int64_t nq[1] = {q};
+      qh = create_common(1, M, nq, &one1, nullptr, device, -1, 0, 1, nullptr, nullptr, /*qr_only=*/true);
+      qh->rank_msg = 1;  // qr_thin's wording of RankDeficient
+      qh->no_qtile = true;
+      qh->X = B;
+      qh->ldx = M;
+      qh->Y = dY;
+      qh->ldy = M;
+      alloc_common(qh);
+      run_qr(qh);
+      Bq = alloc((size_t)(M * q));
+      CK(cudaMemcpy2DAsync(Bq, M * sizeof(double), qh->Q, qh->ldm * sizeof(double), M * sizeof(double), q,
+                           cudaMemcpyDeviceToDevice, qh->s));
+      CK(cudaStreamSynchronize(qh->s));
+    } else {
+      double* tau = alloc((size_t)q);
+      int lw2 = 0, lw3 = 0;
+      blas_check(L.GeqrfBuf(hs, (int)M, (int)q, B, (int)M, &lw2), "cusolverDnDgeqrf_bufferSize");
+      blas_check(L.OrgqrBuf(hs, (int)M, (int)q, (int)q, B, (int)M, tau, &lw3), "cusolverDnDorgqr_bufferSize");
+      double* w2 = alloc((size_t)std::max(std::max(lw2, lw3), 1));
+      blas_check(L.Geqrf(hs, (int)M, (int)q, B, (int)M, tau, w2, std::max(lw2, lw3), info), "cusolverDnDgeqrf");
+      blas_check(L.Orgqr(hs, (int)M, (int)q, (int)q, B, (int)M, tau, w2, std::max(lw2, lw3), info), "cusolverDnDorgqr");
+    }
     // reduced blocks and responses: basis' X_i, basis' Y (structured.cpp:172-176)
     double* xr = alloc((size_t)(q * n));
     double* yr = alloc((size_t)(q * G));
-    blas_check(L.Dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)q, (int)n, (int)M, &one, B, (int)M, dX, (int)M, &zero, xr, (int)q),
-               "cublasDgemm basis' X");
-    blas_check(L.Dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)q, G, (int)M, &one, B, (int)M, dY, (int)M, &zero, yr, (int)q),
-               "cublasDgemm basis' Y");
+    dgemm_dev(s, q, n, M, Bq, M, true, dX, M, false, xr, q, false, bufs);
+    dgemm_dev(s, q, G, M, Bq, M, true, dY, M, false, yr, q, false, bufs);
     CK(cudaMemcpyAsync(X_red, xr, sizeof(double) * q * n, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(Y_red, yr, sizeof(double) * q * G, cudaMemcpyDeviceToHost, s));
-    if (basis) CK(cudaMemcpyAsync(basis, B, sizeof(double) * M * q, cudaMemcpyDeviceToHost, s));
+    if (basis) CK(cudaMemcpyAsync(basis, Bq, sizeof(double) * M * q, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     *q_out = q;
   } catch (...) {
@@ -2897,8 +2945,8 @@ int glsgpu_pcg_ne(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const double* 
   else glsgpu_default_config(&cfg);
   const int G = h->G;
   const int64_t n = h->n;
-  // cholesky(Omega) (linalg.cpp:174-193) -> Omega^-1
-  if (!h->omegaInvT) {
+  // cholesky(Omega) (linalg.cpp:174-193): the factor of Sigma = Omega (x) I_M is L (x) I_M (pcg.cpp:369-373)
+  if (!h->neLr) {
     std::vector<double> L((size_t)G * G, 0.0);
     double max_diag = 0.0;
     for (int i = 0; i < G; ++i) max_diag = std::max(max_diag, std::fabs(h->omega_h[(size_t)i * G + i]));
@@ -2914,45 +2962,37 @@ int glsgpu_pcg_ne(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const double* 
         L[i + (size_t)j * G] = v / L[j + (size_t)j * G];
       }
     }
-    std::vector<double> inv((size_t)G * G);
-    for (int c = 0; c < G; ++c) {  // column c of (L L')^-1
-      std::vector<double> x((size_t)G, 0.0);
-      x[(size_t)c] = 1.0;
-      for (int i = 0; i < G; ++i) {
-        double s = x[(size_t)i];
-        for (int j = 0; j < i; ++j) s -= L[i + (size_t)j * G] * x[(size_t)j];
-        x[(size_t)i] = s / L[i + (size_t)i * G];
-      }
-      for (int i = G; i-- > 0;) {
-        double s = x[(size_t)i];
-        for (int j = i + 1; j < G; ++j) s -= L[j + (size_t)i * G] * x[(size_t)j];
-        x[(size_t)i] = s / L[i + (size_t)i * G];
-      }
-      for (int i = 0; i < G; ++i) inv[(size_t)i + (size_t)c * G] = x[(size_t)i];
-    }
-    std::vector<double> t((size_t)G * G);
-    for (int p = 0; p < G; ++p)
-      for (int c = 0; c < G; ++c)
-        t[(size_t)p * G + c] = 0.5 * (inv[(size_t)p + (size_t)c * G] + inv[(size_t)c + (size_t)p * G]);
-    h->omegaInvT = dalloc<double>((size_t)G * G);
-    CK(cudaMemcpy(h->omegaInvT, t.data(), sizeof(double) * G * G, cudaMemcpyHostToDevice));
+    std::vector<double> Lr((size_t)G * G);
+    for (int i = 0; i < G; ++i)
+      for (int j = 0; j < G; ++j) Lr[(size_t)i * G + j] = L[i + (size_t)j * G];
+    h->neLr = dalloc<double>((size_t)G * G);
+    h->neLc = dalloc<double>((size_t)G * G);
+    CK(cudaMemcpy(h->neLr, Lr.data(), sizeof(double) * G * G, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->neLc, L.data(), sizeof(double) * G * G, cudaMemcpyHostToDevice));
     std::vector<double> ones((size_t)G, 1.0);
     h->d_ones = dalloc<double>((size_t)G);
     CK(cudaMemcpy(h->d_ones, ones.data(), sizeof(double) * G, cudaMemcpyHostToDevice));
+    h->nebuf = dalloc<double>((size_t)n * 7);
   }
-  ensure_solver(h, 1);
+  const int64_t max_iter = cfg.max_iter ? cfg.max_iter : 2 * n;
+  const int64_t cap_d = std::max<int64_t>(1, std::min<int64_t>(max_iter + 1, rows ? std::max<int64_t>(rows_cap, 1) : 1));
+  ensure_solver(h, cap_d);
   cudaStream_t s = h->s;
   Geo g = geo_of(h);
+  double *x = h->nebuf, *f = x + n, *p = f + n, *gp = p + n, *xb = gp + n, *v = xb + n, *hv = v + n;
   const dim3 rgrid((unsigned)std::min<int64_t>((h->ldm + NT - 1) / NT, 64), (unsigned)G);
-  // Sigma^-1 x: the Kronecker pass with Omega^-1 in place of Omega
-  auto sigma_inv = [&](const double* src, double* out) {
-    double* keep = h->omegaT;
-    h->omegaT = h->omegaInvT;
-    launch_kron(h, src, nullptr, nullptr, nullptr, out, h->partA, 0, nullptr, nullptr);
-    h->omegaT = keep;
+  // chol_solve tile: T rows x G columns of shared memory (<= 160 KB)
+  const int cT = (int)std::max<int64_t>(32, std::min<int64_t>(128, (160 * 1024 / (8 * (int64_t)G)) / 32 * 32));
+  const size_t csm = (size_t)cT * G * sizeof(double);
+  CK(cudaFuncSetAttribute(k_chol_solve_kron, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+  const int cgrid = (int)std::min<int64_t>((h->M + cT - 1) / cT, 148 * 8);
+  auto chol = [&](double* vec, const SolveState* gst) {
+    k_chol_solve_kron<<<cgrid, cT, csm, s>>>(G, h->ldm, h->M, h->neLr, h->neLc, vec, gst);
+    if (!h->capturing) h->launches++;
+    CKL("k_chol_solve_kron");
   };
-  // X' x over the user X (unit row weights)
-  auto xt = [&](const double* in, double* out) {
+  // X' x over the user X (unit row weights), gated on st->active when gst is given
+  auto xt = [&](const double* in, double* out, const SolveState* gst) {
     Geo gx = g;
     gx.wts = gx.wtc = h->d_ones;
     ColArgs a = base_args(h);
@@ -2960,176 +3000,139 @@ int glsgpu_pcg_ne(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const double* 
     a.lda = h->ldx;
     a.avalid = h->M;
     a.vin = in;
+    a.gate = gst ? 1 : 0;
     if (h->n_narrow) {
       a.blocks = h->d_blk_narrow;
-      k_colpass<MODE_QT_V, true><<<h->n_narrow * h->nch, NT, 0, s>>>(gx, a, nullptr);
-      h->launches++;
+      k_colpass<MODE_QT_V, true><<<h->n_narrow * h->nch, NT, 0, s>>>(gx, a, gst);
+      if (!h->capturing) h->launches++;
     }
     if (h->n_wide) {
       a.blocks = h->d_blk_wide;
-      k_colpass<MODE_QT_V, false><<<h->n_wide * h->nch, NT, (size_t)h->CH * sizeof(double), s>>>(gx, a, nullptr);
-      h->launches++;
+      k_colpass<MODE_QT_V, false><<<h->n_wide * h->nch, NT, (size_t)h->CH * sizeof(double), s>>>(gx, a, gst);
+      if (!h->capturing) h->launches++;
     }
     CKL("k_colpass X'");
-    launch_reduce_t(h, out, nullptr, 0);
+    launch_reduce_t(h, out, gst, gst ? 1 : 0);
   };
-  std::vector<double> hv((size_t)n), gp((size_t)n);
-  auto apply_g = [&](const std::vector<double>& v, std::vector<double>& out) {
-    CK(cudaMemcpyAsync(h->t, v.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    k_xapply<<<rgrid, NT, 0, s>>>(g, h->X, h->ldx, h->t, h->r);
-    h->launches++;
+  // gp = X' Sigma^-1 X v (pcg.cpp:378-380)
+  auto apply_g = [&](const double* in, double* out, const SolveState* gst) {
+    k_xapply<<<rgrid, NT, 0, s>>>(g, h->X, h->ldx, in, h->r, gst);
+    if (!h->capturing) h->launches++;
     CKL("k_xapply");
-    sigma_inv(h->r, h->su);
-    xt(h->su, h->t2);
-    CK(cudaMemcpyAsync(out.data(), h->t2, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    chol(h->r, gst);
+    xt(h->r, out, gst);
   };
-  auto dot = [](const std::vector<double>& a, const std::vector<double>& b) {
-    double acc = 0.0;
-    for (size_t i = 0; i < a.size(); ++i) acc += a[i] * b[i];
-    return acc;
-  };
-  const auto t0 = std::chrono::steady_clock::now();
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, s));
-  const int64_t max_iter = cfg.max_iter ? cfg.max_iter : 2 * n;
-  const int64_t stride = cfg.record_z_every ? cfg.record_z_every : 1;
-  // crude norm probe for the breakdown scale (pcg.cpp:381-392)
-  double g_scale = 0.0;
-  {
-    std::vector<double> v((size_t)n, 1.0 / std::sqrt((double)n));
-    for (int it = 0; it < 12; ++it) {
-      apply_g(v, gp);
-      v = gp;
-      g_scale = std::sqrt(dot(v, v));
-      if (g_scale == 0.0) break;
-      for (double& t : v) t /= g_scale;
-    }
+  SolveState hs;
+  std::memset(&hs, 0, sizeof(hs));
+  hs.tol_rel = cfg.tol_rel;
+  hs.breakdown_tol = cfg.breakdown_tol;
+  hs.growth_tol = cfg.growth_tol;
+  hs.max_iter = max_iter;
+  hs.stride = cfg.record_z_every ? cfg.record_z_every : 1;
+  hs.stagnation_window = cfg.stagnation_window;
+  hs.growth_window = cfg.growth_window;
+  hs.rows_cap = cap_d;
+  hs.breakdown_iter = -1;
+  hs.active = 1;
+  hs.cont = 1;  // the norm probe runs while cont
+  hs.term = T_MAXITER;
+  hs.have_beta = beta_true ? 1 : 0;
+  CK(cudaMemcpyAsync(h->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+  k_set_t0<<<1, 1, 0, s>>>(h->st);
+  h->launches++;
+  if (beta_true) CK(cudaMemcpyAsync(h->beta_d, beta_true, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  // crude norm probe for the breakdown scale (pcg.cpp:381-392): v = 1/sqrt(n)
+  k_fill<<<(unsigned)std::min<int64_t>((n + NT - 1) / NT, 148), NT, 0, s>>>(v, 1.0 / std::sqrt((double)n), n);
+  h->launches++;
+  for (int it = 0; it < 12; ++it) {
+    apply_g(v, gp, nullptr);
+    k_ne_probe<<<1, NE_NT, 0, s>>>(h->st, gp, v, n);
+    h->launches++;
+    CKL("k_ne_probe");
   }
-  // h = X' Sigma^-1 y
+  // h = X' Sigma^-1 y; x = 0, f = -h, p = f, c, row 0 (pcg.cpp:396-421)
   CK(cudaMemsetAsync(h->r, 0, sizeof(double) * h->ldm * G, s));
   k_ysub<<<rgrid, NT, 0, s>>>(g, h->Y, h->ldy, h->r);
   h->launches++;
-  sigma_inv(h->r, h->su);
-  xt(h->su, h->t2);
-  CK(cudaMemcpyAsync(hv.data(), h->t2, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  std::vector<double> x((size_t)n, 0.0), f((size_t)n), kf, p, x_best;
-  for (int64_t k = 0; k < n; ++k) f[(size_t)k] = -1.0 * hv[(size_t)k];
-  kf = f;
-  double c = std::max(dot(f, kf), 0.0);
-  const double c1 = c, threshold = cfg.tol_rel * cfg.tol_rel * c1;
-  p = kf;
-  double k_gain = 0.0;
-  auto c_floor = [&](double fn2, double kfn) {
-    if (fn2 > 0.0) k_gain = std::max(k_gain, kfn / std::sqrt(fn2));
-    return 16.0 * 2.220446049250313e-16 * std::max(k_gain, 1e-3) * fn2;
-  };
-  (void)c_floor(dot(f, f), std::sqrt(dot(kf, kf)));
-  int64_t nrows = 0;
-  auto push_row = [&](int64_t iter, double cval, bool sampled) {
-    if (rows && nrows < rows_cap) {
-      glsgpu_trace_row& r = rows[nrows];
-      r.iter = iter;
-      r.c = cval;
-      r.aug_residual_norm = r.dual_feas_norm = std::sqrt(dot(f, f));
-      if (sampled && beta_true) {
-        double acc = 0.0;
-        for (int64_t k = 0; k < n; ++k) acc += (x[(size_t)k] - beta_true[k]) * (x[(size_t)k] - beta_true[k]);
-        r.rmse = std::sqrt(acc / (double)n);
-      } else {
-        r.rmse = std::nan("");
-      }
-      r.elapsed_ns = (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
-                         std::chrono::steady_clock::now() - t0).count();
+  chol(h->r, nullptr);
+  xt(h->r, hv, nullptr);
+  const double* bt = beta_true ? h->beta_d : nullptr;
+  k_ne_init<<<1, NE_NT, 0, s>>>(h->st, hv, x, f, p, xb, bt, h->rows_d, n);
+  h->launches++;
+  CKL("k_ne_init");
+  // the iteration: CUDA graphs of `chunk` steps, device-side control
+  int chunk = cfg.graph_chunk > 0 ? cfg.graph_chunk : 16;
+  if (!h->ne_graph || h->ne_chunk != chunk || h->ne_rows != h->rows_d) {
+    if (h->ne_graph) CK(cudaGraphExecDestroy(h->ne_graph));
+    h->ne_graph = nullptr;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    h->capturing = true;
+    for (int k = 0; k < chunk; ++k) {
+      apply_g(p, gp, h->st);
+      k_ne_step<<<1, NE_NT, 0, s>>>(h->st, gp, x, f, p, xb, h->beta_d, h->rows_d, n);
+      CKL("k_ne_step");
     }
-    ++nrows;
-  };
-  push_row(0, c, true);
-  x_best = x;
-  double c_best = c;
-  int64_t best_iter = 0, stagnant = 0, done = 0, bd_iter = -1;
-  int term = T_MAXITER;
-  if (c1 == 0.0) {
-    term = T_CONVERGED;
-  } else {
-    for (int64_t i = 1; i <= max_iter; ++i) {
-      apply_g(p, gp);
-      const double d = dot(p, gp);
-      if (std::fabs(d) <= cfg.breakdown_tol * dot(p, p) * std::max(g_scale, 1e-300)) {
-        term = T_BREAKDOWN;
-        bd_iter = i;
-        break;
-      }
-      const double lambda = c / d;
-      for (int64_t k = 0; k < n; ++k) x[(size_t)k] += -lambda * p[(size_t)k];
-      for (int64_t k = 0; k < n; ++k) f[(size_t)k] += -lambda * gp[(size_t)k];
-      kf = f;
-      double c_next = dot(f, kf);
-      done = i;
-      const bool sampled = (i % stride == 0) || c_next <= threshold || i == max_iter;
-      push_row(i, c_next, sampled);
-      const double floor_c = c_floor(dot(f, f), std::sqrt(dot(kf, kf)));
-      const bool exhausted = std::fabs(c_next) <= floor_c / 64.0 || (std::fabs(c_next) <= floor_c && c_next <= 1e-6 * c);
-      if (c_next < 0.0 && std::fabs(c_next) > floor_c) {
-        term = T_BREAKDOWN;
-        bd_iter = i;
-        break;
-      }
-      if (c_next < 0.0) c_next = 0.0;
-      if (c_next < c_best) {
-        c_best = c_next;
-        x_best = x;
-        best_iter = i;
-      }
-      if (c_next <= threshold || exhausted) {
-        term = T_CONVERGED;
-        break;
-      }
-      if (std::fabs(c_next - c) <= 1e-15 * c) {
-        if (++stagnant >= cfg.stagnation_window) {
-          term = T_STAGNATION;
-          break;
-        }
-      } else {
-        stagnant = 0;
-      }
-      if (c_next > cfg.growth_tol * c_best && i - best_iter >= cfg.growth_window) {
-        term = T_BREAKDOWN;
-        bd_iter = i;
-        break;
-      }
-      const double mu = c_next / c;
-      c = c_next;
-      for (int64_t k = 0; k < n; ++k) p[(size_t)k] = kf[(size_t)k] + mu * p[(size_t)k];
-    }
+    h->capturing = false;
+    CK(cudaStreamEndCapture(s, &graph));
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &nn));
+    CK(cudaGraphInstantiate(&h->ne_graph, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    h->ne_chunk = chunk;
+    h->ne_rows = h->rows_d;
   }
-  const bool keep_last = term == T_CONVERGED;
-  const std::vector<double>& b = keep_last ? x : x_best;
-  std::memcpy(b_out, b.data(), sizeof(double) * n);
-  if (w_out) {  // implied_w(b) = Sigma^-1 (y - X b)
-    CK(cudaMemcpyAsync(h->t, b.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    k_xapply<<<rgrid, NT, 0, s>>>(g, h->X, h->ldx, h->t, h->r);
+  // have_beta gates the rmse: the captured step reads beta through h->beta_d only when st->have_beta
+  for (;;) {
+    CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!h->st_host->active) break;
+    CK(cudaGraphLaunch(h->ne_graph, s));
+    h->launches += (int64_t)chunk * (4 + (h->n_narrow ? 1 : 0) + (h->n_wide ? 1 : 0));
+  }
+  SolveState fin = *h->st_host;
+  const bool keep_last = fin.term == T_CONVERGED;
+  const double* bsel = keep_last ? x : xb;
+  CK(cudaMemcpyAsync(b_out, bsel, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  if (w_out) {  // implied_w(b) = chol_solve(lower, y - X b) (pcg.cpp:414-416,503)
+    k_xapply<<<rgrid, NT, 0, s>>>(g, h->X, h->ldx, bsel, h->r);
     k_ysub<<<rgrid, NT, 0, s>>>(g, h->Y, h->ldy, h->r);
     h->launches += 2;
-    sigma_inv(h->r, h->su);
-    d2h_mvec(h, w_out, h->su);
+    chol(h->r, nullptr);
+    d2h_mvec(h, w_out, h->r);
+  }
+  const int64_t nrows = fin.done + 1;
+  std::vector<TraceRowD> rd;
+  if (rows && rows_cap > 0) {
+    const int64_t k = std::min<int64_t>(std::min<int64_t>(nrows, rows_cap), cap_d);
+    rd.resize((size_t)k);
+    CK(cudaMemcpyAsync(rd.data(), h->rows_d, sizeof(TraceRowD) * k, cudaMemcpyDeviceToHost, s));
   }
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < rd.size(); ++i) {
+    rows[i].iter = rd[i].iter;
+    rows[i].c = rd[i].c;
+    rows[i].aug_residual_norm = rd[i].aug;
+    rows[i].dual_feas_norm = rd[i].dual;
+    rows[i].rmse = rd[i].rmse;
+    rows[i].elapsed_ns = rd[i].elapsed_ns;
+  }
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  res->iterations = done;
-  res->termination = term;
+  res->iterations = fin.done;
+  res->termination = fin.term;
   res->w1_projected = 0;
-  res->breakdown_iteration = bd_iter;
-  res->residual_seminorm = keep_last ? c : c_best;
+  res->breakdown_iteration = fin.term == T_BREAKDOWN ? fin.breakdown_iter : -1;
+  res->residual_seminorm = keep_last ? fin.c : fin.c_best;
   res->n_rows = nrows;
-  res->sigma_scale = g_scale;
+  res->sigma_scale = fin.sigma_scale;
   res->solve_ms = ms;
   API_END((int*)nullptr)
 }

@@ -371,6 +371,7 @@ struct ColArgs {
   int xv_from_x;        // 1: xv = X v; 0: xv = Q s / w_b
   int sel_best;         // MODE_QT_D: use the selected final buffer (cur or best)
   int gate;             // 0: always run; 1: only while st->active; 2: only when st->diag_now
+  int qdiag;            // MODE_DIAG with A = Q (xv_mode QR): X est = Q s / w, column partials Q' w
 };
 
 template <int MODE, bool FUSED>
@@ -461,6 +462,7 @@ __global__ void __launch_bounds__(NT) k_colpass(Geo g, ColArgs a, const SolveSta
         if (k < a.avalid)
           for (int j = 0; j < nb; ++j) xe = xe + Ab[(int64_t)j * a.lda + k] * svec_s[j];
       }
+      if (a.qdiag) xe = xe / wgt;
       const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
       const double res = yv - ((a.swb[cur][off] + (-lp) * a.su[off]) + xe);
       if (k < g.M) rsum += res * res;

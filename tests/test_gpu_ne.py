@@ -1,9 +1,12 @@
 """GPU tests of the PCG-NE comparison solver (glsgpu_pcg_ne, pcg_normal_equations of pcg.cpp:364-511) against
 the restatement (bitwise the reference, tests/test_oracle_ne.py) and the reference fixtures ne_*.npz.
-Sigma^-1 is applied on the device as a Kronecker pass with Omega^-1 instead of the reference's per-row
-triangular solves, so the bar is the SUR one: same termination and iterations, b to 1e-10, where the run is
-not decided by roundoff; unconverged (MaxIter) runs are judged against the restatement's own drift under a
-change of summation order."""
+
+The whole CG loop runs on the device (csrc/ne.cuh: graph-captured steps, device-side termination logic), and
+Sigma^-1 is the reference's own per-row chol_solve with L = cholesky(Omega) (bitwise per row).  What differs
+from the reference is only the summation order of the long sums (X' columns, n-vector dots), so the bar is
+the SUR one: same termination and iterations, b to 1e-10 on converged runs; unconverged (MaxIter) runs of
+the squared-condition normal equations carry the restatement's own drift under a change of summation order
+and are judged against it."""
 import glob
 import os
 
@@ -50,12 +53,13 @@ def check(g, o, o1):
     assert s.termination.name == o.termination
     assert s.iterations == o.iterations
     spread = rel(o1.b, o.b)
-    assert rel(s.b, o.b) <= max(1e-9, 10.0 * spread), (rel(s.b, o.b), spread)
+    bar = 1e-10 if o.termination == "Converged" and spread <= 1e-11 else max(1e-10, 10.0 * spread)
+    assert rel(s.b, o.b) <= bar, (rel(s.b, o.b), spread)
     # the c trace agrees while it carries signal (relative to c1; rows at the roundoff floor carry none)
     c_g, c_o, c_1 = np.asarray(g.trace.rows["c"]), np.asarray(o.trace["c"]), np.asarray(o1.trace["c"])
     k = min(len(c_o), len(c_g), len(c_1))
     tol = 10.0 * np.abs(c_1[:k] - c_o[:k]) + 1e-6 * np.abs(c_o[:k]) + 1e-9 * c_o[0]
-    sig = c_o[:k] >= 1e-5 * c_o[0]  # below, the normal equations carry their rounding noise (Omega^-1 vs L L' solves)
+    sig = c_o[:k] >= 1e-5 * c_o[0]  # below, the normal equations carry their rounding noise
     bad = np.flatnonzero((np.abs(c_g[:k] - c_o[:k]) > tol) & sig)
     assert bad.size == 0, (bad[:5], c_g[bad[:5]], c_o[bad[:5]], c_1[bad[:5]])
 

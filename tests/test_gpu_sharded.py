@@ -113,8 +113,12 @@ def test_sharded_ranks_match_oracle(name, mk, P, part, mode):
     assert g1.solution.iterations == g0.solution.iterations
     assert rel(g0.solution.b, g1.solution.b) <= 1e-12
     k = min(5, len(g1.trace.rows))
-    for col in ("c", "aug_residual_norm", "dual_feas_norm", "rmse"):
+    for col in ("c", "aug_residual_norm", "rmse"):
         assert np.allclose(g0.trace.rows[col][:k], g1.trace.rows[col][:k], rtol=1e-10, equal_nan=True), col
+    # |X'w| sits at the roundoff level (w stays feasible): equal in absolute terms at that level
+    scale = float(np.nanmax(g1.trace.rows["aug_residual_norm"][:k]))
+    assert np.allclose(g0.trace.rows["dual_feas_norm"][:k], g1.trace.rows["dual_feas_norm"][:k], rtol=0,
+                       atol=1e-10 * scale)
     # w is this rank's rows of the unsharded w
     W = np.concatenate([out[r][0].solution.w.reshape(p.G, parts[r][1]) for r in range(P)], axis=1).ravel()
     assert rel(W, g1.solution.w) <= 1e-9
@@ -181,9 +185,13 @@ def test_qr_mode_diagnostics_from_q():
                      true_beta=p.beta)
     gq = api.pcg_aug(sur, op, config=api.PcgConfig(tol_rel=1e-12, max_iter=60, xv_mode="qr", diag_every=1),
                      true_beta=p.beta)
-    for col in ("aug_residual_norm", "dual_feas_norm", "rmse"):
+    for col in ("aug_residual_norm", "rmse"):
         a, b = gq.trace.rows[col][:20], gx.trace.rows[col][:20]
         assert np.allclose(a, b, rtol=1e-9, atol=1e-9 * np.nanmax(np.abs(b)), equal_nan=True), col
+    # |X'w| is a roundoff-level quantity (w stays feasible): the two forms agree at that level
+    scale = float(np.nanmax(gx.trace.rows["aug_residual_norm"][:20]))
+    assert np.allclose(gq.trace.rows["dual_feas_norm"][:20], gx.trace.rows["dual_feas_norm"][:20], rtol=0,
+                       atol=1e-10 * scale)
 
 
 def test_host_sharded_single_rank_update_and_stage():
