@@ -262,6 +262,9 @@ struct glsgpu_sur {
   bool x_released = false;  // X_own holds (or is receiving) the NEXT model's X: nothing may read it now
   double* Y_next = nullptr;
   double* t3 = nullptr;     // Q-side diagnostics: s = R est, then Q' w
+  // diag_every = 1 folded into passes B / C (SMODE_BD / SMODE_CD): the second and third column-partial sets
+  double *tpart2 = nullptr, *tpart3 = nullptr;
+  int fold = 0, graph_fold = -1;
   bool factors_ok = false;          // false after a rank-deficient update / refactor until a good one
   int fused = 0;     // fused_c in effect: Sigma pr in pass C (k_pass_c_mma), element-wise pass A (k_pass_a_ew)
   int graph_fused = -1;
@@ -444,10 +447,10 @@ void launch_colpass(glsgpu_sur* h, ColArgs a, const SolveState* st) {
   }
 }
 
-void launch_reduce_t(glsgpu_sur* h, double* out, const SolveState* st, int gate) {
+void launch_reduce_t(glsgpu_sur* h, double* out, const SolveState* st, int gate, const double* tp = nullptr) {
   const int per = NT / 32;
   const int64_t grid = (h->n + per - 1) / per;
-  k_reduce_t<<<(unsigned)grid, NT, 0, h->s>>>(h->tpart, h->n, h->nch, out, st, gate);
+  k_reduce_t<<<(unsigned)grid, NT, 0, h->s>>>(tp ? tp : h->tpart, h->n, h->nch, out, st, gate);
   if (!h->capturing) h->launches++;
   CKL("k_reduce_t");
 }
@@ -561,10 +564,14 @@ int launch_stream(glsgpu_sur* h, StreamArgs a, const SolveState* st) {
   a.S = c.S;
   a.stage_doubles = c.stage_doubles;
   // narrow blocks: one register-resident row sweep, column partials accumulated in it (k_stream FUSE)
-  if (h->nmax <= 32)
-    k_stream<MODE, true><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
-  else
-    k_stream<MODE, false><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
+  if constexpr (MODE == SMODE_BD || MODE == SMODE_CD) {
+    k_stream<MODE, true><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);  // narrow blocks only (h->fold)
+  } else {
+    if (h->nmax <= 32)
+      k_stream<MODE, true><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
+    else
+      k_stream<MODE, false><<<c.grid, NT, c.smem, h->s>>>(geo_of(h), a, st);
+  }
   if (!h->capturing) h->launches++;
   CKL("k_stream");
   return c.grid;
@@ -600,6 +607,8 @@ void stream_attrs(glsgpu_sur* h) {
   set((const void*)k_stream<SMODE_DIAG, false>, 0, 0);
   set((const void*)k_stream<SMODE_DIAG, true>, 0, 0);
   set((const void*)k_stream<SMODE_XS, false>, 0, 0);
+  set((const void*)k_stream<SMODE_BD, true>, 0, 0);
+  set((const void*)k_stream<SMODE_CD, true>, 0, 0);
 }
 
 // ---- pass wrappers: TMA-staged k_stream when possible, the register kernels otherwise
@@ -788,12 +797,12 @@ std::pair<const double*, int> combine1(glsgpu_sur* h, const double* partials, in
 }
 
 // tpart -> out[n], summed over chunks and then over ranks (gate as k_reduce_t).
-void reduce_t_global(glsgpu_sur* h, double* out, const SolveState* st, int gate) {
+void reduce_t_global(glsgpu_sur* h, double* out, const SolveState* st, int gate, const double* tp = nullptr) {
   if (!h->coll) {
-    launch_reduce_t(h, out, st, gate);
+    launch_reduce_t(h, out, st, gate, tp);
     return;
   }
-  launch_reduce_t(h, h->t_loc, st, gate);
+  launch_reduce_t(h, h->t_loc, st, gate, tp);
   allgather(h, h->t_loc, h->t_all, (size_t)h->n);
   k_sum_ranks<<<(unsigned)std::min<int64_t>((h->n + NT - 1) / NT, 148), NT, 0, h->s>>>(h->t_all, h->nranks, h->n,
                                                                                        out, st, gate);
@@ -1070,6 +1079,38 @@ void launch_formq(glsgpu_sur* h, int64_t max_rows, int grid, int smem, const QrI
   CKL("k_qr_formq");
 }
 
+// lane-per-column leaf kernels: the two-CTA-per-SM forms (default) or the original one-CTA form (GLSGPU_QR_LC1=1)
+bool qr_lc1() {
+  static const bool v = std::getenv("GLSGPU_QR_LC1") != nullptr;
+  return v;
+}
+const void* qrf_lc_fn() { return qr_lc1() ? (const void*)k_qr_factor_lc : (const void*)k_qr_factor_lc2; }
+const void* qrq_lc_fn() { return qr_lc1() ? (const void*)k_qr_formq_lc : (const void*)k_qr_formq_lc2; }
+size_t qr_lc_smem() { return qr_lc1() ? qrc_smem_bytes() : qrc2_smem_bytes(); }
+void launch_qrf_lc(glsgpu_sur* h, const QrItem* items, int count, int grid) {
+  if (qr_lc1()) k_qr_factor_lc<<<grid, QRC_NT, qrc_smem_bytes(), h->s>>>(items, count);
+  else k_qr_factor_lc2<<<grid, QRC_NT, qrc2_smem_bytes(), h->s>>>(items, count);
+  if (!h->capturing) h->launches++;
+  CKL("k_qr_factor_lc");
+}
+void launch_qrq_lc(glsgpu_sur* h, const QrItem* items, int count, int grid) {
+  if (qr_lc1()) k_qr_formq_lc<<<grid, QRC_NT, qrc_smem_bytes(), h->s>>>(items, count);
+  else k_qr_formq_lc2<<<grid, QRC_NT, qrc2_smem_bytes(), h->s>>>(items, count);
+  if (!h->capturing) h->launches++;
+  CKL("k_qr_formq_lc");
+}
+// resident CTAs of the lane-per-column leaves (the item loop strides by gridDim: a second wave would serialise)
+void qr_lc_grids(glsgpu_sur* h, int* gf, int* gq) {
+  CK(cudaFuncSetAttribute(qrf_lc_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qr_lc_smem()));
+  CK(cudaFuncSetAttribute(qrq_lc_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qr_lc_smem()));
+  int occ_f = 1, occ_q = 1, nsm = 148;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, qrf_lc_fn(), QRC_NT, qr_lc_smem()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, qrq_lc_fn(), QRC_NT, qr_lc_smem()));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  *gf = std::max(1, occ_f) * nsm;
+  *gq = std::max(1, occ_q) * nsm;
+}
+
 // The TSQR of blocks [b0, b1) only, every level, when every item is a lane-per-column leaf (narrow blocks):
 // lets glsgpu_sur_create factor one group of blocks while the next group's columns are still in flight.
 bool qr_groupable(const glsgpu_sur* h) {
@@ -1085,19 +1126,13 @@ void run_qr_blocks(glsgpu_sur* h, int b0, int b1, int lc_grid_f, int lc_grid_q) 
     const auto& L = h->qr_levels[l];
     const int64_t f0 = L.fblock[(size_t)b0], cnt = L.fblock[(size_t)b1] - f0;
     if (cnt <= 0) continue;
-    k_qr_factor_lc<<<(int)std::min<int64_t>(cnt, lc_grid_f), QRC_NT, qrc_smem_bytes(), h->s>>>(
-        h->d_items + L.ffirst + f0, (int)cnt);
-    if (!h->capturing) h->launches++;
-    CKL("k_qr_factor_lc group");
+    launch_qrf_lc(h, h->d_items + L.ffirst + f0, (int)cnt, (int)std::min<int64_t>(cnt, lc_grid_f));
   }
   for (int l = nl - 1; l >= 0; --l) {
     const auto& L = h->qr_levels[l];
     const int64_t f0 = L.fblock[(size_t)b0], cnt = L.fblock[(size_t)b1] - f0;
     if (cnt <= 0) continue;
-    k_qr_formq_lc<<<(int)std::min<int64_t>(cnt, lc_grid_q), QRC_NT, qrc_smem_bytes(), h->s>>>(
-        h->d_items + L.ffirst + f0, (int)cnt);
-    if (!h->capturing) h->launches++;
-    CKL("k_qr_formq_lc group");
+    launch_qrq_lc(h, h->d_items + L.ffirst + f0, (int)cnt, (int)std::min<int64_t>(cnt, lc_grid_q));
   }
 }
 
@@ -1106,12 +1141,8 @@ void rank_check(glsgpu_sur* h);
 // group-pipelined setup from host X: group g's columns go up on a copy stream while the solver stream
 // factors group g - 1 (the whole TSQR tree of its blocks), so the QR hides under the host-to-device copy
 void upload_and_qr_pipelined(glsgpu_sur* h, const double* X_host, int groups) {
-  CK(cudaFuncSetAttribute(k_qr_factor_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
-  CK(cudaFuncSetAttribute(k_qr_formq_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
-  int occ_f = 1, occ_q = 1, nsm = 148;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_qr_factor_lc, QRC_NT, qrc_smem_bytes()));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, k_qr_formq_lc, QRC_NT, qrc_smem_bytes()));
-  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  int lc_grid_f = 148, lc_grid_q = 148;
+  qr_lc_grids(h, &lc_grid_f, &lc_grid_q);
   CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));
   cudaStream_t cs = nullptr;
   CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -1134,7 +1165,7 @@ void upload_and_qr_pipelined(glsgpu_sur* h, const double* X_host, int groups) {
     for (int g = 0; g < groups; ++g) {
       const int b0 = (int)((int64_t)g * G / groups), b1 = (int)((int64_t)(g + 1) * G / groups);
       CK(cudaStreamWaitEvent(h->s, ev[(size_t)g], 0));
-      run_qr_blocks(h, b0, b1, std::max(1, occ_f) * nsm, std::max(1, occ_q) * nsm);
+      run_qr_blocks(h, b0, b1, lc_grid_f, lc_grid_q);
     }
     CK(cudaStreamSynchronize(h->s));
     cudaEventDestroy(ready);
@@ -1159,16 +1190,8 @@ void run_qr(glsgpu_sur* h) {
   CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));
   const int nl = (int)h->qr_levels.size();
   CK(cudaFuncSetAttribute(k_qr_formq_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, QRR_ROWS * 32 * 8));
-  CK(cudaFuncSetAttribute(k_qr_factor_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
-  CK(cudaFuncSetAttribute(k_qr_formq_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrc_smem_bytes()));
-  // lane-per-column leaves: grid = resident CTAs (the item loop strides by gridDim; a non-resident
-  // second wave would serialise behind the first)
-  int occ_f = 1, occ_q = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_qr_factor_lc, QRC_NT, qrc_smem_bytes()));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, k_qr_formq_lc, QRC_NT, qrc_smem_bytes()));
-  int nsm = 148;
-  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
-  const int lc_grid_f = std::max(1, occ_f) * nsm, lc_grid_q = std::max(1, occ_q) * nsm;
+  int lc_grid_f = 148, lc_grid_q = 148;
+  qr_lc_grids(h, &lc_grid_f, &lc_grid_q);
   const int fgrid_cap = 2 * 148;  // register-resident leaves: 1-2 CTAs per SM
   for (int l = 0; l < nl; ++l) {
     const auto& L = h->qr_levels[l];
@@ -1181,13 +1204,13 @@ void run_qr(glsgpu_sur* h) {
     }
     if (L.fcount) {
       if (qr_lc())
-        k_qr_factor_lc<<<(int)std::min<int64_t>(L.fcount, lc_grid_f), QRC_NT, qrc_smem_bytes(), h->s>>>(
-            h->d_items + L.ffirst, (int)L.fcount);
-      else
+        launch_qrf_lc(h, h->d_items + L.ffirst, (int)L.fcount, (int)std::min<int64_t>(L.fcount, lc_grid_f));
+      else {
         k_qr_factor_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, 0, h->s>>>(h->d_items + L.ffirst,
                                                                                              (int)L.fcount);
-      if (!h->capturing) h->launches++;
-      CKL("k_qr_factor_reg");
+        if (!h->capturing) h->launches++;
+        CKL("k_qr_factor_reg");
+      }
     }
   }
   if (h->coll) {
@@ -1214,12 +1237,12 @@ void run_qr(glsgpu_sur* h) {
     }
     if (L.fcount) {
       if (qr_lc())
-        k_qr_formq_lc<<<(int)std::min<int64_t>(L.fcount, lc_grid_q), QRC_NT, qrc_smem_bytes(), h->s>>>(
-            h->d_items + L.ffirst, (int)L.fcount);
-      else
+        launch_qrq_lc(h, h->d_items + L.ffirst, (int)L.fcount, (int)std::min<int64_t>(L.fcount, lc_grid_q));
+      else {
         k_qr_formq_reg<32><<<(int)std::min<int64_t>(L.fcount, fgrid_cap), QRR_NT, QRR_ROWS * 32 * 8, h->s>>>(
             h->d_items + L.ffirst, (int)L.fcount);
-      if (!h->capturing) h->launches++;
+        if (!h->capturing) h->launches++;
+      }
       CKL("k_qr_formq_reg");
     }
   }
@@ -1362,6 +1385,8 @@ void destroy_impl(glsgpu_sur* h) {
   if (h->ev_stage) cudaEventDestroy(h->ev_stage);
   if (h->Y_next) cudaFree(h->Y_next);
   if (h->t3) cudaFree(h->t3);
+  if (h->tpart2) cudaFree(h->tpart2);
+  if (h->tpart3) cudaFree(h->tpart3);
   if (h->st_host) cudaFreeHost(h->st_host);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->s) cudaStreamDestroy(h->s);
@@ -1499,6 +1524,8 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     h->zvec = dalloc<double>(h->n);
     h->beta_d = dalloc<double>(h->n);
     h->tpart = dalloc<double>((size_t)h->n * h->nch);
+    h->tpart2 = dalloc<double>((size_t)h->n * h->nch);
+    h->tpart3 = dalloc<double>((size_t)h->n * h->nch);
     h->rpart = dalloc<double>((size_t)std::max<int64_t>((int64_t)h->G * h->nch, 4 * GRID_CAP));
     h->partA = dalloc<double>(GRID_CAP * 3);
     h->partC = dalloc<double>(GRID_CAP * 3);
@@ -1734,6 +1761,48 @@ void capture_iteration(glsgpu_sur* h, int xv_mode, int diag, int timing, int ite
   k_scalar_a<<<1, NT, 0, h->s>>>(pa.first, pa.second, h->st);
   if (!h->capturing) h->launches++;
   CKL("k_scalar_a");
+  if (h->fold) {
+    // passes B and C with the row's diagnostics folded in (SMODE_BD / SMODE_CD)
+    ev(2);
+    StreamArgs ab = stream_args(h);
+    ab.vec = h->vs;
+    ab.gate = 1;
+    ab.zbuf = h->spr;
+    ab.tpart2 = h->tpart2;
+    launch_stream<SMODE_BD>(h, ab, h->st);
+    ev(3);
+    reduce_t_global(h, h->t, h->st, 1);
+    reduce_t_global(h, h->t2, h->st, 1, h->tpart2);  // s_est = Q'(w (y - sw_{i+1}))
+    ev(4);
+    StreamArgs ac = stream_args(h);
+    ac.vec = h->t;
+    ac.vec2 = h->t2;
+    ac.zbuf = h->spr;
+    ac.partials = h->partC;
+    ac.partials2 = h->rpart;
+    ac.tpart3 = h->tpart3;
+    ac.gate = 1;
+    const int gCD = launch_stream<SMODE_CD>(h, ac, h->st);
+    ev(5);
+    const auto pcd = combine3(h, h->partC, gCD);
+    k_scalar_c<<<1, NT, 0, h->s>>>(pcd.first, pcd.second, h->st, h->rows_d);
+    if (!h->capturing) h->launches++;
+    CKL("k_scalar_c");
+    k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t, h->vs, xfx, 0, h->st);
+    if (!h->capturing) h->launches++;
+    CKL("k_vupdate");
+    // the row: est = R^-1 s_est, X'w = R' Q'w / w, |y - sw - X est|, rmse (gated on st->diag_now)
+    reduce_t_global(h, h->t3, h->st, 2, h->tpart3);
+    k_vupdate<<<(h->G + 63) / 64, 64, 0, h->s>>>(g, h->R, h->t2, nullptr, 1, 2, h->st);
+    if (!h->capturing) h->launches++;
+    k_rt_apply<<<dim3((unsigned)((h->nmax + 63) / 64), (unsigned)h->G), 64, 0, h->s>>>(g, h->R, h->t3, h->xtw, h->st);
+    if (!h->capturing) h->launches++;
+    const auto pr1 = combine1(h, h->rpart, gCD);
+    k_diag_finalize<<<1, NT, 0, h->s>>>(pr1.first, pr1.second, h->xtw, h->n, h->t2, h->beta_d, h->st, h->rows_d, -1);
+    if (!h->capturing) h->launches++;
+    CKL("folded diagnostics");
+    return;
+  }
   // pass B: w, sw, r updates + Q'(w r) column partials
   ev(2);
   pass_b(h, xfx, h->st);
@@ -2210,6 +2279,9 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   hs.sw_direct = h->sw_direct;
   // fused_c: needs Sigma w formed where read (the recurrence would need Sigma u_old in the element pass)
   h->fused = (cfg.fused_c == 1 && h->sw_direct && h->qmap_ok && std::getenv("GLSGPU_NO_FUSED") == nullptr) ? 1 : 0;
+  // every row's diagnostics folded into passes B / C: narrow blocks, TMA passes, xv_mode QR, Sigma w by recurrence
+  h->fold = (diag == 1 && xv_mode == GLSGPU_XV_QR && h->use_stream && h->nmax <= 32 && !h->sw_direct && !h->fused &&
+             std::getenv("GLSGPU_NO_FOLD") == nullptr) ? 1 : 0;
   CK(cudaMemcpyAsync(h->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
   k_set_t0<<<1, 1, 0, s>>>(h->st);
   if (!h->capturing) h->launches++;
@@ -2300,7 +2372,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   const bool need_graph = !h->grp && (!h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
                           h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing ||
                           h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct || h->graph_fused != h->fused ||
-                          h->graph_rows != h->rows_d);
+                          h->graph_rows != h->rows_d || h->graph_fold != h->fold);
   if (need_graph) {
     if (h->graph) {
       CK(cudaGraphExecDestroy(h->graph));
@@ -2341,6 +2413,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     h->graph_sw = h->sw_direct;
     h->graph_fused = h->fused;
     h->graph_rows = h->rows_d;
+    h->graph_fold = h->fold;
   }
   std::vector<double> kt_ms(3, 0.0);
   std::vector<int64_t> kt_n(3, 0);
@@ -2463,9 +2536,11 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     // sw_mode 1: no sw / su(old) read, no sw write; fused_c: pass A is element-wise (reads u, pr, su, spr, w;
     // writes u, su, w) and pass C also writes Sigma pr
     const double bA = 8.0 * (h->fused ? 8.0 : h->sw_direct ? 6.0 : 9.0) * M * G;
-    const double bB = 8.0 * (M * n * (xv_mode == GLSGPU_XV_X ? 2.0 : 1.0) + 3.0 * M * G);
-    const double bC = 8.0 * (M * n + (h->fused ? 3.0 : 2.0) * M * G);
-    const char* names[3] = {"passA_kron", "passB_update_qtr", "passC_pi"};
+    // fold (diag_every 1): B also reads sw and y, writes z; C also reads z, w, u
+    const double bB = 8.0 * (M * n * (xv_mode == GLSGPU_XV_X ? 2.0 : 1.0) + (h->fold ? 6.0 : 3.0) * M * G);
+    const double bC = 8.0 * (M * n + (h->fused ? 3.0 : h->fold ? 5.0 : 2.0) * M * G);
+    const char* names[3] = {"passA_kron", h->fold ? "passB_update_qtr_diag" : "passB_update_qtr",
+                            h->fold ? "passC_pi_diag" : "passC_pi"};
     const double bytes[3] = {bA, bB, bC};
     for (int k = 0; k < 3; ++k) {
       glsgpu_kernel_stat ks;

@@ -1407,7 +1407,14 @@ __global__ void __launch_bounds__(NT) k_pass_a_ew(int64_t count, double* __restr
   }
 }
 
-enum { SMODE_B = 0, SMODE_C = 1, SMODE_QT_R = 2, SMODE_QT_D = 3, SMODE_QT_V = 4, SMODE_DIAG = 5, SMODE_XS = 6 };
+enum { SMODE_B = 0, SMODE_C = 1, SMODE_QT_R = 2, SMODE_QT_D = 3, SMODE_QT_V = 4, SMODE_DIAG = 5, SMODE_XS = 6,
+       SMODE_BD = 7, SMODE_CD = 8 };
+// SMODE_BD / SMODE_CD: passes B and C with the trace row's diagnostics folded in (diag_every = 1, xv_mode QR,
+// narrow blocks; the reference fills aug_residual_norm / dual_feas_norm / rmse on every row, pcg.cpp:96-116):
+//   BD: as B, plus z = w_b (y - sw_{i+1}), sw_{i+1} = sw_i - lambda su (written to zbuf), and the column partials
+//       of Q'z (tpart2): est = R^-1 Q'z = X*'(y - sw_{i+1}) (recover, pcg.cpp:96-98), s_est = R est = Q'z;
+//   CD: as C, plus |y - sw_{i+1} - X est|^2 = sum_k ((z_k - Q_k s_est) / w_b)^2 (partials2) and the column
+//       partials of Q' w_{i+1}, w_{i+1} = w_i - lambda u (tpart3): X' w = R' Q' w / w_b (pcg.cpp:112).
 
 struct StreamArgs {
   const double* Q;      // ld = ldm
@@ -1426,6 +1433,11 @@ struct StreamArgs {
   const double* vec;    // per-block n-vector: v / s (B), t (C, XS), est (DIAG)
   double* tpart;        // column partials [(p0 + j) * nch + ch]
   double* partials;     // per-CTA dot partials (C: 3, DIAG: 1)
+  double* zbuf;         // BD: z = w_b (y - sw_{i+1}) out; CD: in
+  const double* vec2;   // CD: s_est = Q'z per block (the reduced tpart2)
+  double* tpart2;       // BD: Q'z column partials
+  double* tpart3;       // CD: Q' w_{i+1} column partials
+  double* partials2;    // CD: per-CTA residual partial
   int xv_from_x, sel_best, gate;
   int T, S, nmax;
   int qdiag;            // SMODE_DIAG from Q instead of X (xv_mode QR): X est = Q s / w with s = R est, and the
@@ -1442,7 +1454,8 @@ __device__ __forceinline__ int stream_nmat(const StreamArgs& a) {
 }
 template <int MODE>
 __host__ __device__ constexpr int stream_nvec() {
-  return MODE == SMODE_B ? 2 : MODE == SMODE_DIAG ? 4 : MODE == SMODE_QT_D ? 2 : MODE == SMODE_XS ? 0 : 1;
+  return MODE == SMODE_B ? 2 : MODE == SMODE_DIAG ? 4 : MODE == SMODE_QT_D ? 2 : MODE == SMODE_XS ? 0
+         : MODE == SMODE_BD ? 3 : MODE == SMODE_CD ? 4 : 1;
 }
 
 template <int MODE, bool FUSE>
@@ -1451,8 +1464,9 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
   if (a.gate == 2 && !st->diag_now) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[4];
-  __shared__ double red[NT / 32 * 3];
+  __shared__ double red[NT / 32 * 4];
   __shared__ double fred[(FUSE && (MODE != SMODE_C && MODE != SMODE_XS)) ? NT : 1];
+  __shared__ double tv2[MODE == SMODE_CD ? 128 : 1];
   const int S = a.S, T = a.T;
   double* xs = sm + (int64_t)S * a.stage_doubles;
   // per-item n-vector slice (nmax <= 128 on this path): a static shared array, so the row dots read it
@@ -1465,8 +1479,8 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
 
   double lam = 0.0, lp = 0.0;  // lp: lambda of a still-pending w / sw update (diagnostics apply it on the fly)
   int cur = 0, sel = 0;
-  if (MODE == SMODE_B) lam = st->lambda;
-  if (MODE == SMODE_DIAG) cur = st->cur;
+  if (MODE == SMODE_B || MODE == SMODE_BD || MODE == SMODE_CD) lam = st->lambda;
+  if (MODE == SMODE_DIAG || MODE == SMODE_BD || MODE == SMODE_CD) cur = st->cur;
   if (MODE == SMODE_QT_D) sel = a.sel_best ? (st->term == T_CONVERGED ? st->cur : st->best) : st->cur;
   if ((MODE == SMODE_DIAG || MODE == SMODE_QT_D) && st && st->upd_pending) lp = st->lam_prev;
 
@@ -1545,6 +1559,8 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
         const int64_t vo = (int64_t)b * g.ldm + kb;
         const double* vb = nullptr;
         if (MODE == SMODE_B) vb = v == 0 ? a.su : a.r;
+        else if (MODE == SMODE_BD) vb = v == 0 ? a.su : v == 1 ? a.r : a.swb[cur];
+        else if (MODE == SMODE_CD) vb = v == 0 ? a.r : v == 1 ? a.zbuf : v == 2 ? a.wb[cur] : a.u;
         else if (MODE == SMODE_C || MODE == SMODE_QT_R) vb = a.r;
         else if (MODE == SMODE_QT_V) vb = a.vin;
         else if (MODE == SMODE_QT_D) vb = v == 0 ? a.swb[sel] : a.su;
@@ -1566,6 +1582,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
   double pc = 0.0, prr = 0.0, ppp = 0.0, rsum = 0.0;
   constexpr int MAXC = 16;  // columns per warp (n_b <= 128 on this path)
   constexpr bool COLS = (MODE != SMODE_C && MODE != SMODE_XS);
+  constexpr bool COLS2 = (MODE == SMODE_BD);  // a second column-partial set (Q'z)
   int64_t it_count = 0;
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
     int64_t k0, k1;
@@ -1579,8 +1596,11 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     const int64_t vbase = (int64_t)b * g.ldm;
     // tv holds >= 32 entries (zero past n_b): the fused row dots read all 32
     for (int j = tid; j < (nb > 32 ? nb : 32); j += NT)
-      if (MODE == SMODE_B || MODE == SMODE_C || MODE == SMODE_XS || MODE == SMODE_DIAG)
+      if (MODE == SMODE_B || MODE == SMODE_C || MODE == SMODE_XS || MODE == SMODE_DIAG || MODE == SMODE_BD ||
+          MODE == SMODE_CD) {
         tv[j] = (j < nb) ? a.vec[p0 + j] : 0.0;
+        if (MODE == SMODE_CD) tv2[j] = (j < nb) ? a.vec2[p0 + j] : 0.0;
+      }
     __syncthreads();
     // column partials live in registers across the item's tiles: lane partial of column warp + 8 c
     double acc[MAXC];
@@ -1589,6 +1609,9 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     double facc[(FUSE && COLS) ? 32 : 1];
 #pragma unroll
     for (int j = 0; j < ((FUSE && COLS) ? 32 : 1); ++j) facc[j] = 0.0;
+    double facc2[(FUSE && COLS2) ? 32 : 1];
+#pragma unroll
+    for (int j = 0; j < ((FUSE && COLS2) ? 32 : 1); ++j) facc2[j] = 0.0;
     for (int64_t kb = k0; kb < k1; kb += T, ++it_count) {
       const int stage = (int)(it_count % S);
       const int rows = (int)((k1 - kb) < T ? (k1 - kb) : T);
@@ -1625,8 +1648,36 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
             }
             return (s0 + s1) + (s2 + s3);
           };
-          double x = 0.0;
-          if (MODE == SMODE_B) {
+          double x = 0.0, x2 = 0.0;
+          if (MODE == SMODE_BD) {
+            const double suv = V[t], rv = V[T + t], swv = V[2 * T + t];
+            const double xv = rdot() * iwgt;
+            const double rn = rv - lam * (suv + xv);
+            a.r[vo] = rn;
+            x = rn * wgt;
+            const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+            x2 = (yv - (swv + (-lam) * suv)) * wgt;
+            a.zbuf[vo] = x2;
+          } else if (MODE == SMODE_CD) {
+            const double proj = rdot();
+            const double rv = V[t];
+            const double pv = (rv * wgt - proj) * wgt;
+            a.pr[vo] = pv;
+            pc += rv * pv;
+            prr += rv * rv;
+            ppp += pv * pv;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              s0 = __fma_rn(arow[j + 0], tv2[j + 0], s0);
+              s1 = __fma_rn(arow[j + 1], tv2[j + 1], s1);
+              s2 = __fma_rn(arow[j + 2], tv2[j + 2], s2);
+              s3 = __fma_rn(arow[j + 3], tv2[j + 3], s3);
+            }
+            const double res = (V[T + t] - ((s0 + s1) + (s2 + s3))) * iwgt;
+            if (k < g.M) rsum += res * res;
+            x = V[2 * T + t] + (-lam) * V[3 * T + t];  // w_{i+1}
+          } else if (MODE == SMODE_B) {
             const double suv = V[t], rv = V[T + t];
             double xv = 0.0;
             if (a.xv_from_x) {
@@ -1665,6 +1716,10 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           if constexpr (COLS) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) facc[j] = __fma_rn(arow[j], x, facc[j]);
+          }
+          if constexpr (COLS2) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) facc2[j] = __fma_rn(arow[j], x2, facc2[j]);
           }
         }
         __syncthreads();  // the stage is free
@@ -1750,15 +1805,27 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     }
     if constexpr (FUSE && COLS) {
       // transpose-reduce the 32 per-lane column partials, then the 8 warps in order
+      double* tp = (MODE == SMODE_CD) ? a.tpart3 : a.tpart;
       warp_transpose_reduce<32>(facc);
       fred[warp * 32 + lane] = facc[0];
       __syncthreads();
       if (tid < nb) {
         double s = 0.0;
         for (int w = 0; w < NT / 32; ++w) s += fred[w * 32 + tid];
-        a.tpart[(p0 + tid) * g.nch + ch] = s;
+        tp[(p0 + tid) * g.nch + ch] = s;
       }
       __syncthreads();
+      if constexpr (COLS2) {
+        warp_transpose_reduce<32>(facc2);
+        fred[warp * 32 + lane] = facc2[0];
+        __syncthreads();
+        if (tid < nb) {
+          double s = 0.0;
+          for (int w = 0; w < NT / 32; ++w) s += fred[w * 32 + tid];
+          a.tpart2[(p0 + tid) * g.nch + ch] = s;
+        }
+        __syncthreads();
+      }
     } else if (COLS) {
 #pragma unroll
       for (int q = 0; q < MAXC; ++q) {
@@ -1770,6 +1837,16 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           if (lane == 0) a.tpart[(p0 + j) * g.nch + ch] = s;
         }
       }
+    }
+  }
+  if (MODE == SMODE_CD) {
+    double v[4] = {pc, prr, ppp, rsum};
+    block_sum<4>(v, red);
+    if (tid == 0) {
+      a.partials[blockIdx.x * 3 + 0] = v[0];
+      a.partials[blockIdx.x * 3 + 1] = v[1];
+      a.partials[blockIdx.x * 3 + 2] = v[2];
+      a.partials2[blockIdx.x] = v[3];
     }
   }
   if (MODE == SMODE_C || MODE == SMODE_DIAG) {
@@ -2733,6 +2810,201 @@ __global__ void __launch_bounds__(QRC_NT, 1) k_qr_formq_lc(const QrItem* items, 
       for (int i = 0; i < 32; ++i) e[i] = fma_rn(h, v[i], e[i]);
     }
     // E out through the panel (coalesced)
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) S[lane * QRC_LD + 8 * i + warp] = e[i];
+    __syncthreads();
+    if (t < L)
+      for (int j = 0; j < n; ++j) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = S[j * QRC_LD + t];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Two-CTA-per-SM forms of the lane-per-column leaves (the default).  The leaf kernels above are bound by the
+// latency of their 32 dependent steps (one CTA reduction + a sqrt and a divide per step) with one CTA per SM;
+// these keep no broadcast copy of column k in registers (it is re-read from lane k with shuffles in the update)
+// and stage one panel instead of two, so two CTAs -- two independent leaves -- share each SM and hide each
+// other's step latency.  Same arithmetic, operation for operation, as k_qr_factor_lc / k_qr_formq_lc.
+constexpr size_t qrc2_smem_bytes() { return (size_t)QRC_PANEL * sizeof(double); }
+
+__global__ void __launch_bounds__(QRC_NT, 2) k_qr_factor_lc2(const QrItem* items, int nitems) {
+  extern __shared__ double S[];                 // one panel buffer [32][QRC_LD]
+  __shared__ double red[2][QRC_NT / 32][32];
+  __shared__ double rowk[2][32];
+  __shared__ double alph[32];
+  __shared__ double redm[QRC_NT / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    __syncthreads();                            // the previous item's panel readers are done
+    qrc_prefetch(S, I.src, I.lds, I.r0, I.rows, I.valid, I.n);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    double* col = S + lane * QRC_LD;            // this lane's column
+    double a[32];
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      a[i] = col[8 * i + warp] * I.scale;
+      mx = fmax(mx, fabs(a[i]));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    if (lane == 0) redm[warp] = mx;
+    __syncthreads();
+    mx = redm[0];
+#pragma unroll
+    for (int w = 1; w < QRC_NT / 32; ++w) mx = fmax(mx, redm[w]);
+    int ex = 0;
+    if (mx > 0.0) frexp(mx, &ex);
+    const double sc = ldexp(1.0, -ex), unsc = ldexp(1.0, ex);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] *= sc;
+    double my_inv = 1.0, my_v0 = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+      const int par = k & 1;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        double x0 = __shfl_sync(FULL, a[i + 0], k), x1 = __shfl_sync(FULL, a[i + 1], k);
+        double x2 = __shfl_sync(FULL, a[i + 2], k), x3 = __shfl_sync(FULL, a[i + 3], k);
+        if (i == 0) {
+          if (0 * 8 + warp < k) x0 = 0.0;
+          if (1 * 8 + warp < k) x1 = 0.0;
+          if (2 * 8 + warp < k) x2 = 0.0;
+          if (3 * 8 + warp < k) x3 = 0.0;
+        }
+        s0 = fma_rn(x0, a[i + 0], s0);
+        s1 = fma_rn(x1, a[i + 1], s1);
+        s2 = fma_rn(x2, a[i + 2], s2);
+        s3 = fma_rn(x3, a[i + 3], s3);
+      }
+      if (warp == (k & 7)) {
+        const int sk = k >> 3;
+        rowk[par][lane] = sk == 0 ? a[0] : sk == 1 ? a[1] : sk == 2 ? a[2] : a[3];
+      }
+      red[par][warp][lane] = (s0 + s1) + (s2 + s3);
+      __syncthreads();
+      double sj = 0.0;
+#pragma unroll
+      for (int w = 0; w < QRC_NT / 32; ++w) sj += red[par][w][lane];
+      const double skk = __shfl_sync(FULL, sj, k);
+      const double akj = rowk[par][lane];
+      const double wkk = rowk[par][k];
+      const double norm_x = sqrt(skk);
+      double alpha = 0.0, v0 = 1.0, beta = 0.0, inv_alpha = 0.0, inv_v0 = 1.0;
+      if (norm_x != 0.0) {
+        alpha = wkk >= 0.0 ? -norm_x : norm_x;
+        v0 = wkk - alpha;
+        const double dd = 1.0 / (alpha * v0);
+        beta = -dd;
+        inv_alpha = v0 * dd;
+        inv_v0 = alpha * dd;
+      }
+      const double f = (lane > k && lane < n) ? (alpha * akj - sj) * inv_alpha : 0.0;
+      const double gg = f * inv_v0;
+      if (lane == k) {
+        my_inv = inv_v0;
+        my_v0 = (norm_x != 0.0) ? v0 : wkk;
+      }
+      if (t == k) {
+        alph[k] = alpha;
+        I.tau[k] = beta;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        double x = __shfl_sync(FULL, a[i], k);  // lane k's column is unchanged by its own step (f = 0 there)
+        if (i < 4 && 8 * i + warp < k) x = 0.0;
+        const double up = fma_rn(-gg, x, a[i]);
+        a[i] = (i < 4 && 8 * i + warp == k) ? a[i] - f : up;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = 8 * i + warp;
+      double v = a[i];
+      if (i >= 4 || r > lane) v = a[i] * my_inv;
+      else if (r == lane) v = my_v0;
+      col[r] = v;
+    }
+    __syncthreads();
+    for (int idx = t; idx < n * n; idx += QRC_NT) {
+      const int j = idx / n, i = idx - j * n;
+      const double r = (i < j) ? S[j * QRC_LD + i] * unsc : (i == j ? alph[j] * unsc : 0.0);
+      I.rout[i + (int64_t)j * I.ldo] = r;
+      if (i == j && I.rdiag) I.rdiag[j] = r;
+    }
+    if (t < L)
+      for (int j = 0; j < n; ++j) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = S[j * QRC_LD + t];
+  }
+}
+
+__global__ void __launch_bounds__(QRC_NT, 2) k_qr_formq_lc2(const QrItem* items, int nitems) {
+  extern __shared__ double S[];                 // one packed-panel buffer [32][QRC_LD]
+  __shared__ double V0[32][33];
+  __shared__ double bh[32];
+  __shared__ int tz[32];
+  __shared__ double red[2][QRC_NT / 32][32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    __syncthreads();
+    qrc_prefetch(S, I.refl + I.rr0, I.ldr, 0, I.rows, I.rows, I.n);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    for (int idx = t; idx < 32 * 32; idx += QRC_NT) {
+      const int k = idx >> 5, i = idx & 31;
+      const double pk = S[k * QRC_LD + i];
+      V0[k][i] = (i > k && i < L) ? pk : (i == k ? 1.0 : 0.0);
+      if (i == k) {
+        const double tk = (k < n) ? I.tau[k] : 0.0;
+        bh[k] = tk * pk * pk;
+        tz[k] = (tk == 0.0);
+      }
+    }
+    double e[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = 8 * i + warp;
+      double v = 0.0;
+      if (i < 4 && r < n && lane < n) v = I.qpar ? I.qpar[r + (int64_t)lane * I.ldp] : (r == lane ? 1.0 : 0.0);
+      e[i] = v;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = n - 1; k >= 0; --k) {
+      if (tz[k]) continue;
+      const double bhk = bh[k];
+      const int par = k & 1;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const double v0_ = (i < 4) ? V0[k][8 * (i + 0) + warp] : S[k * QRC_LD + 8 * (i + 0) + warp];
+        const double v1_ = (i < 4) ? V0[k][8 * (i + 1) + warp] : S[k * QRC_LD + 8 * (i + 1) + warp];
+        const double v2_ = (i < 4) ? V0[k][8 * (i + 2) + warp] : S[k * QRC_LD + 8 * (i + 2) + warp];
+        const double v3_ = (i < 4) ? V0[k][8 * (i + 3) + warp] : S[k * QRC_LD + 8 * (i + 3) + warp];
+        s0 = fma_rn(v0_, e[i + 0], s0);
+        s1 = fma_rn(v1_, e[i + 1], s1);
+        s2 = fma_rn(v2_, e[i + 2], s2);
+        s3 = fma_rn(v3_, e[i + 3], s3);
+      }
+      red[par][warp][lane] = (s0 + s1) + (s2 + s3);
+      __syncthreads();
+      double sj = 0.0;
+#pragma unroll
+      for (int w = 0; w < QRC_NT / 32; ++w) sj += red[par][w][lane];
+      const double h = -(sj * bhk);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const double v = (i < 4) ? V0[k][8 * i + warp] : S[k * QRC_LD + 8 * i + warp];
+        e[i] = fma_rn(h, v, e[i]);
+      }
+    }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 32; ++i) S[lane * QRC_LD + 8 * i + warp] = e[i];

@@ -458,3 +458,34 @@ def test_failed_refactor_invalidates_handle():
     op.update(p.X, p.Y)
     again = api.pcg_aug(sur, op, config=cfg)
     assert np.array_equal(again.solution.b, ok.solution.b)
+
+
+@pytest.mark.parametrize("name,mk", [("c4_G256_M2100", lambda: synth.make_problem(4, M=2100)),
+                                     ("c0", lambda: synth.make_problem(0))], ids=["c4_G256_M2100", "c0"])
+def test_folded_diagnostics(name, mk, monkeypatch):
+    """diag_every = 1 in xv_mode QR folds every row's diagnostics into passes B and C (SMODE_BD / SMODE_CD):
+    the iterates and c trace are bitwise those of the separate diagnostics passes, the diagnostics columns agree
+    to rounding, and the solve still meets the oracle bar with the reference's full trace."""
+    p = mk()
+    sur = api.sur_from_problem(p)
+    op = api.sur_preconditioner(sur)
+    cfg = api.PcgConfig(tol_rel=p.tol_rel, max_iter=p.max_iter or 400, xv_mode="qr", diag_every=1)
+    fold = api.pcg_aug(sur, op, config=cfg, true_beta=p.beta)
+    monkeypatch.setenv("GLSGPU_NO_FOLD", "1")
+    sep = api.pcg_aug(sur, op, config=cfg, true_beta=p.beta)
+    monkeypatch.delenv("GLSGPU_NO_FOLD")
+    assert fold.solution.iterations == sep.solution.iterations
+    assert np.array_equal(fold.solution.b, sep.solution.b)
+    assert np.array_equal(fold.trace.rows["c"], sep.trace.rows["c"])
+    for col in ("aug_residual_norm", "rmse"):
+        assert np.allclose(fold.trace.rows[col], sep.trace.rows[col], rtol=1e-11, equal_nan=True), col
+    scale = float(np.nanmax(sep.trace.rows["aug_residual_norm"]))
+    assert np.allclose(fold.trace.rows["dual_feas_norm"], sep.trace.rows["dual_feas_norm"], rtol=0, atol=1e-10 * scale)
+    assert not np.isnan(fold.trace.rows["aug_residual_norm"]).any()
+    o = oracle.solve(p, "oracle", cfg=oracle.make_config(tol_rel=p.tol_rel, max_iter=p.max_iter or 400),
+                     beta_true=p.beta)
+    assert fold.solution.iterations == o.iterations
+    assert rel(fold.solution.b, o.b) <= B_TOL
+    k = min(5, len(o.trace))
+    assert np.allclose(fold.trace.rows["aug_residual_norm"][:k], o.trace["aug_residual_norm"][:k], rtol=1e-9)
+    assert np.allclose(fold.trace.rows["rmse"][:k], o.trace["rmse"][:k], rtol=1e-9, equal_nan=True)
