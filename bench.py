@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=20000)
     ap.add_argument("--no-witness", action="store_true")
+    ap.add_argument("--no-trace-all", action="store_true", help="skip the diag_every = 1 (full trace) measurement")
     ap.add_argument("--witness-rows", type=int, default=4000)
     return ap.parse_args()
 
@@ -344,6 +345,35 @@ def run_ours(args):
             passes[k] = {"avg_ms": avg, "GB/s": d["bytes_per_launch"] / (avg / 1e3) / 1e9}
             iter_ms += avg
 
+    # ---- the reference-identical trace (aug_residual_norm / dual_feas_norm / rmse on EVERY row, pcg.cpp:96-116):
+    # diag_every = 1 with Sigma w by the reference's recurrence, the diagnostics folded into passes B / C
+    trace_all = None
+    if not args.no_trace_all and args.diag == 0:
+        tcfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, kernel_timing=True,
+                             **dict(knobs, diag_every=1, sw_mode=0, fused_c=0))
+        op.refactor()
+        api.pcg_aug(None, op, config=tcfg, true_beta=beta, want_w=False)  # warm-up (graph capture)
+        t_ms, t_it, tk = 0.0, 0, {}
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            op.refactor()
+            r = api.pcg_aug(None, op, config=tcfg, true_beta=beta, want_w=False)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_ms += e0.elapsed_time(e1)
+            t_it += r.solution.iterations
+            for s_ in op.kernel_stats():
+                d = tk.setdefault(s_["name"], [0, 0.0])
+                d[0] += s_["launches"]
+                d[1] += s_["total_ms"]
+        it_ms_all = sum(v[1] / v[0] for v in tk.values() if v[0])
+        trace_all = {"value": t_it / (t_ms / 1e3), "unit": UNIT, "steps": 2, "diag_every": 1, "sigma_w": "recurrence",
+                     "iter_ms": it_ms_all, "iter_ms_vs_main": it_ms_all / iter_ms if iter_ms else None,
+                     "passes": {k: v[1] / v[0] for k, v in tk.items() if v[0]},
+                     "rows_with_diagnostics": int(np.isfinite(r.trace.rows["aug_residual_norm"]).sum()),
+                     "rows": int(r.trace.rows.size)}
+
     # ---- e2e through the C-ABI with host buffers: per step, that step's X and Y go up from pinned host memory
     # (staged: overlapping the previous step's solve), the refactor, the solve, b back to the host
     e2e = None
@@ -437,6 +467,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "parity_witness": witness_line,
+            "trace_every_row": trace_all,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
