@@ -279,6 +279,7 @@ struct glsgpu_sur {
   int rank = 0, nranks = 1;
   bool coll = false;  // collective path (NCCL all-gathers, cross-rank TSQR level); also nranks == 1 + id
   bool use_stream = false;  // TMA-staged passes (n_i <= 128, 16-byte aligned X columns, ldx >= ldm)
+  bool all_stream = false;  // use_stream on EVERY rank (a pass that changes the collective sequence needs it)
   bool qtiled = false;      // Q tile-contiguous: block b, rows [256 k, 256 k + 256) contiguous (n_i <= 32)
   bool no_qtile = false;    // keep Q column-major (ld ldm): a QR-only handle whose Q is read out as a matrix
   // wide blocks (some n_i > 32, all <= 128): the QR writes column-major Q; the streaming passes read a tiled copy
@@ -1355,6 +1356,17 @@ void alloc_common(glsgpu_sur* h) {
     h->all3 = dalloc<double>((size_t)4 * P);
     h->t_loc = dalloc<double>((size_t)h->n);
     h->t_all = dalloc<double>((size_t)h->n * P);
+    // do all ranks take the TMA-staged passes?  (ranks with unaligned row counts do not)
+    const double mine = h->use_stream ? 1.0 : 0.0;
+    std::vector<double> all((size_t)P);
+    CK(cudaMemcpyAsync(h->loc3, &mine, sizeof(double), cudaMemcpyHostToDevice, h->s));
+    allgather(h, h->loc3, h->all3, 1);
+    CK(cudaMemcpyAsync(all.data(), h->all3, sizeof(double) * P, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    h->all_stream = true;
+    for (double v : all) h->all_stream = h->all_stream && v != 0.0;
+  } else {
+    h->all_stream = h->use_stream;
   }
   build_qr_plan(h);
 }
@@ -2280,7 +2292,8 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   // fused_c: needs Sigma w formed where read (the recurrence would need Sigma u_old in the element pass)
   h->fused = (cfg.fused_c == 1 && h->sw_direct && h->qmap_ok && std::getenv("GLSGPU_NO_FUSED") == nullptr) ? 1 : 0;
   // every row's diagnostics folded into passes B / C: narrow blocks, TMA passes, xv_mode QR, Sigma w by recurrence
-  h->fold = (diag == 1 && xv_mode == GLSGPU_XV_QR && h->use_stream && h->nmax <= 32 && !h->sw_direct && !h->fused &&
+  h->fold = (diag == 1 && xv_mode == GLSGPU_XV_QR && h->all_stream && h->nmax <= 32 && !h->sw_direct && !h->fused &&
+             h->ldy >= h->ldm && (h->ldy % 2) == 0 && (reinterpret_cast<uintptr_t>(h->Y) % 16) == 0 &&
              std::getenv("GLSGPU_NO_FOLD") == nullptr) ? 1 : 0;
   CK(cudaMemcpyAsync(h->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
   k_set_t0<<<1, 1, 0, s>>>(h->st);

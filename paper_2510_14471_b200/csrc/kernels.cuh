@@ -10,6 +10,7 @@
 // Data layout in HBM: every M x G state vector and the concatenated Q / X are
 // column-major with a padded leading dimension ldm = round_up(M, 32); padding rows are zero.
 #pragma once
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -1455,7 +1456,7 @@ __device__ __forceinline__ int stream_nmat(const StreamArgs& a) {
 template <int MODE>
 __host__ __device__ constexpr int stream_nvec() {
   return MODE == SMODE_B ? 2 : MODE == SMODE_DIAG ? 4 : MODE == SMODE_QT_D ? 2 : MODE == SMODE_XS ? 0
-         : MODE == SMODE_BD ? 3 : MODE == SMODE_CD ? 4 : 1;
+         : MODE == SMODE_BD ? 4 : MODE == SMODE_CD ? 4 : 1;
 }
 
 template <int MODE, bool FUSE>
@@ -1467,6 +1468,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
   __shared__ double red[NT / 32 * 4];
   __shared__ double fred[(FUSE && (MODE != SMODE_C && MODE != SMODE_XS)) ? NT : 1];
   __shared__ double tv2[MODE == SMODE_CD ? 128 : 1];
+  __shared__ double pdot[FUSE ? 1 : NT];  // wide blocks: partial row dots [P][T]
   const int S = a.S, T = a.T;
   double* xs = sm + (int64_t)S * a.stage_doubles;
   // per-item n-vector slice (nmax <= 128 on this path): a static shared array, so the row dots read it
@@ -1488,8 +1490,9 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     mbar_fence_init();
   }
-  if (FUSE) {
-    // the narrow-block sweep reads all 32 column slots of a stage: start from finite contents
+  {
+    // the narrow-block sweep reads all 32 column slots of a stage, and the wide-block column pass reads whole
+    // tiles (the rows of a partial tile meet x = 0): start from finite contents
     for (int64_t i = tid; i < (int64_t)S * a.stage_doubles; i += NT) sm[i] = 0.0;
     fence_proxy_async_smem();  // generic writes ordered before the first TMA writes into the ring
   }
@@ -1559,13 +1562,13 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
         const int64_t vo = (int64_t)b * g.ldm + kb;
         const double* vb = nullptr;
         if (MODE == SMODE_B) vb = v == 0 ? a.su : a.r;
-        else if (MODE == SMODE_BD) vb = v == 0 ? a.su : v == 1 ? a.r : a.swb[cur];
+        else if (MODE == SMODE_BD) vb = v == 0 ? a.su : v == 1 ? a.r : v == 2 ? a.swb[cur] : nullptr;
         else if (MODE == SMODE_CD) vb = v == 0 ? a.r : v == 1 ? a.zbuf : v == 2 ? a.wb[cur] : a.u;
         else if (MODE == SMODE_C || MODE == SMODE_QT_R) vb = a.r;
         else if (MODE == SMODE_QT_V) vb = a.vin;
         else if (MODE == SMODE_QT_D) vb = v == 0 ? a.swb[sel] : a.su;
         else if (MODE == SMODE_DIAG) vb = v == 0 ? a.wb[cur] : v == 1 ? a.swb[cur] : v == 2 ? a.u : a.su;
-        src = vb + vo;
+        src = (MODE == SMODE_BD && v == 3) ? a.y + (int64_t)b * a.ldy + kb : vb + vo;  // y: ld ldy >= ldm (h->fold)
         dst = base + (int64_t)(nmat * nb) * T + (int64_t)v * T;
       }
       tma_load_1d(dst, src, bytes, &bars[stage]);
@@ -1634,9 +1637,26 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           const int64_t vo = vbase + k;
           const bool zrow = k < g.msig;
           const double wgt = zrow ? wz : wc, iwgt = zrow ? iwz : iwc;
-          double arow[32];
+          constexpr bool ROWREG = (MODE != SMODE_BD && MODE != SMODE_CD);  // the folded modes read Q from smem
+          double arow[ROWREG ? 32 : 1];
+          if constexpr (ROWREG) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) arow[j] = M0[(int64_t)j * T + t];
+            for (int j = 0; j < 32; ++j) arow[j] = M0[(int64_t)j * T + t];
+          }
+          // row dot from shared memory (the folded modes: two / three column-partial sets leave no room for
+          // the row in registers)
+          auto sdot = [&](const double* tvp) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              s0 = __fma_rn(M0[(int64_t)(j + 0) * T + t], tvp[j + 0], s0);
+              s1 = __fma_rn(M0[(int64_t)(j + 1) * T + t], tvp[j + 1], s1);
+              s2 = __fma_rn(M0[(int64_t)(j + 2) * T + t], tvp[j + 2], s2);
+              s3 = __fma_rn(M0[(int64_t)(j + 3) * T + t], tvp[j + 3], s3);
+            }
+            return (s0 + s1) + (s2 + s3);
+          };
+          (void)sdot;
           auto rdot = [&]() {
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
@@ -1651,30 +1671,23 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           double x = 0.0, x2 = 0.0;
           if (MODE == SMODE_BD) {
             const double suv = V[t], rv = V[T + t], swv = V[2 * T + t];
-            const double xv = rdot() * iwgt;
+            const double xv = sdot(tv) * iwgt;
             const double rn = rv - lam * (suv + xv);
             a.r[vo] = rn;
             x = rn * wgt;
-            const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
+            const double yv = (k < g.M) ? V[3 * T + t] : 0.0;
             x2 = (yv - (swv + (-lam) * suv)) * wgt;
             a.zbuf[vo] = x2;
           } else if (MODE == SMODE_CD) {
-            const double proj = rdot();
+            const double proj = sdot(tv);
             const double rv = V[t];
             const double pv = (rv * wgt - proj) * wgt;
             a.pr[vo] = pv;
             pc += rv * pv;
             prr += rv * rv;
             ppp += pv * pv;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              s0 = __fma_rn(arow[j + 0], tv2[j + 0], s0);
-              s1 = __fma_rn(arow[j + 1], tv2[j + 1], s1);
-              s2 = __fma_rn(arow[j + 2], tv2[j + 2], s2);
-              s3 = __fma_rn(arow[j + 3], tv2[j + 3], s3);
-            }
-            const double res = (V[T + t] - ((s0 + s1) + (s2 + s3))) * iwgt;
+            asm volatile("" ::: "memory");  // re-read the row from shared memory (keeps it out of registers)
+            const double res = (V[T + t] - sdot(tv2)) * iwgt;
             if (k < g.M) rsum += res * res;
             x = V[2 * T + t] + (-lam) * V[3 * T + t];  // w_{i+1}
           } else if (MODE == SMODE_B) {
@@ -1713,13 +1726,18 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
             if (k < g.M) rsum += res * res;
             x = V[t] + (-lp) * V[2 * T + t];
           }
-          if constexpr (COLS) {
+          if constexpr (COLS && ROWREG) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) facc[j] = __fma_rn(arow[j], x, facc[j]);
           }
-          if constexpr (COLS2) {
+          if constexpr (COLS && !ROWREG) {
+            asm volatile("" ::: "memory");  // re-read the row from shared memory (keeps it out of registers)
 #pragma unroll
-            for (int j = 0; j < 32; ++j) facc2[j] = __fma_rn(arow[j], x2, facc2[j]);
+            for (int j = 0; j < 32; ++j) {
+              const double q = M0[(int64_t)j * T + t];
+              facc[j] = __fma_rn(q, x, facc[j]);
+              if constexpr (COLS2) facc2[j] = __fma_rn(q, x2, facc2[j]);
+            }
           }
         }
         __syncthreads();  // the stage is free
@@ -1741,6 +1759,35 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
         for (; j < nb; ++j) s0 = s0 + Mrow[(int64_t)j * T] * tv[j];
         return (s0 + s1) + (s2 + s3);
       };
+      // wide blocks with T < NT: every thread helps with the Q-side row dots -- thread (p, r) = (tid / T, tid % T)
+      // sums columns [p nb / P, (p + 1) nb / P) of row r (consecutive rows per warp: conflict-free), the P
+      // partials are then added in p order; with one thread per row a 118-long dot on 64 of 256 threads was the
+      // pass's critical path
+      constexpr bool QROW = (MODE == SMODE_B || MODE == SMODE_C || MODE == SMODE_XS || MODE == SMODE_DIAG);
+      const int P = NT / T;
+      const bool coop = QROW && P > 1 && !(MODE == SMODE_B && a.xv_from_x) && !(MODE == SMODE_DIAG && !a.qdiag);
+      if (coop) {
+        const int pp = tid / T, rr = tid - pp * T;
+        const int j0 = pp * nb / P, j1 = (pp + 1) * nb / P;
+        double s0 = 0.0, s1 = 0.0;
+        if (rr < rows) {
+          const double* Mrow = M0 + rr;
+          int j = j0;
+          for (; j + 2 <= j1; j += 2) {
+            s0 = __fma_rn(Mrow[(int64_t)(j + 0) * T], tv[j + 0], s0);
+            s1 = __fma_rn(Mrow[(int64_t)(j + 1) * T], tv[j + 1], s1);
+          }
+          if (j < j1) s0 = __fma_rn(Mrow[(int64_t)j * T], tv[j], s0);
+        }
+        pdot[tid] = s0 + s1;
+        __syncthreads();
+      }
+      auto rowq = [&](int t) {
+        if (!coop) return qdot(M0 + t);
+        double s = pdot[t];
+        for (int q = 1; q < P; ++q) s += pdot[q * T + t];
+        return s;
+      };
       for (int t = tid; t < rows; t += NT) {
         const int64_t k = kb + t;
         const int64_t vo = vbase + k;
@@ -1754,13 +1801,13 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
             if (k < g.M)
               for (int j = 0; j < nb; ++j) xv = xv + M1[(int64_t)j * T + t] * tv[j];
           } else {
-            xv = qdot(M0 + t) * iwgt;
+            xv = rowq(t) * iwgt;
           }
           const double rn = rv - lam * (suv + xv);
           a.r[vo] = rn;
           xs[t] = rn * wgt;
         } else if (MODE == SMODE_C || MODE == SMODE_XS) {
-          const double proj = qdot(M0 + t);
+          const double proj = rowq(t);
           if (MODE == SMODE_XS) {
             a.out[vo] = proj * wgt;
           } else {
@@ -1778,7 +1825,7 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           const double swv = V[t] + (-lp) * V[T + t];  // sw_{i+1} = sw_i - lambda_i su_i when pending
           xs[t] = (yv - swv) * wgt;
         } else {  // SMODE_DIAG
-          const double xe = (k < g.M) ? (a.qdiag ? qdot(M0 + t) * iwgt : qdot(M0 + t)) : 0.0;
+          const double xe = (k < g.M) ? (a.qdiag ? rowq(t) * iwgt : rowq(t)) : 0.0;
           const double yv = (k < g.M) ? a.y[(int64_t)b * a.ldy + k] : 0.0;
           const double swv = V[T + t] + (-lp) * V[3 * T + t];
           const double res = yv - (swv + xe);
@@ -1786,19 +1833,33 @@ __global__ void __launch_bounds__(NT) k_stream(Geo g, StreamArgs a, const SolveS
           xs[t] = V[t] + (-lp) * V[2 * T + t];
         }
       }
-      // ---- phase 2: column partials acc_j += sum_rows A[k, j] x_k (warp per column, lanes over rows)
+      // ---- phase 2: column partials acc_j += sum_rows A[k, j] x_k (warp per column, lanes over rows).  The lane's
+      // x values are hoisted into registers and the row loop is unrolled for the tile height (rows of a partial
+      // last tile carry x = 0, set below, so no per-row bound check); fused multiply-adds (tree sums anyway)
       if (COLS) {
+        for (int t = rows + tid; t < T; t += NT) xs[t] = 0.0;
         __syncthreads();
+        auto cols = [&](auto rpl_tag) {
+          constexpr int RPL = decltype(rpl_tag)::value;
+          double xr[RPL];
 #pragma unroll
-        for (int q = 0; q < MAXC; ++q) {
-          const int j = warp + (NT / 32) * q;
-          if (j < nb) {
-            const double* Mj = M0 + (int64_t)j * T;
-            double s = acc[q];
-            for (int t = lane; t < rows; t += 32) s += Mj[t] * xs[t];
-            acc[q] = s;
+          for (int i = 0; i < RPL; ++i) xr[i] = xs[lane + 32 * i];
+#pragma unroll
+          for (int q = 0; q < MAXC; ++q) {
+            const int j = warp + (NT / 32) * q;
+            if (j < nb) {
+              const double* Mj = M0 + (int64_t)j * T + lane;
+              double s = acc[q];
+#pragma unroll
+              for (int i = 0; i < RPL; ++i) s = __fma_rn(Mj[32 * i], xr[i], s);
+              acc[q] = s;
+            }
           }
-        }
+        };
+        if (T == 64) cols(std::integral_constant<int, 2>{});
+        else if (T == 128) cols(std::integral_constant<int, 4>{});
+        else if (T == 256) cols(std::integral_constant<int, 8>{});
+        else cols(std::integral_constant<int, 1>{});
       }
       __syncthreads();  // the stage (and xs) are free
       if (warp == 0) issue(stage);
@@ -2182,6 +2243,9 @@ __global__ void k_diag_finalize(const double* rpart, int count, const double* xt
       const bool sampled = row_override >= 0 ? true : (st->sampled != 0);
       if (sampled && beta) row.rmse = sqrt(v[2] / (double)n);
     }
+    // the row is final: later (inactive) iterations of the same graph chunk must not redo it (the folded
+    // diagnostics' est = R^-1 s_est is computed in place)
+    if (row_override < 0) st->diag_now = 0;
   }
 }
 
