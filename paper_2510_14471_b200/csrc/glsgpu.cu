@@ -346,7 +346,8 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
   const int tr = 8 * rw;
   const int64_t ntiles = h->ldm / tr;
   const int grid = (int)std::min<int64_t>(ntiles, GRID_CAP);
-  const size_t smem = (size_t)h->G * tr * sizeof(double);
+  // pass A with 64 < G <= 128 stages the tile's u, pr, w, sw, su in shared memory (k_kron, in_mode 2)
+  const size_t smem = (size_t)h->G * tr * sizeof(double) * ((in_mode == 2 && cpl == 4) ? 5 : 1);
   if (grid_out) *grid_out = grid;
 #define KRON_CASE(C, RW)                                                                                       \
   k_kron<C, RW><<<grid, NT, smem, h->s>>>(h->G, h->ldm, ntiles, h->omegaT, src, prv, div, u_io, out, partials, \
@@ -842,8 +843,14 @@ void build_geometry(glsgpu_sur* h, int G, int64_t M, const int64_t* n_i, const d
   }
   h->n = p;
   h->nmax = nmax;
-  // row chunk of the column passes: 256-row multiples, at most ~64 chunks per block
-  h->CH = std::min<int64_t>(16384, std::max<int64_t>(256, round_up((h->ldm + 63) / 64, 256)));
+  // row chunk of the column passes (a work item = one chunk of one block): 256-row multiples, at most ~64 chunks
+  // per block; small models take chunks of up to 2048 rows (8 tiles) as long as >= 4 items per SM remain, so the
+  // per-item setup and column reductions are amortised over several tiles
+  {
+    const int64_t ch_large = round_up((h->ldm + 63) / 64, 256);
+    const int64_t ch_cap = round_up((h->ldm + (592 + G - 1) / G - 1) / ((592 + G - 1) / G), 256);
+    h->CH = std::min<int64_t>(16384, std::max<int64_t>(256, std::max(ch_large, std::min<int64_t>(2048, ch_cap))));
+  }
   h->nch = (int)((h->ldm + h->CH - 1) / h->CH);
   h->d_nb = dalloc<int>(G);
   h->d_p0 = dalloc<int64_t>(G);
@@ -1558,6 +1565,7 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     // kron kernels: >48 KB dynamic shared memory at large G
     CK(cudaFuncSetAttribute(k_kron<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 8));
     CK(cudaFuncSetAttribute(k_kron<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16 * 8));
+    CK(cudaFuncSetAttribute(k_kron<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * 128 * 32 * 8));
     CK(cudaFuncSetAttribute(k_colpass<MODE_B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(h->CH * 8)));
     CK(cudaFuncSetAttribute(k_colpass<MODE_QT_R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

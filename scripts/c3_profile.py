@@ -1,4 +1,4 @@
-"""Development aid: where config 3's SUR solve spends its time (setup vs passes)."""
+"""Development aid: where a config's SUR solve spends its time (setup vs passes).  python scripts/c3_profile.py [config]"""
 import os
 import sys
 import time
@@ -6,7 +6,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2510_14471_b200 import api, synth  # noqa: E402
 
-p = synth.make_problem(3)
+p = synth.make_problem(int(sys.argv[1]) if len(sys.argv) > 1 else 3)
 sur = api.sur_from_problem(p)
 print("widths min/max", int(p.nb.min()), int(p.nb.max()), "n", p.n, flush=True)
 t0 = time.perf_counter()
