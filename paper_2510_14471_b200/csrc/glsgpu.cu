@@ -1087,9 +1087,15 @@ void launch_formq(glsgpu_sur* h, int64_t max_rows, int grid, int smem, const QrI
   CKL("k_qr_formq");
 }
 
-// lane-per-column leaf kernels: the two-CTA-per-SM forms (default) or the original one-CTA form (GLSGPU_QR_LC1=1)
+// lane-per-column leaf kernels: the two-CTA-per-SM forms (default) or the original one-CTA form (GLSGPU_QR_LC=1).
+// (Measured and dropped in round 2: a four-warp / 64-rows-per-warp form, 335 vs 338 ms at c4 with one fewer CTA per
+// SM, and a row-per-thread form with the 32 steps unrolled, 570 ms: its per-step transpose-reduce and shuffles cost
+// more than the lane-per-column broadcast.)
 bool qr_lc1() {
-  static const bool v = std::getenv("GLSGPU_QR_LC1") != nullptr;
+  static const bool v = [] {
+    const char* e = std::getenv("GLSGPU_QR_LC");
+    return e && std::atoi(e) == 1;
+  }();
   return v;
 }
 const void* qrf_lc_fn() { return qr_lc1() ? (const void*)k_qr_factor_lc : (const void*)k_qr_factor_lc2; }
