@@ -1099,8 +1099,20 @@ bool qr_lc1() {
   return v;
 }
 const void* qrf_lc_fn() { return qr_lc1() ? (const void*)k_qr_factor_lc : (const void*)k_qr_factor_lc2; }
-const void* qrq_lc_fn() { return qr_lc1() ? (const void*)k_qr_formq_lc : (const void*)k_qr_formq_lc2; }
+// explicit Q of the narrow leaves: the lane-per-column kernel (default) or compact WY on the DMMA
+// (GLSGPU_QR_FORMQ=wy: the same time at c4, 343 vs 337 ms per setup -- both are bound by per-leaf latency)
+bool qrq_wy() {
+  static const bool v = [] {
+    const char* e = std::getenv("GLSGPU_QR_FORMQ");
+    return e && std::strcmp(e, "wy") == 0;
+  }();
+  return v && !qr_lc1();
+}
+const void* qrq_lc_fn() {
+  return qr_lc1() ? (const void*)k_qr_formq_lc : qrq_wy() ? (const void*)k_qr_formq_wy : (const void*)k_qr_formq_lc2;
+}
 size_t qr_lc_smem() { return qr_lc1() ? qrc_smem_bytes() : qrc2_smem_bytes(); }
+size_t qrq_lc_smem() { return qrq_wy() ? qw_smem_bytes() : qr_lc_smem(); }
 void launch_qrf_lc(glsgpu_sur* h, const QrItem* items, int count, int grid) {
   if (qr_lc1()) k_qr_factor_lc<<<grid, QRC_NT, qrc_smem_bytes(), h->s>>>(items, count);
   else k_qr_factor_lc2<<<grid, QRC_NT, qrc2_smem_bytes(), h->s>>>(items, count);
@@ -1109,6 +1121,7 @@ void launch_qrf_lc(glsgpu_sur* h, const QrItem* items, int count, int grid) {
 }
 void launch_qrq_lc(glsgpu_sur* h, const QrItem* items, int count, int grid) {
   if (qr_lc1()) k_qr_formq_lc<<<grid, QRC_NT, qrc_smem_bytes(), h->s>>>(items, count);
+  else if (qrq_wy()) k_qr_formq_wy<<<grid, QW_NT, qw_smem_bytes(), h->s>>>(items, count);
   else k_qr_formq_lc2<<<grid, QRC_NT, qrc2_smem_bytes(), h->s>>>(items, count);
   if (!h->capturing) h->launches++;
   CKL("k_qr_formq_lc");
@@ -1116,10 +1129,10 @@ void launch_qrq_lc(glsgpu_sur* h, const QrItem* items, int count, int grid) {
 // resident CTAs of the lane-per-column leaves (the item loop strides by gridDim: a second wave would serialise)
 void qr_lc_grids(glsgpu_sur* h, int* gf, int* gq) {
   CK(cudaFuncSetAttribute(qrf_lc_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qr_lc_smem()));
-  CK(cudaFuncSetAttribute(qrq_lc_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qr_lc_smem()));
+  CK(cudaFuncSetAttribute(qrq_lc_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qrq_lc_smem()));
   int occ_f = 1, occ_q = 1, nsm = 148;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, qrf_lc_fn(), QRC_NT, qr_lc_smem()));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, qrq_lc_fn(), QRC_NT, qr_lc_smem()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, qrq_lc_fn(), QRC_NT, qrq_lc_smem()));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
   *gf = std::max(1, occ_f) * nsm;
   *gq = std::max(1, occ_q) * nsm;

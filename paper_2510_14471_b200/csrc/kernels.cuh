@@ -3120,6 +3120,212 @@ __global__ void __launch_bounds__(QRC_NT, 2) k_qr_formq_lc2(const QrItem* items,
 }
 
 // ------------------------------------------------------------------------------------------
+// Explicit Q of a narrow leaf in compact WY form on the FP64 tensor cores (round 2, the default).  The leaf's n
+// reflectors H_j = I - bh_j v_j v_j' (unit-head v_j, bh_j = beta_j v0_j^2: the reference's recipe) multiply to
+// H_0 ... H_{n-1} = I - V T V' with T upper triangular, T_jj = bh_j, T_{0:j,j} = -bh_j T_{0:j,0:j} (V'V)_{0:j,j}
+// (the forward accumulation of form_q_columns' product, linalg.cpp:77-95, as LAPACK's larft does).  So
+// E = H_0 ... H_{n-1} [C; 0] = [C; 0] - V (T (V_top' C)), with V'V and the final V (T ...) product as DMMA
+// m16n8k4 tiles: one read of the packed panel, one write of E, and no per-reflector CTA reductions (the
+// lane-per-column k_qr_formq_lc2 runs 32 dependent reduction steps per leaf).  Rounding differs from applying the
+// reflectors one by one only in the order of the sums (Q stays orthonormal to ~1e-15; the TSQR tests pin it).
+constexpr int QW_NT = 256;
+constexpr int QW_LDV = 256 + 4;  // V column stride in shared memory (conflict-free DMMA fragment loads)
+constexpr int QW_LDS = 33;       // 32 x 32 scratch matrices
+constexpr size_t qw_smem_bytes() { return (size_t)(32 * QW_LDV + 6 * 32 * QW_LDS) * sizeof(double); }
+
+__global__ void __launch_bounds__(QW_NT, 2) k_qr_formq_wy(const QrItem* items, int nitems) {
+  extern __shared__ double sm[];
+  double* Vs = sm;                           // V, column j at Vs + j QW_LDV (rows 0..255)
+  double* Gp = Vs + 32 * QW_LDV;             // two K-half partials of V'V, [2][32][QW_LDS]
+  double* Ts = Gp + 2 * 32 * QW_LDS;         // T
+  double* Ys = Ts + 32 * QW_LDS;             // V_top' C, then -(T Y)
+  double* Zs = Ys + 32 * QW_LDS;
+  double* Cs = Zs + 32 * QW_LDS;             // the parent's n x n slice C (or I)
+  __shared__ double bh[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, q4 = lane & 3;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const QrItem I = items[it];
+    const int n = I.n;
+    const int64_t L = I.rows;
+    __syncthreads();  // the previous item's readers of shared memory are done
+    {
+      const bool rv = t < L;
+      for (int j = 0; j < 32; ++j)
+        cp_async8_zfill(Vs + j * QW_LDV + t, I.refl + I.rr0 + (int64_t)j * I.ldr + t, rv && j < n);
+      for (int idx = t; idx < 32 * 32; idx += QW_NT) {  // C row-major in Cs[r][c]
+        const int c = idx >> 5, r = idx & 31;
+        if (I.qpar) cp_async8_zfill(Cs + r * QW_LDS + c, I.qpar + r + (int64_t)c * I.ldp, r < n && c < n);
+        else Cs[r * QW_LDS + c] = (r == c && r < n) ? 1.0 : 0.0;
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (t < 32) {  // bh_j = beta_j v0_j^2 from the packed diagonal, before the unit head replaces it
+      const double v0 = Vs[t * QW_LDV + t];
+      const double tk = (t < n) ? I.tau[t] : 0.0;
+      bh[t] = tk * v0 * v0;
+    }
+    __syncthreads();
+    for (int idx = t; idx < 32 * 32; idx += QW_NT) {  // unit head, zeros above (the R part of the packed panel)
+      const int j = idx >> 5, r = idx & 31;
+      if (r < j) Vs[j * QW_LDV + r] = 0.0;
+      else if (r == j) Vs[j * QW_LDV + r] = (j < n && bh[j] != 0.0) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    // V'V: warp w -> Gram columns [8 (w & 3), +8), rows [128 (w >> 2), +128) of V
+    {
+      double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+      const int c0 = 8 * (warp & 3), rb = 128 * (warp >> 2);
+#pragma unroll 4
+      for (int kk = 0; kk < 32; ++kk) {
+        const int r0 = rb + 4 * kk;
+        const double b0 = Vs[(c0 + g) * QW_LDV + r0 + q4];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const double a0 = Vs[(16 * mi + g) * QW_LDV + r0 + q4];
+          const double a1 = Vs[(16 * mi + g + 8) * QW_LDV + r0 + q4];
+          dmma_16x8x4(acc[mi], a0, a1, b0);
+        }
+      }
+      double* G = Gp + (warp >> 2) * 32 * QW_LDS;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) G[(16 * mi + g + 8 * (e >> 1)) * QW_LDS + c0 + 2 * q4 + (e & 1)] = acc[mi][e];
+    }
+    __syncthreads();
+    // T, blockwise: the four diagonal 8 x 8 blocks by the larft recurrence (warps 0-3 in parallel), then
+    // T_AB = -T_A (V_A' V_B) T_B for the block pairs (0,1), (2,3) and then ({0,1}, {2,3})  [Q_A Q_B = I - [V_A V_B]
+    // [T_A, -T_A V_A'V_B T_B; 0, T_B] [V_A V_B]'].  (V'V: the two K-half partials summed into Gp[0] first.)
+    for (int idx = t; idx < 32 * 32; idx += QW_NT) {
+      const int i = idx >> 5, j = idx & 31;
+      Gp[i * QW_LDS + j] += Gp[32 * QW_LDS + i * QW_LDS + j];
+      Ts[i * QW_LDS + j] = 0.0;
+    }
+    __syncthreads();
+    double* W = Gp + 32 * QW_LDS;  // scratch for the off-diagonal blocks (the second partial is consumed)
+    if (warp < 4) {
+      const int I0 = 8 * warp;
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = I0 + jj;
+        if (lane < 8 && j < n) {
+          const int i = I0 + lane;
+          double v = 0.0;
+          if (i < j) {
+            double s0 = 0.0;
+            for (int l = i; l < j; ++l) s0 += Ts[i * QW_LDS + l] * Gp[l * QW_LDS + j];
+            v = -bh[j] * s0;
+          } else if (i == j) {
+            v = bh[j];
+          }
+          Ts[i * QW_LDS + j] = v;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // level 1 (warps 0, 1): blocks (A, B) = (0, 1), (2, 3): W = G_AB T_B, then T_AB = -T_A W
+    if (warp < 2) {
+      const int A0 = 16 * warp, B0 = A0 + 8;
+      for (int e = lane; e < 64; e += 32) {
+        const int i = e >> 3, j = e & 7;
+        double s0 = 0.0;
+        for (int l = 0; l <= j; ++l) s0 += Gp[(A0 + i) * QW_LDS + B0 + l] * Ts[(B0 + l) * QW_LDS + B0 + j];
+        W[(A0 + i) * QW_LDS + B0 + j] = s0;
+      }
+      __syncwarp();
+      for (int e = lane; e < 64; e += 32) {
+        const int i = e >> 3, j = e & 7;
+        double s0 = 0.0;
+        for (int l = i; l < 8; ++l) s0 += Ts[(A0 + i) * QW_LDS + A0 + l] * W[(A0 + l) * QW_LDS + B0 + j];
+        Ts[(A0 + i) * QW_LDS + B0 + j] = -s0;
+      }
+    }
+    __syncthreads();
+    // level 2 (all warps): A = columns 0..15, B = 16..31: W = G_AB T_B (16 x 16), T_AB = -T_A W
+    {
+      const int i = t >> 4, j = t & 15;  // 256 threads = 16 x 16 outputs
+      double s0 = 0.0;
+      for (int l = 0; l <= j; ++l) s0 += Gp[i * QW_LDS + 16 + l] * Ts[(16 + l) * QW_LDS + 16 + j];
+      W[i * QW_LDS + 16 + j] = s0;
+      __syncthreads();
+      double s1 = 0.0;
+      for (int l = i; l < 16; ++l) s1 += Ts[i * QW_LDS + l] * W[l * QW_LDS + 16 + j];
+      Ts[i * QW_LDS + 16 + j] = -s1;
+    }
+    __syncthreads();
+    // Y = V_top' C and then Z = -(T Y), both 32 x 32 x 32 on the DMMA: warp w -> tile (w >> 2, w & 3)
+    {
+      const int mi = warp >> 2, ni = warp & 3;
+      double y[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double a0 = Vs[(16 * mi + g) * QW_LDV + 4 * kk + q4];      // V'[i][r] = V[r][i], rows r < 32
+        const double a1 = Vs[(16 * mi + g + 8) * QW_LDV + 4 * kk + q4];
+        const double b0 = Cs[(4 * kk + q4) * QW_LDS + 8 * ni + g];
+        dmma_16x8x4(y, a0, a1, b0);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Ys[(16 * mi + g + 8 * (e >> 1)) * QW_LDS + 8 * ni + 2 * q4 + (e & 1)] = y[e];
+      __syncthreads();
+      double z[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double a0 = Ts[(16 * mi + g) * QW_LDS + 4 * kk + q4];
+        const double a1 = Ts[(16 * mi + g + 8) * QW_LDS + 4 * kk + q4];
+        const double b0 = Ys[(4 * kk + q4) * QW_LDS + 8 * ni + g];
+        dmma_16x8x4(z, a0, a1, b0);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Zs[(16 * mi + g + 8 * (e >> 1)) * QW_LDS + 8 * ni + 2 * q4 + (e & 1)] = -z[e];
+    }
+    __syncthreads();
+    // E = [C; 0] + V Z: warp w -> rows [32 w, +32), all 32 columns
+    double acc[2][4][4];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 32 * warp + 16 * mi + g + 8 * (e >> 1);
+          const int c = 8 * ni + 2 * q4 + (e & 1);
+          acc[mi][ni][e] = (r < 32) ? Cs[r * QW_LDS + c] : 0.0;
+        }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      double a0[2], a1[2], b0[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        a0[mi] = Vs[(4 * kk + q4) * QW_LDV + 32 * warp + 16 * mi + g];
+        a1[mi] = Vs[(4 * kk + q4) * QW_LDV + 32 * warp + 16 * mi + g + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b0[ni] = Zs[(4 * kk + q4) * QW_LDS + 8 * ni + g];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_16x8x4(acc[mi][ni], a0[mi], a1[mi], b0[ni]);
+    }
+    __syncthreads();  // every warp is done reading V: E goes through the same buffer
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 32 * warp + 16 * mi + g + 8 * (e >> 1);
+          const int c = 8 * ni + 2 * q4 + (e & 1);
+          Vs[c * QW_LDV + r] = acc[mi][ni][e];
+        }
+    __syncthreads();
+    if (t < L)
+      for (int j = 0; j < n; ++j) I.refl[(int64_t)j * I.ldr + I.rr0 + t] = Vs[j * QW_LDV + t];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Counter-based normal generator for synthetic inputs: Philox4x32-10 on (element, stream) keyed
 // by the seed, Box-Muller on two 53-bit uniforms (u1 in (0,1]).  Element e of a rows x cols
 // matrix is e = col * rows + row, independent of the leading dimension.
