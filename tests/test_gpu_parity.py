@@ -489,3 +489,32 @@ def test_folded_diagnostics(name, mk, monkeypatch):
     k = min(5, len(o.trace))
     assert np.allclose(fold.trace.rows["aug_residual_norm"][:k], o.trace["aug_residual_norm"][:k], rtol=1e-9)
     assert np.allclose(fold.trace.rows["rmse"][:k], o.trace["rmse"][:k], rtol=1e-9, equal_nan=True)
+
+
+def test_compact_wy_formq_option():
+    """GLSGPU_QR_FORMQ=wy (the compact-WY explicit-Q leaf on the DMMA, k_qr_formq_wy) in a fresh process: the
+    factors stay orthonormal with Q R = X and the c0 solve meets the oracle bar."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_2510_14471_b200 import api, synth\n"
+        "p = synth.make_problem(4, M=3000, G=12)\n"
+        "op = api.sur_preconditioner(api.sur_from_problem(p))\n"
+        "Q, R = op.factors()\n"
+        "off = roff = 0\n"
+        "for k in p.nb:\n"
+        "    Qi = Q[:, off:off + k]; Ri = R[roff:roff + k * k].reshape(k, k, order='F')\n"
+        "    assert np.max(np.abs(Qi.T @ Qi - np.eye(k))) < 1e-13\n"
+        "    assert np.max(np.abs(Qi @ Ri - p.X[:, off:off + k])) < 1e-12 * np.abs(p.X).max()\n"
+        "    off += k; roff += k * k\n"
+        "q = synth.make_problem(0)\n"
+        "g = api.pcg_aug(api.sur_from_problem(q), config=api.PcgConfig(tol_rel=q.tol_rel, xv_mode='qr', diag_every=0))\n"
+        "o = oracle.solve(q, 'oracle')\n"
+        "assert g.solution.iterations == o.iterations\n"
+        "assert np.linalg.norm(g.solution.b - o.b) <= 1e-10 * np.linalg.norm(o.b)\n"
+        "print('ok')\n")
+    env = dict(os.environ, GLSGPU_QR_FORMQ="wy")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
