@@ -346,9 +346,20 @@ void launch_kron(glsgpu_sur* h, const double* src, const double* prv, const doub
   const int tr = 8 * rw;
   const int64_t ntiles = h->ldm / tr;
   const int grid = (int)std::min<int64_t>(ntiles, GRID_CAP);
-  // pass A with 64 < G <= 128 stages the tile's u, pr, w, sw, su in shared memory (k_kron, in_mode 2)
-  const size_t smem = (size_t)h->G * tr * sizeof(double) * ((in_mode == 2 && cpl == 4) ? 5 : 1);
+  // G <= 128 (cpl <= 4): Omega behind the tile in shared memory
+  const size_t smem = ((size_t)h->G * tr + (cpl <= 4 ? (size_t)h->G * h->G : 0)) * sizeof(double);
   if (grid_out) *grid_out = grid;
+  {  // the dynamic shared memory bound of every k_kron instance (once; G <= 128 also stages Omega)
+    static bool attrs = false;
+    if (!attrs) {
+      CK(cudaFuncSetAttribute(k_kron<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (32 * 32 + 32 * 32) * 8));
+      CK(cudaFuncSetAttribute(k_kron<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 32 + 64 * 64) * 8));
+      CK(cudaFuncSetAttribute(k_kron<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 32 + 128 * 128) * 8));
+      CK(cudaFuncSetAttribute(k_kron<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 8));
+      CK(cudaFuncSetAttribute(k_kron<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16 * 8));
+      attrs = true;
+    }
+  }
 #define KRON_CASE(C, RW)                                                                                       \
   k_kron<C, RW><<<grid, NT, smem, h->s>>>(h->G, h->ldm, ntiles, h->omegaT, src, prv, div, u_io, out, partials, \
                                           in_mode, st, wbuf_of(h), h->msig)
@@ -1584,7 +1595,8 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     // kron kernels: >48 KB dynamic shared memory at large G
     CK(cudaFuncSetAttribute(k_kron<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 8));
     CK(cudaFuncSetAttribute(k_kron<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16 * 8));
-    CK(cudaFuncSetAttribute(k_kron<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * 128 * 32 * 8));
+    CK(cudaFuncSetAttribute(k_kron<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 32 + 128 * 128) * 8));
+    CK(cudaFuncSetAttribute(k_kron<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 32 + 64 * 64) * 8));
     CK(cudaFuncSetAttribute(k_colpass<MODE_B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(h->CH * 8)));
     CK(cudaFuncSetAttribute(k_colpass<MODE_QT_R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

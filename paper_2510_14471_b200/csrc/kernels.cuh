@@ -171,47 +171,19 @@ __global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles,
     swn = wbuf.sw[st->nxt];
   }
   const double dv = (in_mode == 1) ? *div : 1.0;
+  // G <= 128: Omega (G^2 doubles) lives in shared memory behind the tile, so the p loop's Omega reads are
+  // shared-memory broadcasts instead of L1 / L2 round trips on the accumulation chain
+  constexpr bool OMS = CPL <= 4;
+  double* const oms = xs + G * TR;
+  if (OMS) {
+    for (int i = threadIdx.x; i < G * G; i += NT) oms[i] = omegaT[i];
+    __syncthreads();
+  }
   double p_xo = 0.0, p_xx = 0.0, p_oo = 0.0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t k0 = tile * TR;
     __syncthreads();
-    if (in_mode == 2 && CPL == 4) {
-      // 64 < G <= 128: the tile's u, pr, w, sw, su all go to shared memory by asynchronous copies issued at once (one
-      // memory round trip per tile instead of one per batch), then the element updates run from shared memory
-      const int ne = G * TR;
-      double* pr_s = xs + ne;
-      double* w_s = pr_s + ne;
-      double* sw_s = w_s + ne;
-      double* so_s = sw_s + ne;
-      for (int idx = threadIdx.x; idx < ne; idx += NT) {
-        const int p = idx / TR, r = idx - p * TR;
-        const int64_t off = (int64_t)p * ldm + k0 + r;
-        cp_async8(xs + idx, u_io + off);
-        if (upd) cp_async8(pr_s + idx, pr + off);
-        if (wupd) {
-          cp_async8(w_s + idx, wc + off);
-          cp_async8(sw_s + idx, swc + off);
-          cp_async8(so_s + idx, out + off);
-        }
-      }
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < ne; idx += NT) {
-        const int p = idx / TR, r = idx - p * TR;
-        const int64_t off = (int64_t)p * ldm + k0 + r;
-        const double uo = xs[idx];
-        if (wupd) {
-          wn[off] = w_s[idx] + (-lp) * uo;
-          swn[off] = sw_s[idx] + (-lp) * so_s[idx];
-        }
-        double x = uo;
-        if (upd) {
-          x = pr_s[idx] + mu * uo;
-          u_io[off] = x;
-        }
-        xs[idx] = x;
-      }
-    } else if (in_mode == 2) {
+    if (in_mode == 2) {
       // batches of 4 elements per thread: every load of the batch is issued before any store, so the
       // deferred w / sw update (axpy(-lambda, u, w), axpy(-lambda, su, sw), pcg.cpp:151-152; su read
       // before Sigma u overwrites it) streams under the Kronecker math instead of serialising it
@@ -276,7 +248,7 @@ __global__ void __launch_bounds__(NT) k_kron(int G, int64_t ldm, int64_t ntiles,
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
         const int c = lane + 32 * q;
-        o[q] = (c < G) ? __ldg(omegaT + (int64_t)p * G + c) : 0.0;
+        o[q] = (c < G) ? (OMS ? oms[p * G + c] : __ldg(omegaT + (int64_t)p * G + c)) : 0.0;
       }
       double xr[RW];
 #pragma unroll
