@@ -349,30 +349,37 @@ def run_ours(args):
     # diag_every = 1 with Sigma w by the reference's recurrence, the diagnostics folded into passes B / C
     trace_all = None
     if not args.no_trace_all and args.diag == 0:
-        tcfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, kernel_timing=True,
-                             **dict(knobs, diag_every=1, sw_mode=0, fused_c=0))
-        op.refactor()
-        api.pcg_aug(None, op, config=tcfg, true_beta=beta, want_w=False)  # warm-up (graph capture)
-        t_ms, t_it, tk = 0.0, 0, {}
-        for _ in range(2):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+        def trace_leg(diag_every):
+            tcfg = api.PcgConfig(tol_rel=tol, max_iter=max_iter, kernel_timing=True,
+                                 **dict(knobs, diag_every=diag_every, sw_mode=0, fused_c=0))
             op.refactor()
-            r = api.pcg_aug(None, op, config=tcfg, true_beta=beta, want_w=False)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            t_ms += e0.elapsed_time(e1)
-            t_it += r.solution.iterations
-            for s_ in op.kernel_stats():
-                d = tk.setdefault(s_["name"], [0, 0.0])
-                d[0] += s_["launches"]
-                d[1] += s_["total_ms"]
-        it_ms_all = sum(v[1] / v[0] for v in tk.values() if v[0])
-        trace_all = {"value": t_it / (t_ms / 1e3), "unit": UNIT, "steps": 2, "diag_every": 1, "sigma_w": "recurrence",
-                     "iter_ms": it_ms_all, "iter_ms_vs_main": it_ms_all / iter_ms if iter_ms else None,
-                     "passes": {k: v[1] / v[0] for k, v in tk.items() if v[0]},
-                     "rows_with_diagnostics": int(np.isfinite(r.trace.rows["aug_residual_norm"]).sum()),
-                     "rows": int(r.trace.rows.size)}
+            api.pcg_aug(None, op, config=tcfg, true_beta=beta, want_w=False)  # warm-up (graph capture)
+            t_ms, t_it, tk, last_r = 0.0, 0, {}, None
+            for _ in range(2):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                op.refactor()
+                last_r = api.pcg_aug(None, op, config=tcfg, true_beta=beta, want_w=False)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t_ms += e0.elapsed_time(e1)
+                t_it += last_r.solution.iterations
+                for s_ in op.kernel_stats():
+                    d = tk.setdefault(s_["name"], [0, 0.0])
+                    d[0] += s_["launches"]
+                    d[1] += s_["total_ms"]
+            it_ms = sum(v[1] / v[0] for v in tk.values() if v[0])
+            return t_it / (t_ms / 1e3), it_ms, {k: v[1] / v[0] for k, v in tk.items() if v[0]}, last_r
+
+        v0, it0, _, _ = trace_leg(0)
+        v1, it1, passes1, r1 = trace_leg(1)
+        trace_all = {"value": v1, "unit": UNIT, "steps": 2, "diag_every": 1, "sigma_w": "recurrence (sw_mode 0)",
+                     "iter_ms": it1, "passes": passes1,
+                     "same_knobs_diag_every_0": {"value": v0, "iter_ms": it0},
+                     "iter_overhead_vs_same_knobs": it1 / it0 - 1.0,
+                     "iter_ms_vs_main": it1 / iter_ms if iter_ms else None,
+                     "rows_with_diagnostics": int(np.isfinite(r1.trace.rows["aug_residual_norm"]).sum()),
+                     "rows": int(r1.trace.rows.size)}
 
     # ---- e2e through the C-ABI with host buffers: per step, that step's X and Y go up from pinned host memory
     # (staged: overlapping the previous step's solve), the refactor, the solve, b back to the host
