@@ -268,6 +268,10 @@ int glsgpu_model_dims(const glsgpu_sur* h, int64_t* m, int64_t* n);
 /* Test / bench helpers (not part of the reference surface) ---------------------------------- */
 /* Copy Q (M x n, ld M) and the concatenated R blocks to host. */
 int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R);
+/* How the handle's blocks were factored: *method = 1 CholeskyQR2 on the FP64 tensor cores (csrc/cqr.cuh), 0 the
+ * Householder TSQR (always when the environment says GLSGPU_QR=tsqr at creation); *fallbacks = factorisations of
+ * this handle that failed CholeskyQR2's own orthogonality test and were redone by the TSQR. */
+int glsgpu_factor_info(const glsgpu_sur* h, int* method, int* fallbacks);
 /* Rows [row0, row0 + rows) of a rows_total x cols matrix of N(0,1) draws from the counter-based
  * Philox stream (seed, stream), into device memory with leading dimension ld: every row sharding of
  * the same matrix draws identical values. */

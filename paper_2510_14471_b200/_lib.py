@@ -55,7 +55,7 @@ EXPORTS = [
     "glsgpu_synth_response", "glsgpu_nccl_unique_id", "glsgpu_sur_create_sharded", "glsgpu_sur_shard",
     "glsgpu_mvrglm_create", "glsgpu_mv_reduce", "glsgpu_model_dims", "glsgpu_sur_reduce", "glsgpu_pcg_ne", "glsgpu_sur_update",
     "glsgpu_sur_stage", "glsgpu_sur_update_staged", "glsgpu_sur_create_sharded_host", "glsgpu_local_group_create",
-    "glsgpu_local_group_destroy", "glsgpu_sur_create_sharded_local",
+    "glsgpu_local_group_destroy", "glsgpu_sur_create_sharded_local", "glsgpu_factor_info",
 ]
 
 _lib = None
@@ -105,6 +105,7 @@ def load() -> C.CDLL:
     L.glsgpu_kernel_stats.argtypes = [H, C.POINTER(KernelStatC), C.c_int]
     L.glsgpu_launch_count.argtypes = [H, _PI64]
     L.glsgpu_get_factors.argtypes = [H, _P, _P]
+    L.glsgpu_factor_info.argtypes = [H, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     L.glsgpu_synth_normal.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
                                       C.c_uint64, C.c_int]
     L.glsgpu_synth_response.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, _PI64, C.c_void_p, C.c_int64, _P, _P,

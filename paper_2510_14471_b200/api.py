@@ -386,6 +386,13 @@ class GpuSurPreconditioner:
         _check(self._lib.glsgpu_get_factors(self._h, _dp(Q), _dp(R)), self._lib)
         return Q, R
 
+    def factor_info(self):
+        """(method, fallbacks): method "cholqr2" (csrc/cqr.cuh) or "tsqr" for the current factors; fallbacks = how
+        many factorisations of this operator failed CholeskyQR2's own test and were redone by the Householder TSQR."""
+        m, f = C.c_int(0), C.c_int(0)
+        _check(self._lib.glsgpu_factor_info(self._h, C.byref(m), C.byref(f)), self._lib)
+        return ("cholqr2" if m.value == 1 else "tsqr"), f.value
+
     def update(self, X: np.ndarray, y: np.ndarray):
         """New data of the same shapes (glsgpu_sur_update): upload X (M x n) and Y (M x G), refactor; the device
         memory and the TSQR plan of this operator are reused."""

@@ -16,7 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libglsgpu.so")
 SOURCES = [os.path.join(CSRC, "glsgpu.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "kernels.cuh"), os.path.join(ROOT, "include", "glsgpu.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "ne.cuh", "gemm.cuh", "cqr.cuh")] + [
+    os.path.join(ROOT, "include", "glsgpu.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

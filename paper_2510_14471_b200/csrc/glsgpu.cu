@@ -29,6 +29,7 @@
 #include "kernels.cuh"
 #include "ne.cuh"
 #include "gemm.cuh"
+#include "cqr.cuh"
 
 using namespace glsgpu;
 
@@ -300,6 +301,21 @@ struct glsgpu_sur {
   QrItem* d_gitems = nullptr;
   int gsmem = 0;
   int64_t gmax_rows = 0;
+  // CholeskyQR2 setup (cqr.cuh): the default factorisation of SUR handles on the TMA passes; TSQR is the fallback
+  bool cq = false;
+  int cq_nbp = 0, cq_tr = 0;
+  CqItem* d_cq_items = nullptr;
+  std::vector<int64_t> cq_first;      // [G + 1] first item of block b
+  int64_t* d_cq_first = nullptr;
+  int* d_cq_nsrc = nullptr;           // [G] items of block b
+  int64_t* d_cq_xoff = nullptr;       // [G] p0[b] ldx
+  double *cq_gpart = nullptr, *cq_r1 = nullptr, *cq_rinv = nullptr;
+  int* d_cq_flags = nullptr;
+  int64_t* d_cq_bidx = nullptr;       // sharded: source index b and count P of the all-gathered Grams
+  int* d_cq_np = nullptr;
+  double *cq_gloc = nullptr, *cq_gall = nullptr;
+  int cq_fallbacks = 0;               // factorisations that fell back to the Householder TSQR
+  bool cq_last = false;               // the current factors came from CholeskyQR2
 };
 
 namespace {
@@ -1149,9 +1165,162 @@ void qr_lc_grids(glsgpu_sur* h, int* gf, int* gq) {
   *gq = std::max(1, occ_q) * nsm;
 }
 
+
+// ---- CholeskyQR2 setup (cqr.cuh) ----------------------------------------------------------------------------
+// GLSGPU_QR=tsqr keeps the Householder TSQR as the only factorisation (development comparison / fallback tests)
+bool cqr_enabled() {  // read at every handle creation (the tests switch it)
+  const char* e = std::getenv("GLSGPU_QR");
+  return !(e && std::strcmp(e, "tsqr") == 0);
+}
+
+template <int NBP, int MODE>
+void launch_cqr_pass_t(glsgpu_sur* h, const CqArgs& a) {
+  static bool attr_done[8] = {false};  // per device ordinal (the attribute is per context)
+  if (h->dev >= 8 || !attr_done[h->dev]) {
+    CK(cudaFuncSetAttribute(k_cqr_pass<NBP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)cq_smem_bytes<NBP, MODE>()));
+    if (h->dev < 8) attr_done[h->dev] = true;
+  }
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  const int grid = std::min(a.nitems, nsm);
+  k_cqr_pass<NBP, MODE><<<grid, CQ_NT, cq_smem_bytes<NBP, MODE>(), h->s>>>(a);
+  if (!h->capturing) h->launches++;
+  CKL("k_cqr_pass");
+}
+
+template <int MODE>
+void launch_cqr_pass(glsgpu_sur* h, const CqArgs& a) {
+  if (h->cq_nbp == 32) launch_cqr_pass_t<32, MODE>(h, a);
+  else if (h->cq_nbp == 64) launch_cqr_pass_t<64, MODE>(h, a);
+  else launch_cqr_pass_t<128, MODE>(h, a);
+}
+
+void build_cqr_plan(glsgpu_sur* h) {
+  // (a sharded handle: every rank must take the same factorisation -- its collectives differ -- so all ranks must
+  // be on the TMA passes; GLSGPU_QR must agree across ranks)
+  h->cq = cqr_enabled() && !h->mv && !h->no_qtile && (h->coll ? h->all_stream : h->use_stream) && h->nmax <= 128;
+  if (!h->cq) return;
+  h->cq_nbp = h->nmax <= 32 ? 32 : h->nmax <= 64 ? 64 : 128;
+  h->cq_tr = h->cq_nbp == 32 ? CqCfg<32>::TR : h->cq_nbp == 64 ? CqCfg<64>::TR : CqCfg<128>::TR;
+  const int64_t TR = h->cq_tr;
+  // rows per item: ~4736 / G items per block (about 32 per SM in all), at least 16 tiles and 40 NBP rows (the
+  // item's partial Gram stays below ~3% of its input)
+  const int64_t target = std::max<int64_t>(1, (4736 + h->G - 1) / h->G);
+  const int64_t rpi = round_up(std::max<int64_t>({(h->M + target - 1) / target, 16 * TR, 40 * (int64_t)h->cq_nbp}), TR);
+  std::vector<CqItem> items;
+  std::vector<int> nsrc((size_t)h->G);
+  std::vector<int64_t> xoff((size_t)h->G);
+  h->cq_first.assign((size_t)h->G + 1, 0);
+  for (int b = 0; b < h->G; ++b) {
+    h->cq_first[(size_t)b] = (int64_t)items.size();
+    for (int64_t r = 0; r < h->M; r += rpi) {
+      const int64_t rows = std::min(rpi, h->M - r);
+      items.push_back(CqItem{b, (int)((rows + TR - 1) / TR), r});
+    }
+    nsrc[(size_t)b] = (int)((int64_t)items.size() - h->cq_first[(size_t)b]);
+    xoff[(size_t)b] = h->p0[(size_t)b] * h->ldx;
+  }
+  h->cq_first[(size_t)h->G] = (int64_t)items.size();
+  const int64_t nn = (int64_t)h->cq_nbp * h->cq_nbp;
+  h->d_cq_items = dalloc<CqItem>(items.size());
+  CK(cudaMemcpy(h->d_cq_items, items.data(), sizeof(CqItem) * items.size(), cudaMemcpyHostToDevice));
+  h->d_cq_first = dalloc<int64_t>((size_t)h->G + 1);
+  CK(cudaMemcpy(h->d_cq_first, h->cq_first.data(), sizeof(int64_t) * ((size_t)h->G + 1), cudaMemcpyHostToDevice));
+  h->d_cq_nsrc = dalloc<int>((size_t)h->G);
+  CK(cudaMemcpy(h->d_cq_nsrc, nsrc.data(), sizeof(int) * (size_t)h->G, cudaMemcpyHostToDevice));
+  h->d_cq_xoff = dalloc<int64_t>((size_t)h->G);
+  CK(cudaMemcpy(h->d_cq_xoff, xoff.data(), sizeof(int64_t) * (size_t)h->G, cudaMemcpyHostToDevice));
+  h->cq_gpart = dalloc<double>((size_t)(items.size() * nn));
+  int64_t rtot = 0;
+  for (int b = 0; b < h->G; ++b) rtot += (int64_t)h->nb[b] * h->nb[b];
+  h->cq_r1 = dalloc<double>((size_t)rtot);
+  h->cq_rinv = dalloc<double>((size_t)h->G * h->cq_nbp * (h->cq_nbp + 4));
+  h->d_cq_flags = dalloc<int>((size_t)h->G);
+  if (h->coll) {
+    std::vector<int64_t> bidx((size_t)h->G);
+    for (int b = 0; b < h->G; ++b) bidx[(size_t)b] = b;
+    std::vector<int> np((size_t)h->G, h->nranks);
+    h->d_cq_bidx = dalloc<int64_t>((size_t)h->G);
+    CK(cudaMemcpy(h->d_cq_bidx, bidx.data(), sizeof(int64_t) * (size_t)h->G, cudaMemcpyHostToDevice));
+    h->d_cq_np = dalloc<int>((size_t)h->G);
+    CK(cudaMemcpy(h->d_cq_np, np.data(), sizeof(int) * (size_t)h->G, cudaMemcpyHostToDevice));
+    h->cq_gloc = dalloc<double>((size_t)(h->G * nn));
+    h->cq_gall = dalloc<double>((size_t)(h->G * nn * h->nranks));
+  }
+}
+
+template <bool FINAL>
+void launch_cqr_chol(glsgpu_sur* h, int b0, int b1) {
+  const size_t smem = (size_t)h->nmax * (h->nmax + 1) * sizeof(double);
+  CK(cudaFuncSetAttribute(k_cqr_chol<FINAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (h->coll) {
+    // this rank's Grams -> all ranks -> summed in rank order inside the Cholesky kernel
+    const int64_t nn = (int64_t)h->cq_nbp * h->cq_nbp;
+    k_cqr_sum<<<h->G, 256, 0, h->s>>>(h->cq_nbp, h->cq_gpart, h->d_cq_first, h->d_cq_nsrc, h->cq_gloc);
+    if (!h->capturing) h->launches++;
+    CKL("k_cqr_sum");
+    allgather(h, h->cq_gloc, h->cq_gall, (size_t)(h->G * nn));
+    k_cqr_chol<FINAL><<<h->G, 256, smem, h->s>>>(h->cq_nbp, 0, h->d_nb, h->d_r0, h->d_wts, h->cq_gall, h->d_cq_bidx,
+                                                 h->d_cq_np, h->G, h->cq_r1, h->R, h->cq_rinv, h->d_cq_flags);
+  } else {
+    k_cqr_chol<FINAL><<<b1 - b0, 256, smem, h->s>>>(h->cq_nbp, b0, h->d_nb, h->d_r0, h->d_wts, h->cq_gpart,
+                                                    h->d_cq_first, h->d_cq_nsrc, 1, h->cq_r1, h->R, h->cq_rinv,
+                                                    h->d_cq_flags);
+  }
+  if (!h->capturing) h->launches++;
+  CKL("k_cqr_chol");
+}
+
+// CholeskyQR2 of blocks [b0, b1): Q and R of the handle (flags in d_cq_flags, read by cqr_ok)
+void run_cqr_blocks(glsgpu_sur* h, int b0, int b1) {
+  const int64_t i0 = h->cq_first[(size_t)b0], cnt = h->cq_first[(size_t)b1] - i0;
+  if (cnt <= 0) return;
+  const int64_t nn = (int64_t)h->cq_nbp * h->cq_nbp;
+  CK(cudaMemsetAsync(h->d_cq_flags + b0, 0, sizeof(int) * (size_t)(b1 - b0), h->s));
+  CqArgs a{};
+  a.items = h->d_cq_items + i0;
+  a.nitems = (int)cnt;
+  a.nb = h->d_nb;
+  a.src = h->X;
+  a.src_off = h->d_cq_xoff;
+  a.src_cs = h->ldx;
+  a.src_tiled = 0;
+  a.src_valid = h->M;
+  a.dst = h->Q;
+  a.dst_off = h->d_qoff;
+  a.dst_cs = h->qtiled ? h->cq_tr : h->ldm;
+  a.dst_tiled = h->qtiled ? 1 : 0;
+  a.dst_rows = h->qtiled ? round_up(h->ldm, QRR_NT) : h->ldm;
+  a.rinv = h->cq_rinv;
+  a.gpart = h->cq_gpart + i0 * nn;
+  launch_cqr_pass<0>(h, a);
+  launch_cqr_chol<false>(h, b0, b1);
+  launch_cqr_pass<1>(h, a);
+  launch_cqr_chol<true>(h, b0, b1);
+  CqArgs c = a;  // in place on Q
+  c.src = h->Q;
+  c.src_off = h->d_qoff;
+  c.src_cs = a.dst_cs;
+  c.src_tiled = a.dst_tiled;
+  c.src_valid = a.dst_rows;
+  launch_cqr_pass<2>(h, c);
+}
+
+// did every block take the CholeskyQR2 factor?  (synchronises the solver stream)
+bool cqr_ok(glsgpu_sur* h) {
+  std::vector<int> flags((size_t)h->G);
+  CK(cudaMemcpyAsync(flags.data(), h->d_cq_flags, sizeof(int) * (size_t)h->G, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  for (int f : flags)
+    if (f) return false;
+  return true;
+}
+
 // The TSQR of blocks [b0, b1) only, every level, when every item is a lane-per-column leaf (narrow blocks):
 // lets glsgpu_sur_create factor one group of blocks while the next group's columns are still in flight.
 bool qr_groupable(const glsgpu_sur* h) {
+  if (h->cq) return !h->coll;
   if (h->coll || !qr_lc()) return false;
   for (const auto& L : h->qr_levels)
     if (L.count) return false;
@@ -1159,6 +1328,10 @@ bool qr_groupable(const glsgpu_sur* h) {
 }
 
 void run_qr_blocks(glsgpu_sur* h, int b0, int b1, int lc_grid_f, int lc_grid_q) {
+  if (h->cq) {
+    run_cqr_blocks(h, b0, b1);
+    return;
+  }
   const int nl = (int)h->qr_levels.size();
   for (int l = 0; l < nl; ++l) {
     const auto& L = h->qr_levels[l];
@@ -1175,13 +1348,16 @@ void run_qr_blocks(glsgpu_sur* h, int b0, int b1, int lc_grid_f, int lc_grid_q) 
 }
 
 void rank_check(glsgpu_sur* h);
+void run_tsqr(glsgpu_sur* h);
 
 // group-pipelined setup from host X: group g's columns go up on a copy stream while the solver stream
 // factors group g - 1 (the whole TSQR tree of its blocks), so the QR hides under the host-to-device copy
 void upload_and_qr_pipelined(glsgpu_sur* h, const double* X_host, int groups) {
   int lc_grid_f = 148, lc_grid_q = 148;
-  qr_lc_grids(h, &lc_grid_f, &lc_grid_q);
-  CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));
+  if (!h->cq) {
+    qr_lc_grids(h, &lc_grid_f, &lc_grid_q);
+    CK(cudaMemsetAsync(h->Q, 0, sizeof(double) * (size_t)h->qsize, h->s));  // CholeskyQR2 writes every row itself
+  }
   cudaStream_t cs = nullptr;
   CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   std::vector<cudaEvent_t> ev((size_t)groups, nullptr);
@@ -1216,10 +1392,32 @@ void upload_and_qr_pipelined(glsgpu_sur* h, const double* X_host, int groups) {
   }
   for (auto e : ev) cudaEventDestroy(e);
   cudaStreamDestroy(cs);
+  h->cq_last = h->cq;
+  if (h->cq && !cqr_ok(h)) {
+    h->cq_fallbacks++;
+    h->cq_last = false;
+    run_tsqr(h);
+    return;
+  }
   rank_check(h);
 }
 
+// the factorisation of the handle's resident X: CholeskyQR2 where the handle takes it, Householder TSQR otherwise or
+// when a block fails CholeskyQR2's own test (ill-conditioned or rank-deficient blocks)
 void run_qr(glsgpu_sur* h) {
+  if (h->cq) {
+    run_cqr_blocks(h, 0, h->G);
+    h->cq_last = cqr_ok(h);
+    if (h->cq_last) {
+      rank_check(h);
+      return;
+    }
+    h->cq_fallbacks++;
+  }
+  run_tsqr(h);
+}
+
+void run_tsqr(glsgpu_sur* h) {
   CK(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
   CK(cudaFuncSetAttribute(k_qr_formq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
   CK(cudaFuncSetAttribute(k_qr_formq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM_BYTES));
@@ -1406,6 +1604,7 @@ void alloc_common(glsgpu_sur* h) {
     h->all_stream = h->use_stream;
   }
   build_qr_plan(h);
+  build_cqr_plan(h);
 }
 
 void destroy_impl(glsgpu_sur* h) {
@@ -1423,7 +1622,9 @@ void destroy_impl(glsgpu_sur* h) {
                   h->mvec, h->t,
                   h->vs, h->est, h->t2, h->xtw, h->zvec, h->beta_d, h->tpart, h->rpart, h->partA, h->partC,
                   h->scal, h->d_stop, h->st, h->rows_d, h->loc3, h->all3, h->t_loc, h->t_all, h->rloc, h->rall,
-                  h->rstack, h->gtau, h->d_stack_off, h->d_gitems, h->d_qoff};
+                  h->rstack, h->gtau, h->d_stack_off, h->d_gitems, h->d_qoff, h->d_cq_items, h->d_cq_first,
+                  h->d_cq_nsrc, h->d_cq_xoff, h->cq_gpart, h->cq_r1, h->cq_rinv, h->d_cq_flags, h->d_cq_bidx, h->d_cq_np,
+                  h->cq_gloc, h->cq_gall};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->cs) {
@@ -1576,7 +1777,7 @@ void ensure_solver(glsgpu_sur* h, int64_t rows_cap) {
     h->tpart2 = dalloc<double>((size_t)h->n * h->nch);
     h->tpart3 = dalloc<double>((size_t)h->n * h->nch);
     h->rpart = dalloc<double>((size_t)std::max<int64_t>((int64_t)h->G * h->nch, 4 * GRID_CAP));
-    h->partA = dalloc<double>(GRID_CAP * 3);
+    h->partA = dalloc<double>(std::max(GRID_CAP, EW_GRID) * 3);  // k_pass_a_ew (fused_c) writes EW_GRID rows
     h->partC = dalloc<double>(GRID_CAP * 3);
     h->scal = dalloc<double>(64);
     h->d_stop = dalloc<int>(1);
@@ -2260,6 +2461,13 @@ int glsgpu_get_factors(const glsgpu_sur* h, double* Q, double* R) {
     CK(cudaMemcpy(R, h->R, sizeof(double) * rtot, cudaMemcpyDeviceToHost));
   }
   API_END((int*)nullptr)
+}
+
+int glsgpu_factor_info(const glsgpu_sur* h, int* method, int* fallbacks) {
+  if (!h) return GLSGPU_ERR_INVALID;
+  if (method) *method = (h->cq && h->cq_last) ? 1 : 0;
+  if (fallbacks) *fallbacks = h->cq_fallbacks;
+  return GLSGPU_OK;
 }
 
 int glsgpu_launch_count(const glsgpu_sur* h, int64_t* count) {

@@ -48,8 +48,9 @@ def solve_both(p, mode="x", diag=1, cfg_kw=None, w1=None, z1=None):
 #       "growth" -- singular Omega: c falls to its roundoff floor (best iterate 50) and the run stops on the
 #                   growth test (c_next > 1e4 c_best, pcg.cpp:197-200) when that floor NOISE has grown
 #                   1e4-fold: the oracle's ratio is 8073 at iteration 66 and 12378 at 67
-#                   (oracle.orc_diag), so any rounding difference in Q moves the stop by one.  The
-#                   result is the best iterate: the same iterate must be selected and b agree to 1e-10;
+#                   (oracle.orc_diag), so any rounding difference in Q moves the stop, or lets the floor tests of
+#                   pcg.cpp:167-180 fire first.  Judged against the reference's own envelope; when the stop is the
+#                   same growth Breakdown the same best iterate must be selected and b agree to 1e-10;
 #       "tail"   -- slow tail (c3), see below.
 PARITY = [
     ("c0", lambda: synth.make_problem(0), "strict"),
@@ -72,11 +73,24 @@ def test_solve_parity(name, mk, kind, mode):
         assert s.termination.name == o.termination
         assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
     elif kind == "growth":
-        assert s.termination.name == o.termination == "Breakdown"
-        assert abs(s.iterations - o.iterations) <= 2, (s.iterations, o.iterations)
-        cg, co = np.asarray(g.trace.rows["c"])[1:], np.asarray(o.trace["c"])[1:]
-        assert int(np.argmin(cg)) == int(np.argmin(co))  # the same best iterate is returned
-        assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
+        # the reference's own last-bit envelope, measured on the spot: 1e-15 perturbations of X move its stop between
+        # the growth Breakdown at 67-68 (b unchanged to 2e-11) and a floor "Converged" at 68-71 (b 1e-6 away)
+        from test_gpu_fullshape import oracle_variants
+        _, variants = oracle_variants(p, nperturb=6)
+        assert o.termination == "Breakdown"
+        its = [o.iterations] + [v.iterations for v in variants]
+        assert s.termination.name in {o.termination} | {v.termination for v in variants}
+        assert min(its) - 2 <= s.iterations <= max(its) + 2, (s.iterations, its)
+        if s.termination.name == "Breakdown":
+            cg, co = np.asarray(g.trace.rows["c"])[1:], np.asarray(o.trace["c"])[1:]
+            assert int(np.argmin(cg)) == int(np.argmin(co))  # the same best iterate is returned
+            assert rel(s.b, o.b) <= B_TOL, rel(s.b, o.b)
+        else:
+            spread = max(rel(v.b, o.b) for v in variants)
+            assert rel(s.b, o.b) <= 5.0 * spread + B_TOL, (rel(s.b, o.b), spread)
+        # Omega is singular and the noise lies in its range: the exact GLS estimate is beta itself
+        err_ref = max([rel(o.b, p.beta)] + [rel(v.b, p.beta) for v in variants])
+        assert rel(s.b, p.beta) <= 2.0 * err_ref, (rel(s.b, p.beta), err_ref)
     else:
         # slow-tail config: c crosses tol^2 c1 so gradually that ANY change of summation order moves the
         # stopping iteration by a few -- the oracle itself with pairwise sums stops at 372 vs the
@@ -205,6 +219,64 @@ def test_tsqr_factors(shape):
         assert np.allclose(np.abs(np.diag(Ri)), np.abs(np.diag(Roi)), rtol=1e-11)
         off += k
         roff += k * k
+
+
+CQR_SHAPES = [(3, 1000, [7, 32, 1]), (2, 5000, [16, 20]), (3, 700, [40, 64, 33]), (2, 900, [100, 128]),
+              (2, 4099, [90, 5])]
+
+
+@pytest.mark.parametrize("shape", CQR_SHAPES, ids=[f"n{max(s[2])}_M{s[1]}" for s in CQR_SHAPES])
+def test_cholqr2_factors(shape, monkeypatch):
+    """CholeskyQR2 (the default setup, csrc/cqr.cuh) in its three width classes, ragged last tiles included: Q'Q = I,
+    Q R = w X, R upper with a positive diagonal equal to the reference Householder's |R_kk|, and the same basis as
+    the Householder TSQR (GLSGPU_QR=tsqr) up to column signs."""
+    G, M, nb = shape
+    p = synth.random_sur(G, M, nb, seed=78)
+    scale = np.linspace(0.5, 2.0, G)
+    op = api.sur_preconditioner(api.sur_from_problem(p), block_scale=scale)
+    assert op.factor_info() == ("cholqr2", 0)
+    Q, R = op.factors()
+    monkeypatch.setenv("GLSGPU_QR", "tsqr")
+    op_t = api.sur_preconditioner(api.sur_from_problem(p), block_scale=scale)
+    assert op_t.factor_info() == ("tsqr", 0)
+    Qt, Rt = op_t.factors()
+    off = roff = 0
+    for i, k in enumerate(nb):
+        Qi, Ri = Q[:, off:off + k], R[roff:roff + k * k].reshape(k, k, order="F")
+        Qti, Rti = Qt[:, off:off + k], Rt[roff:roff + k * k].reshape(k, k, order="F")
+        assert np.max(np.abs(Qi.T @ Qi - np.eye(k))) < 1e-13
+        assert np.allclose(np.tril(Ri, -1), 0.0) and np.all(np.diag(Ri) > 0)
+        Xi = p.X[:, off:off + k] / np.sqrt(scale[i])
+        assert np.linalg.norm(Qi @ Ri - Xi) <= 1e-13 * np.linalg.norm(Xi)
+        sg = np.sign(np.diag(Rti))
+        assert np.allclose(Ri, sg[:, None] * Rti, rtol=0, atol=1e-12 * np.abs(Rti).max())
+        assert np.max(np.abs(Qi - Qti * sg[None, :])) < 1e-12
+        off += k
+        roff += k * k
+    # the operator built on either factorisation projects alike
+    xi = np.random.default_rng(5).standard_normal(G * M)
+    assert rel(op.apply_pi(xi), op_t.apply_pi(xi)) < 1e-12
+
+
+def test_cholqr2_falls_back_on_ill_conditioned_blocks():
+    """cond(X_b) ~ 1e9 is beyond CholeskyQR2 (its first Gram squares it): the second Gram's |Q1'Q1 - I| test or a
+    non-positive pivot raises the flag and the handle is re-factored by the Householder TSQR; a truly rank-deficient
+    block still raises the reference's RankDeficient."""
+    p = synth.random_sur(3, 2000, [6, 12, 4], seed=79)
+    X = p.X.copy(order="F")
+    X[:, 7] = X[:, 6] + 1e-9 * X[:, 8]  # block 1: two columns 1e-9 apart
+    op = api.sur_preconditioner(api.SurModel(X, p.nb, p.Y, p.omega))
+    assert op.factor_info() == ("tsqr", 1)
+    Q, R = op.factors()
+    Qi, Ri = Q[:, 6:18], R[36:36 + 144].reshape(12, 12, order="F")
+    assert np.max(np.abs(Qi.T @ Qi - np.eye(12))) < 1e-13
+    assert np.linalg.norm(Qi @ Ri - X[:, 6:18]) <= 1e-13 * np.linalg.norm(X[:, 6:18])
+    # a healthy update of the same handle goes back to CholeskyQR2
+    op.update(p.X, p.Y)
+    assert op.factor_info() == ("cholqr2", 1)
+    X[:, 7] = X[:, 6]
+    with pytest.raises(api.RankDeficient, match="block 1"):
+        api.sur_preconditioner(api.SurModel(X, p.nb, p.Y, p.omega))
 
 
 def test_error_paths():
