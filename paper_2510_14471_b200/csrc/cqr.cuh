@@ -78,6 +78,75 @@ constexpr size_t cq_smem_bytes() {
 
 __device__ __forceinline__ void cq_bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(CQ_CW * 32) : "memory"); }
 
+
+// Product rows of one warp that owns 16 rows and every column of the tile (NBP = 32): column blocks in pairs, last
+// pair first.  A pair reads only the tile columns up to its own (Rinv is upper triangular), so with WRITE_BACK its
+// product goes back into the tile (the tile becomes Q1 in place, for this warp's Gram slice) before the pairs below
+// it are formed -- 8 live accumulators.  FULL: n = 4 K4 = 8 ANW and every row is stored (no guards, constant bounds).
+template <int LDT, int LDB, int ANW, bool WRITE_BACK, bool FULL>
+__device__ __forceinline__ void cq_apply_own(double* T, const double* Rv, int am0, int g, int q4, int K4, int n,
+                                             double* dp, int64_t cs, int64_t rlim) {
+  double* dl = dp + (int64_t)(2 * q4) * cs + am0 + g;  // this lane's (row g, column 2 q4) of column block 0
+#pragma unroll
+  for (int grp = ANW / 2 - 1; grp >= 0; --grp) {
+    const int nb0 = 2 * grp;
+    double acc[2][4];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[ni][e] = 0.0;
+    const int k1 = FULL ? 2 * nb0 + 2 : min(K4, 2 * nb0 + 2), k2 = FULL ? 2 * nb0 + 4 : min(K4, 2 * nb0 + 4);
+#pragma unroll
+    for (int kk = 0; kk < (FULL ? k1 : 0); ++kk) {
+      const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
+      const double a0 = tp[0], a1 = tp[8];
+      const double* bp = Rv + (4 * kk + q4) * LDB + 8 * nb0 + g;
+      dmma_16x8x4(acc[0], a0, a1, bp[0]);
+      dmma_16x8x4(acc[1], a0, a1, bp[8]);
+    }
+    if (!FULL)
+      for (int kk = 0; kk < k1; ++kk) {
+        const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
+        const double a0 = tp[0], a1 = tp[8];
+        const double* bp = Rv + (4 * kk + q4) * LDB + 8 * nb0 + g;
+        dmma_16x8x4(acc[0], a0, a1, bp[0]);
+        dmma_16x8x4(acc[1], a0, a1, bp[8]);
+      }
+#pragma unroll
+    for (int kk = (FULL ? k1 : 0); kk < (FULL ? k2 : 0); ++kk) {
+      const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
+      dmma_16x8x4(acc[1], tp[0], tp[8], Rv[(4 * kk + q4) * LDB + 8 * nb0 + 8 + g]);
+    }
+    if (!FULL)
+      for (int kk = k1; kk < k2; ++kk) {
+        const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
+        dmma_16x8x4(acc[1], tp[0], tp[8], Rv[(4 * kk + q4) * LDB + 8 * nb0 + 8 + g]);
+      }
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        double* q = dl + (int64_t)(8 * (nb0 + ni) + (e & 1)) * cs + 8 * (e >> 1);
+        if (FULL) {
+          stg_cs(q, acc[ni][e]);
+        } else {
+          const int c = 8 * (nb0 + ni) + 2 * q4 + (e & 1);
+          const int row = am0 + g + 8 * (e >> 1);
+          if (c < n && row < rlim) stg_cs(q, acc[ni][e]);
+        }
+      }
+    if (WRITE_BACK) {
+      __syncwarp();  // every lane's operand loads of this pair are done
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          T[(8 * (nb0 + ni) + 2 * q4 + (e & 1)) * LDT + am0 + g + 8 * (e >> 1)] = acc[ni][e];
+    }
+  }
+  if (WRITE_BACK) __syncwarp();
+}
+
 template <int NBP, int MODE>
 __global__ void __launch_bounds__(CQ_NT, 1) k_cqr_pass(CqArgs a) {
   constexpr int TR = CqCfg<NBP>::TR, STAGES = CqCfg<NBP>::STAGES;
@@ -91,7 +160,9 @@ __global__ void __launch_bounds__(CQ_NT, 1) k_cqr_pass(CqArgs a) {
   constexpr int GMW = NBP == 32 ? 2 : 1;
   constexpr int GNW = NBP == 32 ? 4 : 8;
   constexpr int KSTEPS = TR / KS / 4;  // k-steps of one warp per tile
+  constexpr bool OWN_ROWS = NBP == 32;  // apply rows of a warp == its Gram k-slice (16 rows), all columns
   static_assert(MBT * (NBP / 8 / ANW) == CQ_CW, "apply warp layout");
+  static_assert(!OWN_ROWS || (MBT == CQ_CW && KS == CQ_CW && TR / KS == 16), "own-rows layout");
   static_assert(KSTEPS >= 1, "gram warp layout");
 
   extern __shared__ __align__(128) double csm[];
@@ -103,6 +174,8 @@ __global__ void __launch_bounds__(CQ_NT, 1) k_cqr_pass(CqArgs a) {
   const int g = lane >> 2, q4 = lane & 3;
 
   for (int i = t; i < STAGES * TILE; i += CQ_NT) ring[i] = 0.0;  // pad columns / rows are read (times zero)
+  if (MODE <= 1 && KS > 1)
+    for (int i = t; i < NBP * LDG; i += CQ_NT) gbuf[i] = 0.0;    // (the never-accumulated upper block stays 0)
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -190,46 +263,57 @@ __global__ void __launch_bounds__(CQ_NT, 1) k_cqr_pass(CqArgs a) {
       mbar_wait(&full[rp.slot], rp.phase);
       if (MODE >= 1) {
         // product tile = T (TR x n) Rinv (n x n upper triangular): only k-steps 4 kk <= 8 nbi + 7 contribute
-        double acc[ANW][4];
-#pragma unroll
-        for (int ni = 0; ni < ANW; ++ni)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[ni][e] = 0.0;
-        const int kend = min(K4, 2 * (anb0 + ANW));
-        for (int kk = 0; kk < kend; ++kk) {
-          const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
-          const double a0 = tp[0], a1 = tp[8];
-          const double* bp = Rv + (4 * kk + q4) * LDB + 8 * anb0 + g;
-#pragma unroll
-          for (int ni = 0; ni < ANW; ++ni)
-            if (kk < 2 * (anb0 + ni) + 2) dmma_16x8x4(acc[ni], a0, a1, bp[8 * ni]);
-        }
         double* dp = db + (a.dst_tiled ? (r / TR) * (int64_t)TR * n : r);
         const int64_t rlim = a.dst_rows - r;  // rows of this tile that exist in the destination
+        if (OWN_ROWS) {
+          // NBP = 32: the warp owns 16 rows and all columns (cq_apply_own); full-width blocks on a tile that lies
+          // inside the destination take the unguarded instance with constant loop bounds
+          if (n == NBP && rlim >= TR) cq_apply_own<LDT, LDB, ANW, MODE == 1, true>(T, Rv, am0, g, q4, K4, n, dp, a.dst_cs, rlim);
+          else cq_apply_own<LDT, LDB, ANW, MODE == 1, false>(T, Rv, am0, g, q4, K4, n, dp, a.dst_cs, rlim);
+        } else {
+          double acc[ANW][4];
 #pragma unroll
-        for (int ni = 0; ni < ANW; ++ni)
+          for (int ni = 0; ni < ANW; ++ni)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = 8 * (anb0 + ni) + 2 * q4 + (e & 1);
-            const int row = am0 + g + 8 * (e >> 1);
-            if (c < n && row < rlim) stg_cs(dp + (int64_t)c * a.dst_cs + row, acc[ni][e]);
+            for (int e = 0; e < 4; ++e) acc[ni][e] = 0.0;
+          // (segment seg covers the k-steps that first reach column block anb0 + seg: blocks below it are done)
+#pragma unroll
+          for (int seg = 0; seg < ANW; ++seg) {
+            const int kbeg = seg == 0 ? 0 : 2 * (anb0 + seg), kend = min(K4, 2 * (anb0 + seg) + 2);
+            for (int kk = kbeg; kk < kend; ++kk) {
+              const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
+              const double a0 = tp[0], a1 = tp[8];
+              const double* bp = Rv + (4 * kk + q4) * LDB + 8 * anb0 + g;
+#pragma unroll
+              for (int ni = seg; ni < ANW; ++ni) dmma_16x8x4(acc[ni], a0, a1, bp[8 * ni]);
+            }
           }
-        if (MODE == 1) {
-          cq_bar_compute();  // every warp has read its A operands: the tile becomes Q1
 #pragma unroll
           for (int ni = 0; ni < ANW; ++ni)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int c = 8 * (anb0 + ni) + 2 * q4 + (e & 1);
               const int row = am0 + g + 8 * (e >> 1);
-              T[c * LDT + row] = acc[ni][e];
+              if (c < n && row < rlim) stg_cs(dp + (int64_t)c * a.dst_cs + row, acc[ni][e]);
             }
-          cq_bar_compute();
+          if (MODE == 1) {
+            // the tile becomes Q1 in place; the warps share rows: barriers around the overwrite
+            cq_bar_compute();  // every warp has read its A operands
+#pragma unroll
+            for (int ni = 0; ni < ANW; ++ni)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int c = 8 * (anb0 + ni) + 2 * q4 + (e & 1);
+                const int row = am0 + g + 8 * (e >> 1);
+                T[c * LDT + row] = acc[ni][e];
+              }
+            cq_bar_compute();
+          }
         }
       }
       if (MODE <= 1) {
         // Gram of the tile: rows [ks TR / KS, +TR / KS) as the k range of this warp
-#pragma unroll 2
+#pragma unroll(MODE == 0 ? 2 : 1)
         for (int k = 0; k < KSTEPS; ++k) {
           const int rr = ks * (TR / KS) + 4 * k + q4;
           double a0[GMW], a1[GMW];
@@ -278,6 +362,7 @@ __global__ void __launch_bounds__(CQ_NT, 1) k_cqr_pass(CqArgs a) {
               for (int ni = 0; ni < GNW; ++ni)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
+                  if (NBP == 32 && mi == 0 && ni >= 2) continue;  // never accumulated, never read
                   double* p = gbuf + (gm0 + 16 * mi + g + 8 * (e >> 1)) * LDG + gn0 + 8 * ni + 2 * q4 + (e & 1);
                   *p = s == 0 ? gacc[mi][ni][e] : *p + gacc[mi][ni][e];
                 }
