@@ -871,6 +871,9 @@ constexpr int KM_UC = KM_OK * KM_XS;                // U chunk doubles
 constexpr int KM_UR = 16;                           // U chunk slots
 constexpr int KM_ES = 4;                            // element chunk stages
 constexpr int KM_EC = 5 * KM_OK * KM_BM;            // element chunk doubles: 5 vectors x 8 columns x 64 rows
+constexpr int KM_REG_SIDE = 72;                     // setmaxnreg: loader + element warpgroup
+constexpr int KM_REG_MATH = 216;                   // the two math warpgroups: 168 + (168 - 72) / 2
+static_assert(KM_EW == 3 && KW_MATH == 8, "setmaxnreg works on warpgroups of four warps");
 constexpr size_t km_smem_bytes() {
   return (size_t)(KM_UR * KM_UC + KM_OS * KM_OK * KM_OLD + KM_ES * KM_EC) * sizeof(double);
 }
@@ -920,7 +923,12 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     mbar_fence_init();
   }
   __syncthreads();
+  // register reallocation between the warpgroups (launch: 168 per thread): the loader / element warpgroup gives up
+  // registers, the two math warpgroups take them -- the 128 accumulator registers no longer spill and the epilogue
+  // can hold a row block's u values
   double p_a = 0.0, p_b = 0.0;  // math warps: u . Sigma u; element warps: u . u
+  if (warp >= KW_MATH) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(KM_REG_SIDE));
   if (warp == KW_MATH) {
     // ---------------- Omega loader: slab s = rows [8 s, 8 s + 8) of Omega', one bulk copy per row
     if (lane == 0) {
@@ -981,6 +989,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
     double* __restrict__ wn = wbuf.w[st->nxt];
     double* __restrict__ swn = wbuf.sw[st->nxt];
     const bool swd = st->sw_direct != 0;  // no sw recurrence: w alone is updated
+    const bool fast = upd && wupd && swd;
     RingPos cp, up;
     constexpr int NE = (KM_OK * KM_BM + 32 * KM_EW - 1) / (32 * KM_EW);  // elements per thread per chunk
     for (int64_t jl = 0; jl < ntl; ++jl) {
@@ -990,6 +999,37 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
         if (jl * nchunk + k >= KM_UR) mbar_wait(&uc_empty[up.slot], up.phase ^ 1u);
         const double* E = elb + cp.slot * KM_EC;
         double* U = ucb + up.slot * KM_UC;
+        if (fast && k0 + KM_BM <= ldm) {
+          // the iteration's common case (u = pr + mu u, w -= lambda u, no sw recurrence, tile inside the matrix) as
+          // straight-line code: every operand load first, then the fused multiply-adds back to back, then the stores
+          // (u . u is summed by the math warps' epilogue from the u values it reads anyway)
+          double uo[NE], pv[NE], wv[NE];
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            const int i = etid + 32 * KM_EW * e;
+            if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+            uo[e] = E[i];
+            pv[e] = E[KM_OK * KM_BM + i];
+            wv[e] = E[2 * KM_OK * KM_BM + i];
+          }
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            const int i = etid + 32 * KM_EW * e;
+            if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+            wv[e] = __fma_rn(-lp, uo[e], wv[e]);
+            pv[e] = __fma_rn(mu, uo[e], pv[e]);
+          }
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            const int i = etid + 32 * KM_EW * e;
+            if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+            const int cc = i / KM_BM, rr = i % KM_BM;
+            const int64_t off = (int64_t)(k * KM_OK + cc) * ldm + k0 + rr;
+            stg_cs(wn + off, wv[e]);
+            u_io[off] = pv[e];  // read back by the math warps' epilogue (L2)
+            U[cc * KM_XS + rr] = pv[e];
+          }
+        } else {
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
           const int i = etid + 32 * KM_EW * e;
@@ -1012,6 +1052,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
           U[cc * KM_XS + rr] = v;
           p_b = __fma_rn(v, v, p_b);
         }
+        }
         // this warp's reads of the element slot are done; its U chunk writes are published to the math warps
         fence_proxy_async_smem();
         __syncwarp();
@@ -1023,10 +1064,14 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
         up.next(KM_UR);
       }
     }
+  }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(KM_REG_MATH));
     // ---------------- math warps: DMMA m16n8k4, warp owns columns [32 warp, 32 warp + 32) of every tile
     const int g = lane >> 2, t = lane & 3;
     const int n0 = 32 * warp;
+    // (the same condition as the element warps' `fast`)
+    const bool uu_math = !APPLY && st->mu_pending != 0 && st->upd_pending != 0 && st->sw_direct != 0;
     RingPos rp, up;
     for (int64_t jl = 0; jl < ntl; ++jl) {
       const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
@@ -1065,22 +1110,42 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
         up.next(KM_UR);
       }
       // epilogue: acc[mi][ni] = rows 16 mi + (g, g + 8) x columns n0 + 8 ni + 2 t (+1); rows >= msig carry
-      // zero variance; u . Sigma u with the tile's u from global memory (L2)
+      // zero variance; u . Sigma u with the tile's u from global memory (L2).  The registers setmaxnreg moved to
+      // the math warps hold one m16 row block's 16 u values at a time: one L2 round trip per row block instead of
+      // one per small group of loads behind the stores.
+      const bool tile_in = k0 + KM_BM <= ldm && n0 + 32 <= G;
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 4; ++mi) {
+        double uv[4][4];
+        if (!APPLY) {
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int c = n0 + 8 * ni + 2 * t + (q & 1);
+              const int64_t grow = k0 + 16 * mi + g + 8 * (q >> 1);
+              uv[ni][q] = (tile_in || (c < G && grow < ldm)) ? u_io[(int64_t)c * ldm + grow] : 0.0;
+            }
+        }
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int c = n0 + 8 * ni + 2 * t + (q & 1);
             const int64_t grow = k0 + 16 * mi + g + 8 * (q >> 1);
-            if (c < G && grow < ldm) {
+            if (tile_in || (c < G && grow < ldm)) {
               const double o = grow < msig ? acc[mi][ni][q] : 0.0;
-              const int64_t off = (int64_t)c * ldm + grow;
-              stg_cs(out + off, o);
-              if (!APPLY) p_a = __fma_rn(u_io[off], o, p_a);
+              stg_cs(out + (int64_t)c * ldm + grow, o);
+              if (!APPLY) p_a = __fma_rn(uv[ni][q], o, p_a);
             }
           }
+        if (!APPLY && uu_math && k0 + KM_BM <= ldm) {  // u . u of the tiles the element warps' fast path handled
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) p_b = __fma_rn(uv[ni][q], uv[ni][q], p_b);
+        }
+      }
     }
   }
   // (d, u.u) partials of this CTA, fixed order (pcg.cpp:144-145)
