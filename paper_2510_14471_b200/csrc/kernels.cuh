@@ -871,8 +871,8 @@ constexpr int KM_UC = KM_OK * KM_XS;                // U chunk doubles
 constexpr int KM_UR = 16;                           // U chunk slots
 constexpr int KM_ES = 4;                            // element chunk stages
 constexpr int KM_EC = 5 * KM_OK * KM_BM;            // element chunk doubles: 5 vectors x 8 columns x 64 rows
-constexpr int KM_REG_SIDE = 72;                     // setmaxnreg: loader + element warpgroup
-constexpr int KM_REG_MATH = 216;                   // the two math warpgroups: 168 + (168 - 72) / 2
+constexpr int KM_REG_SIDE = 88;                     // setmaxnreg: loader + element warpgroup
+constexpr int KM_REG_MATH = 208;                   // the two math warpgroups: 168 + (168 - 72) / 2
 static_assert(KM_EW == 3 && KW_MATH == 8, "setmaxnreg works on warpgroups of four warps");
 constexpr size_t km_smem_bytes() {
   return (size_t)(KM_UR * KM_UC + KM_OS * KM_OK * KM_OLD + KM_ES * KM_EC) * sizeof(double);
@@ -1053,8 +1053,9 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
           p_b = __fma_rn(v, v, p_b);
         }
         }
-        // this warp's reads of the element slot are done; its U chunk writes are published to the math warps
-        fence_proxy_async_smem();
+        // this warp's reads of the element slot are done; its U chunk writes are published to the math warps (both by
+        // the mbarrier arrivals' release; no proxy fence: it compiles to a MEMBAR that also waits for this chunk's
+        // global stores, and a generic read followed by the next bulk copy into the slot is ordered by the barrier)
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&el_empty[cp.slot]);
