@@ -401,6 +401,16 @@ bool kron_mma_ok(const glsgpu_sur* h) {
   return !off && kron_gemm_ok(h) && h->kron_fma && h->vmap64_ok;
 }
 
+// GLSGPU_KRON_V1=1: the first tensor-core pass A (element warps feed the math warps through a U ring)
+bool kron_mma_v1() {
+  static const bool v = std::getenv("GLSGPU_KRON_V1") != nullptr;
+  return v;
+}
+// ring stages of k_kron_mma2 for nv vectors per stage: what fits beside its static shared memory
+int km2_stages(int nv) {
+  return (int)std::min<size_t>(KM2_MAXS, (size_t)(227 * 1024 - 1024) / km2_stage_bytes(nv));
+}
+
 constexpr int EW_GRID = 148 * 8;  // k_pass_a_ew: grid-stride element-wise pass
 
 int kron_grid(const glsgpu_sur* h) {
@@ -425,6 +435,15 @@ void launch_pass_a(glsgpu_sur* h) {
     return;
   }
   const int grid = kron_grid(h);
+  if (kron_mma_ok(h) && !kron_mma_v1()) {
+    const int nv = h->sw_direct ? 3 : 5, ns = km2_stages(nv);
+    k_kron_mma2<false><<<grid, KM_NT, ns * km2_stage_bytes(nv), h->s>>>(
+        h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, h->su, h->partA, h->st, wbuf_of(h),
+        h->msig, -1, ns, nv);
+    if (!h->capturing) h->launches++;
+    CKL("k_kron_mma2");
+    return;
+  }
   if (kron_mma_ok(h)) {
     k_kron_mma<false><<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM,
                                                              h->omegaT, h->u, h->su, h->partA, h->st, wbuf_of(h),
@@ -449,6 +468,15 @@ bool kron_mma_apply(glsgpu_sur* h, int blk, double* out) {
   // fused multiply-adds: only where the solve runs kron_fma (exact mode keeps the reference's mul / add sums)
   if (!(kron_gemm_ok(h) && h->vmap64_ok && h->kron_fma) || std::getenv("GLSGPU_NO_DMMA")) return false;
   const int grid = (int)std::min<int64_t>((h->ldm + KM_BM - 1) / KM_BM, 148);
+  if (!kron_mma_v1()) {
+    const int nv = 1, ns = km2_stages(nv);
+    k_kron_mma2<true><<<grid, KM_NT, ns * km2_stage_bytes(nv), h->s>>>(
+        h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, out, nullptr, h->st, wbuf_of(h), h->msig,
+        blk, ns, nv);
+    if (!h->capturing) h->launches++;
+    CKL("k_kron_mma2 apply");
+    return true;
+  }
   k_kron_mma<true><<<grid, KM_NT, km_smem_bytes(), h->s>>>(h->vmap64, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM,
                                                           h->omegaT, h->u, out, nullptr, h->st, wbuf_of(h), h->msig, blk);
   if (!h->capturing) h->launches++;
@@ -621,6 +649,8 @@ void stream_attrs(glsgpu_sur* h) {
   set((const void*)k_kron_ws<true>, 0, 0);
   set((const void*)k_kron_mma<false>, 0, 0);
   set((const void*)k_kron_mma<true>, 0, 0);
+  set((const void*)k_kron_mma2<false>, 0, 0);
+  set((const void*)k_kron_mma2<true>, 0, 0);
   set((const void*)k_pass_c_mma, 0, 0);
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);

@@ -1173,6 +1173,290 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma(const __grid_constant__ C
 }
 
 // ------------------------------------------------------------------------------------------
+// Pass A on the FP64 tensor cores, second form (round 2; the default): the math warps build their own A operands.
+// k_kron_mma's element warps produced the U tile (u = pr + mu u) for the math warps through a shared-memory ring, so
+// the DMMA stream waited on three warps whose every DFMA queues behind the math warps' DMMA bursts (ncu: the math
+// warps 23% on the ring's full barriers, the element warps 27% on their loads and 17% on the first DFMA of a chunk).
+// Here one ring of KM2 stages carries, per 8-column chunk, the Omega slab and the raw chunk columns of u_old, pr, w
+// (and sw, su for the recurrence mode), every column one 512-byte bulk copy into a padded (conflict-free) layout:
+//   * the 8 math warps read u_old and pr as fragments and form a = fma(mu, u_old, pr) inline (bitwise the element
+//     warps' value; 16 DFMAs per 32 DMMAs per warp, issued by the warps that own the FP64 pipe);
+//   * the 3 side warps only write: u (read back by the epilogue's u . Sigma u, after a per-tile barrier), the
+//     deferred w (and sw) update, and u . u where the epilogue does not take it; they are off the DMMA stream's
+//     critical path -- a stage is recycled when the math warps AND the side warps have released it;
+//   * the loader warp: lanes 0-7 the Omega rows, lanes 8.. one chunk column each.
+constexpr int KM2_MAXS = 12;                        // ring stages (barrier arrays)
+constexpr int KM2_OM = KM_OK * KM_OLD;              // Omega slab doubles per stage
+constexpr int KM2_VC = KM_OK * KM_XS;               // one vector's chunk, padded: [8 columns][68]
+constexpr size_t km2_stage_bytes(int nv) { return (size_t)(KM2_OM + nv * KM2_VC) * sizeof(double); }
+
+template <bool APPLY>
+__global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict__ slab, int G, int64_t ldm,
+                                                        int64_t ntiles, const double* __restrict__ omegaT,
+                                                        double* __restrict__ u_io, double* __restrict__ out,
+                                                        double* partials, const SolveState* st, WBuf wbuf,
+                                                        int64_t msig, int plain, int nstage, int nv) {
+  // APPLY = false: pass A (plain ignored).  APPLY: out = Sigma x, no updates, no partials, for x = column block
+  // `plain` of the vector slab, or (plain == -2) x = w_cur into sw_cur on a diagnostics row (sw_mode 1).
+  if (!APPLY && !st->active) return;
+  if (APPLY && plain == -2) {
+    if (!st->diag_now) return;
+    out = wbuf.sw[st->cur];
+  }
+  extern __shared__ __align__(128) double ksm[];
+  __shared__ __align__(8) uint64_t full[KM2_MAXS], empty[KM2_MAXS], tile_done;
+  __shared__ double red[KM_NT / 32][2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nchunk = G / KM_OK;   // chunks (= Omega slabs) per tile
+  const int64_t ntl = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA
+  const int sstride = KM2_OM + nv * KM2_VC;
+  const bool upd = !APPLY && st->mu_pending != 0, wupd = !APPLY && st->upd_pending != 0;
+  const bool swd = st->sw_direct != 0;  // no sw recurrence: w alone is updated
+  const bool fast = upd && wupd && swd;  // the iteration's common case: u . u moves to the math epilogue
+  for (int i = tid; i < nstage * sstride; i += KM_NT) ksm[i] = 0.0;  // rows past a short last tile stay 0
+  if (tid == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], KW_MATH + KM_EW);
+    }
+    mbar_init(&tile_done, KM_EW);
+    mbar_fence_init();
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  double p_a = 0.0, p_b = 0.0;  // u . Sigma u (math warps); u . u (math warps' epilogue, or the side warps)
+  if (warp >= KW_MATH) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(KM_REG_SIDE));
+    if (warp == KW_MATH) {
+      // ---------------- loader: per chunk, 8 Omega rows (lanes 0-7) and the chunk columns (lane 8 + 8 v + column)
+      const int cur = st->cur;
+      const int64_t mv = ldm * G;
+      // stage vector v: 0 = u (or the plain vector), 1 = pr, 2 = w_cur, 3 = sw_cur, 4 = su; lanes 8..31 take
+      // (vector, column) pairs idx = lane - 8 + 24 j
+      auto v_on = [&](int v) { return v == 0 || (v == 1 && upd) || (v == 2 && wupd) || (v >= 3 && wupd && !swd); };
+      auto v_src = [&](int v) {
+        const int blk = v == 0 ? (!APPLY ? MV_U : (plain == -2 ? MV_W + cur : plain))
+                        : v == 1 ? MV_PR : v == 2 ? MV_W + cur : v == 3 ? MV_SW + cur : MV_SU;
+        return slab + (int64_t)blk * mv;
+      };
+      const int nvec_on = 1 + (upd ? 1 : 0) + (wupd ? (swd ? 1 : 3) : 0);
+      const uint32_t om_bytes = (uint32_t)(G * sizeof(double)) * KM_OK;
+      RingPos w;
+      int64_t tile = blockIdx.x;
+      int c0 = 0;
+      for (int64_t q = 0; q < ntl * nchunk; ++q) {
+        if (q >= nstage) mbar_wait(&empty[w.slot], w.phase ^ 1u);
+        double* S = ksm + w.slot * sstride;
+        const int64_t k0 = tile * KM_BM;
+        const uint32_t col_bytes = (uint32_t)(min((int64_t)KM_BM, ldm - k0) * sizeof(double));
+        if (lane == 0) mbar_expect_tx(&full[w.slot], om_bytes + (uint32_t)nvec_on * KM_OK * col_bytes);
+        __syncwarp();
+        if (lane < 8)
+          tma_load_1d(S + lane * KM_OLD, omegaT + (int64_t)(c0 + lane) * G, (uint32_t)(G * sizeof(double)), &full[w.slot]);
+        else
+          for (int idx = lane - 8; idx < nv * KM_OK; idx += 24) {
+            const int v = idx >> 3, lc = idx & 7;
+            if (v_on(v))
+              tma_load_1d(S + KM2_OM + v * KM2_VC + lc * KM_XS, v_src(v) + (int64_t)(c0 + lc) * ldm + k0, col_bytes,
+                          &full[w.slot]);
+          }
+        w.next(nstage);
+        c0 += KM_OK;
+        if (c0 == G) {
+          c0 = 0;
+          tile += gridDim.x;
+        }
+      }
+    } else {
+      // ---------------- side warps: element i = (column i / 64, row i % 64) of a chunk, i = etid + 32 KM_EW e
+      const int ew = warp - KW_MATH - 1;
+      const int etid = ew * 32 + lane;
+      const double mu = st->mu, lp = st->lam_prev;
+      double* __restrict__ wn = wbuf.w[st->nxt];
+      double* __restrict__ swn = wbuf.sw[st->nxt];
+      RingPos cp;
+      constexpr int NE = (KM_OK * KM_BM + 32 * KM_EW - 1) / (32 * KM_EW);  // elements per thread per chunk
+      for (int64_t jl = 0; jl < ntl; ++jl) {
+        const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
+        const bool tile_in = k0 + KM_BM <= ldm;
+        for (int k = 0; k < nchunk; ++k) {
+          mbar_wait(&full[cp.slot], cp.phase);
+          const double* E = ksm + cp.slot * sstride + KM2_OM;
+          if (fast && tile_in) {
+            double uo[NE], pv[NE], wv[NE];
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+              const int i = etid + 32 * KM_EW * e;
+              if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+              const int o = (i / KM_BM) * KM_XS + i % KM_BM;
+              uo[e] = E[o];
+              pv[e] = E[KM2_VC + o];
+              wv[e] = E[2 * KM2_VC + o];
+            }
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+              const int i = etid + 32 * KM_EW * e;
+              if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+              wv[e] = __fma_rn(-lp, uo[e], wv[e]);
+              pv[e] = __fma_rn(mu, uo[e], pv[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+              const int i = etid + 32 * KM_EW * e;
+              if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+              const int64_t off = (int64_t)(k * KM_OK + i / KM_BM) * ldm + k0 + i % KM_BM;
+              stg_cs(wn + off, wv[e]);
+              u_io[off] = pv[e];  // read back by the math warps' epilogue (L2)
+            }
+          } else if (!APPLY) {
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+              const int i = etid + 32 * KM_EW * e;
+              if ((KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+              const int cc = i / KM_BM, rr = i % KM_BM;
+              const int64_t grow = k0 + rr;
+              const int64_t off = (int64_t)(k * KM_OK + cc) * ldm + grow;
+              const bool in = grow < ldm;
+              const int o = cc * KM_XS + rr;
+              const double uo = in ? E[o] : 0.0;
+              if (wupd && in) {
+                stg_cs(wn + off, __fma_rn(-lp, uo, E[2 * KM2_VC + o]));
+                if (!swd) stg_cs(swn + off, __fma_rn(-lp, E[4 * KM2_VC + o], E[3 * KM2_VC + o]));
+              }
+              double v = uo;
+              if (upd) {
+                v = in ? __fma_rn(mu, uo, E[KM2_VC + o]) : 0.0;
+                if (in) u_io[off] = v;
+              }
+              p_b = __fma_rn(v, v, p_b);  // (u . u of the fast-path tiles: the math warps' epilogue)
+            }
+          }
+          // this warp's reads of the stage are done (the arrival's release orders them before the next bulk copy)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[cp.slot]);
+          cp.next(nstage);
+        }
+        // the tile's u is in global memory: the math warps' epilogue may read it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tile_done);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(KM_REG_MATH));
+    // ---------------- math warps: DMMA m16n8k4, warp owns columns [32 warp, 32 warp + 32) of every tile
+    const int g = lane >> 2, t = lane & 3;
+    const int n0 = 32 * warp;
+    const double mu = st->mu;
+    RingPos rp;
+    for (int64_t jl = 0; jl < ntl; ++jl) {
+      const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
+      double acc[4][4][4];  // [m16 tile][n8 tile][fragment]
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
+      for (int s = 0; s < nchunk; ++s) {
+        mbar_wait(&full[rp.slot], rp.phase);
+        const double* S = ksm + rp.slot * sstride;
+        const double* om = S + n0 + g;
+        const double* U = S + KM2_OM + t * KM_XS + g;
+#pragma unroll
+        for (int kk = 0; kk < KM_OK / 4; ++kk) {
+          const double* ob = om + (kk * 4 + t) * KM_OLD;
+          const double b0 = ob[0], b1 = ob[8], b2 = ob[16], b3 = ob[24];
+          const double* ua = U + kk * 4 * KM_XS;
+          double a0[4], a1[4];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            a0[mi] = ua[16 * mi];
+            a1[mi] = ua[16 * mi + 8];
+          }
+          if (upd) {  // u = pr + mu u_old (pcg.cpp:210), the value the side warps write
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+              a0[mi] = __fma_rn(mu, a0[mi], ua[KM2_VC + 16 * mi]);
+              a1[mi] = __fma_rn(mu, a1[mi], ua[KM2_VC + 16 * mi + 8]);
+            }
+          }
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            dmma_16x8x4(acc[mi][0], a0[mi], a1[mi], b0);
+            dmma_16x8x4(acc[mi][1], a0[mi], a1[mi], b1);
+            dmma_16x8x4(acc[mi][2], a0[mi], a1[mi], b2);
+            dmma_16x8x4(acc[mi][3], a0[mi], a1[mi], b3);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rp.slot]);
+        rp.next(nstage);
+      }
+      // epilogue: acc[mi][ni] = rows 16 mi + (g, g + 8) x columns n0 + 8 ni + 2 t (+1); rows >= msig carry
+      // zero variance; u . Sigma u with the tile's u from global memory (L2), one m16 row block's 16 values at a
+      // time (one L2 round trip per row block)
+      // the side warps have written this tile's u.  (They cannot be two tiles ahead: a tile has more chunks than the
+      // ring has stages -- G > 128 -- and a stage is recycled only after every math warp released it.)
+      if (!APPLY) mbar_wait(&tile_done, (uint32_t)(jl & 1));
+      const bool tile_in = k0 + KM_BM <= ldm && n0 + 32 <= G;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        double uv[4][4];
+        if (!APPLY) {
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int c = n0 + 8 * ni + 2 * t + (q & 1);
+              const int64_t grow = k0 + 16 * mi + g + 8 * (q >> 1);
+              uv[ni][q] = (tile_in || (c < G && grow < ldm)) ? u_io[(int64_t)c * ldm + grow] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = n0 + 8 * ni + 2 * t + (q & 1);
+            const int64_t grow = k0 + 16 * mi + g + 8 * (q >> 1);
+            if (tile_in || (c < G && grow < ldm)) {
+              const double o = grow < msig ? acc[mi][ni][q] : 0.0;
+              stg_cs(out + (int64_t)c * ldm + grow, o);
+              if (!APPLY) p_a = __fma_rn(uv[ni][q], o, p_a);
+            }
+          }
+        if (!APPLY && fast && k0 + KM_BM <= ldm) {  // u . u of the tiles the side warps' fast path handled
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) p_b = __fma_rn(uv[ni][q], uv[ni][q], p_b);
+        }
+      }
+    }
+  }
+  // (d, u.u) partials of this CTA, fixed order (pcg.cpp:144-145)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    p_a += __shfl_xor_sync(FULL, p_a, o);
+    p_b += __shfl_xor_sync(FULL, p_b, o);
+  }
+  if (lane == 0) {
+    red[warp][0] = p_a;
+    red[warp][1] = p_b;
+  }
+  __syncthreads();
+  if (tid == 0 && !APPLY) {
+    double a = 0.0, bb = 0.0;
+    for (int w = 0; w < KM_NT / 32; ++w) {
+      a += red[w][0];
+      bb += red[w][1];
+    }
+    partials[blockIdx.x * 3 + 0] = a;
+    partials[blockIdx.x * 3 + 1] = bb;
+    partials[blockIdx.x * 3 + 2] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Fused pass C (fused_c knob, OFF by default; the k_kron_mma shapes with tile-contiguous Q): pr = Pi r (structured.cpp:307-317)
 // with c = r.pr, r.r, pr.pr, AND Sigma pr = pr Omega on the FP64 tensor cores, in one sweep over 64-row tiles of
 // all G blocks -- the Kronecker product hides under the Q stream.  Pass A then only needs the element-wise
