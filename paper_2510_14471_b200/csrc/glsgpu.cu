@@ -406,6 +406,11 @@ bool kron_mma_v1() {
   static const bool v = std::getenv("GLSGPU_KRON_V1") != nullptr;
   return v;
 }
+// GLSGPU_KRON_W16=1: sixteen math warps of 16 columns (four per scheduler) instead of eight of 32
+bool kron_mma_w16() {
+  static const bool v = std::getenv("GLSGPU_KRON_W16") != nullptr;
+  return v;
+}
 // ring stages of k_kron_mma2 for nv vectors per stage: what fits beside its static shared memory
 int km2_stages(int nv) {
   return (int)std::min<size_t>(KM2_MAXS, (size_t)(227 * 1024 - 1024) / km2_stage_bytes(nv));
@@ -437,9 +442,14 @@ void launch_pass_a(glsgpu_sur* h) {
   const int grid = kron_grid(h);
   if (kron_mma_ok(h) && !kron_mma_v1()) {
     const int nv = h->sw_direct ? 3 : 5, ns = km2_stages(nv);
-    k_kron_mma2<false><<<grid, KM_NT, ns * km2_stage_bytes(nv), h->s>>>(
-        h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, h->su, h->partA, h->st, wbuf_of(h),
-        h->msig, -1, ns, nv);
+    if (kron_mma_w16())
+      k_kron_mma2<false, 16><<<grid, (16 + 1 + KM_EW) * 32, ns * km2_stage_bytes(nv), h->s>>>(
+          h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, h->su, h->partA, h->st, wbuf_of(h),
+          h->msig, -1, ns, nv);
+    else
+      k_kron_mma2<false, 8><<<grid, KM_NT, ns * km2_stage_bytes(nv), h->s>>>(
+          h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, h->su, h->partA, h->st, wbuf_of(h),
+          h->msig, -1, ns, nv);
     if (!h->capturing) h->launches++;
     CKL("k_kron_mma2");
     return;
@@ -470,9 +480,14 @@ bool kron_mma_apply(glsgpu_sur* h, int blk, double* out) {
   const int grid = (int)std::min<int64_t>((h->ldm + KM_BM - 1) / KM_BM, 148);
   if (!kron_mma_v1()) {
     const int nv = 1, ns = km2_stages(nv);
-    k_kron_mma2<true><<<grid, KM_NT, ns * km2_stage_bytes(nv), h->s>>>(
-        h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, out, nullptr, h->st, wbuf_of(h), h->msig,
-        blk, ns, nv);
+    if (kron_mma_w16())
+      k_kron_mma2<true, 16><<<grid, (16 + 1 + KM_EW) * 32, ns * km2_stage_bytes(nv), h->s>>>(
+          h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, out, nullptr, h->st, wbuf_of(h),
+          h->msig, blk, ns, nv);
+    else
+      k_kron_mma2<true, 8><<<grid, KM_NT, ns * km2_stage_bytes(nv), h->s>>>(
+          h->mvec, h->G, h->ldm, (h->ldm + KM_BM - 1) / KM_BM, h->omegaT, h->u, out, nullptr, h->st, wbuf_of(h),
+          h->msig, blk, ns, nv);
     if (!h->capturing) h->launches++;
     CKL("k_kron_mma2 apply");
     return true;
@@ -649,8 +664,10 @@ void stream_attrs(glsgpu_sur* h) {
   set((const void*)k_kron_ws<true>, 0, 0);
   set((const void*)k_kron_mma<false>, 0, 0);
   set((const void*)k_kron_mma<true>, 0, 0);
-  set((const void*)k_kron_mma2<false>, 0, 0);
-  set((const void*)k_kron_mma2<true>, 0, 0);
+  set((const void*)k_kron_mma2<false, 8>, 0, 0);
+  set((const void*)k_kron_mma2<true, 8>, 0, 0);
+  set((const void*)k_kron_mma2<false, 16>, 0, 0);
+  set((const void*)k_kron_mma2<true, 16>, 0, 0);
   set((const void*)k_pass_c_mma, 0, 0);
   set((const void*)k_stream<SMODE_B, false>, 0, 0);
   set((const void*)k_stream<SMODE_B, true>, 0, 0);

@@ -1190,8 +1190,8 @@ constexpr int KM2_OM = KM_OK * KM_OLD;              // Omega slab doubles per st
 constexpr int KM2_VC = KM_OK * KM_XS;               // one vector's chunk, padded: [8 columns][68]
 constexpr size_t km2_stage_bytes(int nv) { return (size_t)(KM2_OM + nv * KM2_VC) * sizeof(double); }
 
-template <bool APPLY>
-__global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict__ slab, int G, int64_t ldm,
+template <bool APPLY, int MW>
+__global__ void __launch_bounds__((MW + 1 + KM_EW) * 32, 1) k_kron_mma2(const double* __restrict__ slab, int G, int64_t ldm,
                                                         int64_t ntiles, const double* __restrict__ omegaT,
                                                         double* __restrict__ u_io, double* __restrict__ out,
                                                         double* partials, const SolveState* st, WBuf wbuf,
@@ -1203,9 +1203,18 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
     if (!st->diag_now) return;
     out = wbuf.sw[st->cur];
   }
+  // MW math warps (8: 32 columns each, 128 accumulator registers; 16: 16 columns each, 64 accumulator registers and
+  // four math warps per scheduler to cover one another's DMMA issue gaps), one loader warp, KM_EW side warps
+  constexpr int NTH = (MW + 1 + KM_EW) * 32;
+  constexpr int NI = 32 / MW;                      // n8 column blocks per math warp
+  // setmaxnreg.inc only draws on what setmaxnreg.dec released: (launch - side) * 128 >= (math - launch) * 32 MW
+  constexpr int REG_LAUNCH = MW == 8 ? 168 : 96;
+  constexpr int REG_SIDE = MW == 8 ? KM_REG_SIDE : 56, REG_MATH = MW == 8 ? KM_REG_MATH : 104;
+  static_assert((REG_LAUNCH - REG_SIDE) * 128 >= (REG_MATH - REG_LAUNCH) * 32 * MW, "register pool");
+  static_assert(MW == 8 || MW == 16, "math warp layouts");
   extern __shared__ __align__(128) double ksm[];
   __shared__ __align__(8) uint64_t full[KM2_MAXS], empty[KM2_MAXS], tile_done;
-  __shared__ double red[KM_NT / 32][2];
+  __shared__ double red[NTH / 32][2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nchunk = G / KM_OK;   // chunks (= Omega slabs) per tile
   const int64_t ntl = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA
@@ -1213,11 +1222,11 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
   const bool upd = !APPLY && st->mu_pending != 0, wupd = !APPLY && st->upd_pending != 0;
   const bool swd = st->sw_direct != 0;  // no sw recurrence: w alone is updated
   const bool fast = upd && wupd && swd;  // the iteration's common case: u . u moves to the math epilogue
-  for (int i = tid; i < nstage * sstride; i += KM_NT) ksm[i] = 0.0;  // rows past a short last tile stay 0
+  for (int i = tid; i < nstage * sstride; i += NTH) ksm[i] = 0.0;  // rows past a short last tile stay 0
   if (tid == 0) {
     for (int i = 0; i < nstage; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], KW_MATH + KM_EW);
+      mbar_init(&empty[i], MW + KM_EW);
     }
     mbar_init(&tile_done, KM_EW);
     mbar_fence_init();
@@ -1225,9 +1234,9 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
   fence_proxy_async_smem();
   __syncthreads();
   double p_a = 0.0, p_b = 0.0;  // u . Sigma u (math warps); u . u (math warps' epilogue, or the side warps)
-  if (warp >= KW_MATH) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(KM_REG_SIDE));
-    if (warp == KW_MATH) {
+  if (warp >= MW) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_SIDE));
+    if (warp == MW) {
       // ---------------- loader: per chunk, 8 Omega rows (lanes 0-7) and the chunk columns (lane 8 + 8 v + column)
       const int cur = st->cur;
       const int64_t mv = ldm * G;
@@ -1269,7 +1278,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
       }
     } else {
       // ---------------- side warps: element i = (column i / 64, row i % 64) of a chunk, i = etid + 32 KM_EW e
-      const int ew = warp - KW_MATH - 1;
+      const int ew = warp - MW - 1;
       const int etid = ew * 32 + lane;
       const double mu = st->mu, lp = st->lam_prev;
       double* __restrict__ wn = wbuf.w[st->nxt];
@@ -1342,19 +1351,19 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(KM_REG_MATH));
-    // ---------------- math warps: DMMA m16n8k4, warp owns columns [32 warp, 32 warp + 32) of every tile
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_MATH));
+    // ---------------- math warps: DMMA m16n8k4, warp owns columns [8 NI warp, 8 NI (warp + 1)) of every tile
     const int g = lane >> 2, t = lane & 3;
-    const int n0 = 32 * warp;
+    const int n0 = 8 * NI * warp;
     const double mu = st->mu;
     RingPos rp;
     for (int64_t jl = 0; jl < ntl; ++jl) {
       const int64_t k0 = (blockIdx.x + jl * gridDim.x) * KM_BM;
-      double acc[4][4][4];  // [m16 tile][n8 tile][fragment]
+      double acc[4][NI][4];  // [m16 tile][n8 tile][fragment]
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
       for (int s = 0; s < nchunk; ++s) {
@@ -1365,7 +1374,9 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
 #pragma unroll
         for (int kk = 0; kk < KM_OK / 4; ++kk) {
           const double* ob = om + (kk * 4 + t) * KM_OLD;
-          const double b0 = ob[0], b1 = ob[8], b2 = ob[16], b3 = ob[24];
+          double bq[NI];
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) bq[ni] = ob[8 * ni];
           const double* ua = U + kk * 4 * KM_XS;
           double a0[4], a1[4];
 #pragma unroll
@@ -1381,12 +1392,9 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
             }
           }
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) {
-            dmma_16x8x4(acc[mi][0], a0[mi], a1[mi], b0);
-            dmma_16x8x4(acc[mi][1], a0[mi], a1[mi], b1);
-            dmma_16x8x4(acc[mi][2], a0[mi], a1[mi], b2);
-            dmma_16x8x4(acc[mi][3], a0[mi], a1[mi], b3);
-          }
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma_16x8x4(acc[mi][ni], a0[mi], a1[mi], bq[ni]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[rp.slot]);
@@ -1398,13 +1406,14 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
       // the side warps have written this tile's u.  (They cannot be two tiles ahead: a tile has more chunks than the
       // ring has stages -- G > 128 -- and a stage is recycled only after every math warp released it.)
       if (!APPLY) mbar_wait(&tile_done, (uint32_t)(jl & 1));
-      const bool tile_in = k0 + KM_BM <= ldm && n0 + 32 <= G;
+      const bool tile_in = k0 + KM_BM <= ldm && n0 + 8 * NI <= G;
+      // (measured and dropped: requesting the next row block's u before this one's stores -- 5.13 -> 5.37 ms)
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) {
-        double uv[4][4];
+        double uv[NI][4];
         if (!APPLY) {
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
+          for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const int c = n0 + 8 * ni + 2 * t + (q & 1);
@@ -1413,7 +1422,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
             }
         }
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int c = n0 + 8 * ni + 2 * t + (q & 1);
@@ -1426,7 +1435,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
           }
         if (!APPLY && fast && k0 + KM_BM <= ldm) {  // u . u of the tiles the side warps' fast path handled
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
+          for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
             for (int q = 0; q < 4; ++q) p_b = __fma_rn(uv[ni][q], uv[ni][q], p_b);
         }
@@ -1446,7 +1455,7 @@ __global__ void __launch_bounds__(KM_NT, 1) k_kron_mma2(const double* __restrict
   __syncthreads();
   if (tid == 0 && !APPLY) {
     double a = 0.0, bb = 0.0;
-    for (int w = 0; w < KM_NT / 32; ++w) {
+    for (int w = 0; w < NTH / 32; ++w) {
       a += red[w][0];
       bb += red[w][1];
     }
