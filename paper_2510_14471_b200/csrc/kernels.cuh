@@ -1407,7 +1407,8 @@ __global__ void __launch_bounds__((MW + 1 + KM_EW) * 32, 1) k_kron_mma2(const do
       // ring has stages -- G > 128 -- and a stage is recycled only after every math warp released it.)
       if (!APPLY) mbar_wait(&tile_done, (uint32_t)(jl & 1));
       const bool tile_in = k0 + KM_BM <= ldm && n0 + 8 * NI <= G;
-      // (measured and dropped: requesting the next row block's u before this one's stores -- 5.13 -> 5.37 ms)
+      // (measured and dropped: requesting the next row block's u before this one's stores -- 5.13 -> 5.37 ms; and
+      // preparing each k-step's A operands one step ahead, peeking at the next stage with test_wait -- 5.9 ms)
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) {
         double uv[NI][4];
