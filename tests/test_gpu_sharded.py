@@ -48,6 +48,7 @@ def run_group(p, P, cfg, partition=None):
                                                                   Yr.data_ptr(), ml, p.omega)
             g = api.pcg_aug(None, op, config=cfg, true_beta=p.beta, want_w=True)
             Q, R = op.factors()
+            g.factor_method = op.factor_info()[0]
             out[r] = (g, Q, R)
             op.close()
         except Exception as e:  # noqa: BLE001 -- reported below
@@ -66,22 +67,31 @@ def run_group(p, P, cfg, partition=None):
     return out, parts
 
 
+# the last field: the setup every rank must have taken -- CholeskyQR2 with all-gathered Grams when every rank's shard
+# is on the TMA passes (32-row aligned), the cross-rank Householder TSQR otherwise
 CASES = [
-    ("c4_G24_M3000_P2", lambda: synth.make_problem(4, M=3000, G=24), 2, None),
-    ("c4_G24_M3000_P3_uneven", lambda: synth.make_problem(4, M=3000, G=24), 3, [(0, 700), (700, 1500), (2200, 800)]),
-    ("c1_G20_M1200_P2_wide", lambda: synth.make_problem(1, M=1200, G=20), 2, None),
-    ("c0_P2", lambda: synth.make_problem(0), 2, None),
+    ("c4_G24_M2048_P2_aligned", lambda: synth.make_problem(4, M=2048, G=24), 2, None, "cholqr2"),
+    ("c1_G20_M1280_P2_wide_aligned", lambda: synth.make_problem(1, M=1280, G=20), 2, None, "cholqr2"),
+    ("c4_G24_M3000_P2", lambda: synth.make_problem(4, M=3000, G=24), 2, None, None),
+    ("c4_G24_M3000_P3_uneven", lambda: synth.make_problem(4, M=3000, G=24), 3, [(0, 700), (700, 1500), (2200, 800)],
+     "tsqr"),
+    ("c1_G20_M1200_P2_wide", lambda: synth.make_problem(1, M=1200, G=20), 2, None, None),
+    ("c0_P2", lambda: synth.make_problem(0), 2, None, None),
 ]
 
 
 @pytest.mark.parametrize("mode", ["qr", "x"])
-@pytest.mark.parametrize("name,mk,P,part", CASES, ids=[c[0] for c in CASES])
-def test_sharded_ranks_match_oracle(name, mk, P, part, mode):
+@pytest.mark.parametrize("name,mk,P,part,method", CASES, ids=[c[0] for c in CASES])
+def test_sharded_ranks_match_oracle(name, mk, P, part, method, mode):
     p = mk()
     mx = p.max_iter or 400
     cfg = api.PcgConfig(tol_rel=p.tol_rel, max_iter=mx, xv_mode=mode, diag_every=1)
     out, parts = run_group(p, P, cfg, part)
     g0 = out[0][0]
+    methods = {g.factor_method for g, _, _ in out}
+    assert len(methods) == 1, methods  # the collectives of the two factorisations differ: all ranks take the same
+    if method is not None:
+        assert methods == {method}, methods
     # every rank takes bitwise the same decisions and holds the same replicated b and R
     for g, _, R in out[1:]:
         assert g.solution.iterations == g0.solution.iterations
