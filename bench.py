@@ -412,7 +412,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         for s in range(ksteps):
             if s == 0:
-                op2.update(Xh.numpy().T, Yh.numpy().T)  # step 1: the upload pipelined with the TSQR by block groups
+                op2.update(Xh.numpy().T, Yh.numpy().T)  # step 1: the upload pipelined with the factorisation by block groups
             else:
                 op2.update_staged()  # steps 2..K: uploaded under the previous step's solve
             if s + 1 < ksteps:
@@ -429,7 +429,7 @@ def run_ours(args):
         e2e = {"value": e_iters / dt, "unit": UNIT, "h2d_bytes_per_step": int(8 * (Ml * n + Ml * G)),
                "d2h_bytes_per_step": int(8 * n + 48 * (r2.trace.rows.size)), "steps": ksteps,
                "timer": ("host wall clock (max over ranks) around K steps of: the step's X and Y uploaded from pinned "
-                         "host memory -- step 1 by glsgpu_sur_update (the H2D pipelined with the TSQR by block groups), "
+                         "host memory -- step 1 by glsgpu_sur_update (the H2D pipelined with the factorisation by block groups), "
                          "steps 2..K by glsgpu_sur_stage on the copy stream under the previous step's solve, then "
                          "glsgpu_sur_update_staged (refactor) -- the solve, b to the host")}
         del Xh, Yh

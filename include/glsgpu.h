@@ -156,7 +156,7 @@ int glsgpu_sur_create_device(int G, int64_t M, const int64_t* n_i, const double*
 
 /* New X (M x n) and Y (M x G) from HOST buffers for a handle made by glsgpu_sur_create or
  * glsgpu_sur_create_sharded_host (same shapes; a sharded handle takes this rank's rows): upload and refactor,
- * reusing the handle's device memory and TSQR plan (create once, solve many).  This is make_sur +
+ * reusing the handle's device memory and factorisation plan (create once, solve many).  This is make_sur +
  * sur_preconditioner for the next model (proj/src/structured.cpp:97-105,416-453) without reallocating. */
 int glsgpu_sur_update(glsgpu_sur* h, const double* X, const double* Y, int* bad_block);
 
@@ -206,9 +206,9 @@ int glsgpu_launch_count(const glsgpu_sur* h, int64_t* count);
  * Rank r owns rows [row0_r, row0_r + M_local) of every block (any contiguous split; each rank needs
  * at least max n_i rows); Omega, R and every n-vector are replicated.  Per PCG iteration the ranks
  * all-gather three small partial-sum vectors over NCCL (d, u.u | Q'r per block | c, r.r, pr.pr) and
- * reduce them in rank order, so every rank takes bitwise the same decisions.  The setup QR is a
- * TSQR across ranks (all-gather of the per-rank R factors).  Host vectors passed to the probe
- * applies / solve of a sharded handle are the rank's local rows; b is replicated. */
+ * reduce them in rank order, so every rank takes bitwise the same decisions.  The setup factorisation works across
+ * ranks too: CholeskyQR2 all-gathers the per-rank Gram matrices, its TSQR fallback the per-rank R factors.  Host
+ * vectors passed to the probe applies / solve of a sharded handle are the rank's local rows; b is replicated. */
 int glsgpu_nccl_unique_id(void* id_out /* 128 bytes (ncclUniqueId) */);
 int glsgpu_sur_create_sharded(int G, int64_t M_local, int64_t M_global, const int64_t* n_i, const double* X_dev,
                               int64_t ldx, const double* Y_dev, int64_t ldy, const double* omega,

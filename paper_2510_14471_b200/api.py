@@ -210,7 +210,8 @@ def sur_from_problem(prob) -> SurModel:
 class GpuSurPreconditioner:
     """The SUR indefinite preconditioner (SurPreconditioner, structured.cpp:416-453) resident on a B200.
 
-    Construction runs the per-block Householder QR on the device (TSQR tree per block).
+    Construction factors every block on the device: CholeskyQR2 on the FP64 tensor cores, the Householder TSQR tree
+    per block as its fallback (factor_info()).
     """
 
     def __init__(self, sur: SurModel, block_scale: Optional[np.ndarray] = None, device: int = 0):
@@ -395,7 +396,7 @@ class GpuSurPreconditioner:
 
     def update(self, X: np.ndarray, y: np.ndarray):
         """New data of the same shapes (glsgpu_sur_update): upload X (M x n) and Y (M x G), refactor; the device
-        memory and the TSQR plan of this operator are reused."""
+        memory and the factorisation plan of this operator are reused."""
         Xf = np.asfortranarray(X, dtype=np.float64)
         Yf = np.asfortranarray(y, dtype=np.float64)
         if Xf.shape != (self.m // len(self._nb), self.n) or Yf.shape != (self.m // len(self._nb), len(self._nb)):
