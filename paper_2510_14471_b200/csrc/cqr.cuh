@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(CQ_NT, 1) k_cqr_pass(CqArgs a) {
             const int c = idx / TR, i = idx - c * TR;
             T[c * LDT + i] = i < v ? sp[(int64_t)c * a.src_cs + i] : 0.0;
           }
+          fence_proxy_async_smem();  // these generic-proxy writes before a later bulk copy into the same stage
           __syncwarp();
           if (lane == 0) mbar_arrive(&full[rp.slot]);
         }
