@@ -78,7 +78,6 @@ constexpr size_t cq_smem_bytes() {
 
 __device__ __forceinline__ void cq_bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(CQ_CW * 32) : "memory"); }
 
-
 // Product rows of one warp that owns 16 rows and every column of the tile (NBP = 32): column blocks in pairs, last
 // pair first.  A pair reads only the tile columns up to its own (Rinv is upper triangular), so with WRITE_BACK its
 // product goes back into the tile (the tile becomes Q1 in place, for this warp's Gram slice) before the pairs below
@@ -96,32 +95,20 @@ __device__ __forceinline__ void cq_apply_own(double* T, const double* Rv, int am
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[ni][e] = 0.0;
     const int k1 = FULL ? 2 * nb0 + 2 : min(K4, 2 * nb0 + 2), k2 = FULL ? 2 * nb0 + 4 : min(K4, 2 * nb0 + 4);
+    // (FULL: the bounds are compile-time constants after the pair loop is unrolled, so these loops unroll too)
 #pragma unroll
-    for (int kk = 0; kk < (FULL ? k1 : 0); ++kk) {
+    for (int kk = 0; kk < k1; ++kk) {
       const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
       const double a0 = tp[0], a1 = tp[8];
       const double* bp = Rv + (4 * kk + q4) * LDB + 8 * nb0 + g;
       dmma_16x8x4(acc[0], a0, a1, bp[0]);
       dmma_16x8x4(acc[1], a0, a1, bp[8]);
     }
-    if (!FULL)
-      for (int kk = 0; kk < k1; ++kk) {
-        const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
-        const double a0 = tp[0], a1 = tp[8];
-        const double* bp = Rv + (4 * kk + q4) * LDB + 8 * nb0 + g;
-        dmma_16x8x4(acc[0], a0, a1, bp[0]);
-        dmma_16x8x4(acc[1], a0, a1, bp[8]);
-      }
 #pragma unroll
-    for (int kk = (FULL ? k1 : 0); kk < (FULL ? k2 : 0); ++kk) {
+    for (int kk = k1; kk < k2; ++kk) {
       const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
       dmma_16x8x4(acc[1], tp[0], tp[8], Rv[(4 * kk + q4) * LDB + 8 * nb0 + 8 + g]);
     }
-    if (!FULL)
-      for (int kk = k1; kk < k2; ++kk) {
-        const double* tp = T + (4 * kk + q4) * LDT + am0 + g;
-        dmma_16x8x4(acc[1], tp[0], tp[8], Rv[(4 * kk + q4) * LDB + 8 * nb0 + 8 + g]);
-      }
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
