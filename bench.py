@@ -63,7 +63,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: max(5, min(steps, 10)))")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=20000)
+    ap.add_argument("--cpu-rows", type=int, default=0,
+                    help="rows of the CPU baseline's sample (default: 100000 for this arm's cpu_baseline leg, about "
+                         "20 s of CPU work measured once; 20000 per step of --impl reference, which repeats it "
+                         "steps + warmup times)")
     ap.add_argument("--no-witness", action="store_true")
     ap.add_argument("--no-trace-all", action="store_true", help="skip the diag_every = 1 (full trace) measurement")
     ap.add_argument("--witness-rows", type=int, default=4000)
@@ -217,7 +220,7 @@ def run_reference(args):
     meta = synth.config_meta(args.config)
     M = args.rows or meta["M"]
     iters = meta["max_iter"] or 200
-    samp = CpuSample(args.config, min(args.cpu_rows, M), host_cores())
+    samp = CpuSample(args.config, min(args.cpu_rows or 20000, M), host_cores())
     vals = []
     for s in range(args.warmup + args.steps):
         v = samp.value(M, iters)
@@ -449,7 +452,7 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         try:
-            cpu = CpuSample(args.config, min(args.cpu_rows, M), host_cores()).value(M, max_iter or 200)
+            cpu = CpuSample(args.config, min(args.cpu_rows or 100000, M), host_cores()).value(M, max_iter or 200)
         except Exception as e:  # the CPU baseline is a reported number, never the product
             cpu = {"error": str(e)}
 
