@@ -2676,8 +2676,12 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
   const int timing = (cfg.kernel_timing && !h->grp) ? 1 : 0;
   // a local-group (test-only) handle runs the iterations eagerly: its exchange crosses streams, which a
   // captured graph cannot hold
+  // diag_every = 0 (row 0 and the final row only): the captured iterations carry no diagnostics kernels -- nine
+  // gated no-op launches per iteration, 8% of a config-1 iteration -- and the final row's run once after the loop
+  const bool tail_diag = diag == 0 && !h->grp && !h->fold;
+  const int gdiag = (diag >= 0 && !tail_diag) ? 1 : -1;
   const bool need_graph = !h->grp && (!h->graph || h->graph_chunk != chunk || h->graph_xmode != xv_mode ||
-                          h->graph_diag != (diag >= 0 ? 1 : -1) || h->graph_timing != timing ||
+                          h->graph_diag != gdiag || h->graph_timing != timing ||
                           h->graph_fma != h->kron_fma || h->graph_sw != h->sw_direct || h->graph_fused != h->fused ||
                           h->graph_rows != h->rows_d || h->graph_fold != h->fold);
   if (need_graph) {
@@ -2694,7 +2698,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     h->capturing = true;
-    for (int k = 0; k < chunk; ++k) capture_iteration(h, xv_mode, diag >= 0 ? 1 : -1, timing, k);
+    for (int k = 0; k < chunk; ++k) capture_iteration(h, xv_mode, gdiag, timing, k);
     h->capturing = false;
     CK(cudaStreamEndCapture(s, &graph));
     {
@@ -2714,7 +2718,7 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
     CK(cudaGraphDestroy(graph));
     h->graph_chunk = chunk;
     h->graph_xmode = xv_mode;
-    h->graph_diag = diag >= 0 ? 1 : -1;
+    h->graph_diag = gdiag;
     h->graph_timing = timing;
     h->graph_fma = h->kron_fma;
     h->graph_sw = h->sw_direct;
@@ -2760,6 +2764,13 @@ int glsgpu_sur_solve(glsgpu_sur* h, const glsgpu_pcg_config* cfg_in, const doubl
         kt_n[2]++;
       }
     }
+  }
+  if (tail_diag) {
+    // the final row's diagnostics (gated on st->diag_now, which k_scalar_c set on the terminating iteration; the
+    // state is the one the in-graph kernels would have seen: the iterations captured after it did nothing)
+    if (h->sw_direct && !kron_mma_apply(h, -2, nullptr))
+      launch_kron(h, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 3, h->st, nullptr);
+    diag_row(h, xv_mode, true, -1);
   }
   // a w / sw update still pending (the loop stopped in k_scalar_c) is materialized now
   k_apply_pending<<<GRID_CAP, NT, 0, s>>>(h->st, wbuf_of(h), h->u, h->su, h->ldm * h->G);
