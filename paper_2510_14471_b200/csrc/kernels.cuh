@@ -1221,7 +1221,7 @@ __global__ void __launch_bounds__((MW + 1 + KM_EW) * 32, 1) k_kron_mma2(const do
   const int sstride = KM2_OM + nv * KM2_VC;
   const bool upd = !APPLY && st->mu_pending != 0, wupd = !APPLY && st->upd_pending != 0;
   const bool swd = st->sw_direct != 0;  // no sw recurrence: w alone is updated
-  const bool fast = upd && wupd && swd;  // the iteration's common case: u . u moves to the math epilogue
+  const bool fast = upd && wupd;  // the iteration's common case: u . u moves to the math epilogue
   for (int i = tid; i < nstage * sstride; i += NTH) ksm[i] = 0.0;  // rows past a short last tile stay 0
   if (tid == 0) {
     for (int i = 0; i < nstage; ++i) {
@@ -1316,6 +1316,21 @@ __global__ void __launch_bounds__((MW + 1 + KM_EW) * 32, 1) k_kron_mma2(const do
               const int64_t off = (int64_t)(k * KM_OK + i / KM_BM) * ldm + k0 + i % KM_BM;
               stg_cs(wn + off, wv[e]);
               u_io[off] = pv[e];  // read back by the math warps' epilogue (L2)
+            }
+            if (!swd) {  // Sigma w carried by the reference's recurrence (pcg.cpp:152): sw -= lambda su
+#pragma unroll
+              for (int e = 0; e < NE; ++e) {
+                const int i = etid + 32 * KM_EW * e;
+                if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+                const int o = (i / KM_BM) * KM_XS + i % KM_BM;
+                wv[e] = __fma_rn(-lp, E[4 * KM2_VC + o], E[3 * KM2_VC + o]);
+              }
+#pragma unroll
+              for (int e = 0; e < NE; ++e) {
+                const int i = etid + 32 * KM_EW * e;
+                if (e == NE - 1 && (KM_OK * KM_BM) % (32 * KM_EW) != 0 && i >= KM_OK * KM_BM) break;
+                stg_cs(swn + (int64_t)(k * KM_OK + i / KM_BM) * ldm + k0 + i % KM_BM, wv[e]);
+              }
             }
           } else if (!APPLY) {
 #pragma unroll
